@@ -1,0 +1,192 @@
+/*
+ * plv.h -- C ABI of libplv.so, the B200 (sm_100a) parallel-Louvain hot path.
+ *
+ * Drop-in boundary for the reference package `parlouvain` (arXiv 1410.1237).
+ * The reference crosses into native code only through its kernel seam
+ * PL/backend.py:13-22 (decide_moves / apply_moves / color_assign /
+ * color_conflicts, PL/_kernels.pyx) and otherwise runs numpy on the host
+ * (Graph.from_edges, vf_compact, rebuild, modularity).  Each entry point below
+ * replaces one of those, cited as PL/<file>:<line>
+ * (PL/ = /root/reference/pkg/src/parlouvain/).
+ *
+ * Conventions
+ *  - Every array argument is a DEVICE pointer unless its name ends in `_h`
+ *    (host).  Vertex / community ids are int32 (n < 2^31), CSR offsets int64,
+ *    weights and aggregates float64.  The caller owns every buffer; the
+ *    library allocates only private, stream-ordered scratch.
+ *  - `stream` is a cudaStream_t passed as void*.  Work is stream-ordered;
+ *    entry points that return sizes through `_h` arguments synchronise the
+ *    stream before returning.
+ *  - Return value: PLV_OK (0) or a negative PLV_E* code; plv_last_error()
+ *    gives a message for the calling thread.  The Python host maps codes to
+ *    the reference's exception classes (PL/errors.py).
+ *  - No CPU fallback: without a usable sm_100 device every call returns
+ *    PLV_ENODEV.
+ */
+#ifndef PLV_H
+#define PLV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PLV_OK 0
+#define PLV_EINVAL -1     /* bad argument (ValueError)                        */
+#define PLV_EWEIGHT -2    /* non-finite / non-positive weight (GraphParseError) */
+#define PLV_ERANGE -3     /* vertex id out of range (ValueError)              */
+#define PLV_ECUDA -4      /* CUDA runtime error                               */
+#define PLV_ENODEV -5     /* no usable sm_100 device                          */
+#define PLV_EDUP -6       /* subset lists a vertex twice (ValueError)         */
+
+int plv_abi_version(void);
+const char *plv_last_error(void);
+/* 1 when a compute-capability-10.x device is visible, else 0. */
+int plv_device_ok(void);
+
+/* ---------------------------------------------------------------- sums */
+
+/* ndarray.sum() of a float64 array with numpy's pairwise tree, bit-exact
+ * (used by PL/graph.py:80 and PL/modularity.py:64).  out: 1 double. */
+int plv_sum(const double *a, int64_t n, double *out, void *stream);
+
+/* modularity (PL/modularity.py:59-64): q = sum(w_int)/2m - sum((a_tot/2m)^2)
+ * with both sums as numpy pairwise trees.  out: 1 double. */
+int plv_modularity(const double *w_int, const double *a_tot, int64_t n, double m,
+                   double *out, void *stream);
+
+/* ------------------------------------------------------------ CSR build */
+
+/*
+ * Graph.from_edges (PL/graph.py:88-147) + Graph.__init__ (PL/graph.py:64-86).
+ * Records u, v (int32) and w (float64), R of them, in input order.
+ * Outputs: off[n+1]; nbr/wts with room for 2*R entries; selfw[n]; k[n].
+ * info_h[0..5] = {nnz, merged, num_edges, max_degree, integral, num_self};
+ * m_h = total_weight.  `integral` = every merged weight is an integer and the
+ * total is < 2^52 (then every downstream sum is exact in any order).
+ */
+int plv_csr_build(const int32_t *u, const int32_t *v, const double *w, int64_t R, int64_t n,
+                  int64_t *off, int32_t *nbr, double *wts, double *selfw, double *k,
+                  int64_t *info_h, double *m_h, void *stream);
+
+/* Graph.edge_records (PL/graph.py:169-174): the a <= b half, row-major.
+ * ra/rb/rw need room for nnz entries; count_h = records written. */
+int plv_edge_records(const int64_t *off, const int32_t *nbr, const double *wts, int64_t n,
+                     int32_t *ra, int32_t *rb, double *rw, int64_t *count_h, void *stream);
+
+/* ----------------------------------------------------- vertex following */
+
+/*
+ * vf_compact (PL/heuristics.py:46-89): vertex_map[n] (int32) plus the
+ * compacted graph's records (kept edge_records, then (t,t,w) per folded
+ * vertex in ascending id); rec_* need room for nnz + n entries.
+ * info_h = {n_new, merged_count, num_records}.  Feed the records to
+ * plv_csr_build to finish the compaction (PL/heuristics.py:85-87).
+ */
+int plv_vf_records(const int64_t *off, const int32_t *nbr, const double *wts,
+                   const double *selfw, int64_t n, int32_t *vertex_map, int32_t *rec_u,
+                   int32_t *rec_v, double *rec_w, int64_t *info_h, void *stream);
+
+/* ------------------------------------------------------------- coloring */
+
+/*
+ * color_graph (PL/heuristics.py:92-118): speculative rounds of color_assign
+ * (PL/_kernels.pyx:148-174) and color_conflicts (PL/_kernels.pyx:177-195)
+ * until no vertex is rejected; rejects keep ascending order.
+ * colors[n] (int32).  info_h = {num_colors, rounds}.
+ */
+int plv_color(const int64_t *off, const int32_t *nbr, int64_t n, int64_t max_degree,
+              int32_t *colors, int64_t *info_h, void *stream);
+
+/* Kernel-granular seam twins (PL/_kernels.pyx:148-195); `colors` may hold -1. */
+int plv_color_assign(const int64_t *off, const int32_t *nbr, const int32_t *active, int64_t na,
+                     const int32_t *colors, int32_t *out_colors, void *stream);
+int plv_color_conflicts(const int64_t *off, const int32_t *nbr, const int32_t *active,
+                        int64_t na, const int32_t *colors, uint8_t *out_keep, void *stream);
+
+/* Coloring.classes (PL/heuristics.py:34-38): class_off[num_colors+1] and the
+ * vertices of every class in ascending id (stable sort by colour). */
+int plv_color_classes(const int32_t *colors, int64_t n, int64_t num_colors, int64_t *class_off,
+                      int32_t *class_vtx, void *stream);
+
+/* ----------------------------------------------------------- local move */
+
+/* Flags for plv_apply / plv_iteration. */
+#define PLV_F_INDEPENDENT 1  /* no two subset vertices are adjacent (colour class) */
+#define PLV_F_INTEGRAL 2     /* graph weights integral: aggregate in any order   */
+#define PLV_F_IDENTITY 4     /* subset == arange(n)                              */
+
+/*
+ * decide_moves (PL/_kernels.pyx:21-101) for every subset vertex against the
+ * state at entry (the reference's snapshot, PL/engine.py:150-152).
+ * labels may be NULL (labels[c] == c, the case for every state the engine
+ * builds, PL/modularity.py:52).  Outputs per subset index: target, moved,
+ * e_old (= e_{i->c_old}), e_best (= e_{i->target}).  cand_h (nullable) receives
+ * sum over the subset of distinct neighbour communities (roofline bytes).
+ */
+int plv_decide(const int64_t *off, const int32_t *nbr, const double *wts, const double *k,
+               const int32_t *labels, const int32_t *subset, int64_t ns, const int32_t *assign,
+               const double *a_tot, const int32_t *sizes, double m, int32_t *out_target,
+               uint8_t *out_moved, double *out_e_old, double *out_e_best, int64_t *cand_h,
+               void *stream);
+
+/*
+ * apply_moves (PL/_kernels.pyx:104-145): applies the decided moves as if
+ * sequentially in subset order against the live assignment, bit-exactly
+ * (parallel restatement: live e_a/e_b from the decide snapshot plus the
+ * targets of earlier subset vertices, then one ordered fold per community).
+ * moves_h = number of moves (PL/_kernels.pyx:145).
+ */
+int plv_apply(const int64_t *off, const int32_t *nbr, const double *wts, const double *k,
+              const double *selfw, int64_t n, const int32_t *subset, int64_t ns,
+              const int32_t *target, const uint8_t *moved, const double *e_old,
+              const double *e_best, int flags, int32_t *assign, double *a_tot, double *w_int,
+              int32_t *sizes, int64_t *moves_h, void *stream);
+
+/* ---------------------------------------------------------------- rebuild */
+
+/*
+ * rebuild (PL/engine.py:229-256) up to the from_edges call: renumber[n]
+ * (int32, -1 for empty community ids, dense in ascending id), and the merged,
+ * (lo, hi)-sorted coarse records lo/hi/w (room for nnz entries).
+ * info_h = {n_new, num_records}.  Finish with plv_csr_from_sorted.
+ */
+int plv_rebuild_records(const int64_t *off, const int32_t *nbr, const double *wts, int64_t n,
+                        const int32_t *assign, int32_t *renumber, int32_t *lo, int32_t *hi,
+                        double *w, int64_t *info_h, void *stream);
+
+/* Graph.from_edges on records already sorted by (a, b) with a <= b and no
+ * duplicates (sorting and merging are then the identity); same outputs as
+ * plv_csr_build. */
+int plv_csr_from_sorted(const int32_t *a, const int32_t *b, const double *w, int64_t M,
+                        int64_t n, int64_t *off, int32_t *nbr, double *wts, double *selfw,
+                        double *k, int64_t *info_h, double *m_h, void *stream);
+
+/* Hierarchy.flatten step (PL/engine.py:115): out[i] = renumber[assign[map[i]]]
+ * (map may be NULL = identity). */
+int plv_compose(const int32_t *map, const int32_t *assign, const int32_t *renumber, int64_t n,
+                int32_t *out, void *stream);
+
+/* ------------------------------------------------------------ generators */
+
+/* Counter-based synthetic graphs (BASELINE.json configs), identical to the
+ * numpy generators in paper_1410_1237_b200/synthetic.py.  Each writes records
+ * (u, v, w) into caller buffers of capacity `cap` and returns the count in
+ * count_h. */
+int plv_gen_rmat(uint64_t seed, int scale, int64_t edge_factor, double a, double b, double c,
+                 double w_lo, double w_hi, int32_t *u, int32_t *v, double *w, int64_t cap,
+                 int64_t *count_h, void *stream);
+int plv_gen_sbm(uint64_t seed, int64_t n, int64_t block, double p_in, double p_out, int32_t *u,
+                int32_t *v, double *w, int64_t cap, int64_t *count_h, void *stream);
+int plv_gen_grid(uint64_t seed, int64_t side, double keep, int64_t pendants, double w_lo,
+                 int32_t *u, int32_t *v, double *w, int64_t cap, int64_t *count_h,
+                 void *stream);
+/* Chung-Lu: endpoints drawn by searchsorted(cdf, U * cdf[n-1], 'right'). */
+int plv_gen_chung_lu(uint64_t seed, const double *cdf, int64_t n, int64_t records, int32_t *u,
+                     int32_t *v, double *w, int64_t cap, int64_t *count_h, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PLV_H */

@@ -1,0 +1,50 @@
+// api_util.cu -- error reporting and device checks for the libplv C ABI.
+#include "common.cuh"
+#include <cstring>
+
+namespace plv {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+void check_device() {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error("no CUDA device: %s (libplv has no CPU fallback)", cudaGetErrorString(e));
+        throw Fail{PLV_ENODEV};
+    }
+    static thread_local int checked_dev = -1;
+    if (checked_dev == dev) return;
+    int major = 0;
+    e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (e != cudaSuccess || major != 10) {
+        cudaGetLastError();
+        set_error("libplv is built for sm_100a; device %d has compute capability major %d", dev,
+                  major);
+        throw Fail{PLV_ENODEV};
+    }
+    checked_dev = dev;
+}
+
+}  // namespace plv
+
+extern "C" int plv_abi_version(void) { return 1; }
+
+extern "C" const char *plv_last_error(void) { return plv::g_err; }
+
+extern "C" int plv_device_ok(void) {
+    try {
+        plv::check_device();
+    } catch (plv::Fail &) {
+        return 0;
+    }
+    return 1;
+}

@@ -1,0 +1,136 @@
+// common.cuh -- shared helpers for libplv (B200 / sm_100a parallel Louvain).
+//
+// Error model: C++ code throws plv::Fail; every extern "C" entry point wraps
+// its body in PLV_ENTRY / PLV_EXIT, which converts to a PLV_E* status and
+// records a thread-local message for plv_last_error().
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstdarg>
+#include <string>
+#include <stdexcept>
+
+#include "../../include/plv.h"
+
+namespace plv {
+
+struct Fail {
+    int code;
+};
+
+void set_error(const char *fmt, ...);
+void check_device();  // throws PLV_ENODEV unless an sm_100 device is current
+
+#define PLV_CUDA(x)                                                                   \
+    do {                                                                              \
+        cudaError_t _e = (x);                                                         \
+        if (_e != cudaSuccess) {                                                      \
+            plv::set_error("%s: %s (%s:%d)", #x, cudaGetErrorString(_e), __FILE__,     \
+                           __LINE__);                                                 \
+            throw plv::Fail{PLV_ECUDA};                                               \
+        }                                                                             \
+    } while (0)
+
+#define PLV_LAUNCH_CHECK() PLV_CUDA(cudaGetLastError())
+
+#define PLV_FAIL(code, ...)              \
+    do {                                 \
+        plv::set_error(__VA_ARGS__);     \
+        throw plv::Fail{code};           \
+    } while (0)
+
+#define PLV_ENTRY       \
+    try {               \
+        plv::check_device();
+
+#define PLV_EXIT                                  \
+    }                                             \
+    catch (plv::Fail & f) {                       \
+        return f.code;                            \
+    }                                             \
+    catch (std::exception & e) {                  \
+        plv::set_error("%s", e.what());           \
+        return PLV_ECUDA;                         \
+    }                                             \
+    return PLV_OK;
+
+inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Stream-ordered scratch buffer (cudaMallocAsync pool); freed on scope exit.
+template <class T>
+struct Buf {
+    T *p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = nullptr;
+    Buf() = default;
+    Buf(size_t count, cudaStream_t st) { alloc(count, st); }
+    void alloc(size_t count, cudaStream_t st) {
+        release();
+        s = st;
+        n = count;
+        if (count) PLV_CUDA(cudaMallocAsync((void **)&p, sizeof(T) * count, st));
+    }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    ~Buf() { release(); }
+    Buf(const Buf &) = delete;
+    Buf &operator=(const Buf &) = delete;
+    T *get() const { return p; }
+    operator T *() const { return p; }
+};
+
+inline unsigned grid_for(int64_t work, int block, int64_t cap = 148 * 64) {
+    int64_t g = (work + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (unsigned)g;
+}
+
+inline int bits_for(int64_t n) {
+    int b = 1;
+    while (b < 62 && ((int64_t)1 << b) < n) b++;
+    return b;
+}
+
+template <class T>
+T d2h(const T *dev, cudaStream_t s) {
+    T v;
+    PLV_CUDA(cudaMemcpyAsync(&v, dev, sizeof(T), cudaMemcpyDeviceToHost, s));
+    PLV_CUDA(cudaStreamSynchronize(s));
+    return v;
+}
+
+// ------------------------------------------------------------ fp helpers
+// The reference is compiled with -ffp-contract=off (pkg/setup.py:32): every
+// product and sum is rounded separately.  We build with --fmad=false and use
+// explicit _rn intrinsics on every parity-critical expression.
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// --------------------------------------------------- counter-based RNG
+// SplitMix64 finaliser; u64(key, i) is the i-th SplitMix64 output for state
+// `key`.  Mirrored bit-for-bit by paper_1410_1237_b200/synthetic.py.
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+constexpr uint64_t GAMMA = 0x9E3779B97F4A7C15ull;
+__host__ __device__ __forceinline__ uint64_t stream_key(uint64_t seed, uint64_t stream) {
+    return mix64(seed * 0xD1B54A32D192ED03ull + stream * GAMMA + 1ull);
+}
+__host__ __device__ __forceinline__ uint64_t rnd64(uint64_t key, uint64_t i) {
+    return mix64(key + (i + 1ull) * GAMMA);
+}
+__host__ __device__ __forceinline__ double rnd01(uint64_t key, uint64_t i) {
+    return (double)(rnd64(key, i) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+}  // namespace plv

@@ -1,0 +1,171 @@
+// pairwise.cu -- device reductions with numpy's pairwise tree (bit-exact).
+//
+// Whole-array sum: the tree of n is cut at the first depth d0 where every
+// node has <= 256 elements.  Above d0 the tree is a perfect binary tree (no
+// node there is a leaf), so after one thread per depth-d0 node has computed
+// its subtree serially (<= 2 leaves), the remaining levels are an aligned
+// perfect pairwise reduction: value(level, p) = value(p0) + value(p1).
+#include "pairwise.cuh"
+
+namespace plv {
+
+template <class F>
+__global__ void k_pw_nodes(const double *__restrict__ a, int64_t n, int d0, double *vals, F f) {
+    uint64_t cnt = 1ull << d0;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < cnt;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        int64_t lo, len;
+        pw_node(n, d0, t, &lo, &len);
+        vals[t] = pw_serial(a + lo, len, f);
+    }
+}
+
+// Reduce groups of 2^kb consecutive values (a perfect subtree each) to one
+// (ping-pong in shared memory). When `final` the single remaining value is
+// written as 0.0 + root.
+__global__ void k_pw_tree2(const double *in, int64_t count, int kb, double *out, int final) {
+    extern __shared__ double sm[];
+    int64_t group = 1ll << kb;
+    double *A = sm, *B = sm + group;
+    int64_t base = blockIdx.x * group;
+    for (int64_t i = threadIdx.x; i < group; i += blockDim.x)
+        A[i] = (base + i < count) ? in[base + i] : 0.0;
+    __syncthreads();
+    for (int64_t width = group; width > 1; width >>= 1) {
+        int64_t half = width >> 1;
+        for (int64_t i = threadIdx.x; i < half; i += blockDim.x)
+            B[i] = __dadd_rn(A[2 * i], A[2 * i + 1]);
+        __syncthreads();
+        double *t = A; A = B; B = t;
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = final ? __dadd_rn(0.0, A[0]) : A[0];
+}
+
+__global__ void k_zero1(double *out) { out[0] = 0.0; }
+
+template <class F>
+static void pw_launch(const double *a, int64_t n, double *out_dev, cudaStream_t s, F f) {
+    if (n <= 0) {
+        k_zero1<<<1, 1, 0, s>>>(out_dev);
+        PLV_LAUNCH_CHECK();
+        return;
+    }
+    int d0 = pw_depth(n);
+    int64_t cnt = 1ll << d0;
+    Buf<double> v0(cnt, s), v1((cnt + 1023) / 1024 + 1, s);
+    k_pw_nodes<<<grid_for(cnt, 256, 148 * 32), 256, 0, s>>>(a, n, d0, v0.get(), f);
+    PLV_LAUNCH_CHECK();
+    // reduce the perfect top tree, 2^10 values per block per pass
+    double *src = v0.get(), *dst = v1.get();
+    int64_t count = cnt;
+    int levels = d0;
+    while (true) {
+        int kb = levels < 10 ? levels : 10;
+        int64_t blocks = count >> kb;
+        int final = (kb == levels);
+        size_t smem = sizeof(double) * 2 * ((size_t)1 << kb);
+        k_pw_tree2<<<(unsigned)blocks, 256, smem, s>>>(src, count, kb, final ? out_dev : dst, final);
+        PLV_LAUNCH_CHECK();
+        if (final) break;
+        levels -= kb;
+        count = blocks;
+        double *t = src; src = dst; dst = t;
+    }
+}
+
+void pw_sum_async(const double *a, int64_t n, double *out_dev, cudaStream_t s) {
+    pw_launch(a, n, out_dev, s, Ident{});
+}
+
+void pw_sum_sq_async(const double *a, int64_t n, double two_m, double *out_dev, cudaStream_t s) {
+    pw_launch(a, n, out_dev, s, SqScaled{two_m});
+}
+
+// ---------------------------------------------------------------- reduceat
+
+constexpr int64_t SEG_SERIAL_MAX = 4096;
+
+__global__ void k_reduceat_short(const double *__restrict__ w, const int64_t *__restrict__ starts,
+                                 int64_t M, int64_t R, double *out, int64_t *long_list,
+                                 unsigned long long *long_cnt) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < M;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t st = starts[t];
+        int64_t en = (t + 1 < M) ? starts[t + 1] : R;
+        int64_t len = en - st;
+        if (len <= 1) {
+            out[t] = w[st];
+        } else if (len - 1 <= SEG_SERIAL_MAX) {
+            out[t] = __dadd_rn(w[st], pw_serial(w + st + 1, len - 1, Ident{}));
+        } else {
+            unsigned long long p = atomicAdd(long_cnt, 1ull);
+            long_list[p] = t;
+        }
+    }
+}
+
+__global__ void k_seg_finish(const double *w, int64_t st, const double *tail, double *out_t) {
+    out_t[0] = __dadd_rn(w[st], tail[0]);
+}
+
+void reduceat_async(const double *w, const int64_t *starts, int64_t M, int64_t R, double *out,
+                    cudaStream_t s) {
+    if (M <= 0) return;
+    Buf<int64_t> long_list(M, s);
+    Buf<unsigned long long> long_cnt(1, s);
+    PLV_CUDA(cudaMemsetAsync(long_cnt.get(), 0, sizeof(unsigned long long), s));
+    k_reduceat_short<<<grid_for(M, 256), 256, 0, s>>>(w, starts, M, R, out, long_list.get(),
+                                                     long_cnt.get());
+    PLV_LAUNCH_CHECK();
+    unsigned long long nl = d2h(long_cnt.get(), s);
+    if (!nl) return;
+    std::vector<int64_t> lst(nl), st_h(nl), en_h(nl);
+    PLV_CUDA(cudaMemcpyAsync(lst.data(), long_list.get(), sizeof(int64_t) * nl,
+                             cudaMemcpyDeviceToHost, s));
+    PLV_CUDA(cudaStreamSynchronize(s));
+    Buf<double> tail(nl, s);
+    for (unsigned long long q = 0; q < nl; q++) {
+        int64_t t = lst[q];
+        int64_t se[2];
+        PLV_CUDA(cudaMemcpyAsync(se, starts + t, sizeof(int64_t) * ((t + 1 < M) ? 2 : 1),
+                                 cudaMemcpyDeviceToHost, s));
+        PLV_CUDA(cudaStreamSynchronize(s));
+        int64_t st = se[0], en = (t + 1 < M) ? se[1] : R;
+        pw_sum_async(w + st + 1, en - st - 1, tail.get() + q, s);
+        // pw_sum adds a leading 0.0; 0.0 + x == x for every x the weights
+        // produce (x > 0), so the tail value is the pairwise sum itself.
+        k_seg_finish<<<1, 1, 0, s>>>(w, st, tail.get() + q, out + t);
+        PLV_LAUNCH_CHECK();
+    }
+}
+
+}  // namespace plv
+
+// ------------------------------------------------------------- C ABI
+
+extern "C" int plv_sum(const double *a, int64_t n, double *out, void *stream) {
+    PLV_ENTRY
+    if (n < 0) PLV_FAIL(PLV_EINVAL, "plv_sum: negative length");
+    plv::pw_sum_async(a, n, out, plv::S(stream));
+    PLV_EXIT
+}
+
+namespace plv {
+__global__ void k_mod_finish(const double *sw, const double *sq, double two_m, double *out) {
+    out[0] = __dsub_rn(__ddiv_rn(sw[0], two_m), sq[0]);
+}
+}  // namespace plv
+
+extern "C" int plv_modularity(const double *w_int, const double *a_tot, int64_t n, double m,
+                              double *out, void *stream) {
+    PLV_ENTRY
+    cudaStream_t s = plv::S(stream);
+    if (!(m > 0.0)) PLV_FAIL(PLV_EINVAL, "modularity undefined for edgeless graph");
+    double two_m = 2.0 * m;
+    plv::Buf<double> tmp(2, s);
+    plv::pw_sum_async(w_int, n, tmp.get(), s);
+    plv::pw_sum_sq_async(a_tot, n, two_m, tmp.get() + 1, s);
+    plv::k_mod_finish<<<1, 1, 0, s>>>(tmp.get(), tmp.get() + 1, two_m, out);
+    PLV_LAUNCH_CHECK();
+    PLV_EXIT
+}
