@@ -1,0 +1,437 @@
+#!/usr/bin/env python3
+"""Benchmark: parallel-Louvain local-move iteration on B200 (BASELINE.json config 2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (config 2 of BASELINE.json): R-MAT scale 20, edge factor 16,
+(a,b,c,d) = (.57,.19,.19,.05), self loops dropped, duplicates merged,
+f64 weights U[1,10), int32 ids -- generated on device from a counter-based
+RNG (bit-identical to the numpy generator the CPU arms use).  As `run()` does
+with the default RunConfig, the graph is vertex-followed (n 1,048,576 ->
+908,790) and, since n >= color_cutoff, phase 1 is coloured (210 colours).
+
+One step = one phase-1 local-move iteration exactly as the reference's
+run_phase performs it (PL/engine.py:186-197): the state is reset to the
+singleton state, every colour class is swept in ascending colour (decide +
+exact apply per class), then Q is reduced.  Metric: local-move edges/s per
+iteration = M / t_iter with M = num_edges of the iterated graph
+(pkg/benchmarks/bench_backends.py:81 uses num_edges / seconds).  The CSR
+(~380 MB) is larger than L2 (126 MB), so no explicit flush is needed.
+
+`value`: device-resident inputs, CUDA-event timing over K steps, max over
+ranks.  `e2e`: the same step through the C-ABI with host buffers -- the
+step's input state is copied from pinned host memory and the resulting
+assignment + Q are copied back inside the timed region.
+`roofline`: the decide kernels (the dominant kernel family), algorithmic
+bytes 41 n + 16 nnz + 8 sum(cand) per iteration over their summed CUDA-event
+time.  `cpu_baseline`: the unmodified reference (oracle/_ref, compiled
+Cython/OpenMP, all host cores) running the same iteration on the same graph.
+
+Multi-GPU (torchrun): round 1 runs N independent replicas (weak scaling,
+no collective on the data path); see DESIGN.md.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = dict(scale=20, edge_factor=16, seed=0)
+METRIC = "local-move edges/sec per iteration"
+UNIT = "edges/s"
+
+
+def _args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--scale", type=int, default=CONFIG["scale"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-louvain", action="store_true", help="skip the full run() timing")
+    p.add_argument("--mode", choices=["colored", "uncolored"], default="colored")
+    return p.parse_args()
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._loop, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def _peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------- CPU arms
+
+def _reference_module():
+    ref_dir = os.path.join(ROOT, "oracle", "_ref")
+    if os.path.isdir(os.path.join(ref_dir, "ref_parlouvain")):
+        sys.path.insert(0, ref_dir)
+        try:
+            import ref_parlouvain
+            return ref_parlouvain
+        except ImportError:
+            return None
+    return None
+
+
+def cpu_iteration_rate(off, nbr, wts, selfw, classes, steps: int, warmup: int = 0):
+    """Time phase-1 coloured iterations of the reference (or the oracle port)
+    on host cores.  Returns (seconds per iteration list, kind, cores, M)."""
+    ref = _reference_module()
+    n = len(off) - 1
+    if ref is not None:
+        g = ref.Graph(n, off.astype(np.int64), nbr.astype(np.int64), wts.astype(np.float64),
+                      selfw.astype(np.float64))
+        cores = os.cpu_count() or 1
+        kind = "reference"
+
+        def one():
+            s = ref.singleton_state(g)
+            t0 = time.perf_counter()
+            for st in classes:
+                ref.run_iteration(g, s, st, cores)
+            ref.modularity(g, s)
+            return time.perf_counter() - t0
+    else:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as orc
+        og = orc.from_edges(*_csr_to_records(off, nbr, wts, selfw), num_vertices=n)
+        g = og
+        cores = 1
+        kind = "port"
+
+        def one():
+            s = orc.singleton_state(og)
+            t0 = time.perf_counter()
+            for st in classes:
+                orc.run_iteration(og, s, st)
+            orc.modularity(og, s)
+            return time.perf_counter() - t0
+    for _ in range(warmup):
+        one()
+    times = [one() for _ in range(steps)]
+    return times, kind, cores, g.num_edges
+
+
+def _csr_to_records(off, nbr, wts, selfw):
+    n = len(off) - 1
+    src = np.repeat(np.arange(n, dtype=np.int64), np.diff(off))
+    keep = nbr >= src
+    return src[keep], nbr[keep].astype(np.int64), wts[keep]
+
+
+def host_phase1_inputs(scale: int):
+    """numpy generator + CPU oracle (pinned to the reference) -> the VF'd
+    phase-1 graph and its colour classes, without touching the GPU."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+    from paper_1410_1237_b200 import synthetic as syn
+    u, v, w = syn.rmat_records(scale, CONFIG["edge_factor"], seed=CONFIG["seed"])
+    g = orc.from_edges(u, v, w, num_vertices=1 << scale)
+    vf = orc.vf_compact(g)
+    col = orc.color_graph(vf.graph)
+    gg = vf.graph
+    return gg, col.classes(), col.num_colors
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    scale = args.scale
+    gg, classes, ncol = host_phase1_inputs(scale)
+    if args.mode == "uncolored":
+        classes = [np.arange(gg.num_vertices, dtype=np.int64)]
+    times, kind, cores, M = cpu_iteration_rate(gg.adjacency_offsets, gg.neighbors, gg.weights,
+                                               gg.self_loop_weights, classes, args.steps,
+                                               args.warmup)
+    t = float(np.mean(times))
+    val = M / t
+    sample = (f"{len(times)} phase-1 {'coloured (' + str(ncol) + ' stages)' if args.mode == 'colored' else 'uncoloured'} "
+              f"local-move iterations of R-MAT s{scale} after VF, singleton start")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (counter-based R-MAT, numpy generator)",
+        "config": {"workload": f"c2_rmat{scale} phase-1 {args.mode} local-move iteration",
+                   "graph": {"n": gg.num_vertices, "M": M, "nnz": int(len(gg.neighbors))}},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ours
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1410_1237_b200 as pl
+    from paper_1410_1237_b200 import _lib, synthetic as syn
+    from paper_1410_1237_b200.engine import PhaseEngine
+
+    L = _lib.lib()
+    dev = torch.device("cuda", local)
+    scale = args.scale
+    # ---- setup (untimed): generate, build, VF, colour -- all on device
+    u, v, w, n0 = syn.rmat_device(scale, CONFIG["edge_factor"], seed=CONFIG["seed"])
+    g0 = pl.Graph.from_device_records(u, v, w, n0)
+    del u, v, w
+    vf = pl.vf_compact(g0)
+    g = vf.graph
+    n = g.num_vertices
+    col = pl.color_graph(g) if args.mode == "colored" else None
+    ncol = col.num_colors if col is not None else 0
+    s0 = pl.singleton_state(g)
+    d0 = s0.device()
+    st = {k: (t.clone() if t is not None else None) for k, t in d0.items()}
+    state = pl.CommunityState.from_device(st["assignment"], st["a_tot"], st["w_internal"],
+                                          st["sizes"])
+    coloring = col if args.mode == "colored" else None
+    eng = PhaseEngine(g, state, coloring)
+    stream = torch.cuda.current_stream()
+
+    def reset():
+        st["assignment"].copy_(d0["assignment"])
+        st["a_tot"].copy_(d0["a_tot"])
+        st["w_internal"].copy_(d0["w_internal"])
+        st["sizes"].copy_(d0["sizes"])
+
+    def step(e=eng):
+        reset()
+        return e.iterate()
+
+    for _ in range(args.warmup):
+        step()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = L.launch_count()
+    with ClockSampler(local) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            q, moves_it, _ = step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    # kernels launched by graph replays are not re-counted by the host-side
+    # counter: count one iteration's launches at capture time instead
+    graph_kernels = L.launch_count() - launches0
+    if ws > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    if ws > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    t_iter = ms / 1e3 / args.steps
+    M = g.num_edges
+    nnz = g.nnz
+    value = ws * M / t_iter
+    # decide-kernel timing: same iteration through an engine with event
+    # records around every stage's decide launches
+    c0 = L.launch_count()
+    teng = PhaseEngine(g, state, coloring, timing=True)
+    per_iter_launches = L.launch_count() - c0
+    dms, cands = [], []
+    for _ in range(max(3, args.steps // 2)):
+        reset()
+        _, _, cand = teng.iterate()
+        dms.append(teng.decide_ms())
+        cands.append(cand)
+    teng.close()
+    decide_ms = float(np.median(dms))
+    cand_per_iter = float(np.mean(cands))
+    moves_per_iter = float(moves_it)
+    launches = per_iter_launches * args.steps
+    decide_bytes = 41 * n + 16 * nnz + 8 * cand_per_iter
+    iter_bytes = decide_bytes + 84 * moves_per_iter + 16 * n
+    peak, peak_kind = _peak_hbm()
+    achieved = decide_bytes / (decide_ms / 1e3) / 1e9
+    qbuf = torch.tensor([q], dtype=torch.float64, device=dev)
+
+    # ---- e2e through the C ABI with host buffers (pinned), same step
+    h_assign = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    h_atot = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    h_wint = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    h_sizes = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    h_assign.copy_(d0["assignment"].cpu())
+    h_atot.copy_(d0["a_tot"].cpu())
+    h_wint.copy_(d0["w_internal"].cpu())
+    h_sizes.copy_(d0["sizes"].cpu())
+    o_assign = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    o_q = torch.empty(1, dtype=torch.float64, pin_memory=True)
+
+    def e2e_step():
+        st["assignment"].copy_(h_assign, non_blocking=True)
+        st["a_tot"].copy_(h_atot, non_blocking=True)
+        st["w_internal"].copy_(h_wint, non_blocking=True)
+        st["sizes"].copy_(h_sizes, non_blocking=True)
+        qq, _, _ = eng.iterate()          # Q comes back to the host inside
+        o_assign.copy_(st["assignment"], non_blocking=True)
+        stream.synchronize()
+        o_q[0] = qq
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_val = ws * M / (e2e_ms / 1e3 / args.steps)
+
+    # ---- full Louvain run() once (end-to-end Louvain time, final modularity)
+    louv = None
+    if not args.no_louvain:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        uu, vv, ww, nn = syn.rmat_device(scale, CONFIG["edge_factor"], seed=CONFIG["seed"])
+        gg = pl.Graph.from_device_records(uu, vv, ww, nn)
+        h = pl.run(gg, pl.RunConfig())
+        torch.cuda.synchronize()
+        louv = {"seconds": time.perf_counter() - t0, "final_modularity": h.final_modularity,
+                "phases": len(h.phases), "communities": h.num_communities,
+                "iterations": [p.stats.iterations for p in h.phases]}
+
+    # ---- CPU baseline (rank 0, N == 1)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        off = g.adjacency_offsets
+        nb = g.neighbors
+        wt = g.weights
+        sw = g.self_loop_weights
+        if args.mode == "colored":
+            cl = col.classes()
+        else:
+            cl = [np.arange(n, dtype=np.int64)]
+        times, kind, cores, Mc = cpu_iteration_rate(off, nb, wt, sw, cl, steps=2)
+        tc = float(np.mean(times))
+        cpu = {"value": Mc / tc, "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": f"2 phase-1 {args.mode} iterations of the same graph "
+                         f"({len(cl)} stages), singleton start; {tc * 1e3:.0f} ms each"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (counter-based R-MAT, generated on device)",
+            "config": {"workload": f"c2_rmat{scale} phase-1 {args.mode} local-move iteration",
+                       "graph": {"n": n, "M": M, "nnz": nnz, "colours": ncol,
+                                 "integral": g.integral},
+                       "parallelism": "replicas" if ws > 1 else "single",
+                       "l2": "inputs larger than L2 (CSR %.0f MB)" % (nnz * 12 / 1e6)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "decide (tiers 0-3)",
+                         "bytes_per_iter": decide_bytes, "ms_per_iter": decide_ms},
+            "iteration": {"bytes": iter_bytes, "gbs": iter_bytes / t_iter / 1e9,
+                          "frac": iter_bytes / t_iter / 1e9 / peak,
+                          "moves": moves_per_iter, "cand": cand_per_iter, "q": q,
+                          "kernels_per_iter": per_iter_launches},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 24 * n,
+                    "d2h_bytes_per_step": 4 * n + 8},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "louvain": louv,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

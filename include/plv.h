@@ -44,6 +44,9 @@ int plv_abi_version(void);
 const char *plv_last_error(void);
 /* 1 when a compute-capability-10.x device is visible, else 0. */
 int plv_device_ok(void);
+/* Kernels this library has launched so far in this process (CUB's internal
+ * sort/scan kernels not included). */
+unsigned long long plv_launch_count(void);
 
 /* ---------------------------------------------------------------- sums */
 
@@ -131,6 +134,14 @@ int plv_decide(const int64_t *off, const int32_t *nbr, const double *wts, const 
                uint8_t *out_moved, double *out_e_old, double *out_e_best, int64_t *cand_h,
                void *stream);
 
+/* plv_decide with flags (PLV_F_INTEGRAL selects order-free accumulation, exact
+ * for integral graphs). */
+int plv_decide_ex(const int64_t *off, const int32_t *nbr, const double *wts, const double *k,
+                  const int32_t *labels, const int32_t *subset, int64_t ns,
+                  const int32_t *assign, const double *a_tot, const int32_t *sizes, double m,
+                  int flags, int32_t *out_target, uint8_t *out_moved, double *out_e_old,
+                  double *out_e_best, int64_t *cand_h, void *stream);
+
 /*
  * apply_moves (PL/_kernels.pyx:104-145): applies the decided moves as if
  * sequentially in subset order against the live assignment, bit-exactly
@@ -143,6 +154,35 @@ int plv_apply(const int64_t *off, const int32_t *nbr, const double *wts, const d
               const int32_t *target, const uint8_t *moved, const double *e_old,
               const double *e_best, int flags, int32_t *assign, double *a_tot, double *w_int,
               int32_t *sizes, int64_t *moves_h, void *stream);
+
+/* ----------------------------------------------------------- phase engine */
+
+/*
+ * run_phase (PL/engine.py:166-216) on a fixed stage list: the colour classes
+ * in ascending colour (PLV_F_INDEPENDENT) or all of V (PLV_F_IDENTITY), plus
+ * PLV_F_INTEGRAL for integral graphs.  stage_off_h (host, nstages+1) indexes
+ * stage_vtx (device, concatenated stage vertices, ascending within a stage).
+ * The state buffers (assign/a_tot/w_int/sizes) are updated in place by every
+ * iteration.  Creation plans the decide tiers per stage and captures one
+ * iteration (all stages' decide + exact apply, move counter, modularity) into
+ * a CUDA graph; `timing` adds event records around every stage's decide.
+ */
+int plv_phase_create(const int64_t *off, const int32_t *nbr, const double *wts, const double *k,
+                     const double *selfw, int64_t n, double m, int flags, const int32_t *labels,
+                     const int64_t *stage_off_h, const int32_t *stage_vtx, int64_t nstages,
+                     int32_t *assign, double *a_tot, double *w_int, int32_t *sizes, int timing,
+                     void **handle_h, void *stream);
+/* One iteration (PL/engine.py:187-197): q_h = Q after it, moves_h = moves,
+ * cand_h (nullable) = sum of distinct candidate communities over all deciders. */
+int plv_phase_iterate(void *handle, double *q_h, int64_t *moves_h, int64_t *cand_h, void *stream);
+/* The phase loop with the reference's stopping rule (PL/engine.py:203-212):
+ * per-iteration Q / moves / host milliseconds into the *_trace_h arrays
+ * (capacity max_iters); result_h = {iterations, total_moves, hit_cap}. */
+int plv_phase_run(void *handle, double theta, int64_t max_iters, double *q_trace_h,
+                  int64_t *moves_trace_h, double *ms_trace_h, int64_t *result_h, void *stream);
+/* Sum over stages of the decide time of the last iteration (timing handles). */
+int plv_phase_decide_ms(void *handle, double *ms_h);
+int plv_phase_destroy(void *handle);
 
 /* ---------------------------------------------------------------- rebuild */
 

@@ -39,6 +39,7 @@ _SIGS = {
     "plv_abi_version": [],
     "plv_last_error": [],
     "plv_device_ok": [],
+    "plv_launch_count": [],
     "plv_sum": [_P, _I64, _P, _P],
     "plv_modularity": [_P, _P, _I64, _D, _P, _P],
     "plv_csr_build": [_P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P],
@@ -54,6 +55,12 @@ _SIGS = {
                       _P],
     "plv_apply": [_P, _P, _P, _P, _P, _I64, _P, _I64, _P, _P, _P, _P, _INT, _P, _P, _P, _P, _P,
                   _P],
+    "plv_phase_create": [_P, _P, _P, _P, _P, _I64, _D, _INT, _P, _P, _P, _I64, _P, _P, _P, _P,
+                         _INT, _P, _P],
+    "plv_phase_iterate": [_P, _P, _P, _P, _P],
+    "plv_phase_run": [_P, _D, _I64, _P, _P, _P, _P, _P],
+    "plv_phase_decide_ms": [_P, _P],
+    "plv_phase_destroy": [_P],
     "plv_rebuild_records": [_P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P],
     "plv_compose": [_P, _P, _P, _I64, _P, _P],
     "plv_gen_rmat": [_U64, _INT, _I64, _D, _D, _D, _D, _D, _P, _P, _P, _I64, _P, _P],
@@ -61,7 +68,7 @@ _SIGS = {
     "plv_gen_grid": [_U64, _I64, _D, _I64, _D, _P, _P, _P, _I64, _P, _P],
     "plv_gen_chung_lu": [_U64, _P, _I64, _I64, _P, _P, _P, _I64, _P, _P],
 }
-_RESTYPE = {"plv_last_error": ctypes.c_char_p}
+_RESTYPE = {"plv_last_error": ctypes.c_char_p, "plv_launch_count": ctypes.c_ulonglong}
 
 _LIB = None
 

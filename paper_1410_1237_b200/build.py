@@ -24,7 +24,8 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-std=c++17", "--fmad=false", "-lineinfo", "-Xcompiler", "-fPIC",
+FLAGS = ["-O3", "-std=c++17", "--fmad=false", "-lineinfo", "--extended-lambda",
+         "-Xcompiler", "-fPIC",
          "-Xcompiler", "-Wno-deprecated-declarations", f"-I{INCLUDE}"]
 
 

@@ -1,10 +1,14 @@
 // api_util.cu -- error reporting and device checks for the libplv C ABI.
 #include "common.cuh"
 #include <cstring>
+#include <atomic>
 
 namespace plv {
 
 static thread_local char g_err[1024] = "";
+static std::atomic<unsigned long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char *fmt, ...) {
     va_list ap;
@@ -37,6 +41,8 @@ void check_device() {
 }  // namespace plv
 
 extern "C" int plv_abi_version(void) { return 1; }
+
+extern "C" unsigned long long plv_launch_count(void) { return plv::g_launches.load(); }
 
 extern "C" const char *plv_last_error(void) { return plv::g_err; }
 

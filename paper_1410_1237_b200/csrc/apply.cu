@@ -1,0 +1,467 @@
+// apply.cu -- apply_moves (PL/_kernels.pyx:104-145) on device, bit-exactly.
+//
+// The reference applies the decided moves one by one in subset order against
+// the live assignment.  Restated in parallel:
+//  1. e_a / e_b of every mover: sequential folds in adjacency order over the
+//     neighbours whose *live* community is a / b -- the target of an
+//     earlier-moved subset vertex, else the snapshot.  In a colour class no
+//     neighbour is in the subset, so decide's e_old / e_best are those folds
+//     already (PLV_F_INDEPENDENT).
+//  2. events (community, subset position, delta) for a_tot and w_internal,
+//     stable radix sort by community, and one thread per community folds its
+//     events in subset order starting from the current value -- the same
+//     additions in the same order as the sequential loop.  Integral graphs
+//     (PLV_F_INTEGRAL) add with atomics: every partial sum is an exact integer.
+//  3. sizes with integer atomics; the assignment is scattered last.
+// Stages of colour classes with <= 2048 vertices run steps 1-3 in one CTA.
+#include "localmove.cuh"
+#include "csr.cuh"
+#include <cub/cub.cuh>
+
+namespace plv {
+
+__global__ void k_fill_i32_a(int32_t *p, int64_t n, int32_t v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+// Live community of neighbour j for the mover at subset index x.
+__device__ __forceinline__ int32_t live_comm(const StageArgs &A, int32_t j, int64_t x) {
+    int64_t p = (A.flags & PLV_F_IDENTITY) ? (int64_t)j : (int64_t)A.pos[j];
+    if (p >= 0 && p < x && A.moved[p]) return A.target[p];
+    return A.assign[j];
+}
+
+// Per subset index x: events + deltas (+ sizes, moves, and the assignment
+// scatter for independent stages).  Lanes take low-degree movers; whole warps
+// take high-degree ones when the live e_a / e_b must be recomputed.
+__global__ void __launch_bounds__(256) k_stage_prep(StageArgs A) {
+    const bool indep = A.flags & PLV_F_INDEPENDENT;
+    const bool integral = A.flags & PLV_F_INTEGRAL;
+    int lane = threadIdx.x & 31;
+    int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long my_moves = 0;
+    for (int64_t base = gw * 32; base < A.ns; base += nw * 32) {
+        int64_t x = base + lane;
+        bool mover = false, big = false;
+        int32_t i = 0, a = 0, b = 0;
+        if (x < A.ns) {
+            i = A.subset[x];
+            b = A.target[x];
+            a = A.assign[i];
+            mover = A.moved[x] && a != b;
+            if (!integral) {
+                A.ekey[2 * x] = mover ? (uint32_t)a : SENTINEL;
+                A.ekey[2 * x + 1] = mover ? (uint32_t)b : SENTINEL;
+                A.eval[2 * x] = (int32_t)(2 * x);
+                A.eval[2 * x + 1] = (int32_t)(2 * x + 1);
+            }
+        }
+        double e_a = 0.0, e_b = 0.0;
+        if (mover) {
+            my_moves++;
+            if (indep) {
+                e_a = A.e_old[x];
+                e_b = A.e_best[x];
+            } else {
+                int64_t e0 = A.off[i], e1 = A.off[i + 1];
+                big = (e1 - e0) > 32;
+                if (!big) {
+                    for (int64_t e = e0; e < e1; e++) {
+                        int32_t j = A.nbr[e];
+                        if (j == i) continue;
+                        int32_t c = live_comm(A, j, x);
+                        if (c == a)
+                            e_a = dadd(e_a, A.wts[e]);
+                        else if (c == b)
+                            e_b = dadd(e_b, A.wts[e]);
+                    }
+                }
+            }
+        }
+        // warp-cooperative ordered folds for high-degree movers
+        unsigned bigm = __ballot_sync(FULL, big);
+        while (bigm) {
+            int l = __ffs(bigm) - 1;
+            bigm &= bigm - 1;
+            int32_t ii = __shfl_sync(FULL, i, l);
+            int32_t aa = __shfl_sync(FULL, a, l);
+            int32_t bb = __shfl_sync(FULL, b, l);
+            int64_t xx = base + l;
+            int64_t e0 = A.off[ii], e1 = A.off[ii + 1];
+            double fa = 0.0, fb = 0.0;
+            for (int64_t c0 = e0; c0 < e1; c0 += 32) {
+                int64_t e = c0 + lane;
+                int32_t c = -1;
+                double w = 0.0;
+                if (e < e1) {
+                    int32_t j = A.nbr[e];
+                    if (j != ii) {
+                        c = live_comm(A, j, xx);
+                        w = A.wts[e];
+                    }
+                }
+                unsigned ma = __ballot_sync(FULL, c == aa);
+                unsigned mb = __ballot_sync(FULL, c == bb && c != aa);
+                for (unsigned mm = ma; mm; mm &= mm - 1)
+                    fa = dadd(fa, __shfl_sync(FULL, w, __ffs(mm) - 1));
+                for (unsigned mm = mb; mm; mm &= mm - 1)
+                    fb = dadd(fb, __shfl_sync(FULL, w, __ffs(mm) - 1));
+            }
+            if (lane == l) {
+                e_a = fa;
+                e_b = fb;
+            }
+        }
+        if (mover) {
+            double sw = A.selfw[i], ki = A.k[i];
+            double ta = dadd(dmul(2.0, e_a), dmul(2.0, sw));
+            double tb = dadd(dmul(2.0, e_b), dmul(2.0, sw));
+            if (integral) {
+                atomicAdd(A.w_int + a, -ta);
+                atomicAdd(A.w_int + b, tb);
+                atomicAdd(A.a_tot + a, -ki);
+                atomicAdd(A.a_tot + b, ki);
+            } else {
+                A.ta[x] = ta;
+                A.tb[x] = tb;
+            }
+            atomicSub(A.sizes + a, 1);
+            atomicAdd(A.sizes + b, 1);
+        }
+        // independent stages: no stage vertex reads another's assignment, so
+        // the scatter can happen here
+        if (indep && mover) A.assign[i] = b;
+    }
+    for (int o = 16; o > 0; o >>= 1) my_moves += __shfl_xor_sync(FULL, my_moves, o);
+    if (lane == 0 && my_moves) atomicAdd(A.moves, my_moves);
+}
+
+// Event deltas in sorted order: leaving a (-(2 e_a + 2 sw), -k_i), joining b
+// (+(2 e_b + 2 sw), +k_i).  x - y and x + (-y) round identically, so folding
+// the signed deltas reproduces `w_int[a] -= ...; a_tot[a] -= ki` exactly.
+__device__ __forceinline__ void event_delta(const StageArgs &A, int32_t v, double &dw,
+                                            double &da) {
+    int64_t x = v >> 1;
+    double ki = A.k[A.subset[x]];
+    if (v & 1) {
+        dw = A.tb[x];
+        da = ki;
+    } else {
+        dw = -A.ta[x];
+        da = -ki;
+    }
+}
+
+__global__ void k_stage_deltas(StageArgs A, const uint32_t *key, const int32_t *val, int64_t ne,
+                               double *dW, double *dA) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ne;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        if (key[p] == SENTINEL) continue;
+        double dw, da;
+        event_delta(A, val[p], dw, da);
+        dW[p] = dw;
+        dA[p] = da;
+    }
+}
+
+// Sequential fold of the run of community c starting at p from contiguous
+// deltas (loads batched so only the additions are serial).
+__device__ __forceinline__ void fold_deltas(const uint32_t *key, const double *dW,
+                                            const double *dA, int64_t p, int64_t ne, double &W,
+                                            double &At) {
+    const uint32_t c = key[p];
+    while (true) {
+        double w[8], a[8];
+        bool ok[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            int64_t q = p + u;
+            ok[u] = q < ne && key[q] == c;
+            w[u] = ok[u] ? dW[q] : 0.0;
+            a[u] = ok[u] ? dA[q] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            if (!ok[u]) return;
+            W = dadd(W, w[u]);
+            At = dadd(At, a[u]);
+        }
+        p += 8;
+    }
+}
+
+constexpr int SHORT_EVENTS = 32;  // longer community runs are folded by a whole block
+
+__global__ void k_stage_fold(StageArgs A, const uint32_t *key, int64_t ne, const double *dW,
+                             const double *dA, int64_t *lrun, unsigned long long *lcnt) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ne;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t c = key[p];
+        if (c == SENTINEL) continue;
+        if (p > 0 && key[p - 1] == c) continue;
+        if (p + SHORT_EVENTS < ne && key[p + SHORT_EVENTS] == c) {
+            lrun[atomicAdd(lcnt, 1ull)] = p;
+            continue;
+        }
+        double W = A.w_int[c], At = A.a_tot[c];
+        fold_deltas(key, dW, dA, p, ne, W, At);
+        A.w_int[c] = W;
+        A.a_tot[c] = At;
+    }
+}
+
+// Long community runs: one block each, block-staged ordered folds.
+__global__ void __launch_bounds__(256) k_stage_fold_long(StageArgs A, const uint32_t *key,
+                                                        int64_t ne, const double *dW,
+                                                        const double *dA, const int64_t *lrun,
+                                                        const unsigned long long *lcnt) {
+    __shared__ double sb[4 * FOLD_CH];
+    __shared__ int64_t s_end;
+    const int64_t cnt = (int64_t)*lcnt;
+    for (int64_t w = blockIdx.x; w < cnt; w += gridDim.x) {
+        const int64_t p = lrun[w];
+        const uint32_t c = key[p];
+        if (threadIdx.x == 0) {
+            int64_t a = p, b = ne;  // first position past the run
+            while (a < b) {
+                int64_t mid = (a + b) >> 1;
+                if (key[mid] <= c)
+                    a = mid + 1;
+                else
+                    b = mid;
+            }
+            s_end = a;
+        }
+        __syncthreads();
+        double W = A.w_int[c], At = A.a_tot[c];
+        block_fold2(
+            [=] __device__(int64_t t, double &x, double &y) {
+                x = dW[p + t];
+                y = dA[p + t];
+            },
+            s_end - p, W, At, sb);
+        if (threadIdx.x == 0) {
+            A.w_int[c] = W;
+            A.a_tot[c] = At;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_stage_scatter(StageArgs A) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < A.ns;
+         x += (int64_t)gridDim.x * blockDim.x)
+        if (A.moved[x]) A.assign[A.subset[x]] = A.target[x];
+}
+
+// One CTA applies a small independent stage: event keys in registers, block
+// radix sort, deltas staged in shared memory, ordered per-community folds and
+// the scatter, in one launch.  Dynamic smem: 2 * SA_THREADS * SA_ITEMS doubles.
+__global__ void __launch_bounds__(SA_THREADS) k_stage_apply_small(StageArgs A, int nb) {
+    typedef cub::BlockRadixSort<uint32_t, SA_THREADS, SA_ITEMS, int32_t> Sort;
+    __shared__ union {
+        typename Sort::TempStorage sort;
+        struct {
+            uint32_t key[SA_THREADS * SA_ITEMS];
+            int32_t val[SA_THREADS * SA_ITEMS];
+        } s;
+    } sm;
+    extern __shared__ double sdel[];  // dW then dA
+    __shared__ unsigned long long s_moves;
+    const int tid = threadIdx.x;
+    const int64_t ne = 2 * A.ns;
+    if (tid == 0) s_moves = 0;
+    __syncthreads();
+    uint32_t keys[SA_ITEMS];
+    int32_t vals[SA_ITEMS];
+    unsigned long long mv = 0;
+#pragma unroll
+    for (int it = 0; it < SA_ITEMS; it++) {
+        int64_t e = (int64_t)tid * SA_ITEMS + it;
+        keys[it] = SENTINEL;
+        vals[it] = (int32_t)e;
+        if (e < ne) {
+            int64_t x = e >> 1;
+            int32_t i = A.subset[x];
+            int32_t b = A.target[x];
+            int32_t a = A.assign[i];
+            if (A.moved[x] && a != b) {
+                keys[it] = (e & 1) ? (uint32_t)b : (uint32_t)a;
+                if (!(e & 1)) {
+                    double sw = A.selfw[i];
+                    A.ta[x] = dadd(dmul(2.0, A.e_old[x]), dmul(2.0, sw));
+                    A.tb[x] = dadd(dmul(2.0, A.e_best[x]), dmul(2.0, sw));
+                    atomicSub(A.sizes + a, 1);
+                    atomicAdd(A.sizes + b, 1);
+                    mv++;
+                }
+            }
+        }
+    }
+    Sort(sm.sort).Sort(keys, vals, 0, nb);
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < SA_ITEMS; it++) {
+        sm.s.key[tid * SA_ITEMS + it] = keys[it];
+        sm.s.val[tid * SA_ITEMS + it] = vals[it];
+    }
+    if (mv) atomicAdd(&s_moves, mv);
+    __syncthreads();
+    double *dW = sdel, *dA = sdel + SA_THREADS * SA_ITEMS;
+    for (int64_t p = tid; p < ne; p += SA_THREADS)
+        if (sm.s.key[p] != SENTINEL) event_delta(A, sm.s.val[p], dW[p], dA[p]);
+    __syncthreads();
+    for (int64_t p = tid; p < ne; p += SA_THREADS) {
+        uint32_t c = sm.s.key[p];
+        if (c == SENTINEL) continue;
+        if (p > 0 && sm.s.key[p - 1] == c) continue;
+        double W = A.w_int[c], At = A.a_tot[c];
+        for (int64_t q = p; q < ne && sm.s.key[q] == c; q++) {
+            W = dadd(W, dW[q]);
+            At = dadd(At, dA[q]);
+        }
+        A.w_int[c] = W;
+        A.a_tot[c] = At;
+    }
+    __syncthreads();
+    for (int64_t x = tid; x < A.ns; x += SA_THREADS)
+        if (A.moved[x]) A.assign[A.subset[x]] = A.target[x];
+    if (tid == 0 && s_moves) atomicAdd(A.moves, s_moves);
+}
+
+__global__ void k_pos_scatter(const int32_t *subset, int64_t ns, int32_t *pos, int *dup) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < ns;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        int32_t old = atomicExch(pos + subset[x], (int32_t)x);
+        if (old != -1) atomicOr(dup, 1);
+    }
+}
+
+void ApplyBuffers::alloc(int64_t ta_len, int64_t max_ns, int64_t n, cudaStream_t s) {
+    ta = dalloc<double>(ta_len);
+    tb = dalloc<double>(ta_len);
+    int64_t ne = 2 * (max_ns ? max_ns : 1);
+    ekey = dalloc<uint32_t>(ne);
+    ekey2 = dalloc<uint32_t>(ne);
+    eval = dalloc<int32_t>(ne);
+    eval2 = dalloc<int32_t>(ne);
+    dW = dalloc<double>(ne);
+    dA = dalloc<double>(ne);
+    lrun = dalloc<int64_t>(ne);
+    lcnt = dalloc<unsigned long long>(1);
+    nb = bits_for(n + 1);  // SENTINEL's low nb bits exceed every community id
+    PLV_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, ekey, ekey2, eval, eval2, ne, 0, nb, s));
+    PLV_CUDA(cudaMalloc(&tmp, bytes ? bytes : 1));
+    static int dev_done = -1;
+    int dev;
+    PLV_CUDA(cudaGetDevice(&dev));
+    if (dev_done != dev) {
+        PLV_CUDA(cudaFuncSetAttribute(k_stage_apply_small,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(2 * SA_THREADS * SA_ITEMS * sizeof(double))));
+        dev_done = dev;
+    }
+}
+
+void ApplyBuffers::release() {
+    void *ps[] = {ta, tb, ekey, ekey2, eval, eval2, tmp, dW, dA, lrun, lcnt};
+    for (void *p : ps)
+        if (p) cudaFree(p);
+    dW = dA = nullptr;
+    lrun = nullptr;
+    lcnt = nullptr;
+    ta = tb = nullptr;
+    ekey = ekey2 = nullptr;
+    eval = eval2 = nullptr;
+    tmp = nullptr;
+}
+
+void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {
+    if (S.ns == 0) return;
+    S.ekey = B.ekey;
+    S.eval = B.eval;
+    bool indep = S.flags & PLV_F_INDEPENDENT;
+    bool integral = S.flags & PLV_F_INTEGRAL;
+    if (indep && !integral && S.ns <= SMALL_APPLY_MAX) {
+        k_stage_apply_small<<<1, SA_THREADS, 2 * SA_THREADS * SA_ITEMS * sizeof(double), st>>>(
+            S, B.nb);
+        PLV_LAUNCH_CHECK();
+        return;
+    }
+    k_stage_prep<<<grid_for((S.ns + 31) / 32 * 32, 256, 148 * 16), 256, 0, st>>>(S);
+    PLV_LAUNCH_CHECK();
+    if (!integral) {
+        int64_t ne = 2 * S.ns;
+        size_t bytes = B.bytes;
+        PLV_CUDA(cub::DeviceRadixSort::SortPairs(B.tmp, bytes, B.ekey, B.ekey2, B.eval, B.eval2, ne,
+                                                 0, B.nb, st));
+        k_stage_deltas<<<grid_for(ne, 256), 256, 0, st>>>(S, B.ekey2, B.eval2, ne, B.dW, B.dA);
+        PLV_LAUNCH_CHECK();
+        PLV_CUDA(cudaMemsetAsync(B.lcnt, 0, sizeof(unsigned long long), st));
+        k_stage_fold<<<grid_for(ne, 256), 256, 0, st>>>(S, B.ekey2, ne, B.dW, B.dA, B.lrun, B.lcnt);
+        PLV_LAUNCH_CHECK();
+        k_stage_fold_long<<<148 * 2, 256, 0, st>>>(S, B.ekey2, ne, B.dW, B.dA, B.lrun, B.lcnt);
+        PLV_LAUNCH_CHECK();
+    }
+    if (!indep) {
+        k_stage_scatter<<<grid_for(S.ns, 256), 256, 0, st>>>(S);
+        PLV_LAUNCH_CHECK();
+    }
+}
+
+// One-off apply over `subset` (synchronises; returns the move count).
+static int64_t apply_once(const int64_t *off, const int32_t *nbr, const double *wts,
+                          const double *k, const double *selfw, int64_t n, const int32_t *subset,
+                          int64_t ns, const int32_t *target, const uint8_t *moved,
+                          const double *e_old, const double *e_best, int flags, int32_t *assign,
+                          double *a_tot, double *w_int, int32_t *sizes, cudaStream_t s) {
+    if (ns <= 0) return 0;
+    Buf<int32_t> pos;
+    bool general = !(flags & (PLV_F_IDENTITY | PLV_F_INDEPENDENT));
+    if (general) {
+        pos.alloc(n, s);
+        k_fill_i32_a<<<grid_for(n, 256), 256, 0, s>>>(pos, n, -1);
+        PLV_LAUNCH_CHECK();
+        Buf<int> dup(1, s);
+        PLV_CUDA(cudaMemsetAsync(dup.get(), 0, sizeof(int), s));
+        k_pos_scatter<<<grid_for(ns, 256), 256, 0, s>>>(subset, ns, pos, dup);
+        PLV_LAUNCH_CHECK();
+        if (d2h(dup.get(), s)) PLV_FAIL(PLV_EDUP, "subset lists a vertex more than once");
+    }
+    ApplyBuffers B;
+    Buf<unsigned long long> moves(1, s);
+    PLV_CUDA(cudaMemsetAsync(moves.get(), 0, sizeof(unsigned long long), s));
+    int64_t result = 0;
+    try {
+        B.alloc(ns, ns, n, s);
+        StageArgs S{off, nbr, wts, k, selfw, subset, ns, target, moved, e_old, e_best, pos.get(),
+                    flags, assign, a_tot, w_int, sizes, B.ta, B.tb, nullptr, nullptr, moves.get()};
+        launch_apply(S, B, s);
+        result = (int64_t)d2h(moves.get(), s);
+    } catch (...) {
+        cudaStreamSynchronize(s);
+        B.release();
+        throw;
+    }
+    PLV_CUDA(cudaStreamSynchronize(s));
+    B.release();
+    return result;
+}
+
+}  // namespace plv
+
+extern "C" int plv_apply(const int64_t *off, const int32_t *nbr, const double *wts,
+                         const double *k, const double *selfw, int64_t n, const int32_t *subset,
+                         int64_t ns, const int32_t *target, const uint8_t *moved,
+                         const double *e_old, const double *e_best, int flags, int32_t *assign,
+                         double *a_tot, double *w_int, int32_t *sizes, int64_t *moves_h,
+                         void *stream) {
+    PLV_ENTRY
+    int64_t mv = plv::apply_once(off, nbr, wts, k, selfw, n, subset, ns, target, moved, e_old,
+                                 e_best, flags, assign, a_tot, w_int, sizes, plv::S(stream));
+    if (moves_h) *moves_h = mv;
+    PLV_EXIT
+}

@@ -8,18 +8,22 @@
 // uncoloured and form the next active set in ascending order (stable
 // compaction, PL/heuristics.py:113-115).
 //
-// First-fit uses a 64-bit "used" mask per window of 64 colours: thread per
-// vertex for low degree, warp per vertex (OR-reduced masks) above 32.
+// Low-degree vertices (<= 32 entries) are one thread each with a 64-bit
+// "used" mask per window of 64 colours.  Higher-degree vertices are pushed to
+// a worklist and handled one block each: the block marks the colours of the
+// row in a shared-memory bitmap (windows of 4096 colours) and finds the first
+// free bit, or scans the lower-id prefix of the row for a clash.  No host
+// synchronisation inside a round except the rejected count.
 #include "common.cuh"
 #include "csr.cuh"
 #include <cub/cub.cuh>
-#include <thrust/iterator/counting_iterator.h>
-#include <thrust/iterator/transform_iterator.h>
 
 namespace plv {
 
-constexpr unsigned FULLC = 0xffffffffu;
 constexpr int COLOR_THREAD_MAXD = 32;
+constexpr int CB = 256;             // threads per block, big-vertex kernels
+constexpr int CWIN = 4096;          // colours per bitmap window
+constexpr int CBIG_GRID = 148 * 4;  // blocks of the big-vertex kernels
 
 __device__ __forceinline__ int first_free_thread(const int64_t *off, const int32_t *nbr,
                                                  const int32_t *colors, int32_t i) {
@@ -36,95 +40,223 @@ __device__ __forceinline__ int first_free_thread(const int64_t *off, const int32
     }
 }
 
-__device__ __forceinline__ int first_free_warp(const int64_t *off, const int32_t *nbr,
-                                               const int32_t *colors, int32_t i, int lane) {
-    int64_t e0 = off[i], e1 = off[i + 1];
-    for (int base = 0;; base += 64) {
-        uint64_t used = 0;
-        for (int64_t e = e0 + lane; e < e1; e += 32) {
+// Tentative colours of low-degree active vertices; the others go to `big`
+// (one block each) or, above CHUGE entries, to `huge` (split over blocks).
+constexpr int64_t CHUGE = 4096;
+
+__global__ void k_color_assign_small(const int64_t *off, const int32_t *nbr,
+                                     const int32_t *active, int64_t na, const int32_t *colors,
+                                     int32_t *out, int32_t *big, unsigned long long *nbig,
+                                     int32_t *huge, unsigned long long *nhuge) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < na;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        int32_t i = active[x];
+        int64_t d = off[i + 1] - off[i];
+        if (d <= COLOR_THREAD_MAXD)
+            out[x] = first_free_thread(off, nbr, colors, i);
+        else if (d <= CHUGE || !huge)
+            big[atomicAdd(nbig, 1ull)] = (int32_t)x;
+        else
+            huge[atomicAdd(nhuge, 1ull)] = (int32_t)x;
+    }
+}
+
+// Huge rows: block (q, chunk) ORs the colours of CHUGE entries into the
+// global bitmap of huge item q (first window of CWIN colours).
+__global__ void __launch_bounds__(CB) k_color_assign_huge(const int64_t *off, const int32_t *nbr,
+                                                          const int32_t *active,
+                                                          const int32_t *colors,
+                                                          const int32_t *huge,
+                                                          const unsigned long long *nhuge,
+                                                          uint32_t *hbits) {
+    const int64_t cnt = (int64_t)*nhuge;
+    for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
+        int32_t i = active[huge[q]];
+        int64_t e0 = off[i] + (int64_t)blockIdx.y * CHUGE, e1 = off[i + 1];
+        int64_t ee = e0 + CHUGE < e1 ? e0 + CHUGE : e1;
+        uint32_t *bits = hbits + q * (CWIN / 32);
+        for (int64_t e = e0 + threadIdx.x; e < ee; e += CB) {
             int32_t j = nbr[e];
             if (j == i) continue;
-            int32_t cj = colors[j] - base;
-            if (cj >= 0 && cj < 64) used |= 1ull << cj;
-        }
-        unsigned lo = __reduce_or_sync(FULLC, (unsigned)used);
-        unsigned hi = __reduce_or_sync(FULLC, (unsigned)(used >> 32));
-        uint64_t all = ((uint64_t)hi << 32) | lo;
-        if (~all) return base + __ffsll((long long)~all) - 1;
-    }
-}
-
-// tentative colours for active[0..na) -> out[x]
-__global__ void k_color_assign(const int64_t *off, const int32_t *nbr, const int32_t *active,
-                               int64_t na, const int32_t *colors, int32_t *out) {
-    int lane = threadIdx.x & 31;
-    int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    // low-degree vertices: one per thread, taken warp-slice by warp-slice
-    for (int64_t base = gw * 32; base < na; base += nw * 32) {
-        int64_t x = base + lane;
-        bool mine = false;
-        int32_t i = 0;
-        if (x < na) {
-            i = active[x];
-            mine = (off[i + 1] - off[i]) <= COLOR_THREAD_MAXD;
-            if (mine) out[x] = first_free_thread(off, nbr, colors, i);
-        }
-        unsigned big = __ballot_sync(FULLC, x < na && !mine);
-        while (big) {
-            int l = __ffs(big) - 1;
-            big &= big - 1;
-            int32_t ii = __shfl_sync(FULLC, i, l);
-            int c = first_free_warp(off, nbr, colors, ii, lane);
-            if (lane == 0) out[base + l] = c;
+            int32_t cj = colors[j];
+            if (cj >= 0 && cj < CWIN) atomicOr(bits + (cj >> 5), 1u << (cj & 31));
         }
     }
 }
 
-// keep[x] = no lower-id neighbour shares colors[active[x]]
-__global__ void k_color_conflicts(const int64_t *off, const int32_t *nbr, const int32_t *active,
-                                  int64_t na, const int32_t *colors, uint8_t *keep) {
-    int lane = threadIdx.x & 31;
-    int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t base = gw * 32; base < na; base += nw * 32) {
-        int64_t x = base + lane;
-        bool mine = false;
-        int32_t i = 0;
-        if (x < na) {
-            i = active[x];
-            int64_t e0 = off[i], e1 = off[i + 1];
-            mine = (e1 - e0) <= COLOR_THREAD_MAXD;
-            if (mine) {
-                int32_t ci = colors[i];
-                uint8_t k = 1;
-                for (int64_t e = e0; e < e1; e++) {
-                    int32_t j = nbr[e];
-                    if (j < i && colors[j] == ci) {
-                        k = 0;
-                        break;
-                    }
-                }
-                keep[x] = k;
-            }
+// First free colour of every huge item from its bitmap (block per item); a
+// row whose first CWIN colours are all taken falls back to windowed scans.
+__global__ void __launch_bounds__(CB) k_color_huge_final(const int64_t *off, const int32_t *nbr,
+                                                         const int32_t *active,
+                                                         const int32_t *colors,
+                                                         const int32_t *huge,
+                                                         const unsigned long long *nhuge,
+                                                         const uint32_t *hbits, int32_t *out,
+                                                         uint8_t *keep) {
+    __shared__ uint32_t bits[CWIN / 32];
+    __shared__ int s_found;
+    const int tid = threadIdx.x;
+    const int64_t cnt = (int64_t)*nhuge;
+    for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
+        int64_t x = huge[q];
+        int32_t i = active[x];
+        if (tid == 0) s_found = INT32_MAX;
+        __syncthreads();
+        for (int w = tid; w < CWIN / 32; w += CB) {
+            uint32_t free = ~hbits[q * (CWIN / 32) + w];
+            if (free) atomicMin(&s_found, w * 32 + __ffs(free) - 1);
         }
-        unsigned big = __ballot_sync(FULLC, x < na && !mine);
-        while (big) {
-            int l = __ffs(big) - 1;
-            big &= big - 1;
-            int32_t ii = __shfl_sync(FULLC, i, l);
-            int32_t ci = colors[ii];
-            int64_t e0 = off[ii], e1 = off[ii + 1];
-            bool clash = false;
-            // neighbour rows are sorted: only the prefix j < i matters
-            for (int64_t e = e0 + lane; e < e1; e += 32) {
+        __syncthreads();
+        int f = s_found;
+        int64_t e0 = off[i], e1 = off[i + 1];
+        for (int base = CWIN; f == INT32_MAX; base += CWIN) {
+            __syncthreads();
+            for (int w = tid; w < CWIN / 32; w += CB) bits[w] = 0u;
+            __syncthreads();
+            for (int64_t e = e0 + tid; e < e1; e += CB) {
                 int32_t j = nbr[e];
-                if (j >= ii) break;
-                if (colors[j] == ci) clash = true;
+                if (j == i) continue;
+                int32_t cj = colors[j] - base;
+                if (cj >= 0 && cj < CWIN) atomicOr(bits + (cj >> 5), 1u << (cj & 31));
             }
-            clash = __any_sync(FULLC, clash);
-            if (lane == 0) keep[base + l] = clash ? 0 : 1;
+            __syncthreads();
+            for (int w = tid; w < CWIN / 32; w += CB) {
+                uint32_t free = ~bits[w];
+                if (free) atomicMin(&s_found, base + w * 32 + __ffs(free) - 1);
+            }
+            __syncthreads();
+            f = s_found;
         }
+        if (tid == 0) {
+            out[x] = f;
+            keep[x] = 1;  // k_color_conflicts_huge clears it on a clash
+        }
+        __syncthreads();
+    }
+}
+
+// Huge rows: block (q, chunk) scans its entries of the j < i prefix.
+__global__ void __launch_bounds__(CB) k_color_conflicts_huge(const int64_t *off,
+                                                             const int32_t *nbr,
+                                                             const int32_t *active,
+                                                             const int32_t *colors,
+                                                             const int32_t *huge,
+                                                             const unsigned long long *nhuge,
+                                                             uint8_t *keep) {
+    const int64_t cnt = (int64_t)*nhuge;
+    for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
+        int64_t x = huge[q];
+        int32_t i = active[x];
+        int32_t ci = colors[i];
+        int64_t e0 = off[i] + (int64_t)blockIdx.y * CHUGE, e1 = off[i + 1];
+        int64_t ee = e0 + CHUGE < e1 ? e0 + CHUGE : e1;
+        bool clash = false;
+        for (int64_t e = e0 + threadIdx.x; e < ee; e += CB) {
+            int32_t j = nbr[e];
+            if (j < i && colors[j] == ci) clash = true;
+        }
+        if (clash) keep[x] = 0;
+    }
+}
+
+// One block per high-degree active vertex: bitmap of neighbour colours.
+__global__ void __launch_bounds__(CB) k_color_assign_big(const int64_t *off, const int32_t *nbr,
+                                                         const int32_t *active, const int32_t *colors,
+                                                         int32_t *out, const int32_t *big,
+                                                         const unsigned long long *nbig) {
+    __shared__ uint32_t bits[CWIN / 32];
+    __shared__ int s_found;
+    const int tid = threadIdx.x;
+    const int64_t cnt = (int64_t)*nbig;
+    for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
+        int64_t x = big[q];
+        int32_t i = active[x];
+        int64_t e0 = off[i], e1 = off[i + 1];
+        for (int base = 0;; base += CWIN) {
+            for (int w = tid; w < CWIN / 32; w += CB) bits[w] = 0u;
+            if (tid == 0) s_found = INT32_MAX;
+            __syncthreads();
+            for (int64_t e = e0 + tid; e < e1; e += CB) {
+                int32_t j = nbr[e];
+                if (j == i) continue;
+                int32_t cj = colors[j] - base;
+                if (cj >= 0 && cj < CWIN) atomicOr(bits + (cj >> 5), 1u << (cj & 31));
+            }
+            __syncthreads();
+            for (int w = tid; w < CWIN / 32; w += CB) {
+                uint32_t free = ~bits[w];
+                if (free) atomicMin(&s_found, w * 32 + __ffs(free) - 1);
+            }
+            __syncthreads();
+            int f = s_found;
+            __syncthreads();
+            if (f != INT32_MAX) {
+                if (tid == 0) out[x] = base + f;
+                break;
+            }
+        }
+    }
+}
+
+// keep[x] = no lower-id neighbour shares colors[active[x]] (low degree).
+__global__ void k_color_conflicts_small(const int64_t *off, const int32_t *nbr,
+                                        const int32_t *active, int64_t na, const int32_t *colors,
+                                        uint8_t *keep) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < na;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        int32_t i = active[x];
+        int64_t e0 = off[i], e1 = off[i + 1];
+        if (e1 - e0 > COLOR_THREAD_MAXD) continue;
+        int32_t ci = colors[i];
+        uint8_t k = 1;
+        for (int64_t e = e0; e < e1; e++) {
+            int32_t j = nbr[e];
+            if (j >= i) break;  // rows are sorted: only the prefix j < i matters
+            if (colors[j] == ci) {
+                k = 0;
+                break;
+            }
+        }
+        keep[x] = k;
+    }
+}
+
+__global__ void __launch_bounds__(CB) k_color_conflicts_big(const int64_t *off, const int32_t *nbr,
+                                                            const int32_t *active,
+                                                            const int32_t *colors, uint8_t *keep,
+                                                            const int32_t *big,
+                                                            const unsigned long long *nbig) {
+    const int tid = threadIdx.x;
+    const int64_t cnt = (int64_t)*nbig;
+    for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
+        int64_t x = big[q];
+        int32_t i = active[x];
+        int32_t ci = colors[i];
+        int64_t e0 = off[i], e1 = off[i + 1];
+        bool clash = false;
+        for (int64_t c0 = e0; c0 < e1; c0 += CB) {
+            int64_t e = c0 + tid;
+            bool past = true;
+            if (e < e1) {
+                int32_t j = nbr[e];
+                past = j >= i;
+                if (!past && colors[j] == ci) clash = true;
+            }
+            // stop once the whole chunk is past the j < i prefix or a clash is seen
+            int stop = __syncthreads_or(clash || past);
+            if (stop) break;
+        }
+        clash = __syncthreads_or(clash);
+        if (tid == 0) keep[x] = clash ? 0 : 1;
+    }
+}
+
+__global__ void k_big_list(const int64_t *off, const int32_t *active, int64_t na, int32_t *big,
+                           unsigned long long *nbig) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < na;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        int32_t i = active[x];
+        if (off[i + 1] - off[i] > COLOR_THREAD_MAXD) big[atomicAdd(nbig, 1ull)] = (int32_t)x;
     }
 }
 
@@ -166,9 +298,65 @@ __global__ void k_max_color(const int32_t *colors, int64_t n, int *mx) {
     if (threadIdx.x == 0) atomicMax(mx, b);
 }
 
-static unsigned warp_grid(int64_t items) {
-    // one warp handles 32 consecutive active entries per step
-    return grid_for((items + 31) / 32 * 32, 256, 148 * 16);
+// One speculative round over active[0..na): tentative colours, commit, keep flags.
+struct ColorScratch {
+    int32_t *big, *huge;
+    unsigned long long *cnt;  // [0] big, [1] huge
+    uint32_t *hbits;          // nhuge_max * CWIN / 32 words
+    int64_t nhuge_max;
+    unsigned huge_chunks;     // ceil(max_degree / CHUGE)
+};
+
+static void color_round(const int64_t *off, const int32_t *nbr, const int32_t *active, int64_t na,
+                        int32_t *colors, int32_t *tent, uint8_t *keep, const ColorScratch &C,
+                        cudaStream_t s) {
+    PLV_CUDA(cudaMemsetAsync(C.cnt, 0, 2 * sizeof(unsigned long long), s));
+    bool huge = C.nhuge_max > 0;
+    k_color_assign_small<<<grid_for(na, 256), 256, 0, s>>>(
+        off, nbr, active, na, colors, tent, C.big, C.cnt, huge ? C.huge : nullptr, C.cnt + 1);
+    PLV_LAUNCH_CHECK();
+    k_color_assign_big<<<CBIG_GRID, CB, 0, s>>>(off, nbr, active, colors, tent, C.big, C.cnt);
+    PLV_LAUNCH_CHECK();
+    if (huge) {
+        PLV_CUDA(cudaMemsetAsync(C.hbits, 0, sizeof(uint32_t) * C.nhuge_max * (CWIN / 32), s));
+        dim3 g(148, C.huge_chunks);
+        k_color_assign_huge<<<g, CB, 0, s>>>(off, nbr, active, colors, C.huge, C.cnt + 1, C.hbits);
+        PLV_LAUNCH_CHECK();
+        k_color_huge_final<<<148, CB, 0, s>>>(off, nbr, active, colors, C.huge, C.cnt + 1, C.hbits,
+                                              tent, keep);
+        PLV_LAUNCH_CHECK();
+    }
+    k_color_commit<<<grid_for(na, 256), 256, 0, s>>>(active, na, tent, colors);
+    PLV_LAUNCH_CHECK();
+    k_color_conflicts_small<<<grid_for(na, 256), 256, 0, s>>>(off, nbr, active, na, colors, keep);
+    PLV_LAUNCH_CHECK();
+    k_color_conflicts_big<<<CBIG_GRID, CB, 0, s>>>(off, nbr, active, colors, keep, C.big, C.cnt);
+    PLV_LAUNCH_CHECK();
+    if (huge) {
+        dim3 g(148, C.huge_chunks);
+        k_color_conflicts_huge<<<g, CB, 0, s>>>(off, nbr, active, colors, C.huge, C.cnt + 1, keep);
+        PLV_LAUNCH_CHECK();
+    }
+}
+
+__global__ void k_count_huge(const int64_t *off, int64_t n, unsigned long long *cnt,
+                             unsigned long long *maxdeg) {
+    unsigned long long c = 0, md = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long d = (unsigned long long)(off[i + 1] - off[i]);
+        c += d > (unsigned long long)CHUGE;
+        md = d > md ? d : md;
+    }
+    typedef cub::BlockReduce<unsigned long long, 256> BR;
+    __shared__ typename BR::TempStorage t1;
+    unsigned long long tc = BR(t1).Sum(c);
+    __syncthreads();
+    unsigned long long tm = BR(t1).Reduce(md, cub::Max());
+    if (threadIdx.x == 0) {
+        if (tc) atomicAdd(cnt, tc);
+        atomicMax(maxdeg, tm);
+    }
 }
 
 void color(const int64_t *off, const int32_t *nbr, int64_t n, int32_t *colors, int64_t *info_h,
@@ -178,9 +366,20 @@ void color(const int64_t *off, const int32_t *nbr, int64_t n, int32_t *colors, i
         info_h[1] = 0;
         return;
     }
-    Buf<int32_t> act0(n, s), act1(n, s), tent(n, s);
+    Buf<int32_t> act0(n, s), act1(n, s), tent(n, s), big(n, s);
     Buf<uint8_t> keep(n, s), rej(n, s);
     Buf<int64_t> cnt(1, s);
+    Buf<unsigned long long> cnts(4, s);
+    PLV_CUDA(cudaMemsetAsync(cnts.get(), 0, 4 * sizeof(unsigned long long), s));
+    k_count_huge<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(off, n, cnts.get() + 2, cnts.get() + 3);
+    PLV_LAUNCH_CHECK();
+    unsigned long long hc[2];
+    PLV_CUDA(cudaMemcpyAsync(hc, cnts.get() + 2, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    PLV_CUDA(cudaStreamSynchronize(s));
+    Buf<int32_t> huge(hc[0] ? hc[0] : 1, s);
+    Buf<uint32_t> hbits((hc[0] ? hc[0] : 1) * (CWIN / 32), s);
+    ColorScratch C{big.get(), huge.get(), cnts.get(), hbits.get(), (int64_t)hc[0],
+                   (unsigned)((hc[1] + CHUGE - 1) / CHUGE)};
     k_color_init<<<grid_for(n, 256), 256, 0, s>>>(colors, act0, n);
     PLV_LAUNCH_CHECK();
     int32_t *active = act0.get(), *next = act1.get();
@@ -190,12 +389,7 @@ void color(const int64_t *off, const int32_t *nbr, int64_t n, int32_t *colors, i
     Buf<char> tmp(bytes, s);
     while (na > 0) {
         rounds++;
-        k_color_assign<<<warp_grid(na), 256, 0, s>>>(off, nbr, active, na, colors, tent);
-        PLV_LAUNCH_CHECK();
-        k_color_commit<<<grid_for(na, 256), 256, 0, s>>>(active, na, tent, colors);
-        PLV_LAUNCH_CHECK();
-        k_color_conflicts<<<warp_grid(na), 256, 0, s>>>(off, nbr, active, na, colors, keep);
-        PLV_LAUNCH_CHECK();
+        color_round(off, nbr, active, na, colors, tent, keep, C, s);
         k_reject_flags<<<grid_for(na, 256), 256, 0, s>>>(keep, na, rej);
         PLV_LAUNCH_CHECK();
         size_t b2 = bytes;
@@ -236,8 +430,7 @@ void color_classes(const int32_t *colors, int64_t n, int64_t nc, int64_t *class_
     if (n <= 0) return;
     Buf<int32_t> idx(n, s);
     Buf<uint32_t> ks(n, s);
-    // vertex ids ascending in, stable sort by colour
-    iota_i32(idx, n, s);
+    iota_i32(idx, n, s);  // vertex ids ascending in, stable sort by colour
     sort_pairs<uint32_t, int32_t>(reinterpret_cast<const uint32_t *>(colors), ks, idx, class_vtx, n,
                                   0, bits_for(nc > 1 ? nc : 2), s);
 }
@@ -257,9 +450,17 @@ extern "C" int plv_color_assign(const int64_t *off, const int32_t *nbr, const in
                                 void *stream) {
     PLV_ENTRY
     if (na > 0) {
-        plv::k_color_assign<<<plv::warp_grid(na), 256, 0, plv::S(stream)>>>(off, nbr, active, na,
-                                                                           colors, out_colors);
+        cudaStream_t s = plv::S(stream);
+        plv::Buf<int32_t> big(na, s);
+        plv::Buf<unsigned long long> nbig(1, s);
+        PLV_CUDA(cudaMemsetAsync(nbig.get(), 0, sizeof(unsigned long long), s));
+        plv::k_color_assign_small<<<plv::grid_for(na, 256), 256, 0, s>>>(
+            off, nbr, active, na, colors, out_colors, big, nbig, nullptr, nullptr);
         PLV_LAUNCH_CHECK();
+        plv::k_color_assign_big<<<plv::CBIG_GRID, plv::CB, 0, s>>>(off, nbr, active, colors,
+                                                                  out_colors, big, nbig);
+        PLV_LAUNCH_CHECK();
+        PLV_CUDA(cudaStreamSynchronize(s));
     }
     PLV_EXIT
 }
@@ -269,9 +470,19 @@ extern "C" int plv_color_conflicts(const int64_t *off, const int32_t *nbr, const
                                    void *stream) {
     PLV_ENTRY
     if (na > 0) {
-        plv::k_color_conflicts<<<plv::warp_grid(na), 256, 0, plv::S(stream)>>>(off, nbr, active, na,
-                                                                              colors, out_keep);
+        cudaStream_t s = plv::S(stream);
+        plv::Buf<int32_t> big(na, s);
+        plv::Buf<unsigned long long> nbig(1, s);
+        PLV_CUDA(cudaMemsetAsync(nbig.get(), 0, sizeof(unsigned long long), s));
+        plv::k_color_conflicts_small<<<plv::grid_for(na, 256), 256, 0, s>>>(off, nbr, active, na,
+                                                                           colors, out_keep);
         PLV_LAUNCH_CHECK();
+        plv::k_big_list<<<plv::grid_for(na, 256), 256, 0, s>>>(off, active, na, big, nbig);
+        PLV_LAUNCH_CHECK();
+        plv::k_color_conflicts_big<<<plv::CBIG_GRID, plv::CB, 0, s>>>(off, nbr, active, colors,
+                                                                     out_keep, big, nbig);
+        PLV_LAUNCH_CHECK();
+        PLV_CUDA(cudaStreamSynchronize(s));
     }
     PLV_EXIT
 }

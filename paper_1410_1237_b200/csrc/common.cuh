@@ -33,7 +33,14 @@ void check_device();  // throws PLV_ENODEV unless an sm_100 device is current
         }                                                                             \
     } while (0)
 
-#define PLV_LAUNCH_CHECK() PLV_CUDA(cudaGetLastError())
+// Every kernel launch of this library is followed by PLV_LAUNCH_CHECK, which
+// also counts it (plv_launch_count(): evidence of the native path for bench.py).
+void count_launch();
+#define PLV_LAUNCH_CHECK()                \
+    do {                                  \
+        plv::count_launch();              \
+        PLV_CUDA(cudaGetLastError());     \
+    } while (0)
 
 #define PLV_FAIL(code, ...)              \
     do {                                 \
@@ -113,6 +120,78 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// ------------------------------------------------ ordered long folds
+// Exact reproduction of a sequential float64 fold needs its additions in
+// order: the dependency chain is inherent.  To make the chain the only cost,
+// a whole block stages the operands chunk by chunk into shared memory
+// (parallel, high-MLP loads, double-buffered) while thread 0 runs the
+// dependent additions out of shared memory.  `get(t)` yields operand t.
+// Call with every thread of the block; the result is valid in thread 0.
+// `sb` must hold 2 * FOLD_CH doubles.
+constexpr int FOLD_CH = 1024;
+
+template <class Get>
+__device__ double block_fold(Get get, int64_t len, double init, double *sb) {
+    double v = init;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int t = tid; t < FOLD_CH; t += nt)
+        if (t < len) sb[t] = get(t);
+    __syncthreads();
+    const int64_t nch = (len + FOLD_CH - 1) / FOLD_CH;
+    for (int64_t c = 0; c < nch; c++) {
+        const double *cur = sb + (c & 1) * FOLD_CH;
+        double *nxt = sb + ((c + 1) & 1) * FOLD_CH;
+        if (tid == 0) {
+            int64_t m = len - c * FOLD_CH;
+            m = m < FOLD_CH ? m : FOLD_CH;
+            int64_t t = 0;
+            for (; t + 4 <= m; t += 4) {
+                double a0 = cur[t], a1 = cur[t + 1], a2 = cur[t + 2], a3 = cur[t + 3];
+                v = __dadd_rn(v, a0);
+                v = __dadd_rn(v, a1);
+                v = __dadd_rn(v, a2);
+                v = __dadd_rn(v, a3);
+            }
+            for (; t < m; t++) v = __dadd_rn(v, cur[t]);
+        } else {
+            const int64_t base = (c + 1) * FOLD_CH;
+            for (int t = tid - 1; t < FOLD_CH; t += nt - 1)
+                if (base + t < len) nxt[t] = get(base + t);
+        }
+        __syncthreads();
+    }
+    return v;
+}
+
+// Two interleaved folds (independent chains) over operand pairs get(t) ->
+// (x, y); results valid in thread 0.  `sb` holds 4 * FOLD_CH doubles.
+template <class Get>
+__device__ void block_fold2(Get get, int64_t len, double &vx, double &vy, double *sb) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int t = tid; t < FOLD_CH; t += nt)
+        if (t < len) get(t, sb[t], sb[2 * FOLD_CH + t]);
+    __syncthreads();
+    const int64_t nch = (len + FOLD_CH - 1) / FOLD_CH;
+    for (int64_t c = 0; c < nch; c++) {
+        const int b = (int)(c & 1), nb = (int)((c + 1) & 1);
+        if (tid == 0) {
+            int64_t m = len - c * FOLD_CH;
+            m = m < FOLD_CH ? m : FOLD_CH;
+            const double *cx = sb + b * FOLD_CH, *cy = sb + 2 * FOLD_CH + b * FOLD_CH;
+            for (int64_t t = 0; t < m; t++) {
+                vx = __dadd_rn(vx, cx[t]);
+                vy = __dadd_rn(vy, cy[t]);
+            }
+        } else {
+            const int64_t base = (c + 1) * FOLD_CH;
+            for (int t = tid - 1; t < FOLD_CH; t += nt - 1)
+                if (base + t < len)
+                    get(base + t, sb[nb * FOLD_CH + t], sb[2 * FOLD_CH + nb * FOLD_CH + t]);
+        }
+        __syncthreads();
+    }
+}
 
 // --------------------------------------------------- counter-based RNG
 // SplitMix64 finaliser; u64(key, i) is the i-th SplitMix64 output for state

@@ -195,13 +195,29 @@ __global__ void k_place_reverse(const int32_t *bkey, const int32_t *tidx, int64_
 
 // k_i = (((0 + w_0) + w_1) + ...) + selfw_i : the weighted np.bincount fold in
 // CSR order (PL/graph.py:73-78).  Integral graphs may fold in any order.
+constexpr int64_t DEG_LONG = 256;  // longer rows are folded by a whole block
+
 __global__ void k_degrees(const int64_t *off, const double *wts, const double *selfw, int64_t n,
                           double *k) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t e0 = off[i], e1 = off[i + 1];
+        if (e1 - e0 > DEG_LONG) continue;
         double acc = 0.0;
-        for (int64_t e = off[i]; e < off[i + 1]; e++) acc = __dadd_rn(acc, wts[e]);
+        for (int64_t e = e0; e < e1; e++) acc = __dadd_rn(acc, wts[e]);
         k[i] = __dadd_rn(acc, selfw[i]);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_degrees_long(const int64_t *off, const double *wts,
+                                                     const double *selfw, int64_t n, double *k) {
+    __shared__ double sb[2 * FOLD_CH];
+    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const int64_t e0 = off[i], len = off[i + 1] - e0;
+        if (len <= DEG_LONG) continue;
+        double acc = block_fold([=] __device__(int64_t t) { return wts[e0 + t]; }, len, 0.0, sb);
+        if (threadIdx.x == 0) k[i] = __dadd_rn(acc, selfw[i]);
+        __syncthreads();
     }
 }
 
@@ -215,8 +231,15 @@ __global__ void k_graph_stats(const int64_t *off, const double *selfw, int64_t n
         unsigned long long d = (unsigned long long)(off[i + 1] - off[i]);
         md = d > md ? d : md;
     }
-    atomicAdd(stats + 0, ns);
-    atomicMax(stats + 1, md);
+    typedef cub::BlockReduce<unsigned long long, 256> BR;
+    __shared__ typename BR::TempStorage tmp;
+    unsigned long long tns = BR(tmp).Sum(ns);
+    __syncthreads();
+    unsigned long long tmd = BR(tmp).Reduce(md, cub::Max());
+    if (threadIdx.x == 0) {
+        if (tns) atomicAdd(stats + 0, tns);
+        atomicMax(stats + 1, tmd);
+    }
 }
 
 __global__ void k_integral_check(const double *w, int64_t M, unsigned long long *stats) {
@@ -268,11 +291,13 @@ void csr_from_merged(const int32_t *a, const int32_t *b, const double *w, int64_
     if (n > 0) {
         k_degrees<<<grid_for(n, 128), 128, 0, s>>>(off, wts, selfw, n, k);
         PLV_LAUNCH_CHECK();
+        k_degrees_long<<<148 * 4, 256, 0, s>>>(off, wts, selfw, n, k);
+        PLV_LAUNCH_CHECK();
     }
     Buf<unsigned long long> stats(3, s);
     PLV_CUDA(cudaMemsetAsync(stats.get(), 0, sizeof(unsigned long long) * 3, s));
     if (n > 0) {
-        k_graph_stats<<<grid_for(n, 256), 256, 0, s>>>(off, selfw, n, stats);
+        k_graph_stats<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(off, selfw, n, stats);
         PLV_LAUNCH_CHECK();
     }
     if (M > 0) {

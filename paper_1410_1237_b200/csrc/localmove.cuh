@@ -1,0 +1,147 @@
+// localmove.cuh -- shared declarations of the local-moving hot path
+// (decide.cu, apply.cu, phase.cu).
+//
+// decide (PL/_kernels.pyx:21-101): every subset vertex i aggregates
+// e_{i->C} over its neighbours j != i by snapshot community, summed in
+// adjacency order per community (fp64, bit-exact with the reference's
+// sequential hash accumulation), then takes the argmax of the Eq. 4 gain
+// under (gain desc, label asc) with the singleton-pair guard.
+//
+// apply (PL/_kernels.pyx:104-145) is restated in parallel, bit-exactly:
+// e_a / e_b of a mover use the *live* assignment (the target of an
+// earlier-moved subset vertex, else the snapshot) and the per-community
+// a_tot / w_internal updates are folded in subset order, one thread per
+// community, after a stable sort of (community, subset position) events.
+#pragma once
+#include "common.cuh"
+#include <vector>
+
+namespace plv {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int T0_MAXD = 8;
+constexpr int T1_MAXD = 128;
+constexpr int T2_MAXD = 2048;
+constexpr int T1_WARPS = 8;   // warps per block in tier 1
+constexpr int T1_TS = 256;    // slots per warp table (>= 1.5 * (128 + 1))
+constexpr int BLK = 256;      // threads per block in tiers 2/3
+constexpr int T2_TS = 4096;   // smem slots for tier 2 (>= 1.5 * (2048 + 1))
+constexpr size_t T2_SMEM = (sizeof(double) + sizeof(int32_t)) * T2_TS;
+
+constexpr int SMALL_APPLY_MAX = 2048;  // stage size handled by the one-CTA apply
+constexpr int SA_THREADS = 256;
+constexpr int SA_ITEMS = 16;  // 256 * 16 = 4096 events = 2 * SMALL_APPLY_MAX
+constexpr uint32_t SENTINEL = 0xFFFFFFFFu;
+
+struct DecideArgs {
+    const int64_t *off;
+    const int32_t *nbr;
+    const double *wts;
+    const double *k;
+    const int32_t *labels;  // NULL: labels[c] == c
+    const int32_t *subset;  // stage vertices
+    const int32_t *assign;
+    const double *a_tot;
+    const int32_t *sizes;
+    double m, four_m_sq;
+    int integral;
+    int32_t *out_target;  // per stage index
+    uint8_t *out_moved;
+    double *out_e_old;
+    double *out_e_best;
+    unsigned long long *cand;  // nullable: += distinct candidate communities
+};
+
+DecideArgs make_decide_args(const int64_t *off, const int32_t *nbr, const double *wts,
+                            const double *k, const int32_t *labels, const int32_t *subset,
+                            const int32_t *assign, const double *a_tot, const int32_t *sizes,
+                            double m, int integral, int32_t *out_target, uint8_t *out_moved,
+                            double *out_e_old, double *out_e_best, unsigned long long *cand);
+
+struct StagePlan {
+    int64_t off = 0, ns = 0;
+    int64_t tcount[4] = {0, 0, 0, 0};
+    int64_t tstart[4] = {0, 0, 0, 0};  // into the tier list
+    int64_t hub_base = 0;              // this stage's first hub_eoff entry
+    int64_t hub_entries = 0;
+};
+
+// Static per-phase decide plan: each stage's vertices split into the four
+// degree tiers, and the hubs' entries laid out for the sort-based tier.
+struct Plan {
+    std::vector<StagePlan> st;
+    int32_t *tier_list = nullptr;  // stage-local indices grouped by (stage, tier)
+    int64_t *hub_eoff = nullptr;   // per stage: nh+1 entry offsets (from 0)
+    int64_t max_hub_entries = 0, max_hubs = 0;
+    uint64_t *hkey = nullptr, *hkey2 = nullptr;
+    int32_t *hval = nullptr, *hval2 = nullptr;
+    void *htmp = nullptr;
+    size_t hbytes = 0;
+    double *heold = nullptr;  // per hub: e_{i->c_old}
+    double *rgain = nullptr;  // per sorted position: run gain (-inf: not a candidate)
+    int32_t *rc = nullptr;
+    double *rv = nullptr;
+    int64_t *lrun = nullptr;  // heads of long runs (block-folded)
+    unsigned long long *lcnt = nullptr;
+    int cb = 1, qb = 1;
+    int32_t nskip = 0;
+    void release();
+};
+
+void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *stage_off_h,
+                int64_t nst, int64_t n, cudaStream_t s);
+void ensure_decide_attrs();
+// Launch stage `a`'s decide kernels (no host synchronisation; capturable).
+void launch_decide(const Plan &P, int64_t a, DecideArgs A, cudaStream_t st);
+
+struct StageArgs {
+    const int64_t *off;
+    const int32_t *nbr;
+    const double *wts;
+    const double *k;
+    const double *selfw;
+    const int32_t *subset;
+    int64_t ns;
+    const int32_t *target;
+    const uint8_t *moved;
+    const double *e_old;
+    const double *e_best;
+    const int32_t *pos;  // general subsets: subset position per vertex, -1 if absent
+    int flags;
+    int32_t *assign;
+    double *a_tot;
+    double *w_int;
+    int32_t *sizes;
+    double *ta;  // per stage index: 2 e_a + 2 sw (leaving), 2 e_b + 2 sw (joining)
+    double *tb;
+    uint32_t *ekey;
+    int32_t *eval;
+    unsigned long long *moves;
+};
+
+// Event / sort scratch for stages of up to max_ns vertices.
+struct ApplyBuffers {
+    double *ta = nullptr, *tb = nullptr;
+    uint32_t *ekey = nullptr, *ekey2 = nullptr;
+    int32_t *eval = nullptr, *eval2 = nullptr;
+    void *tmp = nullptr;
+    size_t bytes = 0;
+    double *dW = nullptr, *dA = nullptr;  // sorted event deltas
+    int64_t *lrun = nullptr;              // heads of long community runs
+    unsigned long long *lcnt = nullptr;
+    int nb = 1;
+    void alloc(int64_t ta_len, int64_t max_ns, int64_t n, cudaStream_t s);
+    void release();
+};
+
+// Launch one stage's apply (no host synchronisation; capturable).
+void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st);
+
+template <class T>
+T *dalloc(size_t count) {
+    T *p = nullptr;
+    PLV_CUDA(cudaMalloc((void **)&p, sizeof(T) * (count ? count : 1)));
+    return p;
+}
+
+}  // namespace plv

@@ -43,8 +43,16 @@ __global__ void k_pw_tree2(const double *in, int64_t count, int kb, double *out,
 
 __global__ void k_zero1(double *out) { out[0] = 0.0; }
 
+int64_t pw_scratch_doubles(int64_t n) {
+    if (n <= 0) return 2;
+    int64_t cnt = 1ll << pw_depth(n);
+    return cnt + (cnt + 1023) / 1024 + 2;
+}
+
+// scratch: nullptr (stream-ordered allocation) or pw_scratch_doubles(n) doubles.
 template <class F>
-static void pw_launch(const double *a, int64_t n, double *out_dev, cudaStream_t s, F f) {
+static void pw_launch(const double *a, int64_t n, double *out_dev, cudaStream_t s, F f,
+                      double *scratch = nullptr) {
     if (n <= 0) {
         k_zero1<<<1, 1, 0, s>>>(out_dev);
         PLV_LAUNCH_CHECK();
@@ -52,11 +60,16 @@ static void pw_launch(const double *a, int64_t n, double *out_dev, cudaStream_t 
     }
     int d0 = pw_depth(n);
     int64_t cnt = 1ll << d0;
-    Buf<double> v0(cnt, s), v1((cnt + 1023) / 1024 + 1, s);
-    k_pw_nodes<<<grid_for(cnt, 256, 148 * 32), 256, 0, s>>>(a, n, d0, v0.get(), f);
+    Buf<double> own;
+    if (!scratch) {
+        own.alloc(pw_scratch_doubles(n), s);
+        scratch = own.get();
+    }
+    double *v0 = scratch, *v1 = scratch + cnt;
+    k_pw_nodes<<<grid_for(cnt, 256, 148 * 32), 256, 0, s>>>(a, n, d0, v0, f);
     PLV_LAUNCH_CHECK();
     // reduce the perfect top tree, 2^10 values per block per pass
-    double *src = v0.get(), *dst = v1.get();
+    double *src = v0, *dst = v1;
     int64_t count = cnt;
     int levels = d0;
     while (true) {
@@ -79,6 +92,23 @@ void pw_sum_async(const double *a, int64_t n, double *out_dev, cudaStream_t s) {
 
 void pw_sum_sq_async(const double *a, int64_t n, double two_m, double *out_dev, cudaStream_t s) {
     pw_launch(a, n, out_dev, s, SqScaled{two_m});
+}
+
+__global__ void k_mod_finish(const double *sw, const double *sq, double two_m, double *out) {
+    out[0] = __dsub_rn(__ddiv_rn(sw[0], two_m), sq[0]);
+}
+
+int64_t modularity_scratch_doubles(int64_t n) { return 2 * pw_scratch_doubles(n) + 2; }
+
+void modularity_async(const double *w_int, const double *a_tot, int64_t n, double m, double *out,
+                      double *scratch, cudaStream_t s) {
+    double two_m = 2.0 * m;
+    int64_t ps = pw_scratch_doubles(n);
+    double *tmp = scratch + 2 * ps;
+    pw_launch(w_int, n, tmp, s, Ident{}, scratch);
+    pw_launch(a_tot, n, tmp + 1, s, SqScaled{two_m}, scratch + ps);
+    k_mod_finish<<<1, 1, 0, s>>>(tmp, tmp + 1, two_m, out);
+    PLV_LAUNCH_CHECK();
 }
 
 // ---------------------------------------------------------------- reduceat
@@ -150,22 +180,12 @@ extern "C" int plv_sum(const double *a, int64_t n, double *out, void *stream) {
     PLV_EXIT
 }
 
-namespace plv {
-__global__ void k_mod_finish(const double *sw, const double *sq, double two_m, double *out) {
-    out[0] = __dsub_rn(__ddiv_rn(sw[0], two_m), sq[0]);
-}
-}  // namespace plv
-
 extern "C" int plv_modularity(const double *w_int, const double *a_tot, int64_t n, double m,
                               double *out, void *stream) {
     PLV_ENTRY
     cudaStream_t s = plv::S(stream);
     if (!(m > 0.0)) PLV_FAIL(PLV_EINVAL, "modularity undefined for edgeless graph");
-    double two_m = 2.0 * m;
-    plv::Buf<double> tmp(2, s);
-    plv::pw_sum_async(w_int, n, tmp.get(), s);
-    plv::pw_sum_sq_async(a_tot, n, two_m, tmp.get() + 1, s);
-    plv::k_mod_finish<<<1, 1, 0, s>>>(tmp.get(), tmp.get() + 1, two_m, out);
-    PLV_LAUNCH_CHECK();
+    plv::Buf<double> scratch(plv::modularity_scratch_doubles(n), s);
+    plv::modularity_async(w_int, a_tot, n, m, out, scratch.get(), s);
     PLV_EXIT
 }

@@ -156,6 +156,11 @@ void pw_sum_async(const double *a, int64_t n, double *out_dev, cudaStream_t s);
 void pw_sum_sq_async(const double *a, int64_t n, double two_m, double *out_dev, cudaStream_t s);
 // out[t] = w[st] (+ pairwise(w[st+1:en])) for segments t of the sorted run
 // list starts[0..M) (segment t ends at starts[t+1], the last at R).
+int64_t pw_scratch_doubles(int64_t n);
+int64_t modularity_scratch_doubles(int64_t n);
+// q = pairwise(w_int)/2m - pairwise((a_tot/2m)^2); scratch: modularity_scratch_doubles(n).
+void modularity_async(const double *w_int, const double *a_tot, int64_t n, double m, double *out,
+                      double *scratch, cudaStream_t s);
 void reduceat_async(const double *w, const int64_t *starts, int64_t M, int64_t R, double *out,
                     cudaStream_t s);
 
