@@ -33,9 +33,116 @@ __device__ __forceinline__ int32_t live_comm(const StageArgs &A, int32_t j, int6
     return A.assign[j];
 }
 
+// Deltas of one mover: 2 e_a + 2 sw leaving a, 2 e_b + 2 sw joining b (the
+// reference's `w_int[a] -= 2.0 * e_a + 2.0 * sw`, PL/_kernels.pyx:137-142),
+// stored for the ordered fold, or added with atomics for integral graphs;
+// sizes are integers either way.
+__device__ __forceinline__ void mover_deltas(const StageArgs &A, int64_t x, int32_t i, int32_t a,
+                                             int32_t b, double e_a, double e_b, bool integral) {
+    double sw = A.selfw[i], ki = A.k[i];
+    double ta = dadd(dmul(2.0, e_a), dmul(2.0, sw));
+    double tb = dadd(dmul(2.0, e_b), dmul(2.0, sw));
+    if (integral) {
+        atomicAdd(A.w_int + a, -ta);
+        atomicAdd(A.w_int + b, tb);
+        atomicAdd(A.a_tot + a, -ki);
+        atomicAdd(A.a_tot + b, ki);
+    } else {
+        A.ta[x] = ta;
+        A.tb[x] = tb;
+    }
+    atomicSub(A.sizes + a, 1);
+    atomicAdd(A.sizes + b, 1);
+}
+
+// One warp per high-degree mover: live e_a / e_b as ordered folds (the
+// matching lanes of each 32-entry chunk are added in lane order).
+__global__ void __launch_bounds__(256) k_stage_big(StageArgs A) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t cnt = (int64_t)*A.nbig;
+    const bool integral = A.flags & PLV_F_INTEGRAL;
+    for (int64_t q = gw; q < cnt; q += nw) {
+        const int64_t x = A.big[q];
+        const int32_t i = A.subset[x], b = A.target[x], a = A.assign[i];
+        const int64_t e0 = A.off[i], e1 = A.off[i + 1];
+        double fa = 0.0, fb = 0.0;
+        for (int64_t c0 = e0; c0 < e1; c0 += 32) {
+            int64_t e = c0 + lane;
+            int32_t c = -1;
+            double w = 0.0;
+            if (e < e1) {
+                int32_t j = A.nbr[e];
+                if (j != i) {
+                    c = live_comm(A, j, x);
+                    w = A.wts[e];
+                }
+            }
+            unsigned ma = __ballot_sync(FULL, c == a);
+            unsigned mb = __ballot_sync(FULL, c == b && c != a);
+            for (unsigned mm = ma; mm; mm &= mm - 1)
+                fa = dadd(fa, __shfl_sync(FULL, w, __ffs(mm) - 1));
+            for (unsigned mm = mb; mm; mm &= mm - 1)
+                fb = dadd(fb, __shfl_sync(FULL, w, __ffs(mm) - 1));
+        }
+        if (lane == 0) mover_deltas(A, x, i, a, b, fa, fb, integral);
+    }
+}
+
+// One block per huge mover (> APPLY_HUGE entries): the row's entries whose
+// live community is a or b are compacted in order (block scan), then thread 0
+// folds them -- the chain is only the matching entries, the scan is parallel.
+constexpr int64_t APPLY_HUGE = 2048;
+
+__global__ void __launch_bounds__(256) k_stage_huge(StageArgs A) {
+    typedef cub::BlockScan<int, 256> Scan;
+    __shared__ typename Scan::TempStorage scan;
+    __shared__ int8_t sidx[256];
+    __shared__ double sw[256];
+    const int tid = threadIdx.x;
+    const int64_t cnt = (int64_t)*A.nhuge;
+    const bool integral = A.flags & PLV_F_INTEGRAL;
+    for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
+        const int64_t x = A.huge[q];
+        const int32_t i = A.subset[x], b = A.target[x], a = A.assign[i];
+        const int64_t e0 = A.off[i], e1 = A.off[i + 1];
+        double fa = 0.0, fb = 0.0;  // thread 0's accumulators
+        for (int64_t base = e0; base < e1; base += 256) {
+            int64_t e = base + tid;
+            int k = -1;
+            double w = 0.0;
+            if (e < e1) {
+                int32_t j = A.nbr[e];
+                if (j != i) {
+                    int32_t c = live_comm(A, j, x);
+                    k = c == a ? 0 : (c == b ? 1 : -1);
+                    if (k >= 0) w = A.wts[e];
+                }
+            }
+            int pos, total;
+            Scan(scan).ExclusiveSum(k >= 0 ? 1 : 0, pos, total);
+            if (k >= 0) {
+                sidx[pos] = (int8_t)k;
+                sw[pos] = w;
+            }
+            __syncthreads();
+            if (tid == 0)
+                for (int t = 0; t < total; t++) {
+                    if (sidx[t] == 0)
+                        fa = dadd(fa, sw[t]);
+                    else
+                        fb = dadd(fb, sw[t]);
+                }
+            __syncthreads();
+        }
+        if (tid == 0) mover_deltas(A, x, i, a, b, fa, fb, integral);
+    }
+}
+
 // Per subset index x: events + deltas (+ sizes, moves, and the assignment
-// scatter for independent stages).  Lanes take low-degree movers; whole warps
-// take high-degree ones when the live e_a / e_b must be recomputed.
+// scatter for independent stages).  Low-degree movers fold their live
+// e_a / e_b here; high-degree ones go to the k_stage_big worklist.
 __global__ void __launch_bounds__(256) k_stage_prep(StageArgs A) {
     const bool indep = A.flags & PLV_F_INDEPENDENT;
     const bool integral = A.flags & PLV_F_INTEGRAL;
@@ -81,56 +188,15 @@ __global__ void __launch_bounds__(256) k_stage_prep(StageArgs A) {
                 }
             }
         }
-        // warp-cooperative ordered folds for high-degree movers
-        unsigned bigm = __ballot_sync(FULL, big);
-        while (bigm) {
-            int l = __ffs(bigm) - 1;
-            bigm &= bigm - 1;
-            int32_t ii = __shfl_sync(FULL, i, l);
-            int32_t aa = __shfl_sync(FULL, a, l);
-            int32_t bb = __shfl_sync(FULL, b, l);
-            int64_t xx = base + l;
-            int64_t e0 = A.off[ii], e1 = A.off[ii + 1];
-            double fa = 0.0, fb = 0.0;
-            for (int64_t c0 = e0; c0 < e1; c0 += 32) {
-                int64_t e = c0 + lane;
-                int32_t c = -1;
-                double w = 0.0;
-                if (e < e1) {
-                    int32_t j = A.nbr[e];
-                    if (j != ii) {
-                        c = live_comm(A, j, xx);
-                        w = A.wts[e];
-                    }
-                }
-                unsigned ma = __ballot_sync(FULL, c == aa);
-                unsigned mb = __ballot_sync(FULL, c == bb && c != aa);
-                for (unsigned mm = ma; mm; mm &= mm - 1)
-                    fa = dadd(fa, __shfl_sync(FULL, w, __ffs(mm) - 1));
-                for (unsigned mm = mb; mm; mm &= mm - 1)
-                    fb = dadd(fb, __shfl_sync(FULL, w, __ffs(mm) - 1));
-            }
-            if (lane == l) {
-                e_a = fa;
-                e_b = fb;
-            }
+        // high-degree movers are folded by a whole warp (k_stage_big), huge
+        // ones by a whole block (k_stage_huge)
+        if (big) {
+            if (A.off[i + 1] - A.off[i] > APPLY_HUGE)
+                A.huge[atomicAdd(A.nhuge, 1ull)] = (int32_t)x;
+            else
+                A.big[atomicAdd(A.nbig, 1ull)] = (int32_t)x;
         }
-        if (mover) {
-            double sw = A.selfw[i], ki = A.k[i];
-            double ta = dadd(dmul(2.0, e_a), dmul(2.0, sw));
-            double tb = dadd(dmul(2.0, e_b), dmul(2.0, sw));
-            if (integral) {
-                atomicAdd(A.w_int + a, -ta);
-                atomicAdd(A.w_int + b, tb);
-                atomicAdd(A.a_tot + a, -ki);
-                atomicAdd(A.a_tot + b, ki);
-            } else {
-                A.ta[x] = ta;
-                A.tb[x] = tb;
-            }
-            atomicSub(A.sizes + a, 1);
-            atomicAdd(A.sizes + b, 1);
-        }
+        if (mover && !big) mover_deltas(A, x, i, a, b, e_a, e_b, integral);
         // independent stages: no stage vertex reads another's assignment, so
         // the scatter can happen here
         if (indep && mover) A.assign[i] = b;
@@ -260,6 +326,8 @@ __global__ void k_stage_scatter(StageArgs A) {
 // One CTA applies a small independent stage: event keys in registers, block
 // radix sort, deltas staged in shared memory, ordered per-community folds and
 // the scatter, in one launch.  Dynamic smem: 2 * SA_THREADS * SA_ITEMS doubles.
+// (SA_ITEMS, the events per thread, shadows the namespace constant.)
+template <int SA_ITEMS>
 __global__ void __launch_bounds__(SA_THREADS) k_stage_apply_small(StageArgs A, int nb) {
     typedef cub::BlockRadixSort<uint32_t, SA_THREADS, SA_ITEMS, int32_t> Sort;
     __shared__ union {
@@ -350,6 +418,9 @@ void ApplyBuffers::alloc(int64_t ta_len, int64_t max_ns, int64_t n, cudaStream_t
     eval2 = dalloc<int32_t>(ne);
     dW = dalloc<double>(ne);
     dA = dalloc<double>(ne);
+    big_cap = max_ns ? max_ns : 1;
+    big = dalloc<int32_t>(2 * big_cap);  // big movers, then huge movers
+    nbig = dalloc<unsigned long long>(2);
     lrun = dalloc<int64_t>(ne);
     lcnt = dalloc<unsigned long long>(1);
     nb = bits_for(n + 1);  // SENTINEL's low nb bits exceed every community id
@@ -359,7 +430,7 @@ void ApplyBuffers::alloc(int64_t ta_len, int64_t max_ns, int64_t n, cudaStream_t
     int dev;
     PLV_CUDA(cudaGetDevice(&dev));
     if (dev_done != dev) {
-        PLV_CUDA(cudaFuncSetAttribute(k_stage_apply_small,
+        PLV_CUDA(cudaFuncSetAttribute(k_stage_apply_small<SA_ITEMS>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(2 * SA_THREADS * SA_ITEMS * sizeof(double))));
         dev_done = dev;
@@ -367,9 +438,11 @@ void ApplyBuffers::alloc(int64_t ta_len, int64_t max_ns, int64_t n, cudaStream_t
 }
 
 void ApplyBuffers::release() {
-    void *ps[] = {ta, tb, ekey, ekey2, eval, eval2, tmp, dW, dA, lrun, lcnt};
+    void *ps[] = {ta, tb, ekey, ekey2, eval, eval2, tmp, dW, dA, lrun, lcnt, big, nbig};
     for (void *p : ps)
         if (p) cudaFree(p);
+    big = nullptr;
+    nbig = nullptr;
     dW = dA = nullptr;
     lrun = nullptr;
     lcnt = nullptr;
@@ -386,13 +459,30 @@ void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {
     bool indep = S.flags & PLV_F_INDEPENDENT;
     bool integral = S.flags & PLV_F_INTEGRAL;
     if (indep && !integral && S.ns <= SMALL_APPLY_MAX) {
-        k_stage_apply_small<<<1, SA_THREADS, 2 * SA_THREADS * SA_ITEMS * sizeof(double), st>>>(
-            S, B.nb);
+        // events per thread sized to the stage (2 events per vertex)
+        if (2 * S.ns <= SA_THREADS)
+            k_stage_apply_small<1><<<1, SA_THREADS, 2 * SA_THREADS * sizeof(double), st>>>(S, B.nb);
+        else if (2 * S.ns <= 4 * SA_THREADS)
+            k_stage_apply_small<4><<<1, SA_THREADS, 8 * SA_THREADS * sizeof(double), st>>>(S, B.nb);
+        else
+            k_stage_apply_small<SA_ITEMS><<<1, SA_THREADS, 2 * SA_THREADS * SA_ITEMS * sizeof(double),
+                                            st>>>(S, B.nb);
         PLV_LAUNCH_CHECK();
         return;
     }
+    S.big = B.big;
+    S.nbig = B.nbig;
+    S.huge = B.big + B.big_cap;
+    S.nhuge = B.nbig + 1;
+    if (!indep) PLV_CUDA(cudaMemsetAsync(B.nbig, 0, 2 * sizeof(unsigned long long), st));
     k_stage_prep<<<grid_for((S.ns + 31) / 32 * 32, 256, 148 * 16), 256, 0, st>>>(S);
     PLV_LAUNCH_CHECK();
+    if (!indep) {
+        k_stage_big<<<148 * 8, 256, 0, st>>>(S);
+        PLV_LAUNCH_CHECK();
+        k_stage_huge<<<148 * 2, 256, 0, st>>>(S);
+        PLV_LAUNCH_CHECK();
+    }
     if (!integral) {
         int64_t ne = 2 * S.ns;
         size_t bytes = B.bytes;

@@ -1,25 +1,38 @@
 // decide.cu -- decide_moves (PL/_kernels.pyx:21-101) on device.
 //
+// The reference sums e_{i->C} per neighbour community in adjacency order
+// (a sequential left fold per community) and takes the argmax of the Eq. 4
+// gain under (gain desc, label asc), then applies the singleton-pair guard.
 // Vertices of a stage are degree-binned once per plan:
-//   tier 0  deg <= 8      thread per vertex, candidate list in registers
-//   tier 1  deg <= 128    warp per vertex, hash table in shared memory
-//   tier 2  deg <= 2048   block per vertex, hash table in shared memory
-//   tier 3  larger (hubs) sort-based: every hub entry becomes a
-//           (hub, community) key; one stable radix sort over all hubs of the
-//           stage groups each community's entries in adjacency order, and a
-//           block per hub folds the runs in parallel (runs of different
-//           communities are independent; each run is the reference's
-//           sequential left fold, so the critical path is the longest run,
-//           not the row).
-// Tiers 1-2 fold a 32-entry chunk at a time: lanes with the same community
-// are grouped with __match_any_sync and the group leader adds their weights
-// in lane (= adjacency) order; chunks are processed in order.  Integral graphs
-// (every weight an integer, 2m < 2^52) may fold in any order and use atomics.
+//   tier 0  deg <= 8      thread per vertex, candidates in registers, folds
+//                         in adjacency order (exact by construction)
+//   tier 1  deg <= 128    warp per vertex, shared-memory hash table, 32-entry
+//                         chunks folded in lane order (exact by construction)
+//   tier 2  deg <= 2048   block per vertex, shared-memory table  } certified
+//   tier 3  larger (hubs) all entries of the stage's hubs at once,} parallel
+//                         global hash tables                       } sums
+// Certified parallel sums (tiers 2-3).  Reproducing a sequential fold needs
+// its additions in order -- a dependent DADD chain of 8.2 cycles per add on
+// B200 -- so tiers 2-3 first sum every community in ANY order with atomics,
+// along with its term count L.  Both sums are within 2 gamma_{L-1} * sum of
+// each other (gamma_k = k u / (1 - k u), u = 2^-53), which bounds how far
+// every computed gain can be from the reference's.  The decision is kept only
+// when it is certain: the best candidate's lower bound beats every other
+// candidate's (and "stay"'s) upper bound.  Otherwise -- and whenever the vertex
+// moves, because apply needs e_{i->c_old} and e_{i->best} bit-exact -- the
+// few candidates whose intervals overlap are re-folded exactly in adjacency
+// order (ordered block compaction of the row, then one thread adds) and the
+// decision is taken on the exact values.  The result is the reference's
+// decision and the reference's e values, bit for bit.  Integral graphs (all
+// weights integers, 2m < 2^52) are exact in any order and skip the check.
 #include "localmove.cuh"
 #include "csr.cuh"
 #include <cub/cub.cuh>
 
 namespace plv {
+
+constexpr double U_RND = 1.1102230246251565e-16;  // 2^-53
+constexpr int HBLK = 1024;                         // threads per hub block
 
 __device__ __forceinline__ int64_t LBL(const int32_t *labels, int32_t c) {
     return labels ? (int64_t)labels[c] : (int64_t)c;
@@ -39,11 +52,32 @@ __device__ __forceinline__ double gain_of(double e_c, double e_old, double m, do
     return dadd(t2, ddiv(t5, four_m_sq));
 }
 
-__device__ __forceinline__ uint32_t hslot(int32_t c, uint32_t mask) {
-    return ((uint32_t)c * 0x9E3779B1u) & mask;
+// |sequential - any-order| bound for a sum of L positive terms near F.
+__device__ __forceinline__ double sum_err(double F, int32_t L) {
+    return L > 1 ? 2.01 * (double)(L - 1) * U_RND * F : 0.0;
 }
 
-// Find-or-insert c; tables start cleared to key -1 / value 0.0.
+// Bound on |gain from exact sums - gain from any-order sums| (see header):
+// the sums' error divided by m plus the operations' own rounding.
+__device__ __forceinline__ double gain_slack(double Fc, int32_t Lc, double Fo, int32_t Lo,
+                                             double m, double g) {
+    return 1.01 * ((sum_err(Fc, Lc) + sum_err(Fo, Lo)) / m) +
+           8.0 * U_RND * (fabs(Fc - Fo) / m + fabs(g)) + 1e-300;
+}
+
+// Table slot of community c: murmur3's 32-bit finaliser (community ids of a
+// hub's neighbours share low bits, so a plain multiplicative hash clusters).
+__device__ __forceinline__ uint32_t hslot(int32_t c, uint32_t mask) {
+    uint32_t h = (uint32_t)c;
+    h ^= h >> 16;
+    h *= 0x85EBCA6Bu;
+    h ^= h >> 13;
+    h *= 0xC2B2AE35u;
+    h ^= h >> 16;
+    return h & mask;
+}
+
+// Find-or-insert c; tables start cleared to key -1.
 __device__ __forceinline__ uint32_t probe_insert(int32_t *keys, int32_t c, uint32_t mask) {
     uint32_t s = hslot(c, mask);
     while (true) {
@@ -80,56 +114,54 @@ __device__ __forceinline__ void finish_vertex(const DecideArgs &A, int64_t x, in
     A.out_e_best[x] = moved ? be : e_old;
 }
 
-// Warp-level argmax reduction under `better`; result valid in every lane.
-__device__ __forceinline__ void warp_best(double &bg, int64_t &bl, int32_t &bc, double &be) {
+struct Best {
+    double g;
+    int64_t l;
+    int32_t c;
+    double e;
+    int32_t n;  // term count of e (certification)
+};
+
+__device__ __forceinline__ void consider(Best &b, double g, int64_t l, int32_t c, double e,
+                                         int32_t n) {
+    if (better(g, l, b.g, b.l)) b = Best{g, l, c, e, n};
+}
+
+__device__ __forceinline__ void warp_best(Best &b) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        double g2 = __shfl_xor_sync(FULL, bg, o);
-        int64_t l2 = __shfl_xor_sync(FULL, bl, o);
-        int32_t c2 = __shfl_xor_sync(FULL, bc, o);
-        double e2 = __shfl_xor_sync(FULL, be, o);
-        if (better(g2, l2, bg, bl)) {
-            bg = g2;
-            bl = l2;
-            bc = c2;
-            be = e2;
-        }
+        Best o2;
+        o2.g = __shfl_xor_sync(FULL, b.g, o);
+        o2.l = __shfl_xor_sync(FULL, b.l, o);
+        o2.c = __shfl_xor_sync(FULL, b.c, o);
+        o2.e = __shfl_xor_sync(FULL, b.e, o);
+        o2.n = __shfl_xor_sync(FULL, b.n, o);
+        consider(b, o2.g, o2.l, o2.c, o2.e, o2.n);
     }
 }
 
+template <int NT>
 struct BestSmem {
-    double g[BLK / 32];
-    int64_t l[BLK / 32];
-    int32_t c[BLK / 32];
-    double e[BLK / 32];
+    Best w[NT / 32];
+    Best out;
 };
 
-// Block-level argmax (BLK threads); the result is valid in thread 0.
-__device__ __forceinline__ void block_best(BestSmem &S, double &bg, int64_t &bl, int32_t &bc,
-                                           double &be, int64_t l0, int32_t c0) {
+// Block argmax; the result is returned to every thread.
+template <int NT>
+__device__ __forceinline__ Best block_best(BestSmem<NT> &S, Best b) {
     int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    warp_best(bg, bl, bc, be);
-    if (lane == 0) {
-        S.g[wid] = bg;
-        S.l[wid] = bl;
-        S.c[wid] = bc;
-        S.e[wid] = be;
-    }
+    warp_best(b);
+    if (lane == 0) S.w[wid] = b;
     __syncthreads();
     if (wid == 0) {
-        if (lane < BLK / 32) {
-            bg = S.g[lane];
-            bl = S.l[lane];
-            bc = S.c[lane];
-            be = S.e[lane];
-        } else {
-            bg = 0.0;
-            bl = l0;
-            bc = c0;
-            be = 0.0;
-        }
-        warp_best(bg, bl, bc, be);
+        Best c = lane < NT / 32 ? S.w[lane] : S.w[0];
+        warp_best(c);
+        if (lane == 0) S.out = c;
     }
+    __syncthreads();
+    Best r = S.out;
+    __syncthreads();
+    return r;
 }
 
 // ------------------------------------------------------------ tier 0
@@ -180,24 +212,16 @@ __global__ void __launch_bounds__(256) k_decide_t0(DecideArgs A, const int32_t *
             if (s < nc && keys[s] == c_old) e_old = vals[s];
         double ki = A.k[i];
         double a_old_excl = dsub(A.a_tot[c_old], ki);
-        double bg = 0.0, be = 0.0;
-        int32_t bc = c_old;
-        int64_t bl = LBL(A.labels, c_old);
+        Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
 #pragma unroll
         for (int s = 0; s < T0_MAXD; s++) {
             if (s < nc && keys[s] != c_old) {
                 int32_t c = keys[s];
-                double g = gain_of(vals[s], e_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq);
-                int64_t l = LBL(A.labels, c);
-                if (better(g, l, bg, bl)) {
-                    bg = g;
-                    bl = l;
-                    bc = c;
-                    be = vals[s];
-                }
+                consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq),
+                         LBL(A.labels, c), c, vals[s], 0);
             }
         }
-        finish_vertex(A, x, c_old, e_old, bg, bc, be);
+        finish_vertex(A, x, c_old, e_old, b.g, b.c, b.e);
     }
     if (A.cand) {
         typedef cub::BlockReduce<unsigned long long, 256> BR;
@@ -210,19 +234,13 @@ __global__ void __launch_bounds__(256) k_decide_t0(DecideArgs A, const int32_t *
 // Fold one 32-entry chunk (c, w per lane; c = -1 for none) into a table in
 // adjacency order.  wb: the chunk's 32 weights staged in lane order.
 __device__ __forceinline__ void fold_chunk(int32_t *keys, double *vals, uint32_t mask, int32_t c,
-                                           const double *wb, int lane, int integral) {
+                                           const double *wb, int lane) {
     unsigned grp = __match_any_sync(FULL, c);
     if (c >= 0 && lane == __ffs(grp) - 1) {
         uint32_t s = probe_insert(keys, c, mask);
-        if (integral) {
-            double v = 0.0;
-            for (unsigned g = grp; g; g &= g - 1) v = dadd(v, wb[__ffs(g) - 1]);
-            atomicAdd(vals + s, v);  // any order is exact for integral weights
-        } else {
-            double v = vals[s];  // 0.0 when fresh
-            for (unsigned g = grp; g; g &= g - 1) v = dadd(v, wb[__ffs(g) - 1]);
-            vals[s] = v;
-        }
+        double v = vals[s];  // 0.0 when fresh
+        for (unsigned g = grp; g; g &= g - 1) v = dadd(v, wb[__ffs(g) - 1]);
+        vals[s] = v;
     }
 }
 
@@ -266,7 +284,7 @@ __global__ void __launch_bounds__(T1_WARPS * 32) k_decide_t1(DecideArgs A, const
             }
             wb[lane] = w;
             __syncwarp();
-            fold_chunk(keys, vals, mask, c, wb, lane, A.integral);
+            fold_chunk(keys, vals, mask, c, wb, lane);
             __syncwarp();
         }
         double e_old = 0.0;
@@ -277,27 +295,19 @@ __global__ void __launch_bounds__(T1_WARPS * 32) k_decide_t1(DecideArgs A, const
         e_old = __shfl_sync(FULL, e_old, 0);
         double ki = A.k[i];
         double a_old_excl = dsub(A.a_tot[c_old], ki);
-        double bg = 0.0, be = 0.0;
-        int32_t bc = c_old;
-        int64_t bl = LBL(A.labels, c_old);
+        Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
         int nc = 0;
         for (uint32_t s = lane; s < ts; s += 32) {
             int32_t c = keys[s];
             if (c < 0) continue;
             nc++;
             if (c == c_old) continue;
-            double g = gain_of(vals[s], e_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq);
-            int64_t l = LBL(A.labels, c);
-            if (better(g, l, bg, bl)) {
-                bg = g;
-                bl = l;
-                bc = c;
-                be = vals[s];
-            }
+            consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq),
+                     LBL(A.labels, c), c, vals[s], 0);
         }
-        warp_best(bg, bl, bc, be);
+        warp_best(b);
         my_cand += nc;
-        if (lane == 0) finish_vertex(A, x, c_old, e_old, bg, bc, be);
+        if (lane == 0) finish_vertex(A, x, c_old, e_old, b.g, b.c, b.e);
         __syncwarp();
     }
     if (A.cand) {
@@ -306,32 +316,302 @@ __global__ void __launch_bounds__(T1_WARPS * 32) k_decide_t1(DecideArgs A, const
     }
 }
 
+// ------------------------------------------------ certification machinery
+
+template <int NT>
+struct CertSmem {
+    BestSmem<NT> bs;
+    typename cub::BlockScan<int, NT>::TempStorage scan;
+    typename cub::BlockReduce<unsigned long long, NT>::TempStorage red;
+    int32_t cidx[NT];  // ordered compaction of matching entries
+    double cw[NT];
+    int32_t N[MAXS + 2];  // communities to fold exactly (N[0] = c_old)
+    double acc[MAXS + 2];
+    double f_old;
+    int32_t l_old;
+    int nn, nS, flag;  // flag: 1 stay overlaps, 2 overflow
+    unsigned long long ncand;
+};
+
+// Accumulate one entry (c, w) with warp aggregation: lanes with the same
+// community combine (any order) before one atomic per group.
+__device__ __forceinline__ void accum_entry(int32_t *keys, double *vals, int32_t *cnt,
+                                            uint32_t mask, int32_t c, double w, int lane) {
+    unsigned grp = __match_any_sync(FULL, c);
+    double v = 0.0;
+    for (unsigned g = grp; g; g &= g - 1) v = dadd(v, __shfl_sync(grp, w, __ffs(g) - 1));
+    if (c >= 0 && lane == __ffs(grp) - 1) {
+        uint32_t s = probe_insert(keys, c, mask);
+        atomicAdd(vals + s, v);
+        atomicAdd(cnt + s, __popc(grp));
+    }
+}
+
+// Passes over the (any-order) table of vertex i: the best candidate on the
+// approximate gains, then the candidates whose intervals overlap it.  Slots
+// are cleared in the second pass when `clear`.  Returns the approximate best.
+template <int NT>
+__device__ Best certify_table(const DecideArgs &A, int32_t c_old, double ki, int32_t *keys,
+                              double *vals, int32_t *cnt, uint32_t ts, CertSmem<NT> &S,
+                              bool clear) {
+    const int tid = threadIdx.x;
+    const uint32_t mask = ts - 1;
+    if (tid == 0) {
+        int s = probe_find(keys, c_old, mask);
+        S.f_old = s >= 0 ? vals[s] : 0.0;
+        S.l_old = s >= 0 ? cnt[s] : 0;
+        S.nS = 0;
+        S.flag = 0;
+    }
+    __syncthreads();
+    const double f_old = S.f_old;
+    const int32_t l_old_n = S.l_old;
+    const double a_old_excl = dsub(A.a_tot[c_old], ki);
+    const int64_t l_old = LBL(A.labels, c_old);
+    Best b{0.0, l_old, c_old, 0.0, 0};
+    for (uint32_t s = tid; s < ts; s += NT) {
+        int32_t c = keys[s];
+        if (c < 0 || c == c_old) continue;
+        double F = vals[s];
+        consider(b, gain_of(F, f_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq),
+                 LBL(A.labels, c), c, F, cnt[s]);
+    }
+    b = block_best<NT>(S.bs, b);
+    const bool stay_best = b.c == c_old;
+    const double lower = stay_best ? 0.0 : b.g - gain_slack(b.e, b.n, f_old, l_old_n, A.m, b.g);
+    unsigned long long nc = 0;
+    for (uint32_t s = tid; s < ts; s += NT) {
+        int32_t c = keys[s];
+        if (c < 0) continue;
+        nc++;
+        if (c != c_old && c != b.c) {
+            double F = vals[s];
+            double g = gain_of(F, f_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq);
+            if (g + gain_slack(F, cnt[s], f_old, l_old_n, A.m, g) >= lower) {
+                int k = atomicAdd(&S.nS, 1);
+                if (k < MAXS)
+                    S.N[2 + k] = c;
+                else
+                    atomicOr(&S.flag, 2);
+            }
+        }
+        if (clear) {
+            keys[s] = -1;
+            vals[s] = 0.0;
+            cnt[s] = 0;
+        }
+    }
+    if (tid == 0) {
+        if (!stay_best && lower <= 0.0) S.flag |= 1;  // "stay" (exact gain 0) overlaps
+        S.ncand = 0;
+    }
+    __syncthreads();
+    unsigned long long tot = cub::BlockReduce<unsigned long long, NT>(S.red).Sum(nc);
+    if (tid == 0) S.ncand = tot;
+    __syncthreads();
+    return b;
+}
+
+// Exact left folds (adjacency order) of the communities S.N[0..S.nn) over the
+// row of i: ordered block compaction of the matching entries, then thread 0
+// adds them in order.  Results in S.acc.
+template <int NT>
+__device__ void exact_folds(const DecideArgs &A, int32_t i, CertSmem<NT> &S) {
+    const int tid = threadIdx.x;
+    const int64_t e0 = A.off[i], e1 = A.off[i + 1];
+    const int nn = S.nn;
+    if (tid < nn) S.acc[tid] = 0.0;
+    __syncthreads();
+    for (int64_t base = e0; base < e1; base += NT) {
+        int64_t e = base + tid;
+        int idx = -1;
+        double w = 0.0;
+        if (e < e1) {
+            int32_t j = A.nbr[e];
+            if (j != i) {
+                int32_t c = A.assign[j];
+                for (int t = 0; t < nn; t++)
+                    if (S.N[t] == c) {
+                        idx = t;
+                        break;
+                    }
+                if (idx >= 0) w = A.wts[e];
+            }
+        }
+        int pos, total;
+        cub::BlockScan<int, NT>(S.scan).ExclusiveSum(idx >= 0 ? 1 : 0, pos, total);
+        if (idx >= 0) {
+            S.cidx[pos] = idx;
+            S.cw[pos] = w;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double a0 = S.acc[0], a1 = nn > 1 ? S.acc[1] : 0.0;
+            for (int t = 0; t < total; t++) {
+                int k = S.cidx[t];
+                double v = S.cw[t];
+                if (k == 0)
+                    a0 = dadd(a0, v);
+                else if (k == 1)
+                    a1 = dadd(a1, v);
+                else
+                    S.acc[k] = dadd(S.acc[k], v);
+            }
+            S.acc[0] = a0;
+            if (nn > 1) S.acc[1] = a1;
+        }
+        __syncthreads();
+    }
+}
+
+// After certify_table: either finish (certain, no move) or fold the needed
+// communities exactly and decide on exact values.  Returns false on overflow
+// (more than MAXS overlapping candidates): the caller must decide exactly.
+template <int NT>
+__device__ bool resolve(const DecideArgs &A, int64_t x, int32_t i, int32_t c_old, double ki,
+                        const Best &b, CertSmem<NT> &S) {
+    const int tid = threadIdx.x;
+    if (S.flag & 2) return false;
+    const bool certain = S.nS == 0 && !(S.flag & 1);
+    if (certain) {
+        bool moved = b.c != c_old;  // certain: exact gain > 0 and the best
+        if (moved && A.sizes[c_old] == 1 && A.sizes[b.c] == 1 &&
+            LBL(A.labels, b.c) > LBL(A.labels, c_old))
+            moved = false;
+        if (!moved) {
+            if (tid == 0) finish_vertex(A, x, c_old, S.f_old, 0.0, c_old, 0.0);
+            __syncthreads();
+            return true;
+        }
+    }
+    if (tid == 0) {
+        S.N[0] = c_old;
+        int nn = 1;
+        if (b.c != c_old) S.N[nn++] = b.c;
+        for (int t = 0; t < S.nS; t++) S.N[nn++] = S.N[2 + t];
+        S.nn = nn;
+    }
+    __syncthreads();
+    exact_folds<NT>(A, i, S);
+    if (tid == 0) {
+        double a_old_excl = dsub(A.a_tot[c_old], ki);
+        Best e{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
+        for (int t = 1; t < S.nn; t++) {
+            int32_t c = S.N[t];
+            consider(e, gain_of(S.acc[t], S.acc[0], A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq),
+                     LBL(A.labels, c), c, S.acc[t], 0);
+        }
+        finish_vertex(A, x, c_old, S.acc[0], e.g, e.c, e.e);
+    }
+    __syncthreads();
+    return true;
+}
+
 // ------------------------------------------------------------ tier 2
+
+// Exact fallback: in-order fold into the (clean) table, communities split
+// over the warps so each community sees one ordered left fold, then the exact
+// argmax.  Leaves the table clean.
+__device__ void t2_exact(const DecideArgs &A, int64_t x, int32_t i, int32_t c_old, double ki,
+                         int32_t *keys, double *vals, uint32_t mask, int32_t *cbuf, double *wbuf,
+                         CertSmem<BLK> &S) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int64_t e0 = A.off[i], e1 = A.off[i + 1];
+    for (int64_t base = e0; base < e1; base += BLK) {
+        int64_t e = base + tid;
+        int32_t c = -1;
+        double w = 0.0;
+        if (e < e1) {
+            int32_t j = A.nbr[e];
+            if (j != i) {
+                c = A.assign[j];
+                w = A.wts[e];
+            }
+        }
+        cbuf[tid] = c;
+        wbuf[tid] = w;
+        __syncthreads();
+        int nsub = (int)((e1 - base + 31) / 32);
+        if (nsub > BLK / 32) nsub = BLK / 32;
+        for (int sc = 0; sc < nsub; sc++) {
+            int32_t cc = cbuf[sc * 32 + lane];
+            bool mine = cc >= 0 && (int)(((uint32_t)cc * 0x85EBCA6Bu) >> 29) == wid;
+            if (__any_sync(FULL, mine))
+                fold_chunk(keys, vals, mask, mine ? cc : -1, wbuf + sc * 32, lane);
+            __syncwarp();
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        int s = probe_find(keys, c_old, mask);
+        S.f_old = s >= 0 ? vals[s] : 0.0;
+    }
+    __syncthreads();
+    const double e_old = S.f_old, a_old_excl = dsub(A.a_tot[c_old], ki);
+    Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
+    for (uint32_t s = tid; s <= mask; s += BLK) {
+        int32_t c = keys[s];
+        if (c >= 0 && c != c_old)
+            consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq),
+                     LBL(A.labels, c), c, vals[s], 0);
+    }
+    b = block_best<BLK>(S.bs, b);
+    for (uint32_t s = tid; s <= mask; s += BLK) {
+        keys[s] = -1;
+        vals[s] = 0.0;
+    }
+    if (tid == 0) finish_vertex(A, x, c_old, e_old, b.g, b.c, b.e);
+    __syncthreads();
+}
 
 __global__ void __launch_bounds__(BLK) k_decide_t2(DecideArgs A, const int32_t *list, int64_t cnt) {
     extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ CertSmem<BLK> S;
     __shared__ int32_t cbuf[BLK];
     __shared__ double wbuf[BLK];
-    __shared__ BestSmem bs;
-    __shared__ double s_e_old;
-    int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
     double *vals = reinterpret_cast<double *>(dsm);
     int32_t *keys = reinterpret_cast<int32_t *>(dsm + sizeof(double) * T2_TS);
+    int32_t *cntt = keys + T2_TS;
     unsigned long long my_cand = 0;
+    for (uint32_t s = tid; s < T2_TS; s += BLK) {
+        keys[s] = -1;
+        vals[s] = 0.0;
+        cntt[s] = 0;
+    }
+    __syncthreads();
     for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
-        int64_t x = list[q];
-        int32_t i = A.subset[x];
-        int32_t c_old = A.assign[i];
-        int64_t e0 = A.off[i], e1 = A.off[i + 1];
-        int64_t deg = e1 - e0;
+        const int64_t x = list[q];
+        const int32_t i = A.subset[x];
+        const int32_t c_old = A.assign[i];
+        const int64_t e0 = A.off[i], e1 = A.off[i + 1];
+        const int64_t deg = e1 - e0;
         uint32_t ts = 64;
         while (ts < (uint64_t)(deg + deg / 2 + 2)) ts <<= 1;
-        uint32_t mask = ts - 1;
-        for (uint32_t s = tid; s < ts; s += BLK) {
-            keys[s] = -1;
-            vals[s] = 0.0;
+        const uint32_t mask = ts - 1;
+        const double ki = A.k[i];
+        if (A.integral) {
+            // exact in any order: accumulate, then the plain argmax
+            for (int64_t base = e0; base < e1; base += BLK) {
+                int64_t e = base + tid;
+                int32_t c = -1;
+                double w = 0.0;
+                if (e < e1) {
+                    int32_t j = A.nbr[e];
+                    if (j != i) {
+                        c = A.assign[j];
+                        w = A.wts[e];
+                    }
+                }
+                accum_entry(keys, vals, cntt, mask, c, w, lane);
+            }
+            __syncthreads();
+            Best b = certify_table<BLK>(A, c_old, ki, keys, vals, cntt, ts, S, true);
+            my_cand += tid == 0 ? S.ncand : 0;
+            if (tid == 0) finish_vertex(A, x, c_old, S.f_old, b.g, b.c, b.e);
+            __syncthreads();
+            continue;
         }
-        __syncthreads();
         for (int64_t base = e0; base < e1; base += BLK) {
             int64_t e = base + tid;
             int32_t c = -1;
@@ -343,116 +623,59 @@ __global__ void __launch_bounds__(BLK) k_decide_t2(DecideArgs A, const int32_t *
                     w = A.wts[e];
                 }
             }
-            cbuf[tid] = c;
-            wbuf[tid] = w;
-            __syncthreads();
-            if (A.integral) {
-                // every warp folds its own sub-chunk; order is irrelevant
-                fold_chunk(keys, vals, mask, c, wbuf + wid * 32, lane, 1);
-            } else {
-                // communities are partitioned over the warps; each warp walks
-                // the sub-chunks in order and folds only its own communities,
-                // so every community still sees a single in-order left fold
-                int nsub = (int)((e1 - base + 31) / 32);
-                if (nsub > BLK / 32) nsub = BLK / 32;
-                for (int sc = 0; sc < nsub; sc++) {
-                    int32_t cc = cbuf[sc * 32 + lane];
-                    bool mine = cc >= 0 && (int)(((uint32_t)cc * 0x85EBCA6Bu) >> 29) == wid;
-                    if (__any_sync(FULL, mine))
-                        fold_chunk(keys, vals, mask, mine ? cc : -1, wbuf + sc * 32, lane, 0);
-                    __syncwarp();
-                }
-            }
-            __syncthreads();
-        }
-        if (tid == 0) {
-            int s = probe_find(keys, c_old, mask);
-            s_e_old = s >= 0 ? vals[s] : 0.0;
+            accum_entry(keys, vals, cntt, mask, c, w, lane);
         }
         __syncthreads();
-        double e_old = s_e_old;
-        double ki = A.k[i];
-        double a_old_excl = dsub(A.a_tot[c_old], ki);
-        int64_t l_old = LBL(A.labels, c_old);
-        double bg = 0.0, be = 0.0;
-        int32_t bc = c_old;
-        int64_t bl = l_old;
-        int nc = 0;
-        for (uint32_t s = tid; s < ts; s += BLK) {
-            int32_t c = keys[s];
-            if (c < 0) continue;
-            nc++;
-            if (c == c_old) continue;
-            double g = gain_of(vals[s], e_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq);
-            int64_t l = LBL(A.labels, c);
-            if (better(g, l, bg, bl)) {
-                bg = g;
-                bl = l;
-                bc = c;
-                be = vals[s];
-            }
-        }
-        my_cand += nc;
-        block_best(bs, bg, bl, bc, be, l_old, c_old);
-        if (tid == 0) finish_vertex(A, x, c_old, e_old, bg, bc, be);
-        __syncthreads();
+        Best b = certify_table<BLK>(A, c_old, ki, keys, vals, cntt, ts, S, true);
+        my_cand += tid == 0 ? S.ncand : 0;
+        if (!resolve<BLK>(A, x, i, c_old, ki, b, S))
+            t2_exact(A, x, i, c_old, ki, keys, vals, mask, cbuf, wbuf, S);
     }
-    if (A.cand) {
-        typedef cub::BlockReduce<unsigned long long, BLK> BR;
-        __shared__ typename BR::TempStorage tmp;
-        unsigned long long tot = BR(tmp).Sum(my_cand);
-        if (threadIdx.x == 0 && tot) atomicAdd(A.cand, tot);
-    }
+    if (A.cand && tid == 0 && my_cand) atomicAdd(A.cand, my_cand);
 }
 
 // ------------------------------------------------------------ tier 3 (hubs)
 
-// key = (hub << cb) | community, val = entry index within the hub row.  A
-// self-loop entry gets the community id `nskip` (>= n) and is ignored.
-__global__ void k_hub_keys(DecideArgs A, const int32_t *list, const int64_t *eoff, int64_t nh,
-                           int64_t E, int cb, int32_t nskip, uint64_t *key, int32_t *val) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < E;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t lo = 0, hi = nh;  // largest q with eoff[q] <= t
-        while (hi - lo > 1) {
-            int64_t mid = (lo + hi) >> 1;
-            if (eoff[mid] <= t)
-                lo = mid;
-            else
-                hi = mid;
-        }
-        int32_t i = A.subset[list[lo]];
-        int64_t loc = t - eoff[lo];
-        int32_t j = A.nbr[A.off[i] + loc];
-        int32_t c = (j == i) ? nskip : A.assign[j];
-        key[t] = ((uint64_t)lo << cb) | (uint32_t)c;
-        val[t] = (int32_t)loc;
-    }
-}
+constexpr int HSB = 256;      // threads per hub pass block
+constexpr int HSLICE = 2048;  // candidate slots per hub pass block
+constexpr int HCPAD = 32;     // hub candidate counters one 128-byte line apart
 
-// Sequential fold of the run starting at sorted position p: every entry of
-// one community of the hub row starting at e0, in adjacency order.  Loads are
-// batched eight at a time so only the additions form the dependency chain.
-__device__ __forceinline__ double fold_hub_run(const uint64_t *key, const int32_t *val,
-                                               const double *wts, int64_t e0, int64_t p,
-                                               int64_t hi) {
-    const uint64_t k0 = key[p];
-    double v = 0.0;
+// Per-stage hub scratch (device pointers; hub index q is stage-local).
+struct HubScratch {
+    int32_t *cand;   // candidate slot lists, laid out like the table slices
+    int32_t *ncand;  // [nh] candidates per hub      } one zeroed block
+    int32_t *nS;     // [nh] overlapping candidates  } of 3 * max_hubs
+    int32_t *flag;   // [nh] 1 stay overlaps, 2 overflow
+    int32_t *S;      // [nh * MAXS] overlapping communities
+    Best *part;      // [nh * slices] pass-1 partial bests
+    Best *best;      // [nh]
+    double *fold;    // [nh] any-order e_{i->c_old}
+    int32_t *lold;   // [nh] its term count
+    int slices;
+    int64_t nh;
+};
+
+__device__ __forceinline__ uint32_t probe_insert_f(int32_t *keys, int32_t c, uint32_t mask,
+                                                   bool *fresh) {
+    uint32_t s = hslot(c, mask);
     while (true) {
-        double w[8];
-        bool ok[8];
-#pragma unroll
-        for (int u = 0; u < 8; u++) {
-            int64_t q = p + u;
-            ok[u] = q < hi && key[q] == k0;
-            w[u] = ok[u] ? wts[e0 + val[q]] : 0.0;
+        int32_t k = keys[s];
+        if (k == c) {
+            *fresh = false;
+            return s;
         }
-#pragma unroll
-        for (int u = 0; u < 8; u++) {
-            if (!ok[u]) return v;
-            v = dadd(v, w[u]);
+        if (k == -1) {
+            int32_t old = atomicCAS(keys + s, -1, c);
+            if (old == -1) {
+                *fresh = true;
+                return s;
+            }
+            if (old == c) {
+                *fresh = false;
+                return s;
+            }
         }
-        p += 8;
+        s = (s + 1) & mask;
     }
 }
 
@@ -469,163 +692,243 @@ __device__ __forceinline__ int64_t hub_of(const int64_t *eoff, int64_t nh, int64
     return lo;
 }
 
-// Sorted range [a, b) of hub q's entries with key `want`.
-__device__ __forceinline__ void key_range(const uint64_t *key, int64_t lo, int64_t hi,
-                                          uint64_t want, int64_t *a_out, int64_t *b_out) {
-    int64_t a = lo, b = hi;
-    while (a < b) {
-        int64_t mid = (a + b) >> 1;
-        if (key[mid] < want)
-            a = mid + 1;
-        else
-            b = mid;
+// Every entry of every hub of the stage: any-order sums into the hub's slice
+// of the global table (warp-aggregated per (hub, community)).
+__global__ void k_hub_accum(DecideArgs A, const int32_t *list, const int64_t *eoff,
+                            const int64_t *toff, int64_t nh, int64_t E, int32_t *hkeys,
+                            double *hvals, int32_t *hcnt, HubScratch H) {
+    const int lane = threadIdx.x & 31;
+    // warp-uniform loop: the whole warp takes 32 consecutive entries per step
+    for (int64_t w0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); w0 < E;
+         w0 += (int64_t)gridDim.x * blockDim.x) {
+        int64_t t = w0 + lane;
+        int32_t c = -1;
+        double w = 0.0;
+        int64_t q = 0;
+        if (t < E) {
+            q = hub_of(eoff, nh, t);
+            int32_t i = A.subset[list[q]];
+            int64_t e = A.off[i] + (t - eoff[q]);
+            int32_t j = A.nbr[e];
+            if (j != i) {
+                c = A.assign[j];
+                w = A.wts[e];
+            }
+        }
+        // group lanes by (hub, community)
+        uint64_t key = c >= 0 ? (((uint64_t)q << 32) | (uint32_t)c) : ~0ull;
+        unsigned grp = __match_any_sync(FULL, key);
+        double v = 0.0;
+        for (unsigned g = grp; g; g &= g - 1) v = dadd(v, __shfl_sync(grp, w, __ffs(g) - 1));
+        const bool leader = c >= 0 && lane == __ffs(grp) - 1;
+        const int64_t base = toff[q];
+        bool fresh = false;
+        uint32_t s = 0;
+        if (leader) {
+            uint32_t mask = (uint32_t)(toff[q + 1] - base - 1);
+            s = probe_insert_f(hkeys + base, c, mask, &fresh);
+            atomicAdd(hvals + base + s, v);
+            atomicAdd(hcnt + base + s, __popc(grp));
+        }
+        // append fresh slots to the hub's candidate list: one counter atomic
+        // per (warp, hub), counters one cache line apart
+        unsigned fm = __ballot_sync(FULL, fresh);
+        if (fm) {
+            unsigned same = __match_any_sync(FULL, fresh ? q : -1ll) & fm;
+            int rank = __popc(same & ((1u << lane) - 1));
+            int first = __ffs(same) - 1;
+            int pos = 0;
+            if (fresh && lane == first) pos = atomicAdd(H.ncand + q * HCPAD, __popc(same));
+            pos = __shfl_sync(FULL, pos, fresh ? first : lane);
+            if (fresh) H.cand[base + pos + rank] = (int32_t)s;
+        }
     }
-    int64_t c = a, d = hi;
-    while (c < d) {
-        int64_t mid = (c + d) >> 1;
-        if (key[mid] <= want)
-            c = mid + 1;
-        else
-            d = mid;
-    }
-    *a_out = a;
-    *b_out = c;
 }
 
-constexpr int SHORT_RUN = 32;  // longer runs are folded by a whole block
-
-// e_{i->c_old} of every hub: its c_old run, one block per hub.
-__global__ void __launch_bounds__(BLK) k_hub_eold(DecideArgs A, const int32_t *list,
-                                                 const int64_t *eoff, const uint64_t *key,
-                                                 const int32_t *val, int cb, double *eold) {
-    __shared__ double sb[2 * FOLD_CH];
-    __shared__ int64_t s_a, s_b;
+// Pass 1, block (hub q, slice y): best candidate of the slice on the
+// any-order sums.  Slice 0 also records the hub's e_{i->c_old} sum.
+__global__ void __launch_bounds__(HSB) k_hub_pass1(DecideArgs A, const int32_t *list,
+                                                  const int64_t *toff, const int32_t *hkeys,
+                                                  const double *hvals, const int32_t *hcnt,
+                                                  HubScratch H) {
+    __shared__ BestSmem<HSB> bs;
+    __shared__ double s_fo;
+    __shared__ int32_t s_lo;
     const int64_t q = blockIdx.x;
     const int32_t i = A.subset[list[q]];
     const int32_t c_old = A.assign[i];
+    const int64_t base = toff[q];
+    const uint32_t mask = (uint32_t)(toff[q + 1] - base - 1);
     if (threadIdx.x == 0) {
-        int64_t a, b;
-        key_range(key, eoff[q], eoff[q + 1], ((uint64_t)q << cb) | (uint32_t)c_old, &a, &b);
-        s_a = a;
-        s_b = b;
+        int s = probe_find(hkeys + base, c_old, mask);
+        s_fo = s >= 0 ? hvals[base + s] : 0.0;
+        s_lo = s >= 0 ? hcnt[base + s] : 0;
+        if (blockIdx.y == 0) {
+            H.fold[q] = s_fo;
+            H.lold[q] = s_lo;
+        }
     }
     __syncthreads();
-    const int64_t a = s_a, len = s_b - s_a, e0 = A.off[i];
-    const double *wts = A.wts;
-    double v = block_fold([=] __device__(int64_t t) { return wts[e0 + val[a + t]]; }, len, 0.0,
-                          sb);
-    if (threadIdx.x == 0) eold[q] = v;
+    const double f_old = s_fo, ki = A.k[i], a_old_excl = dsub(A.a_tot[c_old], ki);
+    const int64_t n = H.ncand[q * HCPAD];
+    const int64_t p0 = (int64_t)blockIdx.y * HSLICE;
+    const int64_t p1 = p0 + HSLICE < n ? p0 + HSLICE : n;
+    Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
+    for (int64_t p = p0 + threadIdx.x; p < p1; p += HSB) {
+        int32_t s = H.cand[base + p];
+        int32_t c = hkeys[base + s];
+        if (c == c_old) continue;
+        double F = hvals[base + s];
+        consider(b, gain_of(F, f_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq),
+                 LBL(A.labels, c), c, F, hcnt[base + s]);
+    }
+    b = block_best<HSB>(bs, b);
+    if (threadIdx.x == 0) H.part[q * H.slices + blockIdx.y] = b;
 }
 
-// One thread per sorted position: heads of short runs fold their community
-// and compute its gain (all hubs of the stage at once); heads of long runs go
-// to a worklist for k_hub_long; every other position is marked -inf.
-__global__ void k_hub_runs(DecideArgs A, const int32_t *list, const int64_t *eoff, int64_t nh,
-                           int64_t E, const uint64_t *key, const int32_t *val, int cb,
-                           int32_t nskip, const double *eold, double *rgain, int32_t *rc,
-                           double *rv, int64_t *lrun, unsigned long long *lcnt) {
-    const uint64_t cmask = (1ull << cb) - 1ull;
+// Pass 2, block (hub q, slice y): the hub's best from the partials, then
+// every candidate of the slice whose interval overlaps it; clears the slice.
+__global__ void __launch_bounds__(HSB) k_hub_pass2(DecideArgs A, const int32_t *list,
+                                                  const int64_t *toff, int32_t *hkeys,
+                                                  double *hvals, int32_t *hcnt, HubScratch H) {
+    __shared__ BestSmem<HSB> bs;
+    typedef cub::BlockReduce<unsigned long long, HSB> BR;
+    __shared__ typename BR::TempStorage red;
+    const int64_t q = blockIdx.x;
+    const int32_t i = A.subset[list[q]];
+    const int32_t c_old = A.assign[i];
+    const int64_t base = toff[q];
+    Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
+    for (int t = threadIdx.x; t < H.slices; t += HSB) {
+        Best o = H.part[q * H.slices + t];
+        consider(b, o.g, o.l, o.c, o.e, o.n);
+    }
+    b = block_best<HSB>(bs, b);
+    const double f_old = H.fold[q], ki = A.k[i], a_old_excl = dsub(A.a_tot[c_old], ki);
+    const int32_t lo_n = H.lold[q];
+    const bool stay_best = b.c == c_old;
+    const double lower = stay_best ? 0.0 : b.g - gain_slack(b.e, b.n, f_old, lo_n, A.m, b.g);
+    const int64_t n = H.ncand[q * HCPAD];
+    const int64_t p0 = (int64_t)blockIdx.y * HSLICE;
+    const int64_t p1 = p0 + HSLICE < n ? p0 + HSLICE : n;
     unsigned long long nc = 0;
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < E;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t kk = key[p];
-        int64_t q = (int64_t)(kk >> cb);
-        int32_t c = (int32_t)(kk & cmask);
-        double g = -INFINITY;
-        bool head = (p == eoff[q]) || key[p - 1] != kk;
-        if (head && c != nskip) {
-            nc++;
-            int32_t i = A.subset[list[q]];
-            int32_t c_old = A.assign[i];
-            int64_t hi = eoff[q + 1];
-            if (c != c_old) {
-                if (p + SHORT_RUN < hi && key[p + SHORT_RUN] == kk) {
-                    lrun[atomicAdd(lcnt, 1ull)] = p;
-                } else {
-                    double v = fold_hub_run(key, val, A.wts, A.off[i], p, hi);
-                    double ki = A.k[i];
-                    g = gain_of(v, eold[q], A.m, ki, dsub(A.a_tot[c_old], ki), A.a_tot[c],
-                                A.four_m_sq);
-                    rv[p] = v;
-                }
+    for (int64_t p = p0 + threadIdx.x; p < p1; p += HSB) {
+        int32_t s = H.cand[base + p];
+        int32_t c = hkeys[base + s];
+        nc++;
+        if (!A.integral && c != c_old && c != b.c) {
+            double F = hvals[base + s];
+            double g = gain_of(F, f_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq);
+            if (g + gain_slack(F, hcnt[base + s], f_old, lo_n, A.m, g) >= lower) {
+                int k = atomicAdd(H.nS + q, 1);
+                if (k < MAXS)
+                    H.S[q * MAXS + k] = c;
+                else
+                    atomicOr(H.flag + q, 2);
             }
         }
-        rgain[p] = g;
-        rc[p] = c;
+        hkeys[base + s] = -1;
+        hvals[base + s] = 0.0;
+        hcnt[base + s] = 0;
     }
-    if (A.cand) {
-        typedef cub::BlockReduce<unsigned long long, 256> BR;
-        __shared__ typename BR::TempStorage tmp;
-        unsigned long long tot = BR(tmp).Sum(nc);
-        if (threadIdx.x == 0 && tot) atomicAdd(A.cand, tot);
+    unsigned long long tot = BR(red).Sum(nc);
+    if (threadIdx.x == 0) {
+        if (A.cand && tot) atomicAdd(A.cand, tot);
+        if (blockIdx.y == 0) {
+            H.best[q] = b;
+            if (!stay_best && lower <= 0.0) atomicOr(H.flag + q, 1);  // "stay" overlaps
+        }
     }
 }
 
-// Long runs: one block each (block-staged ordered fold), then the gain.
-__global__ void __launch_bounds__(BLK) k_hub_long(DecideArgs A, const int32_t *list,
-                                                 const int64_t *eoff, const uint64_t *key,
-                                                 const int32_t *val, int cb, const double *eold,
-                                                 const int64_t *lrun,
-                                                 const unsigned long long *lcnt, double *rgain,
-                                                 double *rv) {
-    __shared__ double sb[2 * FOLD_CH];
-    __shared__ int64_t s_b;
-    const int64_t cnt = (int64_t)*lcnt;
-    const uint64_t cmask = (1ull << cb) - 1ull;
-    for (int64_t w = blockIdx.x; w < cnt; w += gridDim.x) {
-        const int64_t p = lrun[w];
-        const uint64_t kk = key[p];
-        const int64_t q = (int64_t)(kk >> cb);
-        const int32_t c = (int32_t)(kk & cmask);
-        const int32_t i = A.subset[list[q]];
-        if (threadIdx.x == 0) {
-            int64_t a, b;
-            key_range(key, p, eoff[q + 1], kk, &a, &b);
-            s_b = b;
+// Block per hub: the decision.  Certain non-moves (and integral graphs) finish
+// at once; otherwise the listed communities are folded exactly (or, on
+// overflow, the whole row in order through the hub's table slice) and the
+// decision is taken on exact values.
+__global__ void __launch_bounds__(HBLK) k_hub_decide(DecideArgs A, const int32_t *list,
+                                                    const int64_t *toff, int32_t *hkeys,
+                                                    double *hvals, int32_t *hcnt, HubScratch H) {
+    __shared__ CertSmem<HBLK> S;
+    const int tid = threadIdx.x;
+    for (int64_t q = blockIdx.x; q < H.nh; q += gridDim.x) {
+        const int64_t x = list[q];
+        const int32_t i = A.subset[x];
+        const int32_t c_old = A.assign[i];
+        const double ki = A.k[i];
+        const Best b = H.best[q];
+        const int nS = H.nS[q], flag = H.flag[q];
+        bool done = false;
+        if (A.integral) {
+            if (tid == 0) finish_vertex(A, x, c_old, H.fold[q], b.g, b.c, b.e);
+            done = true;
+        } else if (nS == 0 && !flag) {
+            bool moved = b.c != c_old;  // certain: the exact best, with exact gain > 0
+            if (moved && A.sizes[c_old] == 1 && A.sizes[b.c] == 1 &&
+                LBL(A.labels, b.c) > LBL(A.labels, c_old))
+                moved = false;
+            if (!moved) {
+                if (tid == 0) finish_vertex(A, x, c_old, H.fold[q], 0.0, c_old, 0.0);
+                done = true;
+            }
+        }
+        if (done) continue;
+        if (!(flag & 2)) {
+            if (tid == 0) {
+                int nn = 0;
+                S.N[nn++] = c_old;
+                if (b.c != c_old) S.N[nn++] = b.c;
+                for (int t = 0; t < nS; t++) S.N[nn++] = H.S[q * MAXS + t];
+                S.nn = nn;
+            }
+            __syncthreads();
+            exact_folds<HBLK>(A, i, S);
+            if (tid == 0) {
+                double a_old_excl = dsub(A.a_tot[c_old], ki);
+                Best e{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
+                for (int t = 1; t < S.nn; t++) {
+                    int32_t c = S.N[t];
+                    consider(e,
+                             gain_of(S.acc[t], S.acc[0], A.m, ki, a_old_excl, A.a_tot[c],
+                                     A.four_m_sq),
+                             LBL(A.labels, c), c, S.acc[t], 0);
+                }
+                finish_vertex(A, x, c_old, S.acc[0], e.g, e.c, e.e);
+            }
+            __syncthreads();
+            continue;
+        }
+        // overflow: sequential in-order fold of the whole row (rare)
+        const int64_t base = toff[q];
+        const uint32_t ts = (uint32_t)(toff[q + 1] - base);
+        int32_t *keys = hkeys + base;
+        double *vals = hvals + base;
+        if (tid == 0) {
+            for (int64_t e = A.off[i]; e < A.off[i + 1]; e++) {
+                int32_t j = A.nbr[e];
+                if (j == i) continue;
+                uint32_t s = probe_insert(keys, A.assign[j], ts - 1);
+                vals[s] = dadd(vals[s], A.wts[e]);
+            }
+            int s = probe_find(keys, c_old, ts - 1);
+            S.f_old = s >= 0 ? vals[s] : 0.0;
         }
         __syncthreads();
-        const int64_t len = s_b - p, e0 = A.off[i];
-        const double *wts = A.wts;
-        double v = block_fold([=] __device__(int64_t t) { return wts[e0 + val[p + t]]; }, len,
-                              0.0, sb);
-        if (threadIdx.x == 0) {
-            int32_t c_old = A.assign[i];
-            double ki = A.k[i];
-            rgain[p] = gain_of(v, eold[q], A.m, ki, dsub(A.a_tot[c_old], ki), A.a_tot[c],
-                               A.four_m_sq);
-            rv[p] = v;
+        const double e_old = S.f_old, a_old_excl = dsub(A.a_tot[c_old], ki);
+        Best bx{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
+        for (uint32_t s = tid; s < ts; s += HBLK) {
+            int32_t c = keys[s];
+            if (c >= 0 && c != c_old)
+                consider(bx, gain_of(vals[s], e_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq),
+                         LBL(A.labels, c), c, vals[s], 0);
         }
+        bx = block_best<HBLK>(S.bs, bx);
+        for (uint32_t s = tid; s < ts; s += HBLK) {
+            keys[s] = -1;
+            vals[s] = 0.0;
+        }
+        if (tid == 0) finish_vertex(A, x, c_old, e_old, bx.g, bx.c, bx.e);
         __syncthreads();
     }
-}
-
-// Block per hub: argmax over its run candidates, then the decision.
-__global__ void __launch_bounds__(BLK) k_hub_final(DecideArgs A, const int32_t *list,
-                                                  const int64_t *eoff, const double *eold,
-                                                  const double *rgain, const int32_t *rc,
-                                                  const double *rv) {
-    __shared__ BestSmem bs;
-    const int64_t q = blockIdx.x;
-    const int64_t x = list[q];
-    const int32_t c_old = A.assign[A.subset[x]];
-    const int64_t l_old = LBL(A.labels, c_old);
-    double bg = 0.0, be = 0.0;
-    int32_t bc = c_old;
-    int64_t bl = l_old;
-    for (int64_t p = eoff[q] + threadIdx.x; p < eoff[q + 1]; p += BLK) {
-        double g = rgain[p];
-        if (g == -INFINITY) continue;
-        int32_t c = rc[p];
-        int64_t l = LBL(A.labels, c);
-        if (better(g, l, bg, bl)) {
-            bg = g;
-            bl = l;
-            bc = c;
-            be = rv[p];
-        }
-    }
-    block_best(bs, bg, bl, bc, be, l_old, c_old);
-    if (threadIdx.x == 0) finish_vertex(A, x, c_old, eold[q], bg, bc, be);
 }
 
 // ================================================================ planning
@@ -668,32 +971,33 @@ __global__ void k_hub_degrees(const int64_t *off, const int32_t *vtx, const int6
     }
 }
 
+__global__ void k_fill_i32_d(int32_t *p, int64_t n, int32_t v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
 void Plan::release() {
-    void *ps[] = {tier_list, hub_eoff, hkey, hkey2, hval, hval2, htmp, heold, rgain, rc, rv,
-                  lrun, lcnt};
+    void *ps[] = {tier_list, hub_eoff, hub_toff, hkeys, hvals, hcnt, hcand, hsmall, hS, hpart,
+                  hbest, hfold, hlold};
     for (void *p : ps)
         if (p) cudaFree(p);
-    heold = rgain = rv = nullptr;
-    lrun = nullptr;
-    lcnt = nullptr;
-    rc = nullptr;
     tier_list = nullptr;
-    hub_eoff = nullptr;
-    hkey = hkey2 = nullptr;
-    hval = hval2 = nullptr;
-    htmp = nullptr;
+    hub_eoff = hub_toff = nullptr;
+    hkeys = hcnt = hcand = hsmall = hS = hlold = nullptr;
+    hvals = hfold = nullptr;
+    hpart = hbest = nullptr;
 }
 
 void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *stage_off_h,
                 int64_t nst, int64_t n, cudaStream_t s) {
+    (void)n;
     int64_t total = stage_off_h[nst];
     P.st.assign(nst, StagePlan{});
     for (int64_t a = 0; a < nst; a++) {
         P.st[a].off = stage_off_h[a];
         P.st[a].ns = stage_off_h[a + 1] - stage_off_h[a];
     }
-    P.cb = bits_for(n + 2);
-    P.nskip = (int32_t)n;
     P.tier_list = dalloc<int32_t>(total);
     if (total == 0) return;
     Buf<int64_t> d_soff(nst + 1, s);
@@ -740,42 +1044,60 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
     PLV_CUDA(cudaMemcpyAsync(deg.data(), d_deg.get(), sizeof(int64_t) * nh, cudaMemcpyDeviceToHost,
                              s));
     PLV_CUDA(cudaStreamSynchronize(s));
-    std::vector<int64_t> eoff;
+    std::vector<int64_t> eoff, toff;
     int64_t h0 = 0;
     for (int64_t a = 0; a < nst; a++) {
         StagePlan &sp = P.st[a];
         sp.hub_base = (int64_t)eoff.size();
-        int64_t acc = 0;
+        int64_t acc = 0, tacc = 0;
         eoff.push_back(0);
+        toff.push_back(0);
         for (int64_t z = 0; z < sp.tcount[3]; z++) {
-            acc += deg[h0 + z];
+            int64_t d = deg[h0 + z];
+            int64_t cap = 64;
+            while (cap < 2 * d + 2) cap <<= 1;
+            int64_t sl = (d + HSLICE - 1) / HSLICE;  // candidates <= degree
+            sp.hub_slices = sl > sp.hub_slices ? sl : sp.hub_slices;
+            acc += d;
+            tacc += cap;
             eoff.push_back(acc);
+            toff.push_back(tacc);
         }
         h0 += sp.tcount[3];
         sp.hub_entries = acc;
         P.max_hub_entries = acc > P.max_hub_entries ? acc : P.max_hub_entries;
         P.max_hubs = sp.tcount[3] > P.max_hubs ? sp.tcount[3] : P.max_hubs;
+        P.max_table = tacc > P.max_table ? tacc : P.max_table;
     }
     P.hub_eoff = dalloc<int64_t>(eoff.size());
+    P.hub_toff = dalloc<int64_t>(toff.size());
     PLV_CUDA(cudaMemcpyAsync(P.hub_eoff, eoff.data(), sizeof(int64_t) * eoff.size(),
                              cudaMemcpyHostToDevice, s));
-    P.qb = bits_for(P.max_hubs + 1);
-    int64_t E = P.max_hub_entries;
-    P.hkey = dalloc<uint64_t>(E);
-    P.hkey2 = dalloc<uint64_t>(E);
-    P.hval = dalloc<int32_t>(E);
-    P.hval2 = dalloc<int32_t>(E);
-    P.heold = dalloc<double>(P.max_hubs);
-    P.rgain = dalloc<double>(E);
-    P.rc = dalloc<int32_t>(E);
-    P.rv = dalloc<double>(E);
-    P.lrun = dalloc<int64_t>(E);
-    P.lcnt = dalloc<unsigned long long>(1);
-    PLV_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, P.hbytes, P.hkey, P.hkey2, P.hval, P.hval2,
-                                             E, 0, P.cb + P.qb, s));
-    PLV_CUDA(cudaMalloc(&P.htmp, P.hbytes ? P.hbytes : 1));
+    PLV_CUDA(cudaMemcpyAsync(P.hub_toff, toff.data(), sizeof(int64_t) * toff.size(),
+                             cudaMemcpyHostToDevice, s));
+    int64_t T = P.max_table;
+    P.hkeys = dalloc<int32_t>(T);
+    P.hvals = dalloc<double>(T);
+    P.hcnt = dalloc<int32_t>(T);
+    k_fill_i32_d<<<grid_for(T, 256), 256, 0, s>>>(P.hkeys, T, -1);
+    PLV_LAUNCH_CHECK();
+    PLV_CUDA(cudaMemsetAsync(P.hvals, 0, sizeof(double) * T, s));
+    PLV_CUDA(cudaMemsetAsync(P.hcnt, 0, sizeof(int32_t) * T, s));
+    int64_t H = P.max_hubs;
+    P.hcand = dalloc<int32_t>(T);
+    P.hsmall = dalloc<int32_t>((HCPAD + 2) * H);
+    PLV_CUDA(cudaMemsetAsync(P.hsmall, 0, sizeof(int32_t) * (HCPAD + 2) * H, s));
+    P.hS = dalloc<int32_t>(H * MAXS);
+    P.max_slices = 1;
+    for (auto &sp : P.st) P.max_slices = sp.hub_slices > P.max_slices ? sp.hub_slices : P.max_slices;
+    P.hpart = dalloc<Best>(H * P.max_slices);
+    P.hbest = dalloc<Best>(H);
+    P.hfold = dalloc<double>(H);
+    P.hlold = dalloc<int32_t>(H);
     PLV_CUDA(cudaStreamSynchronize(s));
 }
+
+static size_t t2_smem() { return (sizeof(double) + 2 * sizeof(int32_t)) * T2_TS; }
 
 void ensure_decide_attrs() {
     static int dev_done = -1;
@@ -783,49 +1105,74 @@ void ensure_decide_attrs() {
     PLV_CUDA(cudaGetDevice(&dev));
     if (dev_done == dev) return;
     PLV_CUDA(cudaFuncSetAttribute(k_decide_t2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)T2_SMEM));
+                                  (int)t2_smem()));
     dev_done = dev;
 }
 
 void launch_decide(const Plan &P, int64_t a, DecideArgs A, cudaStream_t st) {
+    cudaStream_t ts[4] = {st, st, st, st};
+    launch_decide_tiers(P, a, A, ts);
+}
+
+void launch_decide_par(const Plan &P, int64_t a, DecideArgs A, cudaStream_t st,
+                       const cudaStream_t *side, cudaEvent_t fork, const cudaEvent_t *join) {
+    const StagePlan &sp = P.st[a];
+    int used[4], nu = 0;
+    for (int t = 3; t >= 0; t--)  // hubs (longest) first, on the main stream
+        if (sp.tcount[t]) used[nu++] = t;
+    cudaStream_t ts[4] = {st, st, st, st};
+    if (nu > 1) {
+        PLV_CUDA(cudaEventRecord(fork, st));
+        for (int u = 1; u < nu; u++) {
+            PLV_CUDA(cudaStreamWaitEvent(side[u - 1], fork, 0));
+            ts[used[u]] = side[u - 1];
+        }
+    }
+    launch_decide_tiers(P, a, A, ts);
+    for (int u = 1; u < nu; u++) {
+        PLV_CUDA(cudaEventRecord(join[u - 1], side[u - 1]));
+        PLV_CUDA(cudaStreamWaitEvent(st, join[u - 1], 0));
+    }
+}
+
+void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStream_t *ts) {
     const StagePlan &sp = P.st[a];
     if (sp.tcount[0]) {
-        k_decide_t0<<<grid_for(sp.tcount[0], 256), 256, 0, st>>>(A, P.tier_list + sp.tstart[0],
-                                                                 sp.tcount[0]);
+        k_decide_t0<<<grid_for(sp.tcount[0], 256), 256, 0, ts[0]>>>(A, P.tier_list + sp.tstart[0],
+                                                                    sp.tcount[0]);
         PLV_LAUNCH_CHECK();
     }
     if (sp.tcount[1]) {
-        k_decide_t1<<<grid_for(sp.tcount[1], T1_WARPS), T1_WARPS * 32, 0, st>>>(
+        k_decide_t1<<<grid_for(sp.tcount[1], T1_WARPS), T1_WARPS * 32, 0, ts[1]>>>(
             A, P.tier_list + sp.tstart[1], sp.tcount[1]);
         PLV_LAUNCH_CHECK();
     }
     if (sp.tcount[2]) {
-        k_decide_t2<<<grid_for(sp.tcount[2], 1, 148 * 8), BLK, T2_SMEM, st>>>(
+        k_decide_t2<<<grid_for(sp.tcount[2], 1, 148 * 3), BLK, t2_smem(), ts[2]>>>(
             A, P.tier_list + sp.tstart[2], sp.tcount[2]);
         PLV_LAUNCH_CHECK();
     }
+    cudaStream_t st = ts[3];
     if (sp.tcount[3]) {
         const int32_t *list = P.tier_list + sp.tstart[3];
         const int64_t *eoff = P.hub_eoff + sp.hub_base;
-        int64_t E = sp.hub_entries;
-        k_hub_keys<<<grid_for(E, 256), 256, 0, st>>>(A, list, eoff, sp.tcount[3], E, P.cb, P.nskip,
-                                                     P.hkey, P.hval);
+        const int64_t *toff = P.hub_toff + sp.hub_base;
+        int64_t nh = sp.tcount[3], E = sp.hub_entries;
+        const int64_t Hm = P.max_hubs;
+        HubScratch H{P.hcand,   P.hsmall, P.hsmall + HCPAD * Hm, P.hsmall + (HCPAD + 1) * Hm,
+                     P.hS,      P.hpart,  P.hbest,              P.hfold,
+                     P.hlold,   (int)sp.hub_slices,             nh};
+        PLV_CUDA(cudaMemsetAsync(P.hsmall, 0, sizeof(int32_t) * (HCPAD + 2) * Hm, st));
+        k_hub_accum<<<grid_for(E, 256), 256, 0, st>>>(A, list, eoff, toff, nh, E, P.hkeys, P.hvals,
+                                                      P.hcnt, H);
         PLV_LAUNCH_CHECK();
-        size_t bytes = P.hbytes;
-        PLV_CUDA(cub::DeviceRadixSort::SortPairs(P.htmp, bytes, P.hkey, P.hkey2, P.hval, P.hval2, E,
-                                                 0, P.cb + P.qb, st));
-        int64_t nh = sp.tcount[3];
-        k_hub_eold<<<(unsigned)nh, BLK, 0, st>>>(A, list, eoff, P.hkey2, P.hval2, P.cb, P.heold);
+        dim3 g2((unsigned)nh, (unsigned)sp.hub_slices);
+        k_hub_pass1<<<g2, HSB, 0, st>>>(A, list, toff, P.hkeys, P.hvals, P.hcnt, H);
         PLV_LAUNCH_CHECK();
-        PLV_CUDA(cudaMemsetAsync(P.lcnt, 0, sizeof(unsigned long long), st));
-        k_hub_runs<<<grid_for(E, 256), 256, 0, st>>>(A, list, eoff, nh, E, P.hkey2, P.hval2, P.cb,
-                                                     P.nskip, P.heold, P.rgain, P.rc, P.rv, P.lrun,
-                                                     P.lcnt);
+        k_hub_pass2<<<g2, HSB, 0, st>>>(A, list, toff, P.hkeys, P.hvals, P.hcnt, H);
         PLV_LAUNCH_CHECK();
-        k_hub_long<<<148 * 2, BLK, 0, st>>>(A, list, eoff, P.hkey2, P.hval2, P.cb, P.heold, P.lrun,
-                                            P.lcnt, P.rgain, P.rv);
-        PLV_LAUNCH_CHECK();
-        k_hub_final<<<(unsigned)nh, BLK, 0, st>>>(A, list, eoff, P.heold, P.rgain, P.rc, P.rv);
+        k_hub_decide<<<(unsigned)(nh < 148 * 2 ? nh : 148 * 2), HBLK, 0, st>>>(
+            A, list, toff, P.hkeys, P.hvals, P.hcnt, H);
         PLV_LAUNCH_CHECK();
     }
 }
@@ -865,15 +1212,12 @@ static void decide_once(const int64_t *off, const int32_t *nbr, const double *wt
     if (cand_h) *cand_h = 0;
     if (ns <= 0) return;
     ensure_decide_attrs();
-    // community ids are vertex ids of the graph: < 2^31 - 2 is enough for the
-    // hub keys' community field
-    const int64_t n_bound = (int64_t)INT32_MAX - 2;
     Plan P;
     int64_t soff[2] = {0, ns};
     Buf<unsigned long long> cand(1, s);
     PLV_CUDA(cudaMemsetAsync(cand.get(), 0, sizeof(unsigned long long), s));
     try {
-        plan_build(P, off, subset, soff, 1, n_bound, s);
+        plan_build(P, off, subset, soff, 1, 0, s);
         DecideArgs A = make_decide_args(off, nbr, wts, k, labels, subset, assign, a_tot, sizes, m,
                                         integral, out_target, out_moved, out_e_old, out_e_best,
                                         cand.get());

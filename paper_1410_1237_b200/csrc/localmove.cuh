@@ -62,29 +62,33 @@ struct StagePlan {
     int64_t off = 0, ns = 0;
     int64_t tcount[4] = {0, 0, 0, 0};
     int64_t tstart[4] = {0, 0, 0, 0};  // into the tier list
-    int64_t hub_base = 0;              // this stage's first hub_eoff entry
+    int64_t hub_base = 0;              // this stage's first hub_eoff / hub_toff entry
     int64_t hub_entries = 0;
+    int64_t hub_slices = 0;  // candidate slices per hub (pass blocks)
 };
 
+struct Best;  // decide.cu
+
+constexpr int MAXS = 32;  // overlapping candidates resolved exactly per vertex
+
 // Static per-phase decide plan: each stage's vertices split into the four
-// degree tiers, and the hubs' entries laid out for the sort-based tier.
+// degree tiers; hubs get entry offsets and a slice of a global hash table.
 struct Plan {
     std::vector<StagePlan> st;
     int32_t *tier_list = nullptr;  // stage-local indices grouped by (stage, tier)
     int64_t *hub_eoff = nullptr;   // per stage: nh+1 entry offsets (from 0)
-    int64_t max_hub_entries = 0, max_hubs = 0;
-    uint64_t *hkey = nullptr, *hkey2 = nullptr;
-    int32_t *hval = nullptr, *hval2 = nullptr;
-    void *htmp = nullptr;
-    size_t hbytes = 0;
-    double *heold = nullptr;  // per hub: e_{i->c_old}
-    double *rgain = nullptr;  // per sorted position: run gain (-inf: not a candidate)
-    int32_t *rc = nullptr;
-    double *rv = nullptr;
-    int64_t *lrun = nullptr;  // heads of long runs (block-folded)
-    unsigned long long *lcnt = nullptr;
-    int cb = 1, qb = 1;
-    int32_t nskip = 0;
+    int64_t *hub_toff = nullptr;   // per stage: nh+1 table offsets (from 0, pow2 sizes)
+    int64_t max_hub_entries = 0, max_hubs = 0, max_table = 0;
+    int32_t *hkeys = nullptr;  // hub tables: key -1 / val 0 / cnt 0 when clean
+    double *hvals = nullptr;
+    int32_t *hcnt = nullptr;
+    int32_t *hcand = nullptr;   // candidate slot lists (table layout)
+    int32_t *hsmall = nullptr;  // per hub: ncand, nS, flag
+    int32_t *hS = nullptr;      // per hub: MAXS overlapping communities
+    Best *hpart = nullptr, *hbest = nullptr;
+    double *hfold = nullptr;
+    int32_t *hlold = nullptr;
+    int64_t max_slices = 1;
     void release();
 };
 
@@ -93,6 +97,12 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
 void ensure_decide_attrs();
 // Launch stage `a`'s decide kernels (no host synchronisation; capturable).
 void launch_decide(const Plan &P, int64_t a, DecideArgs A, cudaStream_t st);
+// Tier t on stream ts[t].
+void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStream_t *ts);
+// The stage's non-empty tiers as parallel branches (3 side streams, a fork
+// event and 3 join events), joined back into `st`.
+void launch_decide_par(const Plan &P, int64_t a, DecideArgs A, cudaStream_t st,
+                       const cudaStream_t *side, cudaEvent_t fork, const cudaEvent_t *join);
 
 struct StageArgs {
     const int64_t *off;
@@ -117,6 +127,10 @@ struct StageArgs {
     uint32_t *ekey;
     int32_t *eval;
     unsigned long long *moves;
+    int32_t *big = nullptr;  // high-degree movers (live folds by whole warps)
+    unsigned long long *nbig = nullptr;
+    int32_t *huge = nullptr;  // huge movers (live folds by whole blocks)
+    unsigned long long *nhuge = nullptr;
 };
 
 // Event / sort scratch for stages of up to max_ns vertices.
@@ -129,6 +143,9 @@ struct ApplyBuffers {
     double *dW = nullptr, *dA = nullptr;  // sorted event deltas
     int64_t *lrun = nullptr;              // heads of long community runs
     unsigned long long *lcnt = nullptr;
+    int32_t *big = nullptr;               // high-degree movers, then huge movers
+    unsigned long long *nbig = nullptr;   // [0] big, [1] huge
+    int64_t big_cap = 0;
     int nb = 1;
     void alloc(int64_t ta_len, int64_t max_ns, int64_t n, cudaStream_t s);
     void release();

@@ -41,6 +41,8 @@ struct Phase {
     double *h_out = nullptr;  // pinned: q, moves, cand
     bool timing = false;
     std::vector<cudaEvent_t> ev;
+    cudaStream_t side[3] = {nullptr, nullptr, nullptr};  // decide tiers in parallel branches
+    cudaEvent_t fork = nullptr, join[3] = {nullptr, nullptr, nullptr};
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
 
@@ -51,6 +53,14 @@ struct Phase {
         graph = nullptr;
         for (auto e : ev) cudaEventDestroy(e);
         ev.clear();
+        for (int t = 0; t < 3; t++) {
+            if (side[t]) cudaStreamDestroy(side[t]);
+            if (join[t]) cudaEventDestroy(join[t]);
+            side[t] = nullptr;
+            join[t] = nullptr;
+        }
+        if (fork) cudaEventDestroy(fork);
+        fork = nullptr;
         plan.release();
         ab.release();
         void *ps[] = {target, moved, e_old, e_best, counters, q, mod_scratch};
@@ -73,7 +83,10 @@ static void record_iteration(Phase &P, cudaStream_t st) {
                                         P.counters + 1);
         if (P.timing)
             PLV_CUDA(cudaEventRecordWithFlags(P.ev[2 * a], st, cudaEventRecordExternal));
-        launch_decide(P.plan, (int64_t)a, A, st);
+        if (P.timing)
+            launch_decide(P.plan, (int64_t)a, A, st);  // serial, so the events bracket all tiers
+        else
+            launch_decide_par(P.plan, (int64_t)a, A, st, P.side, P.fork, P.join);
         if (P.timing)
             PLV_CUDA(cudaEventRecordWithFlags(P.ev[2 * a + 1], st, cudaEventRecordExternal));
         StageArgs S{P.off, P.nbr, P.wts, P.k, P.selfw, P.vtx + sp.off, sp.ns, P.target + sp.off,
@@ -130,6 +143,11 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
             P->ev.resize(2 * nst);
             for (auto &e : P->ev) PLV_CUDA(cudaEventCreate(&e));
         }
+        for (int t = 0; t < 3; t++) {
+            PLV_CUDA(cudaStreamCreateWithFlags(&P->side[t], cudaStreamNonBlocking));
+            PLV_CUDA(cudaEventCreateWithFlags(&P->join[t], cudaEventDisableTiming));
+        }
+        PLV_CUDA(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming));
         PLV_CUDA(cudaStreamSynchronize(s));
         cudaStream_t cs;
         PLV_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));

@@ -197,3 +197,53 @@ def test_edge_cases():
     g = pl.Graph.from_edges([0], [1], num_vertices=4)   # isolated vertices
     assert g.degree(2) == 0 and g.weighted_degrees[3] == 0.0
     g.validate()
+
+
+def _tie_graph(n_leaves, w=0.1, extra=3):
+    """A hub (vertex 0) whose neighbour communities give bitwise-identical
+    gains: every leaf has the same fp weight to the hub and the same degree,
+    so certification must fall back to exact folds (and, above MAXS ties, to
+    the fully exact path)."""
+    u, v, ww = [], [], []
+    nxt = n_leaves + 1
+    for leaf in range(1, n_leaves + 1):
+        u.append(0), v.append(leaf), ww.append(w)
+        for _ in range(extra):                       # private pendant triangle
+            u.append(leaf), v.append(nxt), ww.append(0.3)
+            nxt += 1
+    return np.array(u), np.array(v), np.array(ww), nxt
+
+
+@pytest.mark.parametrize("n_leaves", [10, 40, 3000])
+def test_exact_ties_are_resolved_like_the_reference(orc, n_leaves):
+    u, v, w, n = _tie_graph(n_leaves)
+    g = pl.Graph.from_edges(u, v, w, num_vertices=n)
+    og = orc.from_edges(u, v, w, num_vertices=n)
+    for flags_colored in (False, True):
+        s = pl.singleton_state(g)
+        os_ = orc.singleton_state(og)
+        if flags_colored:
+            col = pl.color_graph(g)
+            for stage in col.classes():
+                s, _ = pl.run_iteration(g, s, stage)
+                orc.run_iteration(og, os_, stage)
+        else:
+            s, _ = pl.run_iteration(g, s, np.arange(n))
+            orc.run_iteration(og, os_, np.arange(n))
+        assert np.array_equal(s.assignment, os_.assignment)
+        assert np.array_equal(s.a_tot, os_.a_tot)
+        assert np.array_equal(s.w_internal, os_.w_internal)
+
+
+@pytest.mark.parametrize("scale,cutoff", [(16, 0), (16, 100_000), (17, 0)])
+def test_rmat_with_hubs_matches_oracle(orc, scale, cutoff):
+    from paper_1410_1237_b200 import synthetic as syn
+    u, v, w = syn.rmat_records(scale, 16, seed=5)
+    n = 1 << scale
+    og = orc.from_edges(u, v, w, num_vertices=n)
+    g = pl.Graph.from_edges(u, v, w, num_vertices=n)
+    assert g.max_degree > 2048        # the hub tier is exercised
+    oh = orc.run(og, color_cutoff=cutoff, max_iterations=30)
+    h = pl.run(g, pl.RunConfig(color_cutoff=cutoff, max_iterations_per_phase=30))
+    assert np.array_equal(h.final_assignment, oh.final_assignment)
+    assert h.final_modularity == oh.final_modularity
