@@ -60,6 +60,12 @@ def lib():
                                         ctypes.c_double, ctypes.c_void_p, _i64p, _i64,
                                         _i64p, _f64p, _f64p, _i64p, ctypes.c_void_p,
                                         ctypes.c_void_p]
+        L.orc_decide.restype = None
+        L.orc_decide.argtypes = [_i64, _i64p, _i64p, _f64p, _f64p, ctypes.c_double,
+                                 ctypes.c_void_p, _i64p, _i64, _i64p, _f64p, _i64p, _i64p, _u8p]
+        L.orc_apply.restype = _i64
+        L.orc_apply.argtypes = [_i64p, _i64p, _f64p, _f64p, _f64p, _i64p, _i64, _i64p, _u8p,
+                                _i64p, _f64p, _f64p, _i64p]
         L.orc_modularity.restype = ctypes.c_double
         L.orc_modularity.argtypes = [_i64, _f64p, _f64p, ctypes.c_double]
         L.orc_rebuild_records.restype = ctypes.c_int
@@ -178,6 +184,28 @@ def run_iteration(g: OGraph, s: OState, vertices, want_decisions=False):
     if want_decisions:
         return int(cnt), tg[:ns], mv[:ns]
     return int(cnt)
+
+
+def decide(g: OGraph, s: OState, vertices):
+    """decide_moves (PL/_kernels.pyx:21-101) alone: (targets, moved)."""
+    subset = np.ascontiguousarray(vertices, dtype=np.int64)
+    ns = len(subset)
+    tg = np.empty(ns + 1, np.int64)
+    mv = np.empty(ns + 1, np.uint8)
+    lib().orc_decide(g.num_vertices, g.adjacency_offsets, g.neighbors, g.weights,
+                     g.weighted_degrees, g.total_weight, None, subset, ns, s.assignment,
+                     s.a_tot, s.sizes, tg, mv)
+    return tg[:ns], mv[:ns]
+
+
+def apply(g: OGraph, s: OState, vertices, targets, moved) -> int:
+    """apply_moves (PL/_kernels.pyx:104-145) alone; mutates s."""
+    subset = np.ascontiguousarray(vertices, dtype=np.int64)
+    return int(lib().orc_apply(g.adjacency_offsets, g.neighbors, g.weights, g.weighted_degrees,
+                               g.self_loop_weights, subset, len(subset),
+                               np.ascontiguousarray(targets, dtype=np.int64),
+                               np.ascontiguousarray(moved, dtype=np.uint8), s.assignment,
+                               s.a_tot, s.w_internal, s.sizes))
 
 
 @dataclass

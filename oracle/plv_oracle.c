@@ -313,11 +313,11 @@ int64_t orc_color(int64_t n, const int64_t *off, const int64_t *nbr, int64_t max
  * out_targets/out_moved (optional, may be NULL) receive the decide outputs.
  * Returns the move count.
  */
-int64_t orc_run_iteration(int64_t n, const int64_t *off, const int64_t *nbr, const double *wts,
-                          const double *kdeg, const double *selfw, double m,
-                          const int64_t *labels, const int64_t *subset, int64_t ns,
-                          int64_t *assign, double *a_tot, double *w_int, int64_t *sizes,
-                          int64_t *out_targets, uint8_t *out_moved)
+/* decide_moves alone (PL/_kernels.pyx:21-101): targets / moved per subset index. */
+void orc_decide(int64_t n, const int64_t *off, const int64_t *nbr, const double *wts,
+                const double *kdeg, double m, const int64_t *labels, const int64_t *subset,
+                int64_t ns, const int64_t *assign, const double *a_tot, const int64_t *sizes,
+                int64_t *tg, uint8_t *mv)
 {
     /* per-community scratch is kept across calls (colour stages call this
      * hundreds of times per iteration); stamps grow monotonically so the
@@ -332,8 +332,6 @@ int64_t orc_run_iteration(int64_t n, const int64_t *off, const int64_t *nbr, con
         cands = (int64_t *)malloc(sizeof(int64_t) * cap);
         stamp_base = 0;
     }
-    int64_t *tg = (int64_t *)malloc(sizeof(int64_t) * (ns + 1));
-    uint8_t *mv = (uint8_t *)malloc(ns + 1);
     const double four_m_sq = (2.0 * m) * (2.0 * m);
 #define LBL(c) (labels ? labels[c] : (c))
     for (int64_t x = 0; x < ns; x++) {
@@ -374,8 +372,15 @@ int64_t orc_run_iteration(int64_t n, const int64_t *off, const int64_t *nbr, con
         mv[x] = (uint8_t)moved;
     }
 #undef LBL
-    if (out_targets) memcpy(out_targets, tg, sizeof(int64_t) * ns);
-    if (out_moved) memcpy(out_moved, mv, ns);
+}
+
+/* apply_moves alone (PL/_kernels.pyx:104-145): sequential in subset order
+ * against the live assignment; returns the move count. */
+int64_t orc_apply(const int64_t *off, const int64_t *nbr, const double *wts, const double *kdeg,
+                  const double *selfw, const int64_t *subset, int64_t ns, const int64_t *tg,
+                  const uint8_t *mv, int64_t *assign, double *a_tot, double *w_int,
+                  int64_t *sizes)
+{
     int64_t count = 0;
     for (int64_t x = 0; x < ns; x++) {
         if (!mv[x]) continue;
@@ -399,6 +404,22 @@ int64_t orc_run_iteration(int64_t n, const int64_t *off, const int64_t *nbr, con
         assign[i] = b;
         count++;
     }
+    return count;
+}
+
+int64_t orc_run_iteration(int64_t n, const int64_t *off, const int64_t *nbr, const double *wts,
+                          const double *kdeg, const double *selfw, double m,
+                          const int64_t *labels, const int64_t *subset, int64_t ns,
+                          int64_t *assign, double *a_tot, double *w_int, int64_t *sizes,
+                          int64_t *out_targets, uint8_t *out_moved)
+{
+    int64_t *tg = (int64_t *)malloc(sizeof(int64_t) * (ns + 1));
+    uint8_t *mv = (uint8_t *)malloc(ns + 1);
+    orc_decide(n, off, nbr, wts, kdeg, m, labels, subset, ns, assign, a_tot, sizes, tg, mv);
+    if (out_targets) memcpy(out_targets, tg, sizeof(int64_t) * ns);
+    if (out_moved) memcpy(out_moved, mv, ns);
+    int64_t count = orc_apply(off, nbr, wts, kdeg, selfw, subset, ns, tg, mv, assign, a_tot,
+                              w_int, sizes);
     free(tg); free(mv);
     return count;
 }

@@ -91,6 +91,31 @@ __device__ __forceinline__ uint32_t probe_insert(int32_t *keys, int32_t c, uint3
     }
 }
 
+// probe_insert that also reports whether this call inserted the key.
+__device__ __forceinline__ uint32_t probe_insert_f(int32_t *keys, int32_t c, uint32_t mask,
+                                                   bool *fresh) {
+    uint32_t s = hslot(c, mask);
+    while (true) {
+        int32_t k = keys[s];
+        if (k == c) {
+            *fresh = false;
+            return s;
+        }
+        if (k == -1) {
+            int32_t old = atomicCAS(keys + s, -1, c);
+            if (old == -1) {
+                *fresh = true;
+                return s;
+            }
+            if (old == c) {
+                *fresh = false;
+                return s;
+            }
+        }
+        s = (s + 1) & mask;
+    }
+}
+
 __device__ __forceinline__ int probe_find(const int32_t *keys, int32_t c, uint32_t mask) {
     uint32_t s = hslot(c, mask);
     while (true) {
@@ -336,24 +361,44 @@ struct CertSmem {
 // Accumulate one entry (c, w) with warp aggregation: lanes with the same
 // community combine (any order) before one atomic per group.
 __device__ __forceinline__ void accum_entry(int32_t *keys, double *vals, int32_t *cnt,
-                                            uint32_t mask, int32_t c, double w, int lane) {
+                                            uint32_t mask, int32_t c, double w, int lane,
+                                            int16_t *clist, int *ncl) {
     unsigned grp = __match_any_sync(FULL, c);
     double v = 0.0;
     for (unsigned g = grp; g; g &= g - 1) v = dadd(v, __shfl_sync(grp, w, __ffs(g) - 1));
+    bool fresh = false;
+    uint32_t s = 0;
     if (c >= 0 && lane == __ffs(grp) - 1) {
-        uint32_t s = probe_insert(keys, c, mask);
+        s = probe_insert_f(keys, c, mask, &fresh);
         atomicAdd(vals + s, v);
         atomicAdd(cnt + s, __popc(grp));
     }
+    unsigned fm = __ballot_sync(FULL, fresh);  // one list append per warp
+    if (fm) {
+        int first = __ffs(fm) - 1, pos = 0;
+        if (lane == first) pos = atomicAdd(ncl, __popc(fm));
+        pos = __shfl_sync(FULL, pos, first);
+        if (fresh) clist[pos + __popc(fm & ((1u << lane) - 1))] = (int16_t)s;
+    }
 }
 
-// Passes over the (any-order) table of vertex i: the best candidate on the
-// approximate gains, then the candidates whose intervals overlap it.  Slots
-// are cleared in the second pass when `clear`.  Returns the approximate best.
+// |gain(exact sums) - gain(any-order sums)| bound without divisions (it is a
+// bound, so the reciprocal's rounding is absorbed by the 1.01 / 8u factors).
+__device__ __forceinline__ double gain_slack_r(double Fc, int32_t Lc, double Fo, int32_t Lo,
+                                               double inv_m, double g) {
+    return 1.02 * ((sum_err(Fc, Lc) + sum_err(Fo, Lo)) * inv_m) +
+           8.0 * U_RND * (fabs(Fc - Fo) * inv_m * 1.001 + fabs(g)) + 1e-300;
+}
+
+// Passes over the candidates (slots clist[0..ncl)) of the any-order table of
+// vertex i: pass 1 finds the best on the approximate gains and stores every
+// candidate's gain in vals[] and its slack (rounded up to float) in cnt[];
+// pass 2 collects the candidates whose intervals overlap the best and clears
+// the slots when `clear`.  Returns the approximate best.
 template <int NT>
 __device__ Best certify_table(const DecideArgs &A, int32_t c_old, double ki, int32_t *keys,
-                              double *vals, int32_t *cnt, uint32_t ts, CertSmem<NT> &S,
-                              bool clear) {
+                              double *vals, int32_t *cnt, uint32_t ts, const int16_t *clist,
+                              int ncl, CertSmem<NT> &S, bool clear) {
     const int tid = threadIdx.x;
     const uint32_t mask = ts - 1;
     if (tid == 0) {
@@ -367,27 +412,31 @@ __device__ Best certify_table(const DecideArgs &A, int32_t c_old, double ki, int
     const double f_old = S.f_old;
     const int32_t l_old_n = S.l_old;
     const double a_old_excl = dsub(A.a_tot[c_old], ki);
+    const double inv_m = 1.0 / A.m;
     const int64_t l_old = LBL(A.labels, c_old);
     Best b{0.0, l_old, c_old, 0.0, 0};
-    for (uint32_t s = tid; s < ts; s += NT) {
+    for (int p = tid; p < ncl; p += NT) {
+        uint32_t s = (uint16_t)clist[p];
         int32_t c = keys[s];
-        if (c < 0 || c == c_old) continue;
+        if (c == c_old) continue;
         double F = vals[s];
-        consider(b, gain_of(F, f_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq),
-                 LBL(A.labels, c), c, F, cnt[s]);
+        int32_t L = cnt[s];
+        double g = gain_of(F, f_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq);
+        consider(b, g, LBL(A.labels, c), c, F, L);
+        vals[s] = g;
+        cnt[s] = __float_as_int(__double2float_ru(gain_slack_r(F, L, f_old, l_old_n, inv_m, g)));
     }
     b = block_best<NT>(S.bs, b);
     const bool stay_best = b.c == c_old;
-    const double lower = stay_best ? 0.0 : b.g - gain_slack(b.e, b.n, f_old, l_old_n, A.m, b.g);
+    const double lower =
+        stay_best ? 0.0 : b.g - gain_slack_r(b.e, b.n, f_old, l_old_n, inv_m, b.g);
     unsigned long long nc = 0;
-    for (uint32_t s = tid; s < ts; s += NT) {
+    for (int p = tid; p < ncl; p += NT) {
+        uint32_t s = (uint16_t)clist[p];
         int32_t c = keys[s];
-        if (c < 0) continue;
         nc++;
         if (c != c_old && c != b.c) {
-            double F = vals[s];
-            double g = gain_of(F, f_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq);
-            if (g + gain_slack(F, cnt[s], f_old, l_old_n, A.m, g) >= lower) {
+            if (vals[s] + (double)__int_as_float(cnt[s]) >= lower) {
                 int k = atomicAdd(&S.nS, 1);
                 if (k < MAXS)
                     S.N[2 + k] = c;
@@ -569,6 +618,8 @@ __global__ void __launch_bounds__(BLK) k_decide_t2(DecideArgs A, const int32_t *
     __shared__ CertSmem<BLK> S;
     __shared__ int32_t cbuf[BLK];
     __shared__ double wbuf[BLK];
+    __shared__ int16_t clist[T2_MAXD];  // candidate slots (<= degree of them)
+    __shared__ int ncl;
     const int tid = threadIdx.x, lane = tid & 31;
     double *vals = reinterpret_cast<double *>(dsm);
     int32_t *keys = reinterpret_cast<int32_t *>(dsm + sizeof(double) * T2_TS);
@@ -579,7 +630,6 @@ __global__ void __launch_bounds__(BLK) k_decide_t2(DecideArgs A, const int32_t *
         vals[s] = 0.0;
         cntt[s] = 0;
     }
-    __syncthreads();
     for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
         const int64_t x = list[q];
         const int32_t i = A.subset[x];
@@ -590,28 +640,8 @@ __global__ void __launch_bounds__(BLK) k_decide_t2(DecideArgs A, const int32_t *
         while (ts < (uint64_t)(deg + deg / 2 + 2)) ts <<= 1;
         const uint32_t mask = ts - 1;
         const double ki = A.k[i];
-        if (A.integral) {
-            // exact in any order: accumulate, then the plain argmax
-            for (int64_t base = e0; base < e1; base += BLK) {
-                int64_t e = base + tid;
-                int32_t c = -1;
-                double w = 0.0;
-                if (e < e1) {
-                    int32_t j = A.nbr[e];
-                    if (j != i) {
-                        c = A.assign[j];
-                        w = A.wts[e];
-                    }
-                }
-                accum_entry(keys, vals, cntt, mask, c, w, lane);
-            }
-            __syncthreads();
-            Best b = certify_table<BLK>(A, c_old, ki, keys, vals, cntt, ts, S, true);
-            my_cand += tid == 0 ? S.ncand : 0;
-            if (tid == 0) finish_vertex(A, x, c_old, S.f_old, b.g, b.c, b.e);
-            __syncthreads();
-            continue;
-        }
+        if (tid == 0) ncl = 0;
+        __syncthreads();
         for (int64_t base = e0; base < e1; base += BLK) {
             int64_t e = base + tid;
             int32_t c = -1;
@@ -623,11 +653,17 @@ __global__ void __launch_bounds__(BLK) k_decide_t2(DecideArgs A, const int32_t *
                     w = A.wts[e];
                 }
             }
-            accum_entry(keys, vals, cntt, mask, c, w, lane);
+            accum_entry(keys, vals, cntt, mask, c, w, lane, clist, &ncl);
         }
         __syncthreads();
-        Best b = certify_table<BLK>(A, c_old, ki, keys, vals, cntt, ts, S, true);
+        Best b = certify_table<BLK>(A, c_old, ki, keys, vals, cntt, ts, clist, ncl, S, true);
         my_cand += tid == 0 ? S.ncand : 0;
+        if (A.integral) {
+            // exact in any order: the plain argmax is the reference's
+            if (tid == 0) finish_vertex(A, x, c_old, S.f_old, b.g, b.c, b.e);
+            __syncthreads();
+            continue;
+        }
         if (!resolve<BLK>(A, x, i, c_old, ki, b, S))
             t2_exact(A, x, i, c_old, ki, keys, vals, mask, cbuf, wbuf, S);
     }
@@ -637,7 +673,7 @@ __global__ void __launch_bounds__(BLK) k_decide_t2(DecideArgs A, const int32_t *
 // ------------------------------------------------------------ tier 3 (hubs)
 
 constexpr int HSB = 256;      // threads per hub pass block
-constexpr int HSLICE = 2048;  // candidate slots per hub pass block
+constexpr int HSLICE = 512;   // candidate slots per hub pass block (2 per thread)
 constexpr int HCPAD = 32;     // hub candidate counters one 128-byte line apart
 
 // Per-stage hub scratch (device pointers; hub index q is stage-local).
@@ -647,37 +683,14 @@ struct HubScratch {
     int32_t *nS;     // [nh] overlapping candidates  } of 3 * max_hubs
     int32_t *flag;   // [nh] 1 stay overlaps, 2 overflow
     int32_t *S;      // [nh * MAXS] overlapping communities
-    Best *part;      // [nh * slices] pass-1 partial bests
+    Best *part;      // [poff[nh]] pass-1 partial bests (one per slice)
     Best *best;      // [nh]
     double *fold;    // [nh] any-order e_{i->c_old}
     int32_t *lold;   // [nh] its term count
-    int slices;
+    const int64_t *blk;   // pass blocks of the stage: (hub << 32) | slice
+    const int64_t *poff;  // [nh + 1] first partial of each hub
     int64_t nh;
 };
-
-__device__ __forceinline__ uint32_t probe_insert_f(int32_t *keys, int32_t c, uint32_t mask,
-                                                   bool *fresh) {
-    uint32_t s = hslot(c, mask);
-    while (true) {
-        int32_t k = keys[s];
-        if (k == c) {
-            *fresh = false;
-            return s;
-        }
-        if (k == -1) {
-            int32_t old = atomicCAS(keys + s, -1, c);
-            if (old == -1) {
-                *fresh = true;
-                return s;
-            }
-            if (old == c) {
-                *fresh = false;
-                return s;
-            }
-        }
-        s = (s + 1) & mask;
-    }
-}
 
 // Largest hub q with eoff[q] <= t.
 __device__ __forceinline__ int64_t hub_of(const int64_t *eoff, int64_t nh, int64_t t) {
@@ -749,12 +762,12 @@ __global__ void k_hub_accum(DecideArgs A, const int32_t *list, const int64_t *eo
 // any-order sums.  Slice 0 also records the hub's e_{i->c_old} sum.
 __global__ void __launch_bounds__(HSB) k_hub_pass1(DecideArgs A, const int32_t *list,
                                                   const int64_t *toff, const int32_t *hkeys,
-                                                  const double *hvals, const int32_t *hcnt,
-                                                  HubScratch H) {
+                                                  double *hvals, int32_t *hcnt, HubScratch H) {
     __shared__ BestSmem<HSB> bs;
     __shared__ double s_fo;
     __shared__ int32_t s_lo;
-    const int64_t q = blockIdx.x;
+    const int64_t pk = H.blk[blockIdx.x];
+    const int64_t q = pk >> 32, y = pk & 0xffffffffll;
     const int32_t i = A.subset[list[q]];
     const int32_t c_old = A.assign[i];
     const int64_t base = toff[q];
@@ -763,7 +776,7 @@ __global__ void __launch_bounds__(HSB) k_hub_pass1(DecideArgs A, const int32_t *
         int s = probe_find(hkeys + base, c_old, mask);
         s_fo = s >= 0 ? hvals[base + s] : 0.0;
         s_lo = s >= 0 ? hcnt[base + s] : 0;
-        if (blockIdx.y == 0) {
+        if (y == 0) {
             H.fold[q] = s_fo;
             H.lold[q] = s_lo;
         }
@@ -771,19 +784,25 @@ __global__ void __launch_bounds__(HSB) k_hub_pass1(DecideArgs A, const int32_t *
     __syncthreads();
     const double f_old = s_fo, ki = A.k[i], a_old_excl = dsub(A.a_tot[c_old], ki);
     const int64_t n = H.ncand[q * HCPAD];
-    const int64_t p0 = (int64_t)blockIdx.y * HSLICE;
+    const int64_t p0 = y * HSLICE;
     const int64_t p1 = p0 + HSLICE < n ? p0 + HSLICE : n;
+    const double inv_m = 1.0 / A.m;
     Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
     for (int64_t p = p0 + threadIdx.x; p < p1; p += HSB) {
         int32_t s = H.cand[base + p];
         int32_t c = hkeys[base + s];
         if (c == c_old) continue;
         double F = hvals[base + s];
-        consider(b, gain_of(F, f_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq),
-                 LBL(A.labels, c), c, F, hcnt[base + s]);
+        int32_t L = hcnt[base + s];
+        double g = gain_of(F, f_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq);
+        consider(b, g, LBL(A.labels, c), c, F, L);
+        // pass 2 needs only the gain and its slack (rounded up to float)
+        hvals[base + s] = g;
+        hcnt[base + s] =
+            __float_as_int(__double2float_ru(gain_slack_r(F, L, f_old, s_lo, inv_m, g)));
     }
     b = block_best<HSB>(bs, b);
-    if (threadIdx.x == 0) H.part[q * H.slices + blockIdx.y] = b;
+    if (threadIdx.x == 0) H.part[H.poff[q] + y] = b;
 }
 
 // Pass 2, block (hub q, slice y): the hub's best from the partials, then
@@ -794,22 +813,26 @@ __global__ void __launch_bounds__(HSB) k_hub_pass2(DecideArgs A, const int32_t *
     __shared__ BestSmem<HSB> bs;
     typedef cub::BlockReduce<unsigned long long, HSB> BR;
     __shared__ typename BR::TempStorage red;
-    const int64_t q = blockIdx.x;
+    const int64_t pk = H.blk[blockIdx.x];
+    const int64_t q = pk >> 32, y = pk & 0xffffffffll;
     const int32_t i = A.subset[list[q]];
     const int32_t c_old = A.assign[i];
     const int64_t base = toff[q];
     Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
-    for (int t = threadIdx.x; t < H.slices; t += HSB) {
-        Best o = H.part[q * H.slices + t];
+    for (int64_t t = H.poff[q] + threadIdx.x; t < H.poff[q + 1]; t += HSB) {
+        Best o = H.part[t];
         consider(b, o.g, o.l, o.c, o.e, o.n);
     }
     b = block_best<HSB>(bs, b);
     const double f_old = H.fold[q], ki = A.k[i], a_old_excl = dsub(A.a_tot[c_old], ki);
     const int32_t lo_n = H.lold[q];
     const bool stay_best = b.c == c_old;
-    const double lower = stay_best ? 0.0 : b.g - gain_slack(b.e, b.n, f_old, lo_n, A.m, b.g);
+    const double lower =
+        stay_best ? 0.0 : b.g - gain_slack_r(b.e, b.n, f_old, lo_n, 1.0 / A.m, b.g);
+    (void)ki;
+    (void)a_old_excl;
     const int64_t n = H.ncand[q * HCPAD];
-    const int64_t p0 = (int64_t)blockIdx.y * HSLICE;
+    const int64_t p0 = y * HSLICE;
     const int64_t p1 = p0 + HSLICE < n ? p0 + HSLICE : n;
     unsigned long long nc = 0;
     for (int64_t p = p0 + threadIdx.x; p < p1; p += HSB) {
@@ -817,9 +840,7 @@ __global__ void __launch_bounds__(HSB) k_hub_pass2(DecideArgs A, const int32_t *
         int32_t c = hkeys[base + s];
         nc++;
         if (!A.integral && c != c_old && c != b.c) {
-            double F = hvals[base + s];
-            double g = gain_of(F, f_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq);
-            if (g + gain_slack(F, hcnt[base + s], f_old, lo_n, A.m, g) >= lower) {
+            if (hvals[base + s] + (double)__int_as_float(hcnt[base + s]) >= lower) {
                 int k = atomicAdd(H.nS + q, 1);
                 if (k < MAXS)
                     H.S[q * MAXS + k] = c;
@@ -834,7 +855,7 @@ __global__ void __launch_bounds__(HSB) k_hub_pass2(DecideArgs A, const int32_t *
     unsigned long long tot = BR(red).Sum(nc);
     if (threadIdx.x == 0) {
         if (A.cand && tot) atomicAdd(A.cand, tot);
-        if (blockIdx.y == 0) {
+        if (y == 0) {
             H.best[q] = b;
             if (!stay_best && lower <= 0.0) atomicOr(H.flag + q, 1);  // "stay" overlaps
         }
@@ -978,12 +999,13 @@ __global__ void k_fill_i32_d(int32_t *p, int64_t n, int32_t v) {
 }
 
 void Plan::release() {
-    void *ps[] = {tier_list, hub_eoff, hub_toff, hkeys, hvals, hcnt, hcand, hsmall, hS, hpart,
+    void *ps[] = {tier_list, hub_eoff, hub_toff, hub_poff, hub_blk, hkeys, hvals, hcnt, hcand,
+                  hsmall, hS, hpart,
                   hbest, hfold, hlold};
     for (void *p : ps)
         if (p) cudaFree(p);
     tier_list = nullptr;
-    hub_eoff = hub_toff = nullptr;
+    hub_eoff = hub_toff = hub_poff = hub_blk = nullptr;
     hkeys = hcnt = hcand = hsmall = hS = hlold = nullptr;
     hvals = hfold = nullptr;
     hpart = hbest = nullptr;
@@ -1044,36 +1066,48 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
     PLV_CUDA(cudaMemcpyAsync(deg.data(), d_deg.get(), sizeof(int64_t) * nh, cudaMemcpyDeviceToHost,
                              s));
     PLV_CUDA(cudaStreamSynchronize(s));
-    std::vector<int64_t> eoff, toff;
-    int64_t h0 = 0;
+    std::vector<int64_t> eoff, toff, poff, blk;
+    int64_t h0 = 0, max_parts = 1;
     for (int64_t a = 0; a < nst; a++) {
         StagePlan &sp = P.st[a];
         sp.hub_base = (int64_t)eoff.size();
-        int64_t acc = 0, tacc = 0;
+        sp.hub_blk_base = (int64_t)blk.size();
+        int64_t acc = 0, tacc = 0, pacc = 0;
         eoff.push_back(0);
         toff.push_back(0);
+        poff.push_back(0);
         for (int64_t z = 0; z < sp.tcount[3]; z++) {
             int64_t d = deg[h0 + z];
             int64_t cap = 64;
             while (cap < 2 * d + 2) cap <<= 1;
             int64_t sl = (d + HSLICE - 1) / HSLICE;  // candidates <= degree
-            sp.hub_slices = sl > sp.hub_slices ? sl : sp.hub_slices;
+            for (int64_t y = 0; y < sl; y++) blk.push_back((z << 32) | y);
             acc += d;
             tacc += cap;
+            pacc += sl;
             eoff.push_back(acc);
             toff.push_back(tacc);
+            poff.push_back(pacc);
         }
         h0 += sp.tcount[3];
         sp.hub_entries = acc;
+        sp.hub_nblk = pacc;
+        max_parts = pacc > max_parts ? pacc : max_parts;
         P.max_hub_entries = acc > P.max_hub_entries ? acc : P.max_hub_entries;
         P.max_hubs = sp.tcount[3] > P.max_hubs ? sp.tcount[3] : P.max_hubs;
         P.max_table = tacc > P.max_table ? tacc : P.max_table;
     }
     P.hub_eoff = dalloc<int64_t>(eoff.size());
     P.hub_toff = dalloc<int64_t>(toff.size());
+    P.hub_poff = dalloc<int64_t>(poff.size());
+    P.hub_blk = dalloc<int64_t>(blk.size());
     PLV_CUDA(cudaMemcpyAsync(P.hub_eoff, eoff.data(), sizeof(int64_t) * eoff.size(),
                              cudaMemcpyHostToDevice, s));
     PLV_CUDA(cudaMemcpyAsync(P.hub_toff, toff.data(), sizeof(int64_t) * toff.size(),
+                             cudaMemcpyHostToDevice, s));
+    PLV_CUDA(cudaMemcpyAsync(P.hub_poff, poff.data(), sizeof(int64_t) * poff.size(),
+                             cudaMemcpyHostToDevice, s));
+    PLV_CUDA(cudaMemcpyAsync(P.hub_blk, blk.data(), sizeof(int64_t) * blk.size(),
                              cudaMemcpyHostToDevice, s));
     int64_t T = P.max_table;
     P.hkeys = dalloc<int32_t>(T);
@@ -1088,9 +1122,7 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
     P.hsmall = dalloc<int32_t>((HCPAD + 2) * H);
     PLV_CUDA(cudaMemsetAsync(P.hsmall, 0, sizeof(int32_t) * (HCPAD + 2) * H, s));
     P.hS = dalloc<int32_t>(H * MAXS);
-    P.max_slices = 1;
-    for (auto &sp : P.st) P.max_slices = sp.hub_slices > P.max_slices ? sp.hub_slices : P.max_slices;
-    P.hpart = dalloc<Best>(H * P.max_slices);
+    P.hpart = dalloc<Best>(max_parts);
     P.hbest = dalloc<Best>(H);
     P.hfold = dalloc<double>(H);
     P.hlold = dalloc<int32_t>(H);
@@ -1159,14 +1191,15 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
         const int64_t *toff = P.hub_toff + sp.hub_base;
         int64_t nh = sp.tcount[3], E = sp.hub_entries;
         const int64_t Hm = P.max_hubs;
-        HubScratch H{P.hcand,   P.hsmall, P.hsmall + HCPAD * Hm, P.hsmall + (HCPAD + 1) * Hm,
-                     P.hS,      P.hpart,  P.hbest,              P.hfold,
-                     P.hlold,   (int)sp.hub_slices,             nh};
+        HubScratch H{P.hcand,  P.hsmall, P.hsmall + HCPAD * Hm, P.hsmall + (HCPAD + 1) * Hm,
+                     P.hS,     P.hpart,  P.hbest,              P.hfold,
+                     P.hlold,  P.hub_blk + sp.hub_blk_base,    P.hub_poff + sp.hub_base,
+                     nh};
         PLV_CUDA(cudaMemsetAsync(P.hsmall, 0, sizeof(int32_t) * (HCPAD + 2) * Hm, st));
         k_hub_accum<<<grid_for(E, 256), 256, 0, st>>>(A, list, eoff, toff, nh, E, P.hkeys, P.hvals,
                                                       P.hcnt, H);
         PLV_LAUNCH_CHECK();
-        dim3 g2((unsigned)nh, (unsigned)sp.hub_slices);
+        unsigned g2 = (unsigned)sp.hub_nblk;
         k_hub_pass1<<<g2, HSB, 0, st>>>(A, list, toff, P.hkeys, P.hvals, P.hcnt, H);
         PLV_LAUNCH_CHECK();
         k_hub_pass2<<<g2, HSB, 0, st>>>(A, list, toff, P.hkeys, P.hvals, P.hcnt, H);

@@ -64,7 +64,8 @@ struct StagePlan {
     int64_t tstart[4] = {0, 0, 0, 0};  // into the tier list
     int64_t hub_base = 0;              // this stage's first hub_eoff / hub_toff entry
     int64_t hub_entries = 0;
-    int64_t hub_slices = 0;  // candidate slices per hub (pass blocks)
+    int64_t hub_nblk = 0;      // hub pass blocks (one per candidate slice)
+    int64_t hub_blk_base = 0;  // first of them in hub_blk
 };
 
 struct Best;  // decide.cu
@@ -78,6 +79,8 @@ struct Plan {
     int32_t *tier_list = nullptr;  // stage-local indices grouped by (stage, tier)
     int64_t *hub_eoff = nullptr;   // per stage: nh+1 entry offsets (from 0)
     int64_t *hub_toff = nullptr;   // per stage: nh+1 table offsets (from 0, pow2 sizes)
+    int64_t *hub_poff = nullptr;   // per stage: nh+1 partial-best offsets (slices)
+    int64_t *hub_blk = nullptr;    // pass blocks, (hub << 32) | slice, stage after stage
     int64_t max_hub_entries = 0, max_hubs = 0, max_table = 0;
     int32_t *hkeys = nullptr;  // hub tables: key -1 / val 0 / cnt 0 when clean
     double *hvals = nullptr;

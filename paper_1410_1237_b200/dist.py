@@ -1,0 +1,151 @@
+"""Multi-GPU local moving: 1D vertex partition, replicated state.
+
+The reference has no distributed mode; this is new design.  decide
+(PL/_kernels.pyx:21-101) is independent per vertex given the stage's entry
+state, so the vertices of every stage are split across ranks by contiguous,
+nnz-balanced vertex ranges.  Because a stage lists its vertices in ascending
+id, each rank's share of a stage is one contiguous slice of it, and rank
+order is subset order.  Per stage:
+
+  1. every rank decides its slice (target, moved, e_old, e_best);
+  2. the slices are all-gathered in rank order (one padded all_gather per
+     array over NCCL / gloo);
+  3. every rank applies the whole stage with the same exact, order-preserving
+     apply, so assignment / a_tot / w_internal / sizes stay bit-identical on
+     all ranks and to the 1-GPU run (no reduction of float64 deltas, whose
+     order would change the bits).
+
+Modularity needs no communication (replicated aggregates).  Uncoloured
+iterations gather (target, moved) and replay the apply with the live rule on
+every rank.  The compute steps are callbacks, so the same driver runs the CUDA
+kernels (`CudaStageOps`) on GPUs over NCCL and a CPU checker over gloo in the
+tests.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def partition_bounds(offsets, world: int) -> np.ndarray:
+    """Contiguous vertex ranges balancing adjacency entries: rank r owns
+    vertices [bounds[r], bounds[r+1])."""
+    off = np.asarray(offsets, dtype=np.int64)
+    n = len(off) - 1
+    total = int(off[-1])
+    targets = (total * np.arange(1, world, dtype=np.float64) / world).astype(np.int64)
+    cuts = np.searchsorted(off, targets, side="left").clip(0, n)
+    bounds = np.concatenate([[0], cuts, [n]]).astype(np.int64)
+    return np.maximum.accumulate(bounds)
+
+
+def stage_slices(stage, bounds) -> np.ndarray:
+    """Slice boundaries of an ascending stage vertex list per rank:
+    rank r decides stage[s[r]:s[r+1]]."""
+    return np.searchsorted(np.asarray(stage), np.asarray(bounds), side="left").astype(np.int64)
+
+
+def allgather_slices(local_arrays, counts, group=None):
+    """All-gather 1-D tensors whose per-rank lengths are `counts`, concatenated
+    in rank order (padded to the largest count)."""
+    import torch
+    import torch.distributed as dist
+    world = len(counts)
+    cmax = max(1, max(counts))
+    out = []
+    for t in local_arrays:
+        pad = torch.zeros(cmax, dtype=t.dtype, device=t.device)
+        pad[:t.numel()] = t
+        parts = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(parts, pad, group=group)
+        out.append(torch.cat([parts[r][:counts[r]] for r in range(world)]))
+    return out
+
+
+@dataclass
+class DecideSlice:
+    target: object
+    moved: object
+    e_old: object
+    e_best: object
+
+
+class DistributedIteration:
+    """One local-move iteration over a stage list, decide split across ranks.
+
+    ops.decide(stage_index, lo, hi) -> DecideSlice for stage[lo:hi]
+    ops.apply(stage_index, DecideSlice_full) -> moves (replicated, exact)
+    ops.modularity() -> Q (replicated)
+    """
+
+    def __init__(self, ops, stages_host, bounds, rank: int, world: int, group=None):
+        self.ops, self.rank, self.world, self.group = ops, rank, world, group
+        self.slices = [stage_slices(st, bounds) for st in stages_host]
+
+    def run(self):
+        moves = 0
+        for a, sl in enumerate(self.slices):
+            lo, hi = int(sl[self.rank]), int(sl[self.rank + 1])
+            d = self.ops.decide(a, lo, hi)
+            counts = [int(sl[r + 1] - sl[r]) for r in range(self.world)]
+            if self.world > 1:
+                t, m, eo, eb = allgather_slices([d.target, d.moved, d.e_old, d.e_best], counts,
+                                                self.group)
+                d = DecideSlice(t, m, eo, eb)
+            moves += self.ops.apply(a, d)
+        return moves, self.ops.modularity()
+
+
+class CudaStageOps:
+    """Stage callbacks on the device (libplv): decide a slice of a stage with
+    plv_decide_ex, apply a whole stage with plv_apply."""
+
+    def __init__(self, g, state, stages, flags):
+        import torch
+        from . import _lib
+        self._lib = _lib
+        self.g, self.d = g, state.device()
+        self.stages = stages          # list of device int32 tensors
+        self.flags = flags | (_lib.F_INTEGRAL if g.integral else 0)
+        dev = self.d["assignment"].device
+        cap = max(1, max(int(s.numel()) for s in stages))
+        self.tg = torch.empty(cap, dtype=torch.int32, device=dev)
+        self.mv = torch.empty(cap, dtype=torch.uint8, device=dev)
+        self.eo = torch.empty(cap, dtype=torch.float64, device=dev)
+        self.eb = torch.empty(cap, dtype=torch.float64, device=dev)
+        self.q = torch.empty(1, dtype=torch.float64, device=dev)
+
+    def decide(self, a, lo, hi):
+        L, g, d, _lib = self._lib.lib(), self.g, self.d, self._lib
+        sub = self.stages[a][lo:hi]
+        ns = hi - lo
+        if ns:
+            _lib.check(L.decide_ex(
+                _lib.ptr(g.d_off), _lib.ptr(g.d_nbr), _lib.ptr(g.d_w), _lib.ptr(g.d_k),
+                _lib.ptr(d["labels"]), _lib.ptr(sub), ns, _lib.ptr(d["assignment"]),
+                _lib.ptr(d["a_tot"]), _lib.ptr(d["sizes"]), g.total_weight, self.flags,
+                _lib.ptr(self.tg), _lib.ptr(self.mv), _lib.ptr(self.eo), _lib.ptr(self.eb),
+                None, _lib.stream()), "decide")
+        return DecideSlice(self.tg[:ns].clone(), self.mv[:ns].clone(), self.eo[:ns].clone(),
+                           self.eb[:ns].clone())
+
+    def apply(self, a, dfull):
+        L, g, d, _lib = self._lib.lib(), self.g, self.d, self._lib
+        sub = self.stages[a]
+        moves = _lib.i64_host(1)
+        _lib.check(L.apply(
+            _lib.ptr(g.d_off), _lib.ptr(g.d_nbr), _lib.ptr(g.d_w), _lib.ptr(g.d_k),
+            _lib.ptr(g.d_selfw), g.num_vertices, _lib.ptr(sub), int(sub.numel()),
+            _lib.ptr(dfull.target), _lib.ptr(dfull.moved), _lib.ptr(dfull.e_old),
+            _lib.ptr(dfull.e_best), self.flags, _lib.ptr(d["assignment"]), _lib.ptr(d["a_tot"]),
+            _lib.ptr(d["w_internal"]), _lib.ptr(d["sizes"]), _lib.hp(moves), _lib.stream()),
+            "apply")
+        return int(moves[0])
+
+    def modularity(self):
+        from .modularity import CommunityState, modularity_device
+        s = CommunityState.from_device(self.d["assignment"], self.d["a_tot"],
+                                       self.d["w_internal"], self.d["sizes"], self.d["labels"])
+        return float(modularity_device(self.g, s, self.q).item())

@@ -247,3 +247,30 @@ def test_rmat_with_hubs_matches_oracle(orc, scale, cutoff):
     h = pl.run(g, pl.RunConfig(color_cutoff=cutoff, max_iterations_per_phase=30))
     assert np.array_equal(h.final_assignment, oh.final_assignment)
     assert h.final_modularity == oh.final_modularity
+
+
+def test_distributed_iteration_single_rank_cuda(orc):
+    """The multi-GPU driver with the CUDA callbacks (world 1) equals the
+    phase engine's coloured iteration and the oracle."""
+    from paper_1410_1237_b200 import dist as pdist
+    from paper_1410_1237_b200 import synthetic as syn
+    import torch
+    u, v, w = syn.rmat_records(13, 16, seed=2)
+    n = 1 << 13
+    g = pl.Graph.from_edges(u, v, w, num_vertices=n)
+    og = orc.from_edges(u, v, w, num_vertices=n)
+    col = pl.color_graph(g)
+    off, vtx = col.device_classes()
+    stages = [vtx[int(off[c]):int(off[c + 1])] for c in range(col.num_colors)]
+    stages_h = [s_.cpu().numpy().astype(np.int64) for s_ in stages]
+    s = pl.singleton_state(g)
+    from paper_1410_1237_b200 import _lib
+    ops = pdist.CudaStageOps(g, s, stages, _lib.F_INDEPENDENT)
+    it = pdist.DistributedIteration(ops, stages_h, pdist.partition_bounds(g.adjacency_offsets, 1),
+                                    0, 1)
+    os_ = orc.singleton_state(og)
+    for _ in range(2):
+        moves, q = it.run()
+        omoves = sum(orc.run_iteration(og, os_, st) for st in stages_h)
+        assert moves == omoves and q == orc.modularity(og, os_)
+    assert np.array_equal(s.assignment, os_.assignment)
