@@ -74,11 +74,14 @@ def _dist():
 # ------------------------------------------------------------------ clocks
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + throttle reasons during the timed region (NVML every 5 ms,
+    nvidia-smi as a fallback)."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits: hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+    BITS = (0x8, 0x40, 0x20, 0x4)
 
     def __init__(self, index: int):
         self.index = index
@@ -87,6 +90,20 @@ class ClockSampler:
         self._t = None
 
     def _loop(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append([str(self.index), str(sm), str(mx), "", ""] +
+                                 ["Active" if rs & b else "Not Active" for b in self.BITS])
+                self._stop.wait(0.005)
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -388,10 +405,10 @@ def run_ours(args):
             cl = col.classes()
         else:
             cl = [np.arange(n, dtype=np.int64)]
-        times, kind, cores, Mc = cpu_iteration_rate(off, nb, wt, sw, cl, steps=2)
+        times, kind, cores, Mc = cpu_iteration_rate(off, nb, wt, sw, cl, steps=3, warmup=1)
         tc = float(np.mean(times))
         cpu = {"value": Mc / tc, "unit": UNIT, "cores": cores, "kind": kind,
-               "sample": f"2 phase-1 {args.mode} iterations of the same graph "
+               "sample": f"3 phase-1 {args.mode} iterations of the same graph (after 1 warm-up) "
                          f"({len(cl)} stages), singleton start; {tc * 1e3:.0f} ms each"}
 
     if rank == 0:

@@ -53,8 +53,10 @@ __device__ __forceinline__ double gain_of(double e_c, double e_old, double m, do
 }
 
 // |sequential - any-order| bound for a sum of L positive terms near F.
+// A sum of at most two positive terms is the same in every order (0 + a = a,
+// a + b = b + a), so it carries no error.
 __device__ __forceinline__ double sum_err(double F, int32_t L) {
-    return L > 1 ? 2.01 * (double)(L - 1) * U_RND * F : 0.0;
+    return L > 2 ? 2.01 * (double)(L - 1) * U_RND * F : 0.0;
 }
 
 // Bound on |gain from exact sums - gain from any-order sums| (see header):
@@ -386,6 +388,9 @@ __device__ __forceinline__ void accum_entry(int32_t *keys, double *vals, int32_t
 // bound, so the reciprocal's rounding is absorbed by the 1.01 / 8u factors).
 __device__ __forceinline__ double gain_slack_r(double Fc, int32_t Lc, double Fo, int32_t Lo,
                                                double inv_m, double g) {
+    // both sums exact -> the gain is computed from the reference's own
+    // operands with the reference's operations: no slack at all
+    if (Lc <= 2 && Lo <= 2) return 0.0;
     return 1.02 * ((sum_err(Fc, Lc) + sum_err(Fo, Lo)) * inv_m) +
            8.0 * U_RND * (fabs(Fc - Fo) * inv_m * 1.001 + fabs(g)) + 1e-300;
 }
@@ -428,15 +433,17 @@ __device__ Best certify_table(const DecideArgs &A, int32_t c_old, double ki, int
     }
     b = block_best<NT>(S.bs, b);
     const bool stay_best = b.c == c_old;
-    const double lower =
-        stay_best ? 0.0 : b.g - gain_slack_r(b.e, b.n, f_old, l_old_n, inv_m, b.g);
+    const double slack_b = stay_best ? 0.0 : gain_slack_r(b.e, b.n, f_old, l_old_n, inv_m, b.g);
+    const double lower = stay_best ? 0.0 : b.g - slack_b;
     unsigned long long nc = 0;
     for (int p = tid; p < ncl; p += NT) {
         uint32_t s = (uint16_t)clist[p];
         int32_t c = keys[s];
         nc++;
         if (c != c_old && c != b.c) {
-            if (vals[s] + (double)__int_as_float(cnt[s]) >= lower) {
+            // two exact gains were already ordered exactly by block_best
+            double sl = (double)__int_as_float(cnt[s]);
+            if ((sl > 0.0 || slack_b > 0.0) && vals[s] + sl >= lower) {
                 int k = atomicAdd(&S.nS, 1);
                 if (k < MAXS)
                     S.N[2 + k] = c;
@@ -451,7 +458,8 @@ __device__ Best certify_table(const DecideArgs &A, int32_t c_old, double ki, int
         }
     }
     if (tid == 0) {
-        if (!stay_best && lower <= 0.0) S.flag |= 1;  // "stay" (exact gain 0) overlaps
+        // "stay" (exact gain 0) overlaps an inexact best
+        if (!stay_best && slack_b > 0.0 && lower <= 0.0) S.flag |= 1;
         S.ncand = 0;
     }
     __syncthreads();
@@ -523,12 +531,20 @@ __device__ bool resolve(const DecideArgs &A, int64_t x, int32_t i, int32_t c_old
     if (S.flag & 2) return false;
     const bool certain = S.nS == 0 && !(S.flag & 1);
     if (certain) {
-        bool moved = b.c != c_old;  // certain: exact gain > 0 and the best
+        // certain: b is the exact best; the exact gain is > 0 iff b.g > 0
+        // (an inexact best has lower > 0 when "stay" does not overlap it)
+        bool moved = b.c != c_old && b.g > 0.0;
         if (moved && A.sizes[c_old] == 1 && A.sizes[b.c] == 1 &&
             LBL(A.labels, b.c) > LBL(A.labels, c_old))
             moved = false;
-        if (!moved) {
-            if (tid == 0) finish_vertex(A, x, c_old, S.f_old, 0.0, c_old, 0.0);
+        // a mover whose two sums have <= 2 terms already holds the exact e values
+        if (!moved || (b.n <= 2 && S.l_old <= 2)) {
+            if (tid == 0) {
+                if (moved)
+                    finish_vertex(A, x, c_old, S.f_old, b.g, b.c, b.e);
+                else
+                    finish_vertex(A, x, c_old, S.f_old, 0.0, c_old, 0.0);
+            }
             __syncthreads();
             return true;
         }
@@ -827,8 +843,9 @@ __global__ void __launch_bounds__(HSB) k_hub_pass2(DecideArgs A, const int32_t *
     const double f_old = H.fold[q], ki = A.k[i], a_old_excl = dsub(A.a_tot[c_old], ki);
     const int32_t lo_n = H.lold[q];
     const bool stay_best = b.c == c_old;
-    const double lower =
-        stay_best ? 0.0 : b.g - gain_slack_r(b.e, b.n, f_old, lo_n, 1.0 / A.m, b.g);
+    const double slack_b =
+        stay_best ? 0.0 : gain_slack_r(b.e, b.n, f_old, lo_n, 1.0 / A.m, b.g);
+    const double lower = stay_best ? 0.0 : b.g - slack_b;
     (void)ki;
     (void)a_old_excl;
     const int64_t n = H.ncand[q * HCPAD];
@@ -840,7 +857,8 @@ __global__ void __launch_bounds__(HSB) k_hub_pass2(DecideArgs A, const int32_t *
         int32_t c = hkeys[base + s];
         nc++;
         if (!A.integral && c != c_old && c != b.c) {
-            if (hvals[base + s] + (double)__int_as_float(hcnt[base + s]) >= lower) {
+            double sl = (double)__int_as_float(hcnt[base + s]);
+            if ((sl > 0.0 || slack_b > 0.0) && hvals[base + s] + sl >= lower) {
                 int k = atomicAdd(H.nS + q, 1);
                 if (k < MAXS)
                     H.S[q * MAXS + k] = c;
@@ -857,7 +875,8 @@ __global__ void __launch_bounds__(HSB) k_hub_pass2(DecideArgs A, const int32_t *
         if (A.cand && tot) atomicAdd(A.cand, tot);
         if (y == 0) {
             H.best[q] = b;
-            if (!stay_best && lower <= 0.0) atomicOr(H.flag + q, 1);  // "stay" overlaps
+            if (!stay_best && slack_b > 0.0 && lower <= 0.0)
+                atomicOr(H.flag + q, 1);  // "stay" overlaps an inexact best
         }
     }
 }
@@ -883,12 +902,17 @@ __global__ void __launch_bounds__(HBLK) k_hub_decide(DecideArgs A, const int32_t
             if (tid == 0) finish_vertex(A, x, c_old, H.fold[q], b.g, b.c, b.e);
             done = true;
         } else if (nS == 0 && !flag) {
-            bool moved = b.c != c_old;  // certain: the exact best, with exact gain > 0
+            bool moved = b.c != c_old && b.g > 0.0;  // certain: the exact best
             if (moved && A.sizes[c_old] == 1 && A.sizes[b.c] == 1 &&
                 LBL(A.labels, b.c) > LBL(A.labels, c_old))
                 moved = false;
-            if (!moved) {
-                if (tid == 0) finish_vertex(A, x, c_old, H.fold[q], 0.0, c_old, 0.0);
+            if (!moved || (b.n <= 2 && H.lold[q] <= 2)) {  // exact sums: no refold
+                if (tid == 0) {
+                    if (moved)
+                        finish_vertex(A, x, c_old, H.fold[q], b.g, b.c, b.e);
+                    else
+                        finish_vertex(A, x, c_old, H.fold[q], 0.0, c_old, 0.0);
+                }
                 done = true;
             }
         }
