@@ -360,14 +360,33 @@ struct CertSmem {
     unsigned long long ncand;
 };
 
+// Sum of w over the lanes of this lane's match group `grp` (any order).  Every
+// shuffle is a full-warp shuffle inside a warp-uniform loop: a shuffle under
+// the per-group mask would split the warp into one serialised shuffle per
+// distinct group.
+__device__ __forceinline__ double group_sum(unsigned grp, double w) {
+    const int n = __popc(grp);
+    const int nmax = __reduce_max_sync(FULL, (unsigned)n);
+    double v = 0.0;
+    unsigned g = grp;
+    for (int t = 0; t < nmax; t++) {
+        const int src = g ? __ffs(g) - 1 : (int)(threadIdx.x & 31);
+        const double x = __shfl_sync(FULL, w, src);
+        if (g) {
+            v = dadd(v, x);
+            g &= g - 1;
+        }
+    }
+    return v;
+}
+
 // Accumulate one entry (c, w) with warp aggregation: lanes with the same
 // community combine (any order) before one atomic per group.
 __device__ __forceinline__ void accum_entry(int32_t *keys, double *vals, int32_t *cnt,
                                             uint32_t mask, int32_t c, double w, int lane,
                                             int16_t *clist, int *ncl) {
     unsigned grp = __match_any_sync(FULL, c);
-    double v = 0.0;
-    for (unsigned g = grp; g; g &= g - 1) v = dadd(v, __shfl_sync(grp, w, __ffs(g) - 1));
+    double v = group_sum(grp, w);
     bool fresh = false;
     uint32_t s = 0;
     if (c >= 0 && lane == __ffs(grp) - 1) {
@@ -747,8 +766,7 @@ __global__ void k_hub_accum(DecideArgs A, const int32_t *list, const int64_t *eo
         // group lanes by (hub, community)
         uint64_t key = c >= 0 ? (((uint64_t)q << 32) | (uint32_t)c) : ~0ull;
         unsigned grp = __match_any_sync(FULL, key);
-        double v = 0.0;
-        for (unsigned g = grp; g; g &= g - 1) v = dadd(v, __shfl_sync(grp, w, __ffs(g) - 1));
+        double v = group_sum(grp, w);
         const bool leader = c >= 0 && lane == __ffs(grp) - 1;
         const int64_t base = toff[q];
         bool fresh = false;

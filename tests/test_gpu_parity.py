@@ -214,7 +214,7 @@ def _tie_graph(n_leaves, w=0.1, extra=3):
     return np.array(u), np.array(v), np.array(ww), nxt
 
 
-@pytest.mark.parametrize("n_leaves", [10, 40, 3000])
+@pytest.mark.parametrize("n_leaves", [10, 40, 3000, 12000, 20000])
 def test_exact_ties_are_resolved_like_the_reference(orc, n_leaves):
     u, v, w, n = _tie_graph(n_leaves)
     g = pl.Graph.from_edges(u, v, w, num_vertices=n)
@@ -243,6 +243,34 @@ def test_rmat_with_hubs_matches_oracle(orc, scale, cutoff):
     og = orc.from_edges(u, v, w, num_vertices=n)
     g = pl.Graph.from_edges(u, v, w, num_vertices=n)
     assert g.max_degree > 2048        # the hub tier is exercised
+    oh = orc.run(og, color_cutoff=cutoff, max_iterations=30)
+    h = pl.run(g, pl.RunConfig(color_cutoff=cutoff, max_iterations_per_phase=30))
+    assert np.array_equal(h.final_assignment, oh.final_assignment)
+    assert h.final_modularity == oh.final_modularity
+
+
+def _multi_hub_graph(seed=3):
+    """Random background plus vertices on both sides of the block-tier / hub-tier
+    boundary (degree 2048) and hubs up to 40000 entries."""
+    rng = np.random.default_rng(seed)
+    n = 60000
+    u = [rng.integers(0, n, 200000)]
+    v = [rng.integers(0, n, 200000)]
+    for h, d in enumerate([2030, 2049, 9000, 16370, 16385, 20000, 40000]):
+        u.append(np.full(d, h))
+        v.append(rng.choice(np.arange(100, n), d, replace=False))
+    u, v = np.concatenate(u), np.concatenate(v)
+    w = rng.uniform(1.0, 10.0, len(u))
+    return u, v, w, n
+
+
+@pytest.mark.parametrize("cutoff", [0, 100_000])
+def test_hub_tiers_match_oracle(orc, cutoff):
+    u, v, w, n = _multi_hub_graph()
+    og = orc.from_edges(u, v, w, num_vertices=n)
+    g = pl.Graph.from_edges(u, v, w, num_vertices=n)
+    deg = np.diff(g.adjacency_offsets)
+    assert (deg <= 2048).sum() >= 1 and (deg > 2048).sum() >= 6
     oh = orc.run(og, color_cutoff=cutoff, max_iterations=30)
     h = pl.run(g, pl.RunConfig(color_cutoff=cutoff, max_iterations_per_phase=30))
     assert np.array_equal(h.final_assignment, oh.final_assignment)

@@ -1,0 +1,19 @@
+# Round profile capture: tests, bench (both arms), launch list, per-iteration
+# kernel/DRAM summaries, one full ncu capture of the top decide kernel.
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests.log
+timeout 600 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 300 python bench.py --mode uncolored --no-cpu-baseline --no-louvain > gpurun_out/bench_u.json 2> gpurun_out/bench_u.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv \
+  --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-louvain \
+  > gpurun_out/ncu_launch.log 2>&1
+for m in colored uncolored; do
+timeout 600 ncu --profile-from-start off --clock-control none \
+  --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv \
+  --log-file gpurun_out/iter_$m.csv python tools/profile_iter.py --mode $m > gpurun_out/pi_$m.log 2>&1
+done
+timeout 900 ncu --profile-from-start off -k regex:k_decide_t2 -c 1 --set full --import-source on \
+  --clock-control none -f -o gpurun_out/t2_full python tools/profile_iter.py --mode uncolored \
+  > gpurun_out/t2_full.log 2>&1
