@@ -137,6 +137,18 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def _traffic(mode: str, scale: int):
+    """DRAM bytes per iteration of the decide kernels, from the committed ncu
+    capture (profiles/r01_traffic.json; C2 only), else None."""
+    if scale != CONFIG["scale"]:
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+            return float(json.load(fh)[mode])
+    except Exception:
+        return None
+
+
 def _peak_hbm():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -423,8 +435,10 @@ def run_ours(args):
                        "parallelism": "replicas" if ws > 1 else "single",
                        "l2": "inputs larger than L2 (CSR %.0f MB)" % (nnz * 12 / 1e6)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "decide (tiers 0-3)",
+                         "frac": achieved / peak, "traffic": _traffic(args.mode, scale),
+                         "traffic_unit": "bytes per iteration (ncu, cold caches)",
+                         "peak_kind": peak_kind,
+                         "kernel": "decide (tiers 0-4)",
                          "bytes_per_iter": decide_bytes, "ms_per_iter": decide_ms},
             "iteration": {"bytes": iter_bytes, "gbs": iter_bytes / t_iter / 1e9,
                           "frac": iter_bytes / t_iter / 1e9 / peak,

@@ -8,12 +8,13 @@
 //                         in adjacency order (exact by construction)
 //   tier 1  deg <= 128    warp per vertex, shared-memory hash table, 32-entry
 //                         chunks folded in lane order (exact by construction)
-//   tier 2  deg <= 2048   block per vertex, shared-memory table  } certified
-//   tier 3  larger (hubs) all entries of the stage's hubs at once,} parallel
-//                         global hash tables                       } sums
-// Certified parallel sums (tiers 2-3).  Reproducing a sequential fold needs
+//   tier 2  deg <= 680    block per vertex, 16 KB shared table    } certified
+//   tier 3  deg <= 2048   block per vertex, 64 KB shared table    } parallel
+//   tier 4  larger (hubs) all entries of the stage's hubs at once,} sums
+//                         global hash tables                       }
+// Certified parallel sums (tiers 2-4).  Reproducing a sequential fold needs
 // its additions in order -- a dependent DADD chain of 8.2 cycles per add on
-// B200 -- so tiers 2-3 first sum every community in ANY order with atomics,
+// B200 -- so tiers 2-4 first sum every community in ANY order with atomics,
 // along with its term count L.  Both sums are within 2 gamma_{L-1} * sum of
 // each other (gamma_k = k u / (1 - k u), u = 2^-53), which bounds how far
 // every computed gain can be from the reference's.  The decision is kept only
@@ -79,9 +80,28 @@ __device__ __forceinline__ uint32_t hslot(int32_t c, uint32_t mask) {
     return h & mask;
 }
 
+// Open-addressing geometry: power-of-two tables (mask) and arbitrary-size
+// tables (multiply-shift range reduction of the same hash), linear probing.
+struct PowTab {
+    uint32_t mask;
+    __device__ __forceinline__ uint32_t first(int32_t c) const { return hslot(c, mask); }
+    __device__ __forceinline__ uint32_t next(uint32_t s) const { return (s + 1) & mask; }
+    __device__ __forceinline__ uint32_t size() const { return mask + 1; }
+};
+
+struct ModTab {
+    uint32_t ts;
+    __device__ __forceinline__ uint32_t first(int32_t c) const {
+        return (uint32_t)(((uint64_t)hslot(c, 0xffffffffu) * ts) >> 32);
+    }
+    __device__ __forceinline__ uint32_t next(uint32_t s) const { return s + 1 == ts ? 0 : s + 1; }
+    __device__ __forceinline__ uint32_t size() const { return ts; }
+};
+
 // Find-or-insert c; tables start cleared to key -1.
-__device__ __forceinline__ uint32_t probe_insert(int32_t *keys, int32_t c, uint32_t mask) {
-    uint32_t s = hslot(c, mask);
+template <class Tab>
+__device__ __forceinline__ uint32_t probe_insert(int32_t *keys, int32_t c, Tab T) {
+    uint32_t s = T.first(c);
     while (true) {
         int32_t k = keys[s];
         if (k == c) return s;
@@ -89,14 +109,17 @@ __device__ __forceinline__ uint32_t probe_insert(int32_t *keys, int32_t c, uint3
             int32_t old = atomicCAS(keys + s, -1, c);
             if (old == -1 || old == c) return s;
         }
-        s = (s + 1) & mask;
+        s = T.next(s);
     }
+}
+__device__ __forceinline__ uint32_t probe_insert(int32_t *keys, int32_t c, uint32_t mask) {
+    return probe_insert(keys, c, PowTab{mask});
 }
 
 // probe_insert that also reports whether this call inserted the key.
-__device__ __forceinline__ uint32_t probe_insert_f(int32_t *keys, int32_t c, uint32_t mask,
-                                                   bool *fresh) {
-    uint32_t s = hslot(c, mask);
+template <class Tab>
+__device__ __forceinline__ uint32_t probe_insert_f(int32_t *keys, int32_t c, Tab T, bool *fresh) {
+    uint32_t s = T.first(c);
     while (true) {
         int32_t k = keys[s];
         if (k == c) {
@@ -114,18 +137,26 @@ __device__ __forceinline__ uint32_t probe_insert_f(int32_t *keys, int32_t c, uin
                 return s;
             }
         }
-        s = (s + 1) & mask;
+        s = T.next(s);
     }
 }
+__device__ __forceinline__ uint32_t probe_insert_f(int32_t *keys, int32_t c, uint32_t mask,
+                                                   bool *fresh) {
+    return probe_insert_f(keys, c, PowTab{mask}, fresh);
+}
 
-__device__ __forceinline__ int probe_find(const int32_t *keys, int32_t c, uint32_t mask) {
-    uint32_t s = hslot(c, mask);
+template <class Tab>
+__device__ __forceinline__ int probe_find(const int32_t *keys, int32_t c, Tab T) {
+    uint32_t s = T.first(c);
     while (true) {
         int32_t k = keys[s];
         if (k == c) return (int)s;
         if (k == -1) return -1;
-        s = (s + 1) & mask;
+        s = T.next(s);
     }
+}
+__device__ __forceinline__ int probe_find(const int32_t *keys, int32_t c, uint32_t mask) {
+    return probe_find(keys, c, PowTab{mask});
 }
 
 // Final decision of PL/_kernels.pyx:92-98.
@@ -260,11 +291,12 @@ __global__ void __launch_bounds__(256) k_decide_t0(DecideArgs A, const int32_t *
 
 // Fold one 32-entry chunk (c, w per lane; c = -1 for none) into a table in
 // adjacency order.  wb: the chunk's 32 weights staged in lane order.
-__device__ __forceinline__ void fold_chunk(int32_t *keys, double *vals, uint32_t mask, int32_t c,
+template <class Tab>
+__device__ __forceinline__ void fold_chunk(int32_t *keys, double *vals, Tab T, int32_t c,
                                            const double *wb, int lane) {
     unsigned grp = __match_any_sync(FULL, c);
     if (c >= 0 && lane == __ffs(grp) - 1) {
-        uint32_t s = probe_insert(keys, c, mask);
+        uint32_t s = probe_insert(keys, c, T);
         double v = vals[s];  // 0.0 when fresh
         for (unsigned g = grp; g; g &= g - 1) v = dadd(v, wb[__ffs(g) - 1]);
         vals[s] = v;
@@ -311,7 +343,7 @@ __global__ void __launch_bounds__(T1_WARPS * 32) k_decide_t1(DecideArgs A, const
             }
             wb[lane] = w;
             __syncwarp();
-            fold_chunk(keys, vals, mask, c, wb, lane);
+            fold_chunk(keys, vals, PowTab{mask}, c, wb, lane);
             __syncwarp();
         }
         double e_old = 0.0;
@@ -350,8 +382,8 @@ struct CertSmem {
     BestSmem<NT> bs;
     typename cub::BlockScan<int, NT>::TempStorage scan;
     typename cub::BlockReduce<unsigned long long, NT>::TempStorage red;
-    int32_t cidx[NT];  // ordered compaction of matching entries
-    double cw[NT];
+    int32_t *cidx;  // [NT * FU] ordered compaction of matching entries (set by the kernel)
+    double *cw;     // [NT * FU]
     int32_t N[MAXS + 2];  // communities to fold exactly (N[0] = c_old)
     double acc[MAXS + 2];
     double f_old;
@@ -382,15 +414,15 @@ __device__ __forceinline__ double group_sum(unsigned grp, double w) {
 
 // Accumulate one entry (c, w) with warp aggregation: lanes with the same
 // community combine (any order) before one atomic per group.
-__device__ __forceinline__ void accum_entry(int32_t *keys, double *vals, int32_t *cnt,
-                                            uint32_t mask, int32_t c, double w, int lane,
-                                            int16_t *clist, int *ncl) {
+template <class Tab, class CL>
+__device__ __forceinline__ void accum_entry(int32_t *keys, double *vals, int32_t *cnt, Tab T,
+                                            int32_t c, double w, int lane, CL *clist, int *ncl) {
     unsigned grp = __match_any_sync(FULL, c);
     double v = group_sum(grp, w);
     bool fresh = false;
     uint32_t s = 0;
     if (c >= 0 && lane == __ffs(grp) - 1) {
-        s = probe_insert_f(keys, c, mask, &fresh);
+        s = probe_insert_f(keys, c, T, &fresh);
         atomicAdd(vals + s, v);
         atomicAdd(cnt + s, __popc(grp));
     }
@@ -399,7 +431,7 @@ __device__ __forceinline__ void accum_entry(int32_t *keys, double *vals, int32_t
         int first = __ffs(fm) - 1, pos = 0;
         if (lane == first) pos = atomicAdd(ncl, __popc(fm));
         pos = __shfl_sync(FULL, pos, first);
-        if (fresh) clist[pos + __popc(fm & ((1u << lane) - 1))] = (int16_t)s;
+        if (fresh) clist[pos + __popc(fm & ((1u << lane) - 1))] = (CL)s;
     }
 }
 
@@ -414,19 +446,24 @@ __device__ __forceinline__ double gain_slack_r(double Fc, int32_t Lc, double Fo,
            8.0 * U_RND * (fabs(Fc - Fo) * inv_m * 1.001 + fabs(g)) + 1e-300;
 }
 
-// Passes over the candidates (slots clist[0..ncl)) of the any-order table of
+// Passes over the candidates (slots clist[0..ncl), or with clist == NULL every
+// slot 0..ncl of the table, empty ones skipped) of the any-order table of
 // vertex i: pass 1 finds the best on the approximate gains and stores every
 // candidate's gain in vals[] and its slack (rounded up to float) in cnt[];
 // pass 2 collects the candidates whose intervals overlap the best and clears
 // the slots when `clear`.  Returns the approximate best.
-template <int NT>
+template <class CL>
+__device__ __forceinline__ uint32_t slot_at(const CL *clist, int p) {
+    return clist ? (uint32_t)clist[p] : (uint32_t)p;
+}
+
+template <int NT, class Tab, class CL, int CU = 1>
 __device__ Best certify_table(const DecideArgs &A, int32_t c_old, double ki, int32_t *keys,
-                              double *vals, int32_t *cnt, uint32_t ts, const int16_t *clist,
-                              int ncl, CertSmem<NT> &S, bool clear) {
+                              double *vals, int32_t *cnt, Tab T, const CL *clist, int ncl,
+                              CertSmem<NT> &S, bool clear) {
     const int tid = threadIdx.x;
-    const uint32_t mask = ts - 1;
     if (tid == 0) {
-        int s = probe_find(keys, c_old, mask);
+        int s = probe_find(keys, c_old, T);
         S.f_old = s >= 0 ? vals[s] : 0.0;
         S.l_old = s >= 0 ? cnt[s] : 0;
         S.nS = 0;
@@ -439,41 +476,71 @@ __device__ Best certify_table(const DecideArgs &A, int32_t c_old, double ki, int
     const double inv_m = 1.0 / A.m;
     const int64_t l_old = LBL(A.labels, c_old);
     Best b{0.0, l_old, c_old, 0.0, 0};
-    for (int p = tid; p < ncl; p += NT) {
-        uint32_t s = (uint16_t)clist[p];
-        int32_t c = keys[s];
-        if (c == c_old) continue;
-        double F = vals[s];
-        int32_t L = cnt[s];
-        double g = gain_of(F, f_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq);
-        consider(b, g, LBL(A.labels, c), c, F, L);
-        vals[s] = g;
-        cnt[s] = __float_as_int(__double2float_ru(gain_slack_r(F, L, f_old, l_old_n, inv_m, g)));
+    // CU candidates per thread in flight: the slot, table and a_tot loads of
+    // a batch are issued before any of them is used
+    for (int p0 = tid; p0 < ncl; p0 += NT * CU) {
+        uint32_t sl[CU];
+        int32_t c[CU], L[CU];
+        double F[CU], at[CU];
+#pragma unroll
+        for (int u = 0; u < CU; u++) sl[u] = p0 + u * NT < ncl ? slot_at(clist, p0 + u * NT) : 0;
+#pragma unroll
+        for (int u = 0; u < CU; u++) {
+            const bool ok = p0 + u * NT < ncl;
+            c[u] = ok ? keys[sl[u]] : -1;
+            F[u] = ok ? vals[sl[u]] : 0.0;
+            L[u] = ok ? cnt[sl[u]] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < CU; u++) at[u] = c[u] >= 0 && c[u] != c_old ? A.a_tot[c[u]] : 0.0;
+#pragma unroll
+        for (int u = 0; u < CU; u++) {
+            if (c[u] < 0 || c[u] == c_old) continue;
+            double g = gain_of(F[u], f_old, A.m, ki, a_old_excl, at[u], A.four_m_sq);
+            consider(b, g, LBL(A.labels, c[u]), c[u], F[u], L[u]);
+            vals[sl[u]] = g;
+            cnt[sl[u]] = __float_as_int(
+                __double2float_ru(gain_slack_r(F[u], L[u], f_old, l_old_n, inv_m, g)));
+        }
     }
     b = block_best<NT>(S.bs, b);
     const bool stay_best = b.c == c_old;
     const double slack_b = stay_best ? 0.0 : gain_slack_r(b.e, b.n, f_old, l_old_n, inv_m, b.g);
     const double lower = stay_best ? 0.0 : b.g - slack_b;
     unsigned long long nc = 0;
-    for (int p = tid; p < ncl; p += NT) {
-        uint32_t s = (uint16_t)clist[p];
-        int32_t c = keys[s];
-        nc++;
-        if (c != c_old && c != b.c) {
-            // two exact gains were already ordered exactly by block_best
-            double sl = (double)__int_as_float(cnt[s]);
-            if ((sl > 0.0 || slack_b > 0.0) && vals[s] + sl >= lower) {
-                int k = atomicAdd(&S.nS, 1);
-                if (k < MAXS)
-                    S.N[2 + k] = c;
-                else
-                    atomicOr(&S.flag, 2);
-            }
+    for (int p0 = tid; p0 < ncl; p0 += NT * CU) {
+        uint32_t sl[CU];
+        int32_t c[CU];
+        float slk[CU];
+        double g[CU];
+#pragma unroll
+        for (int u = 0; u < CU; u++) sl[u] = p0 + u * NT < ncl ? slot_at(clist, p0 + u * NT) : 0;
+#pragma unroll
+        for (int u = 0; u < CU; u++) {
+            const bool ok = p0 + u * NT < ncl;
+            c[u] = ok ? keys[sl[u]] : -1;
+            slk[u] = ok ? __int_as_float(cnt[sl[u]]) : 0.0f;
+            g[u] = ok ? vals[sl[u]] : 0.0;
+            nc += c[u] >= 0 ? 1 : 0;
         }
-        if (clear) {
-            keys[s] = -1;
-            vals[s] = 0.0;
-            cnt[s] = 0;
+#pragma unroll
+        for (int u = 0; u < CU; u++) {
+            if (c[u] >= 0 && c[u] != c_old && c[u] != b.c) {
+                // two exact gains were already ordered exactly by block_best
+                double slv = (double)slk[u];
+                if ((slv > 0.0 || slack_b > 0.0) && g[u] + slv >= lower) {
+                    int k = atomicAdd(&S.nS, 1);
+                    if (k < MAXS)
+                        S.N[2 + k] = c[u];
+                    else
+                        atomicOr(&S.flag, 2);
+                }
+            }
+            if (clear && c[u] >= 0) {
+                keys[sl[u]] = -1;
+                vals[sl[u]] = 0.0;
+                cnt[sl[u]] = 0;
+            }
         }
     }
     if (tid == 0) {
@@ -489,37 +556,45 @@ __device__ Best certify_table(const DecideArgs &A, int32_t c_old, double ki, int
 }
 
 // Exact left folds (adjacency order) of the communities S.N[0..S.nn) over the
-// row of i: ordered block compaction of the matching entries, then thread 0
-// adds them in order.  Results in S.acc.
-template <int NT>
+// row of i: ordered block compaction of the matching entries (each thread
+// takes FU consecutive entries per chunk, loads in flight together), then
+// thread 0 adds them in order.  S.cidx / S.cw hold NT * FU entries.  Results
+// in S.acc.
+template <int NT, int FU>
 __device__ void exact_folds(const DecideArgs &A, int32_t i, CertSmem<NT> &S) {
     const int tid = threadIdx.x;
     const int64_t e0 = A.off[i], e1 = A.off[i + 1];
     const int nn = S.nn;
     if (tid < nn) S.acc[tid] = 0.0;
     __syncthreads();
-    for (int64_t base = e0; base < e1; base += NT) {
-        int64_t e = base + tid;
-        int idx = -1;
-        double w = 0.0;
-        if (e < e1) {
-            int32_t j = A.nbr[e];
-            if (j != i) {
-                int32_t c = A.assign[j];
+    for (int64_t base = e0; base < e1; base += (int64_t)NT * FU) {
+        const int64_t eb = base + (int64_t)tid * FU;
+        int32_t j[FU], c[FU], idx[FU];
+#pragma unroll
+        for (int u = 0; u < FU; u++) j[u] = eb + u < e1 ? A.nbr[eb + u] : i;
+#pragma unroll
+        for (int u = 0; u < FU; u++) c[u] = j[u] != i ? A.assign[j[u]] : -1;
+        int cntm = 0;
+#pragma unroll
+        for (int u = 0; u < FU; u++) {
+            idx[u] = -1;
+            if (c[u] >= 0)
                 for (int t = 0; t < nn; t++)
-                    if (S.N[t] == c) {
-                        idx = t;
+                    if (S.N[t] == c[u]) {
+                        idx[u] = t;
                         break;
                     }
-                if (idx >= 0) w = A.wts[e];
-            }
+            cntm += idx[u] >= 0;
         }
         int pos, total;
-        cub::BlockScan<int, NT>(S.scan).ExclusiveSum(idx >= 0 ? 1 : 0, pos, total);
-        if (idx >= 0) {
-            S.cidx[pos] = idx;
-            S.cw[pos] = w;
-        }
+        cub::BlockScan<int, NT>(S.scan).ExclusiveSum(cntm, pos, total);
+#pragma unroll
+        for (int u = 0; u < FU; u++)
+            if (idx[u] >= 0) {
+                S.cidx[pos] = idx[u];
+                S.cw[pos] = A.wts[eb + u];
+                pos++;
+            }
         __syncthreads();
         if (tid == 0) {
             double a0 = S.acc[0], a1 = nn > 1 ? S.acc[1] : 0.0;
@@ -543,7 +618,7 @@ __device__ void exact_folds(const DecideArgs &A, int32_t i, CertSmem<NT> &S) {
 // After certify_table: either finish (certain, no move) or fold the needed
 // communities exactly and decide on exact values.  Returns false on overflow
 // (more than MAXS overlapping candidates): the caller must decide exactly.
-template <int NT>
+template <int NT, int FU = 1>
 __device__ bool resolve(const DecideArgs &A, int64_t x, int32_t i, int32_t c_old, double ki,
                         const Best &b, CertSmem<NT> &S) {
     const int tid = threadIdx.x;
@@ -576,7 +651,7 @@ __device__ bool resolve(const DecideArgs &A, int64_t x, int32_t i, int32_t c_old
         S.nn = nn;
     }
     __syncthreads();
-    exact_folds<NT>(A, i, S);
+    exact_folds<NT, FU>(A, i, S);
     if (tid == 0) {
         double a_old_excl = dsub(A.a_tot[c_old], ki);
         Best e{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
@@ -595,13 +670,20 @@ __device__ bool resolve(const DecideArgs &A, int64_t x, int32_t i, int32_t c_old
 
 // Exact fallback: in-order fold into the (clean) table, communities split
 // over the warps so each community sees one ordered left fold, then the exact
-// argmax.  Leaves the table clean.
-__device__ void t2_exact(const DecideArgs &A, int64_t x, int32_t i, int32_t c_old, double ki,
-                         int32_t *keys, double *vals, uint32_t mask, int32_t *cbuf, double *wbuf,
-                         CertSmem<BLK> &S) {
+// argmax.  Leaves the table clean.  cbuf / wbuf: NT staging slots (the
+// CertSmem compaction buffers, idle here).
+template <int NT, class Tab>
+__device__ void table_exact(const DecideArgs &A, int64_t x, int32_t i, int32_t c_old, double ki,
+                            int32_t *keys, double *vals, Tab T, CertSmem<NT> &S) {
+    constexpr int NW = NT / 32;
+    constexpr int LOGW = NW >= 32 ? 5 : NW >= 16 ? 4 : NW >= 8 ? 3 : NW >= 4 ? 2 : NW >= 2 ? 1 : 0;
+    static_assert((1 << LOGW) == NW, "warps per block must be a power of two");
+    int32_t *cbuf = S.cidx;
+    double *wbuf = S.cw;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int64_t e0 = A.off[i], e1 = A.off[i + 1];
-    for (int64_t base = e0; base < e1; base += BLK) {
+    __syncthreads();
+    for (int64_t base = e0; base < e1; base += NT) {
         int64_t e = base + tid;
         int32_t c = -1;
         double w = 0.0;
@@ -616,31 +698,32 @@ __device__ void t2_exact(const DecideArgs &A, int64_t x, int32_t i, int32_t c_ol
         wbuf[tid] = w;
         __syncthreads();
         int nsub = (int)((e1 - base + 31) / 32);
-        if (nsub > BLK / 32) nsub = BLK / 32;
+        if (nsub > NW) nsub = NW;
         for (int sc = 0; sc < nsub; sc++) {
             int32_t cc = cbuf[sc * 32 + lane];
-            bool mine = cc >= 0 && (int)(((uint32_t)cc * 0x85EBCA6Bu) >> 29) == wid;
+            bool mine = cc >= 0 &&
+                        (LOGW == 0 || (int)(((uint32_t)cc * 0x85EBCA6Bu) >> (32 - LOGW)) == wid);
             if (__any_sync(FULL, mine))
-                fold_chunk(keys, vals, mask, mine ? cc : -1, wbuf + sc * 32, lane);
+                fold_chunk(keys, vals, T, mine ? cc : -1, wbuf + sc * 32, lane);
             __syncwarp();
         }
         __syncthreads();
     }
     if (tid == 0) {
-        int s = probe_find(keys, c_old, mask);
+        int s = probe_find(keys, c_old, T);
         S.f_old = s >= 0 ? vals[s] : 0.0;
     }
     __syncthreads();
     const double e_old = S.f_old, a_old_excl = dsub(A.a_tot[c_old], ki);
     Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
-    for (uint32_t s = tid; s <= mask; s += BLK) {
+    for (uint32_t s = tid; s < T.size(); s += NT) {
         int32_t c = keys[s];
         if (c >= 0 && c != c_old)
             consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq),
                      LBL(A.labels, c), c, vals[s], 0);
     }
-    b = block_best<BLK>(S.bs, b);
-    for (uint32_t s = tid; s <= mask; s += BLK) {
+    b = block_best<NT>(S.bs, b);
+    for (uint32_t s = tid; s < T.size(); s += NT) {
         keys[s] = -1;
         vals[s] = 0.0;
     }
@@ -648,19 +731,75 @@ __device__ void t2_exact(const DecideArgs &A, int64_t x, int32_t i, int32_t c_ol
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(BLK) k_decide_t2(DecideArgs A, const int32_t *list, int64_t cnt) {
-    extern __shared__ __align__(16) unsigned char dsm[];
-    __shared__ CertSmem<BLK> S;
-    __shared__ int32_t cbuf[BLK];
-    __shared__ double wbuf[BLK];
-    __shared__ int16_t clist[T2_MAXD];  // candidate slots (<= degree of them)
-    __shared__ int ncl;
+// One block decides one vertex at a time from a shared-memory table `keys /
+// vals / cntt` (clean on entry and exit) with candidate list `clist`:
+// any-order accumulation of the row (U entries per thread in flight), the
+// certification passes, then the exact resolution when needed.
+template <int NT, int U, int FU, class Tab, class CL>
+__device__ __forceinline__ void block_decide(const DecideArgs &A, int64_t x, Tab T, int32_t *keys,
+                                             double *vals, int32_t *cntt, CL *clist, int *ncl,
+                                             CertSmem<NT> &S, unsigned long long &my_cand) {
     const int tid = threadIdx.x, lane = tid & 31;
+    const int32_t i = A.subset[x];
+    const int32_t c_old = A.assign[i];
+    const int64_t e0 = A.off[i], e1 = A.off[i + 1];
+    const double ki = A.k[i];
+    if (tid == 0) *ncl = 0;
+    __syncthreads();
+    for (int64_t b0 = e0; b0 < e1; b0 += (int64_t)NT * U) {
+        int32_t j[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            int64_t e = b0 + u * NT + tid;
+            j[u] = e < e1 ? A.nbr[e] : i;
+        }
+        int32_t c[U];
+        double w[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            int64_t e = b0 + u * NT + tid;
+            bool ok = j[u] != i;  // out-of-range entries carry j = i
+            c[u] = ok ? A.assign[j[u]] : -1;
+            w[u] = ok ? A.wts[e] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) accum_entry(keys, vals, cntt, T, c[u], w[u], lane, clist, ncl);
+    }
+    __syncthreads();
+    Best b = certify_table<NT>(A, c_old, ki, keys, vals, cntt, T, clist, *ncl, S, true);
+    my_cand += tid == 0 ? S.ncand : 0;
+    if (A.integral) {
+        // exact in any order: the plain argmax is the reference's
+        if (tid == 0) finish_vertex(A, x, c_old, S.f_old, b.g, b.c, b.e);
+        __syncthreads();
+        return;
+    }
+    if (!resolve<NT, FU>(A, x, i, c_old, ki, b, S))
+        table_exact<NT>(A, x, i, c_old, ki, keys, vals, T, S);
+}
+
+constexpr int T2_FU = 1;  // row entries per thread per exact-fold chunk in tier 2
+
+// Tiers 2 and 3: block per vertex, the table (TS slots) in dynamic shared
+// memory; tier 2's small tables let 3x more vertices be in flight per SM.
+template <int TS, int MAXD, int NT>
+__global__ void __launch_bounds__(NT) k_decide_t2(DecideArgs A, const int32_t *list, int64_t cnt) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ CertSmem<NT> S;
+    __shared__ int32_t cidx[NT * T2_FU];
+    __shared__ double cw[NT * T2_FU];
+    __shared__ uint16_t clist[MAXD];  // candidate slots (<= degree of them)
+    __shared__ int ncl;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        S.cidx = cidx;
+        S.cw = cw;
+    }
     double *vals = reinterpret_cast<double *>(dsm);
-    int32_t *keys = reinterpret_cast<int32_t *>(dsm + sizeof(double) * T2_TS);
-    int32_t *cntt = keys + T2_TS;
+    int32_t *keys = reinterpret_cast<int32_t *>(dsm + sizeof(double) * TS);
+    int32_t *cntt = keys + TS;
     unsigned long long my_cand = 0;
-    for (uint32_t s = tid; s < T2_TS; s += BLK) {
+    for (uint32_t s = tid; s < TS; s += NT) {
         keys[s] = -1;
         vals[s] = 0.0;
         cntt[s] = 0;
@@ -668,44 +807,15 @@ __global__ void __launch_bounds__(BLK) k_decide_t2(DecideArgs A, const int32_t *
     for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
         const int64_t x = list[q];
         const int32_t i = A.subset[x];
-        const int32_t c_old = A.assign[i];
-        const int64_t e0 = A.off[i], e1 = A.off[i + 1];
-        const int64_t deg = e1 - e0;
+        const int64_t deg = A.off[i + 1] - A.off[i];
         uint32_t ts = 64;
         while (ts < (uint64_t)(deg + deg / 2 + 2)) ts <<= 1;
-        const uint32_t mask = ts - 1;
-        const double ki = A.k[i];
-        if (tid == 0) ncl = 0;
-        __syncthreads();
-        for (int64_t base = e0; base < e1; base += BLK) {
-            int64_t e = base + tid;
-            int32_t c = -1;
-            double w = 0.0;
-            if (e < e1) {
-                int32_t j = A.nbr[e];
-                if (j != i) {
-                    c = A.assign[j];
-                    w = A.wts[e];
-                }
-            }
-            accum_entry(keys, vals, cntt, mask, c, w, lane, clist, &ncl);
-        }
-        __syncthreads();
-        Best b = certify_table<BLK>(A, c_old, ki, keys, vals, cntt, ts, clist, ncl, S, true);
-        my_cand += tid == 0 ? S.ncand : 0;
-        if (A.integral) {
-            // exact in any order: the plain argmax is the reference's
-            if (tid == 0) finish_vertex(A, x, c_old, S.f_old, b.g, b.c, b.e);
-            __syncthreads();
-            continue;
-        }
-        if (!resolve<BLK>(A, x, i, c_old, ki, b, S))
-            t2_exact(A, x, i, c_old, ki, keys, vals, mask, cbuf, wbuf, S);
+        block_decide<NT, 1, T2_FU>(A, x, PowTab{ts - 1}, keys, vals, cntt, clist, &ncl, S, my_cand);
     }
     if (A.cand && tid == 0 && my_cand) atomicAdd(A.cand, my_cand);
 }
 
-// ------------------------------------------------------------ tier 3 (hubs)
+// ------------------------------------------------------------ tier 4 (hubs)
 
 constexpr int HSB = 256;      // threads per hub pass block
 constexpr int HSLICE = 512;   // candidate slots per hub pass block (2 per thread)
@@ -907,7 +1017,14 @@ __global__ void __launch_bounds__(HBLK) k_hub_decide(DecideArgs A, const int32_t
                                                     const int64_t *toff, int32_t *hkeys,
                                                     double *hvals, int32_t *hcnt, HubScratch H) {
     __shared__ CertSmem<HBLK> S;
+    __shared__ int32_t cidx[HBLK];
+    __shared__ double cw[HBLK];
     const int tid = threadIdx.x;
+    if (tid == 0) {
+        S.cidx = cidx;
+        S.cw = cw;
+    }
+    __syncthreads();
     for (int64_t q = blockIdx.x; q < H.nh; q += gridDim.x) {
         const int64_t x = list[q];
         const int32_t i = A.subset[x];
@@ -944,7 +1061,7 @@ __global__ void __launch_bounds__(HBLK) k_hub_decide(DecideArgs A, const int32_t
                 S.nn = nn;
             }
             __syncthreads();
-            exact_folds<HBLK>(A, i, S);
+            exact_folds<HBLK, 1>(A, i, S);
             if (tid == 0) {
                 double a_old_excl = dsub(A.a_tot[c_old], ki);
                 Best e{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
@@ -1010,8 +1127,12 @@ __global__ void k_tier_keys(const int64_t *off, const int32_t *vtx, const int64_
         }
         int32_t i = vtx[g];
         int64_t d = off[i + 1] - off[i];
-        uint32_t t = d <= T0_MAXD ? 0 : d <= T1_MAXD ? 1 : d <= T2_MAXD ? 2 : 3;
-        uint32_t kk = (uint32_t)(a * 4 + t);
+        uint32_t t = d <= T0_MAXD    ? 0
+                     : d <= T1_MAXD  ? 1
+                     : d <= T2A_MAXD ? 2
+                     : d <= T2_MAXD  ? 3
+                                     : 4;
+        uint32_t kk = (uint32_t)(a * NTIER + t);
         key[g] = kk;
         atomicAdd(hist + kk, 1ull);
     }
@@ -1021,7 +1142,7 @@ __global__ void k_tier_local(const uint32_t *skey, const int32_t *sidx, const in
                              int64_t total, int32_t *local) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < total;
          p += (int64_t)gridDim.x * blockDim.x)
-        local[p] = (int32_t)(sidx[p] - stage_off[skey[p] >> 2]);
+        local[p] = (int32_t)(sidx[p] - stage_off[skey[p] / NTIER]);
 }
 
 __global__ void k_hub_degrees(const int64_t *off, const int32_t *vtx, const int64_t *stage_off,
@@ -1069,30 +1190,30 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
                              cudaMemcpyHostToDevice, s));
     Buf<uint32_t> key(total, s), skey(total, s);
     Buf<int32_t> gidx(total, s), sidx(total, s);
-    Buf<unsigned long long> hist(4 * nst, s);
-    PLV_CUDA(cudaMemsetAsync(hist.get(), 0, sizeof(unsigned long long) * 4 * nst, s));
+    Buf<unsigned long long> hist(NTIER * nst, s);
+    PLV_CUDA(cudaMemsetAsync(hist.get(), 0, sizeof(unsigned long long) * NTIER * nst, s));
     k_tier_keys<<<grid_for(total, 256), 256, 0, s>>>(off, vtx, d_soff, nst, total, key, hist);
     PLV_LAUNCH_CHECK();
     iota_i32(gidx, total, s);
-    sort_pairs<uint32_t, int32_t>(key, skey, gidx, sidx, total, 0, bits_for(4 * nst + 4), s);
+    sort_pairs<uint32_t, int32_t>(key, skey, gidx, sidx, total, 0, bits_for(NTIER * nst + NTIER), s);
     k_tier_local<<<grid_for(total, 256), 256, 0, s>>>(skey, sidx, d_soff, total, P.tier_list);
     PLV_LAUNCH_CHECK();
-    std::vector<unsigned long long> h(4 * nst);
-    PLV_CUDA(cudaMemcpyAsync(h.data(), hist.get(), sizeof(unsigned long long) * 4 * nst,
+    std::vector<unsigned long long> h(NTIER * nst);
+    PLV_CUDA(cudaMemcpyAsync(h.data(), hist.get(), sizeof(unsigned long long) * NTIER * nst,
                              cudaMemcpyDeviceToHost, s));
     PLV_CUDA(cudaStreamSynchronize(s));
     int64_t pos = 0;
     std::vector<int64_t> hub_pos, hub_stage;
     for (int64_t a = 0; a < nst; a++)
-        for (int t = 0; t < 4; t++) {
+        for (int t = 0; t < NTIER; t++) {
             P.st[a].tstart[t] = pos;
-            P.st[a].tcount[t] = (int64_t)h[4 * a + t];
-            if (t == 3)
-                for (int64_t z = 0; z < P.st[a].tcount[3]; z++) {
+            P.st[a].tcount[t] = (int64_t)h[NTIER * a + t];
+            if (t == 4)
+                for (int64_t z = 0; z < P.st[a].tcount[4]; z++) {
                     hub_pos.push_back(pos + z);
                     hub_stage.push_back(a);
                 }
-            pos += (int64_t)h[4 * a + t];
+            pos += (int64_t)h[NTIER * a + t];
         }
     int64_t nh = (int64_t)hub_pos.size();
     if (nh == 0) return;
@@ -1118,7 +1239,7 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
         eoff.push_back(0);
         toff.push_back(0);
         poff.push_back(0);
-        for (int64_t z = 0; z < sp.tcount[3]; z++) {
+        for (int64_t z = 0; z < sp.tcount[4]; z++) {
             int64_t d = deg[h0 + z];
             int64_t cap = 64;
             while (cap < 2 * d + 2) cap <<= 1;
@@ -1131,12 +1252,12 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
             toff.push_back(tacc);
             poff.push_back(pacc);
         }
-        h0 += sp.tcount[3];
+        h0 += sp.tcount[4];
         sp.hub_entries = acc;
         sp.hub_nblk = pacc;
         max_parts = pacc > max_parts ? pacc : max_parts;
         P.max_hub_entries = acc > P.max_hub_entries ? acc : P.max_hub_entries;
-        P.max_hubs = sp.tcount[3] > P.max_hubs ? sp.tcount[3] : P.max_hubs;
+        P.max_hubs = sp.tcount[4] > P.max_hubs ? sp.tcount[4] : P.max_hubs;
         P.max_table = tacc > P.max_table ? tacc : P.max_table;
     }
     P.hub_eoff = dalloc<int64_t>(eoff.size());
@@ -1171,30 +1292,34 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
     PLV_CUDA(cudaStreamSynchronize(s));
 }
 
-static size_t t2_smem() { return (sizeof(double) + 2 * sizeof(int32_t)) * T2_TS; }
+static size_t t2_smem(int ts) { return (sizeof(double) + 2 * sizeof(int32_t)) * ts; }
 
 void ensure_decide_attrs() {
     static int dev_done = -1;
     int dev;
     PLV_CUDA(cudaGetDevice(&dev));
     if (dev_done == dev) return;
-    PLV_CUDA(cudaFuncSetAttribute(k_decide_t2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)t2_smem()));
+    PLV_CUDA(cudaFuncSetAttribute(k_decide_t2<T2A_TS, T2A_MAXD, 128>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)t2_smem(T2A_TS)));
+    PLV_CUDA(cudaFuncSetAttribute(k_decide_t2<T2_TS, T2_MAXD, BLK>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)t2_smem(T2_TS)));
     dev_done = dev;
 }
 
 void launch_decide(const Plan &P, int64_t a, DecideArgs A, cudaStream_t st) {
-    cudaStream_t ts[4] = {st, st, st, st};
+    cudaStream_t ts[NTIER] = {st, st, st, st, st};
     launch_decide_tiers(P, a, A, ts);
 }
 
 void launch_decide_par(const Plan &P, int64_t a, DecideArgs A, cudaStream_t st,
                        const cudaStream_t *side, cudaEvent_t fork, const cudaEvent_t *join) {
     const StagePlan &sp = P.st[a];
-    int used[4], nu = 0;
-    for (int t = 3; t >= 0; t--)  // hubs (longest) first, on the main stream
+    int used[NTIER], nu = 0;
+    for (int t = NTIER - 1; t >= 0; t--)  // hubs (longest) first, on the main stream
         if (sp.tcount[t]) used[nu++] = t;
-    cudaStream_t ts[4] = {st, st, st, st};
+    cudaStream_t ts[NTIER] = {st, st, st, st, st};
     if (nu > 1) {
         PLV_CUDA(cudaEventRecord(fork, st));
         for (int u = 1; u < nu; u++) {
@@ -1222,16 +1347,23 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
         PLV_LAUNCH_CHECK();
     }
     if (sp.tcount[2]) {
-        k_decide_t2<<<grid_for(sp.tcount[2], 1, 148 * 3), BLK, t2_smem(), ts[2]>>>(
+        k_decide_t2<T2A_TS, T2A_MAXD, 128><<<grid_for(sp.tcount[2], 1, 148 * 8), 128,
+                                             t2_smem(T2A_TS), ts[2]>>>(
             A, P.tier_list + sp.tstart[2], sp.tcount[2]);
         PLV_LAUNCH_CHECK();
     }
-    cudaStream_t st = ts[3];
     if (sp.tcount[3]) {
-        const int32_t *list = P.tier_list + sp.tstart[3];
+        k_decide_t2<T2_TS, T2_MAXD, BLK><<<grid_for(sp.tcount[3], 1, 148 * 3), BLK,
+                                           t2_smem(T2_TS), ts[3]>>>(
+            A, P.tier_list + sp.tstart[3], sp.tcount[3]);
+        PLV_LAUNCH_CHECK();
+    }
+    cudaStream_t st = ts[4];
+    if (sp.tcount[4]) {
+        const int32_t *list = P.tier_list + sp.tstart[4];
         const int64_t *eoff = P.hub_eoff + sp.hub_base;
         const int64_t *toff = P.hub_toff + sp.hub_base;
-        int64_t nh = sp.tcount[3], E = sp.hub_entries;
+        int64_t nh = sp.tcount[4], E = sp.hub_entries;
         const int64_t Hm = P.max_hubs;
         HubScratch H{P.hcand,  P.hsmall, P.hsmall + HCPAD * Hm, P.hsmall + (HCPAD + 1) * Hm,
                      P.hS,     P.hpart,  P.hbest,              P.hfold,

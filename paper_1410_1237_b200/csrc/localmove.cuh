@@ -21,12 +21,14 @@ namespace plv {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int T0_MAXD = 8;
 constexpr int T1_MAXD = 128;
-constexpr int T2_MAXD = 2048;
+constexpr int T2A_MAXD = 680;  // tier 2: 1024-slot tables (>= 1.5 * (680 + 1))
+constexpr int T2_MAXD = 2048;   // tier 3: 4096-slot tables
 constexpr int T1_WARPS = 8;   // warps per block in tier 1
 constexpr int T1_TS = 256;    // slots per warp table (>= 1.5 * (128 + 1))
 constexpr int BLK = 256;      // threads per block in tiers 2/3
 constexpr int T2_TS = 4096;   // smem slots for tier 2 (>= 1.5 * (2048 + 1))
-constexpr size_t T2_SMEM = (sizeof(double) + sizeof(int32_t)) * T2_TS;
+constexpr int T2A_TS = 1024;
+constexpr int NTIER = 5;  // t0, t1, t2 (block, small table), t3 (block), t4 (hubs)
 
 constexpr int SMALL_APPLY_MAX = 2048;  // stage size handled by the one-CTA apply
 constexpr int SA_THREADS = 256;
@@ -60,8 +62,8 @@ DecideArgs make_decide_args(const int64_t *off, const int32_t *nbr, const double
 
 struct StagePlan {
     int64_t off = 0, ns = 0;
-    int64_t tcount[4] = {0, 0, 0, 0};
-    int64_t tstart[4] = {0, 0, 0, 0};  // into the tier list
+    int64_t tcount[NTIER] = {0, 0, 0, 0, 0};
+    int64_t tstart[NTIER] = {0, 0, 0, 0, 0};  // into the tier list
     int64_t hub_base = 0;              // this stage's first hub_eoff / hub_toff entry
     int64_t hub_entries = 0;
     int64_t hub_nblk = 0;      // hub pass blocks (one per candidate slice)
@@ -72,8 +74,9 @@ struct Best;  // decide.cu
 
 constexpr int MAXS = 32;  // overlapping candidates resolved exactly per vertex
 
-// Static per-phase decide plan: each stage's vertices split into the four
-// degree tiers; hubs get entry offsets and a slice of a global hash table.
+// Static per-phase decide plan: each stage's vertices split into the five
+// degree tiers; hubs (tier 4) get entry offsets and a slice of a global hash
+// table.
 struct Plan {
     std::vector<StagePlan> st;
     int32_t *tier_list = nullptr;  // stage-local indices grouped by (stage, tier)
@@ -102,8 +105,8 @@ void ensure_decide_attrs();
 void launch_decide(const Plan &P, int64_t a, DecideArgs A, cudaStream_t st);
 // Tier t on stream ts[t].
 void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStream_t *ts);
-// The stage's non-empty tiers as parallel branches (3 side streams, a fork
-// event and 3 join events), joined back into `st`.
+// The stage's non-empty tiers as parallel branches (NTIER - 1 side streams, a
+// fork event and NTIER - 1 join events), joined back into `st`.
 void launch_decide_par(const Plan &P, int64_t a, DecideArgs A, cudaStream_t st,
                        const cudaStream_t *side, cudaEvent_t fork, const cudaEvent_t *join);
 

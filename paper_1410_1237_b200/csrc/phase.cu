@@ -41,8 +41,8 @@ struct Phase {
     double *h_out = nullptr;  // pinned: q, moves, cand
     bool timing = false;
     std::vector<cudaEvent_t> ev;
-    cudaStream_t side[3] = {nullptr, nullptr, nullptr};  // decide tiers in parallel branches
-    cudaEvent_t fork = nullptr, join[3] = {nullptr, nullptr, nullptr};
+    cudaStream_t side[NTIER - 1] = {};  // decide tiers in parallel branches
+    cudaEvent_t fork = nullptr, join[NTIER - 1] = {};
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
 
@@ -53,7 +53,7 @@ struct Phase {
         graph = nullptr;
         for (auto e : ev) cudaEventDestroy(e);
         ev.clear();
-        for (int t = 0; t < 3; t++) {
+        for (int t = 0; t < NTIER - 1; t++) {
             if (side[t]) cudaStreamDestroy(side[t]);
             if (join[t]) cudaEventDestroy(join[t]);
             side[t] = nullptr;
@@ -143,7 +143,7 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
             P->ev.resize(2 * nst);
             for (auto &e : P->ev) PLV_CUDA(cudaEventCreate(&e));
         }
-        for (int t = 0; t < 3; t++) {
+        for (int t = 0; t < NTIER - 1; t++) {
             PLV_CUDA(cudaStreamCreateWithFlags(&P->side[t], cudaStreamNonBlocking));
             PLV_CUDA(cudaEventCreateWithFlags(&P->join[t], cudaEventDisableTiming));
         }
