@@ -33,6 +33,41 @@
 namespace plv {
 
 constexpr double U_RND = 1.1102230246251565e-16;  // 2^-53
+
+// ---- optional per-block timeline (off unless plv_debug_trace(1) was called):
+// thread 0 of a block records globaltimer stamps at up to 6 marks.
+__device__ unsigned long long g_tr[1 << 21];
+__device__ unsigned int g_tr_n;
+__device__ int g_tr_on;
+struct Trace {
+    unsigned long long t[6];
+    int n;
+    __device__ __forceinline__ void mark() {
+        if (n < 6) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t[n]));
+        n++;
+    }
+    __device__ __forceinline__ void flush(int kid) {
+        unsigned k = atomicAdd(&g_tr_n, 1u);
+        if (k < (1u << 21) / 8) {
+            unsigned long long *o = g_tr + 8 * k;
+            o[0] = ((unsigned long long)kid << 32) | blockIdx.x;
+            for (int i = 0; i < 6; i++) o[1 + i] = i < n ? t[i] : 0ull;
+            o[7] = (unsigned long long)n;
+        }
+    }
+};
+#define TR_BEGIN                                    \
+    const bool tr_on = g_tr_on && threadIdx.x == 0; \
+    Trace tr;                                       \
+    tr.n = 0;                                       \
+    if (tr_on) tr.mark();
+#define TR_MARK \
+    if (tr_on) tr.mark();
+#define TR_END(kid)    \
+    if (tr_on) {       \
+        tr.mark();     \
+        tr.flush(kid); \
+    }
 constexpr int HBLK = 1024;                         // threads per hub block
 
 __device__ __forceinline__ int64_t LBL(const int32_t *labels, int32_t c) {
@@ -157,6 +192,21 @@ __device__ __forceinline__ int probe_find(const int32_t *keys, int32_t c, Tab T)
 }
 __device__ __forceinline__ int probe_find(const int32_t *keys, int32_t c, uint32_t mask) {
     return probe_find(keys, c, PowTab{mask});
+}
+
+// Find-or-insert c by CAS alone (no separate probe load: one L2 round trip per
+// probed slot); reports whether this call inserted the key.
+__device__ __forceinline__ uint32_t probe_claim(int32_t *keys, int32_t c, uint32_t mask,
+                                                bool *fresh) {
+    uint32_t s = hslot(c, mask);
+    while (true) {
+        const int32_t old = atomicCAS(keys + s, -1, c);
+        if (old == -1 || old == c) {
+            *fresh = old == -1;
+            return s;
+        }
+        s = (s + 1) & mask;
+    }
 }
 
 // Final decision of PL/_kernels.pyx:92-98.
@@ -778,7 +828,8 @@ __device__ __forceinline__ void block_decide(const DecideArgs &A, int64_t x, Tab
         table_exact<NT>(A, x, i, c_old, ki, keys, vals, T, S);
 }
 
-constexpr int T2_FU = 1;  // row entries per thread per exact-fold chunk in tier 2
+constexpr int T2_FU = 1;
+constexpr int T2_WIDE_MAX = 148;  // tiers 2-3 with at most this many vertices: wide blocks  // row entries per thread per exact-fold chunk in tier 2
 
 // Tiers 2 and 3: block per vertex, the table (TS slots) in dynamic shared
 // memory; tier 2's small tables let 3x more vertices be in flight per SM.
@@ -817,23 +868,30 @@ __global__ void __launch_bounds__(NT) k_decide_t2(DecideArgs A, const int32_t *l
 
 // ------------------------------------------------------------ tier 4 (hubs)
 
-constexpr int HSB = 256;      // threads per hub pass block
-constexpr int HSLICE = 512;   // candidate slots per hub pass block (2 per thread)
-constexpr int HCPAD = 32;     // hub candidate counters one 128-byte line apart
+constexpr int HSB = 256;            // threads per hub pass block
+constexpr int HSU = 8;              // table slots per thread in a pass block
+constexpr int HTSL = HSB * HSU;     // table slots per pass block
+constexpr int HCPAD = 32;           // per-hub counters one 128-byte line apart
+
+// A candidate near its slice's best: community, gain, slack (rounded up).
+struct NearCand {
+    int32_t c;
+    float sl;
+    double g;
+};
 
 // Per-stage hub scratch (device pointers; hub index q is stage-local).
+// Idle state: sold = -1, counters 0, table slices clean.
 struct HubScratch {
-    int32_t *cand;   // candidate slot lists, laid out like the table slices
-    int32_t *ncand;  // [nh] candidates per hub      } one zeroed block
-    int32_t *nS;     // [nh] overlapping candidates  } of 3 * max_hubs
-    int32_t *flag;   // [nh] 1 stay overlaps, 2 overflow
-    int32_t *S;      // [nh * MAXS] overlapping communities
-    Best *part;      // [poff[nh]] pass-1 partial bests (one per slice)
-    Best *best;      // [nh]
-    double *fold;    // [nh] any-order e_{i->c_old}
-    int32_t *lold;   // [nh] its term count
-    const int64_t *blk;   // pass blocks of the stage: (hub << 32) | slice
-    const int64_t *poff;  // [nh + 1] first partial of each hub
+    const int64_t *row;  // [nh] first entry of the hub's row
+    const int32_t *vid;  // [nh] the hub
+    int32_t *sold;       // [nh] table slot of c_old (-1: absent)
+    int32_t *ncnt;       // [nh * HCPAD]: [0] near candidates with slack, [1] exact ones
+    NearCand *nearA;     // [nh * MAXS] near candidates with slack > 0
+    NearCand *nearB;     // [nh * MAXS] near candidates with exact gains
+    Best *part;          // [poff[nh]] pass-1 partial bests (one per slice)
+    const int64_t *blk;  // pass blocks of the stage: (hub << 32) | slice
+    const int64_t *poff; // [nh + 1] first partial of each hub
     int64_t nh;
 };
 
@@ -851,171 +909,137 @@ __device__ __forceinline__ int64_t hub_of(const int64_t *eoff, int64_t nh, int64
 }
 
 // Every entry of every hub of the stage: any-order sums into the hub's slice
-// of the global table (warp-aggregated per (hub, community)).
-__global__ void k_hub_accum(DecideArgs A, const int32_t *list, const int64_t *eoff,
-                            const int64_t *toff, int64_t nh, int64_t E, int32_t *hkeys,
-                            double *hvals, int32_t *hcnt, HubScratch H) {
+// of the global table (warp-aggregated per (hub, community)); the inserter of
+// c_old records its slot.
+__global__ void k_hub_accum(DecideArgs A, const int64_t *eoff, const int64_t *toff, int64_t nh,
+                            int64_t E, int32_t *hkeys, double *hvals, int32_t *hcnt, HubScratch H) {
+    TR_BEGIN
     const int lane = threadIdx.x & 31;
     // warp-uniform loop: the whole warp takes 32 consecutive entries per step
     for (int64_t w0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); w0 < E;
          w0 += (int64_t)gridDim.x * blockDim.x) {
         int64_t t = w0 + lane;
-        int32_t c = -1;
+        int32_t c = -1, c_old = -1;
         double w = 0.0;
         int64_t q = 0;
         if (t < E) {
             q = hub_of(eoff, nh, t);
-            int32_t i = A.subset[list[q]];
-            int64_t e = A.off[i] + (t - eoff[q]);
-            int32_t j = A.nbr[e];
+            const int32_t i = H.vid[q];
+            const int64_t e = H.row[q] + (t - eoff[q]);
+            const int32_t j = A.nbr[e];
+            c_old = A.assign[i];
             if (j != i) {
                 c = A.assign[j];
                 w = A.wts[e];
             }
         }
+        TR_MARK
         // group lanes by (hub, community)
-        uint64_t key = c >= 0 ? (((uint64_t)q << 32) | (uint32_t)c) : ~0ull;
-        unsigned grp = __match_any_sync(FULL, key);
-        double v = group_sum(grp, w);
-        const bool leader = c >= 0 && lane == __ffs(grp) - 1;
-        const int64_t base = toff[q];
-        bool fresh = false;
-        uint32_t s = 0;
-        if (leader) {
-            uint32_t mask = (uint32_t)(toff[q + 1] - base - 1);
-            s = probe_insert_f(hkeys + base, c, mask, &fresh);
+        const uint64_t key = c >= 0 ? (((uint64_t)q << 32) | (uint32_t)c) : ~0ull;
+        const unsigned grp = __match_any_sync(FULL, key);
+        const double v = group_sum(grp, w);
+        if (c >= 0 && lane == __ffs(grp) - 1) {
+            const int64_t base = toff[q];
+            const uint32_t mask = (uint32_t)(toff[q + 1] - base - 1);
+            bool fresh;
+            const uint32_t s = probe_claim(hkeys + base, c, mask, &fresh);
             atomicAdd(hvals + base + s, v);
             atomicAdd(hcnt + base + s, __popc(grp));
-        }
-        // append fresh slots to the hub's candidate list: one counter atomic
-        // per (warp, hub), counters one cache line apart
-        unsigned fm = __ballot_sync(FULL, fresh);
-        if (fm) {
-            unsigned same = __match_any_sync(FULL, fresh ? q : -1ll) & fm;
-            int rank = __popc(same & ((1u << lane) - 1));
-            int first = __ffs(same) - 1;
-            int pos = 0;
-            if (fresh && lane == first) pos = atomicAdd(H.ncand + q * HCPAD, __popc(same));
-            pos = __shfl_sync(FULL, pos, fresh ? first : lane);
-            if (fresh) H.cand[base + pos + rank] = (int32_t)s;
+            if (fresh && c == c_old) H.sold[q] = (int32_t)s;
         }
     }
+    TR_END(1)
 }
 
-// Pass 1, block (hub q, slice y): best candidate of the slice on the
-// any-order sums.  Slice 0 also records the hub's e_{i->c_old} sum.
-__global__ void __launch_bounds__(HSB) k_hub_pass1(DecideArgs A, const int32_t *list,
-                                                  const int64_t *toff, const int32_t *hkeys,
-                                                  double *hvals, int32_t *hcnt, HubScratch H) {
-    __shared__ BestSmem<HSB> bs;
-    __shared__ double s_fo;
-    __shared__ int32_t s_lo;
-    const int64_t pk = H.blk[blockIdx.x];
-    const int64_t q = pk >> 32, y = pk & 0xffffffffll;
-    const int32_t i = A.subset[list[q]];
-    const int32_t c_old = A.assign[i];
-    const int64_t base = toff[q];
-    const uint32_t mask = (uint32_t)(toff[q + 1] - base - 1);
-    if (threadIdx.x == 0) {
-        int s = probe_find(hkeys + base, c_old, mask);
-        s_fo = s >= 0 ? hvals[base + s] : 0.0;
-        s_lo = s >= 0 ? hcnt[base + s] : 0;
-        if (y == 0) {
-            H.fold[q] = s_fo;
-            H.lold[q] = s_lo;
-        }
-    }
-    __syncthreads();
-    const double f_old = s_fo, ki = A.k[i], a_old_excl = dsub(A.a_tot[c_old], ki);
-    const int64_t n = H.ncand[q * HCPAD];
-    const int64_t p0 = y * HSLICE;
-    const int64_t p1 = p0 + HSLICE < n ? p0 + HSLICE : n;
-    const double inv_m = 1.0 / A.m;
-    Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
-    for (int64_t p = p0 + threadIdx.x; p < p1; p += HSB) {
-        int32_t s = H.cand[base + p];
-        int32_t c = hkeys[base + s];
-        if (c == c_old) continue;
-        double F = hvals[base + s];
-        int32_t L = hcnt[base + s];
-        double g = gain_of(F, f_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq);
-        consider(b, g, LBL(A.labels, c), c, F, L);
-        // pass 2 needs only the gain and its slack (rounded up to float)
-        hvals[base + s] = g;
-        hcnt[base + s] =
-            __float_as_int(__double2float_ru(gain_slack_r(F, L, f_old, s_lo, inv_m, g)));
-    }
-    b = block_best<HSB>(bs, b);
-    if (threadIdx.x == 0) H.part[H.poff[q] + y] = b;
+// Bound on the certification slack of any candidate of vertex i (degree d,
+// weighted degree ki): every sum is <= ki with <= d terms and |gain| <= 2 ki / m.
+__device__ __forceinline__ double slack_max(double ki, int64_t d, double inv_m) {
+    const double se = 2.01 * (double)(d > 1 ? d - 1 : 0) * U_RND * ki;
+    return 1.1 * (1.02 * (2.0 * se * inv_m) + 8.0 * U_RND * (3.01 * ki * inv_m)) + 1e-300;
 }
 
-// Pass 2, block (hub q, slice y): the hub's best from the partials, then
-// every candidate of the slice whose interval overlaps it; clears the slice.
-__global__ void __launch_bounds__(HSB) k_hub_pass2(DecideArgs A, const int32_t *list,
-                                                  const int64_t *toff, int32_t *hkeys,
-                                                  double *hvals, int32_t *hcnt, HubScratch H) {
+// Pass block (hub q, table slice y): gains and slack of the slice's entries
+// on the any-order sums, the slice's best (incl. "stay"), and every entry
+// within slack_max of it -- a superset of the entries that can overlap the
+// hub's best -- listed for the decision.  Clears the slice (c_old's slot is
+// cleared by the decision, which reads it).
+__global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int64_t *eoff,
+                                                 const int64_t *toff, int32_t *hkeys,
+                                                 double *hvals, int32_t *hcnt, HubScratch H) {
+    TR_BEGIN
     __shared__ BestSmem<HSB> bs;
     typedef cub::BlockReduce<unsigned long long, HSB> BR;
     __shared__ typename BR::TempStorage red;
+    const int tid = threadIdx.x;
     const int64_t pk = H.blk[blockIdx.x];
     const int64_t q = pk >> 32, y = pk & 0xffffffffll;
-    const int32_t i = A.subset[list[q]];
+    const int32_t i = H.vid[q];
     const int32_t c_old = A.assign[i];
     const int64_t base = toff[q];
-    Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
-    for (int64_t t = H.poff[q] + threadIdx.x; t < H.poff[q + 1]; t += HSB) {
-        Best o = H.part[t];
-        consider(b, o.g, o.l, o.c, o.e, o.n);
+    const int64_t cap = toff[q + 1] - base;
+    const int32_t so = H.sold[q];
+    const double f_old = so >= 0 ? hvals[base + so] : 0.0;
+    const int32_t l_old = so >= 0 ? hcnt[base + so] : 0;
+    const double ki = A.k[i], a_old_excl = dsub(A.a_tot[c_old], ki);
+    const double inv_m = 1.0 / A.m;
+    int32_t c[HSU];
+    double F[HSU], g[HSU];
+    int32_t L[HSU];
+    float sl[HSU];
+    const int64_t s0 = y * HTSL + tid;
+#pragma unroll
+    for (int u = 0; u < HSU; u++) {
+        const int64_t s = s0 + u * HSB;
+        c[u] = s < cap ? hkeys[base + s] : -1;
+        F[u] = s < cap ? hvals[base + s] : 0.0;
+        L[u] = s < cap ? hcnt[base + s] : 0;
     }
-    b = block_best<HSB>(bs, b);
-    const double f_old = H.fold[q], ki = A.k[i], a_old_excl = dsub(A.a_tot[c_old], ki);
-    const int32_t lo_n = H.lold[q];
-    const bool stay_best = b.c == c_old;
-    const double slack_b =
-        stay_best ? 0.0 : gain_slack_r(b.e, b.n, f_old, lo_n, 1.0 / A.m, b.g);
-    const double lower = stay_best ? 0.0 : b.g - slack_b;
-    (void)ki;
-    (void)a_old_excl;
-    const int64_t n = H.ncand[q * HCPAD];
-    const int64_t p0 = y * HSLICE;
-    const int64_t p1 = p0 + HSLICE < n ? p0 + HSLICE : n;
+    Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
     unsigned long long nc = 0;
-    for (int64_t p = p0 + threadIdx.x; p < p1; p += HSB) {
-        int32_t s = H.cand[base + p];
-        int32_t c = hkeys[base + s];
+#pragma unroll
+    for (int u = 0; u < HSU; u++) {
+        const int64_t s = s0 + u * HSB;
+        if (c[u] < 0) continue;
         nc++;
-        if (!A.integral && c != c_old && c != b.c) {
-            double sl = (double)__int_as_float(hcnt[base + s]);
-            if ((sl > 0.0 || slack_b > 0.0) && hvals[base + s] + sl >= lower) {
-                int k = atomicAdd(H.nS + q, 1);
-                if (k < MAXS)
-                    H.S[q * MAXS + k] = c;
-                else
-                    atomicOr(H.flag + q, 2);
-            }
+        if (c[u] == c_old) {
+            c[u] = -1;  // not a candidate
+            continue;
         }
+        g[u] = gain_of(F[u], f_old, A.m, ki, a_old_excl, A.a_tot[c[u]], A.four_m_sq);
+        sl[u] = __double2float_ru(gain_slack_r(F[u], L[u], f_old, l_old, inv_m, g[u]));
+        consider(b, g[u], LBL(A.labels, c[u]), c[u], F[u], L[u]);
         hkeys[base + s] = -1;
         hvals[base + s] = 0.0;
         hcnt[base + s] = 0;
     }
-    unsigned long long tot = BR(red).Sum(nc);
-    if (threadIdx.x == 0) {
-        if (A.cand && tot) atomicAdd(A.cand, tot);
-        if (y == 0) {
-            H.best[q] = b;
-            if (!stay_best && slack_b > 0.0 && lower <= 0.0)
-                atomicOr(H.flag + q, 1);  // "stay" overlaps an inexact best
+    b = block_best<HSB>(bs, b);
+    if (!A.integral) {
+        const double thr = b.g - slack_max(ki, eoff[q + 1] - eoff[q], inv_m);
+#pragma unroll
+        for (int u = 0; u < HSU; u++) {
+            if (c[u] < 0 || g[u] + (double)sl[u] < thr) continue;
+            const int cat = sl[u] > 0.0f ? 0 : 1;
+            const int k = atomicAdd(H.ncnt + q * HCPAD + cat, 1);
+            if (k < MAXS) (cat ? H.nearB : H.nearA)[q * MAXS + k] = NearCand{c[u], sl[u], g[u]};
         }
     }
+    const unsigned long long tot = BR(red).Sum(nc);
+    if (tid == 0) {
+        H.part[H.poff[q] + y] = b;
+        if (A.cand && tot) atomicAdd(A.cand, tot);
+    }
+    TR_END(2)
 }
 
-// Block per hub: the decision.  Certain non-moves (and integral graphs) finish
-// at once; otherwise the listed communities are folded exactly (or, on
-// overflow, the whole row in order through the hub's table slice) and the
-// decision is taken on exact values.
+// Block per hub: the hub's best from the partials, the overlap test on the
+// listed near candidates, then the decision.  Certain non-moves (and integral
+// graphs) finish at once; otherwise the overlapping communities are folded
+// exactly (or, past MAXS of them, the whole row through the hub's clean table
+// slice) and the decision is taken on exact values.  Resets the hub's state.
 __global__ void __launch_bounds__(HBLK) k_hub_decide(DecideArgs A, const int32_t *list,
                                                     const int64_t *toff, int32_t *hkeys,
                                                     double *hvals, int32_t *hcnt, HubScratch H) {
+    TR_BEGIN
     __shared__ CertSmem<HBLK> S;
     __shared__ int32_t cidx[HBLK];
     __shared__ double cw[HBLK];
@@ -1027,37 +1051,95 @@ __global__ void __launch_bounds__(HBLK) k_hub_decide(DecideArgs A, const int32_t
     __syncthreads();
     for (int64_t q = blockIdx.x; q < H.nh; q += gridDim.x) {
         const int64_t x = list[q];
-        const int32_t i = A.subset[x];
+        const int32_t i = H.vid[q];
         const int32_t c_old = A.assign[i];
         const double ki = A.k[i];
-        const Best b = H.best[q];
-        const int nS = H.nS[q], flag = H.flag[q];
+        const int64_t base = toff[q];
+        Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
+        for (int64_t t = H.poff[q] + tid; t < H.poff[q + 1]; t += HBLK) {
+            const Best o = H.part[t];
+            consider(b, o.g, o.l, o.c, o.e, o.n);
+        }
+        b = block_best<HBLK>(S.bs, b);
+        const int32_t so = H.sold[q];
+        const double f_old = so >= 0 ? hvals[base + so] : 0.0;
+        const int32_t l_old = so >= 0 ? hcnt[base + so] : 0;
+        const int na = H.ncnt[q * HCPAD], nb = H.ncnt[q * HCPAD + 1];
+        if (tid == 0) {
+            const bool stay_best = b.c == c_old;
+            const double slack_b =
+                stay_best ? 0.0 : gain_slack_r(b.e, b.n, f_old, l_old, 1.0 / A.m, b.g);
+            const double lower = stay_best ? 0.0 : b.g - slack_b;
+            int nS = 0, flag = 0;
+            if (!A.integral) {
+                if (na > MAXS || (slack_b > 0.0 && nb > MAXS)) flag |= 2;
+                for (int t = 0; t < na && t < MAXS && !(flag & 2); t++) {
+                    const NearCand o = H.nearA[q * MAXS + t];
+                    if (o.c != b.c && o.g + (double)o.sl >= lower) {
+                        if (nS < MAXS)
+                            S.N[2 + nS++] = o.c;
+                        else
+                            flag |= 2;
+                    }
+                }
+                if (slack_b > 0.0)
+                    for (int t = 0; t < nb && t < MAXS && !(flag & 2); t++) {
+                        const NearCand o = H.nearB[q * MAXS + t];
+                        if (o.c != b.c && o.g >= lower) {
+                            if (nS < MAXS)
+                                S.N[2 + nS++] = o.c;
+                            else
+                                flag |= 2;
+                        }
+                    }
+                if (!stay_best && slack_b > 0.0 && lower <= 0.0) flag |= 1;  // "stay" overlaps
+            }
+            S.nS = nS;
+            S.flag = flag;
+            S.f_old = f_old;
+            S.l_old = l_old;
+        }
+        __syncthreads();
+        const int nS = S.nS, flag = S.flag;
+        if (tid == 0) {  // back to idle: c_old's slot, the counters
+            if (so >= 0) {
+                hkeys[base + so] = -1;
+                hvals[base + so] = 0.0;
+                hcnt[base + so] = 0;
+            }
+            H.sold[q] = -1;
+            H.ncnt[q * HCPAD] = 0;
+            H.ncnt[q * HCPAD + 1] = 0;
+        }
         bool done = false;
         if (A.integral) {
-            if (tid == 0) finish_vertex(A, x, c_old, H.fold[q], b.g, b.c, b.e);
+            if (tid == 0) finish_vertex(A, x, c_old, f_old, b.g, b.c, b.e);
             done = true;
         } else if (nS == 0 && !flag) {
             bool moved = b.c != c_old && b.g > 0.0;  // certain: the exact best
             if (moved && A.sizes[c_old] == 1 && A.sizes[b.c] == 1 &&
                 LBL(A.labels, b.c) > LBL(A.labels, c_old))
                 moved = false;
-            if (!moved || (b.n <= 2 && H.lold[q] <= 2)) {  // exact sums: no refold
+            if (!moved || (b.n <= 2 && l_old <= 2)) {  // exact sums: no refold
                 if (tid == 0) {
                     if (moved)
-                        finish_vertex(A, x, c_old, H.fold[q], b.g, b.c, b.e);
+                        finish_vertex(A, x, c_old, f_old, b.g, b.c, b.e);
                     else
-                        finish_vertex(A, x, c_old, H.fold[q], 0.0, c_old, 0.0);
+                        finish_vertex(A, x, c_old, f_old, 0.0, c_old, 0.0);
                 }
                 done = true;
             }
         }
-        if (done) continue;
+        if (done) {
+            __syncthreads();
+            continue;
+        }
         if (!(flag & 2)) {
             if (tid == 0) {
-                int nn = 0;
-                S.N[nn++] = c_old;
+                S.N[0] = c_old;
+                int nn = 1;
                 if (b.c != c_old) S.N[nn++] = b.c;
-                for (int t = 0; t < nS; t++) S.N[nn++] = H.S[q * MAXS + t];
+                for (int t = 0; t < nS; t++) S.N[nn++] = S.N[2 + t];
                 S.nn = nn;
             }
             __syncthreads();
@@ -1077,38 +1159,12 @@ __global__ void __launch_bounds__(HBLK) k_hub_decide(DecideArgs A, const int32_t
             __syncthreads();
             continue;
         }
-        // overflow: sequential in-order fold of the whole row (rare)
-        const int64_t base = toff[q];
-        const uint32_t ts = (uint32_t)(toff[q + 1] - base);
-        int32_t *keys = hkeys + base;
-        double *vals = hvals + base;
-        if (tid == 0) {
-            for (int64_t e = A.off[i]; e < A.off[i + 1]; e++) {
-                int32_t j = A.nbr[e];
-                if (j == i) continue;
-                uint32_t s = probe_insert(keys, A.assign[j], ts - 1);
-                vals[s] = dadd(vals[s], A.wts[e]);
-            }
-            int s = probe_find(keys, c_old, ts - 1);
-            S.f_old = s >= 0 ? vals[s] : 0.0;
-        }
+        // overflow: ordered folds of the whole row through the (clean) slice
         __syncthreads();
-        const double e_old = S.f_old, a_old_excl = dsub(A.a_tot[c_old], ki);
-        Best bx{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
-        for (uint32_t s = tid; s < ts; s += HBLK) {
-            int32_t c = keys[s];
-            if (c >= 0 && c != c_old)
-                consider(bx, gain_of(vals[s], e_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq),
-                         LBL(A.labels, c), c, vals[s], 0);
-        }
-        bx = block_best<HBLK>(S.bs, bx);
-        for (uint32_t s = tid; s < ts; s += HBLK) {
-            keys[s] = -1;
-            vals[s] = 0.0;
-        }
-        if (tid == 0) finish_vertex(A, x, c_old, e_old, bx.g, bx.c, bx.e);
-        __syncthreads();
+        table_exact<HBLK>(A, x, i, c_old, ki, hkeys + base, hvals + base,
+                          PowTab{(uint32_t)(toff[q + 1] - base - 1)}, S);
     }
+    TR_END(4)
 }
 
 // ================================================================ planning
@@ -1147,11 +1203,13 @@ __global__ void k_tier_local(const uint32_t *skey, const int32_t *sidx, const in
 
 __global__ void k_hub_degrees(const int64_t *off, const int32_t *vtx, const int64_t *stage_off,
                               const int32_t *local, const int64_t *hub_pos, const int64_t *hub_stage,
-                              int64_t nh, int64_t *deg) {
+                              int64_t nh, int64_t *deg, int64_t *row, int32_t *vid) {
     for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < nh;
          h += (int64_t)gridDim.x * blockDim.x) {
         int32_t i = vtx[stage_off[hub_stage[h]] + local[hub_pos[h]]];
         deg[h] = off[i + 1] - off[i];
+        row[h] = off[i];
+        vid[h] = i;
     }
 }
 
@@ -1162,16 +1220,17 @@ __global__ void k_fill_i32_d(int32_t *p, int64_t n, int32_t v) {
 }
 
 void Plan::release() {
-    void *ps[] = {tier_list, hub_eoff, hub_toff, hub_poff, hub_blk, hkeys, hvals, hcnt, hcand,
-                  hsmall, hS, hpart,
-                  hbest, hfold, hlold};
+    void *ps[] = {tier_list, hub_eoff, hub_toff, hub_poff, hub_blk, hub_row, hub_vid, hkeys,
+                  hvals,     hcnt,     hsold,    hncnt,    hnear,   hpart};
     for (void *p : ps)
         if (p) cudaFree(p);
     tier_list = nullptr;
-    hub_eoff = hub_toff = hub_poff = hub_blk = nullptr;
-    hkeys = hcnt = hcand = hsmall = hS = hlold = nullptr;
-    hvals = hfold = nullptr;
-    hpart = hbest = nullptr;
+    hub_eoff = hub_toff = hub_poff = hub_blk = hub_row = nullptr;
+    hub_vid = nullptr;
+    hkeys = hcnt = hsold = hncnt = nullptr;
+    hvals = nullptr;
+    hnear = nullptr;
+    hpart = nullptr;
 }
 
 void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *stage_off_h,
@@ -1217,19 +1276,26 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
         }
     int64_t nh = (int64_t)hub_pos.size();
     if (nh == 0) return;
-    Buf<int64_t> d_hpos(nh, s), d_hst(nh, s), d_deg(nh, s);
+    Buf<int64_t> d_hpos(nh, s), d_hst(nh, s), d_deg(nh, s), d_row(nh, s);
+    Buf<int32_t> d_vid(nh, s);
     PLV_CUDA(cudaMemcpyAsync(d_hpos.get(), hub_pos.data(), sizeof(int64_t) * nh,
                              cudaMemcpyHostToDevice, s));
     PLV_CUDA(cudaMemcpyAsync(d_hst.get(), hub_stage.data(), sizeof(int64_t) * nh,
                              cudaMemcpyHostToDevice, s));
     k_hub_degrees<<<grid_for(nh, 256), 256, 0, s>>>(off, vtx, d_soff, P.tier_list, d_hpos, d_hst,
-                                                   nh, d_deg);
+                                                   nh, d_deg, d_row, d_vid);
     PLV_LAUNCH_CHECK();
-    std::vector<int64_t> deg(nh);
+    std::vector<int64_t> deg(nh), row(nh);
+    std::vector<int32_t> vid(nh);
     PLV_CUDA(cudaMemcpyAsync(deg.data(), d_deg.get(), sizeof(int64_t) * nh, cudaMemcpyDeviceToHost,
                              s));
+    PLV_CUDA(cudaMemcpyAsync(row.data(), d_row.get(), sizeof(int64_t) * nh, cudaMemcpyDeviceToHost,
+                             s));
+    PLV_CUDA(cudaMemcpyAsync(vid.data(), d_vid.get(), sizeof(int32_t) * nh, cudaMemcpyDeviceToHost,
+                             s));
     PLV_CUDA(cudaStreamSynchronize(s));
-    std::vector<int64_t> eoff, toff, poff, blk;
+    std::vector<int64_t> eoff, toff, poff, blk, hrow;
+    std::vector<int32_t> hvid;
     int64_t h0 = 0, max_parts = 1;
     for (int64_t a = 0; a < nst; a++) {
         StagePlan &sp = P.st[a];
@@ -1243,7 +1309,7 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
             int64_t d = deg[h0 + z];
             int64_t cap = 64;
             while (cap < 2 * d + 2) cap <<= 1;
-            int64_t sl = (d + HSLICE - 1) / HSLICE;  // candidates <= degree
+            int64_t sl = (cap + HTSL - 1) / HTSL;  // table slices
             for (int64_t y = 0; y < sl; y++) blk.push_back((z << 32) | y);
             acc += d;
             tacc += cap;
@@ -1251,7 +1317,11 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
             eoff.push_back(acc);
             toff.push_back(tacc);
             poff.push_back(pacc);
+            hrow.push_back(row[h0 + z]);
+            hvid.push_back(vid[h0 + z]);
         }
+        hrow.push_back(0);  // indexed like eoff
+        hvid.push_back(0);
         h0 += sp.tcount[4];
         sp.hub_entries = acc;
         sp.hub_nblk = pacc;
@@ -1264,6 +1334,12 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
     P.hub_toff = dalloc<int64_t>(toff.size());
     P.hub_poff = dalloc<int64_t>(poff.size());
     P.hub_blk = dalloc<int64_t>(blk.size());
+    P.hub_row = dalloc<int64_t>(hrow.size());
+    P.hub_vid = dalloc<int32_t>(hvid.size());
+    PLV_CUDA(cudaMemcpyAsync(P.hub_row, hrow.data(), sizeof(int64_t) * hrow.size(),
+                             cudaMemcpyHostToDevice, s));
+    PLV_CUDA(cudaMemcpyAsync(P.hub_vid, hvid.data(), sizeof(int32_t) * hvid.size(),
+                             cudaMemcpyHostToDevice, s));
     PLV_CUDA(cudaMemcpyAsync(P.hub_eoff, eoff.data(), sizeof(int64_t) * eoff.size(),
                              cudaMemcpyHostToDevice, s));
     PLV_CUDA(cudaMemcpyAsync(P.hub_toff, toff.data(), sizeof(int64_t) * toff.size(),
@@ -1281,14 +1357,13 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
     PLV_CUDA(cudaMemsetAsync(P.hvals, 0, sizeof(double) * T, s));
     PLV_CUDA(cudaMemsetAsync(P.hcnt, 0, sizeof(int32_t) * T, s));
     int64_t H = P.max_hubs;
-    P.hcand = dalloc<int32_t>(T);
-    P.hsmall = dalloc<int32_t>((HCPAD + 2) * H);
-    PLV_CUDA(cudaMemsetAsync(P.hsmall, 0, sizeof(int32_t) * (HCPAD + 2) * H, s));
-    P.hS = dalloc<int32_t>(H * MAXS);
+    P.hsold = dalloc<int32_t>(H);
+    k_fill_i32_d<<<grid_for(H, 256), 256, 0, s>>>(P.hsold, H, -1);
+    PLV_LAUNCH_CHECK();
+    P.hncnt = dalloc<int32_t>(HCPAD * H);
+    PLV_CUDA(cudaMemsetAsync(P.hncnt, 0, sizeof(int32_t) * HCPAD * H, s));
+    P.hnear = dalloc<NearCand>(2 * H * MAXS);
     P.hpart = dalloc<Best>(max_parts);
-    P.hbest = dalloc<Best>(H);
-    P.hfold = dalloc<double>(H);
-    P.hlold = dalloc<int32_t>(H);
     PLV_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -1303,6 +1378,12 @@ void ensure_decide_attrs() {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)t2_smem(T2A_TS)));
     PLV_CUDA(cudaFuncSetAttribute(k_decide_t2<T2_TS, T2_MAXD, BLK>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)t2_smem(T2_TS)));
+    PLV_CUDA(cudaFuncSetAttribute(k_decide_t2<T2A_TS, T2A_MAXD, 512>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)t2_smem(T2A_TS)));
+    PLV_CUDA(cudaFuncSetAttribute(k_decide_t2<T2_TS, T2_MAXD, 1024>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)t2_smem(T2_TS)));
     dev_done = dev;
@@ -1346,15 +1427,25 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
             A, P.tier_list + sp.tstart[1], sp.tcount[1]);
         PLV_LAUNCH_CHECK();
     }
-    if (sp.tcount[2]) {
+    // few vertices (a late colour class): one wide block each, so a vertex's
+    // latency-bound rounds shrink; many: narrow blocks, more vertices per SM
+    if (sp.tcount[2] > T2_WIDE_MAX) {
         k_decide_t2<T2A_TS, T2A_MAXD, 128><<<grid_for(sp.tcount[2], 1, 148 * 8), 128,
                                              t2_smem(T2A_TS), ts[2]>>>(
             A, P.tier_list + sp.tstart[2], sp.tcount[2]);
         PLV_LAUNCH_CHECK();
+    } else if (sp.tcount[2]) {
+        k_decide_t2<T2A_TS, T2A_MAXD, 512><<<(unsigned)sp.tcount[2], 512, t2_smem(T2A_TS), ts[2]>>>(
+            A, P.tier_list + sp.tstart[2], sp.tcount[2]);
+        PLV_LAUNCH_CHECK();
     }
-    if (sp.tcount[3]) {
+    if (sp.tcount[3] > T2_WIDE_MAX) {
         k_decide_t2<T2_TS, T2_MAXD, BLK><<<grid_for(sp.tcount[3], 1, 148 * 3), BLK,
                                            t2_smem(T2_TS), ts[3]>>>(
+            A, P.tier_list + sp.tstart[3], sp.tcount[3]);
+        PLV_LAUNCH_CHECK();
+    } else if (sp.tcount[3]) {
+        k_decide_t2<T2_TS, T2_MAXD, 1024><<<(unsigned)sp.tcount[3], 1024, t2_smem(T2_TS), ts[3]>>>(
             A, P.tier_list + sp.tstart[3], sp.tcount[3]);
         PLV_LAUNCH_CHECK();
     }
@@ -1365,18 +1456,16 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
         const int64_t *toff = P.hub_toff + sp.hub_base;
         int64_t nh = sp.tcount[4], E = sp.hub_entries;
         const int64_t Hm = P.max_hubs;
-        HubScratch H{P.hcand,  P.hsmall, P.hsmall + HCPAD * Hm, P.hsmall + (HCPAD + 1) * Hm,
-                     P.hS,     P.hpart,  P.hbest,              P.hfold,
-                     P.hlold,  P.hub_blk + sp.hub_blk_base,    P.hub_poff + sp.hub_base,
+        HubScratch H{P.hub_row + sp.hub_base, P.hub_vid + sp.hub_base,
+                     P.hsold,  P.hncnt,
+                     (NearCand *)P.hnear, (NearCand *)P.hnear + Hm * MAXS,
+                     P.hpart,  P.hub_blk + sp.hub_blk_base,    P.hub_poff + sp.hub_base,
                      nh};
-        PLV_CUDA(cudaMemsetAsync(P.hsmall, 0, sizeof(int32_t) * (HCPAD + 2) * Hm, st));
-        k_hub_accum<<<grid_for(E, 256), 256, 0, st>>>(A, list, eoff, toff, nh, E, P.hkeys, P.hvals,
+        k_hub_accum<<<grid_for(E, 256), 256, 0, st>>>(A, eoff, toff, nh, E, P.hkeys, P.hvals,
                                                       P.hcnt, H);
         PLV_LAUNCH_CHECK();
         unsigned g2 = (unsigned)sp.hub_nblk;
-        k_hub_pass1<<<g2, HSB, 0, st>>>(A, list, toff, P.hkeys, P.hvals, P.hcnt, H);
-        PLV_LAUNCH_CHECK();
-        k_hub_pass2<<<g2, HSB, 0, st>>>(A, list, toff, P.hkeys, P.hvals, P.hcnt, H);
+        k_hub_pass<<<g2, HSB, 0, st>>>(A, eoff, toff, P.hkeys, P.hvals, P.hcnt, H);
         PLV_LAUNCH_CHECK();
         k_hub_decide<<<(unsigned)(nh < 148 * 2 ? nh : 148 * 2), HBLK, 0, st>>>(
             A, list, toff, P.hkeys, P.hvals, P.hcnt, H);
@@ -1465,4 +1554,26 @@ extern "C" int plv_decide_ex(const int64_t *off, const int32_t *nbr, const doubl
                      (flags & PLV_F_INTEGRAL) ? 1 : 0, out_target, out_moved, out_e_old,
                      out_e_best, cand_h, plv::S(stream));
     PLV_EXIT
+}
+
+// Debug timeline: plv_debug_trace(on) enables / disables recording (and
+// resets the buffer); plv_debug_trace_read copies n records of 8 u64:
+// [kernel id << 32 | block, stamps t0..t5, number of stamps].
+extern "C" int plv_debug_trace(int on) {
+    unsigned int z = 0;
+    if (cudaMemcpyToSymbol(plv::g_tr_on, &on, sizeof(int)) != cudaSuccess) return -4;
+    if (cudaMemcpyToSymbol(plv::g_tr_n, &z, sizeof(z)) != cudaSuccess) return -4;
+    return 0;
+}
+
+extern "C" int plv_debug_trace_read(unsigned long long *out, int64_t max_records, int64_t *n) {
+    unsigned int cnt = 0;
+    if (cudaMemcpyFromSymbol(&cnt, plv::g_tr_n, sizeof(cnt)) != cudaSuccess) return -4;
+    int64_t m = cnt;
+    if (m > (1 << 21) / 8) m = (1 << 21) / 8;
+    if (m > max_records) m = max_records;
+    if (m && cudaMemcpyFromSymbol(out, plv::g_tr, sizeof(unsigned long long) * 8 * m) != cudaSuccess)
+        return -4;
+    *n = m;
+    return 0;
 }

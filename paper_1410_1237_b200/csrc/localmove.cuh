@@ -84,16 +84,16 @@ struct Plan {
     int64_t *hub_toff = nullptr;   // per stage: nh+1 table offsets (from 0, pow2 sizes)
     int64_t *hub_poff = nullptr;   // per stage: nh+1 partial-best offsets (slices)
     int64_t *hub_blk = nullptr;    // pass blocks, (hub << 32) | slice, stage after stage
+    int64_t *hub_row = nullptr;    // per stage: nh (+1 pad) row starts
+    int32_t *hub_vid = nullptr;    // per stage: nh (+1 pad) hub vertices
     int64_t max_hub_entries = 0, max_hubs = 0, max_table = 0;
     int32_t *hkeys = nullptr;  // hub tables: key -1 / val 0 / cnt 0 when clean
     double *hvals = nullptr;
     int32_t *hcnt = nullptr;
-    int32_t *hcand = nullptr;   // candidate slot lists (table layout)
-    int32_t *hsmall = nullptr;  // per hub: ncand, nS, flag
-    int32_t *hS = nullptr;      // per hub: MAXS overlapping communities
-    Best *hpart = nullptr, *hbest = nullptr;
-    double *hfold = nullptr;
-    int32_t *hlold = nullptr;
+    int32_t *hsold = nullptr;   // per hub: table slot of c_old (-1 idle)
+    int32_t *hncnt = nullptr;   // per hub: near-candidate counters (0 idle)
+    void *hnear = nullptr;      // per hub: 2 * MAXS near candidates
+    Best *hpart = nullptr;      // pass partial bests
     int64_t max_slices = 1;
     void release();
 };
