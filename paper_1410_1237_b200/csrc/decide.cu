@@ -1396,22 +1396,22 @@ void launch_decide(const Plan &P, int64_t a, DecideArgs A, cudaStream_t st) {
 
 void launch_decide_par(const Plan &P, int64_t a, DecideArgs A, cudaStream_t st,
                        const cudaStream_t *side, cudaEvent_t fork, const cudaEvent_t *join) {
+    // tier t < NTIER - 1 on its own stream side[t]; the hubs on `st`
     const StagePlan &sp = P.st[a];
-    int used[NTIER], nu = 0;
-    for (int t = NTIER - 1; t >= 0; t--)  // hubs (longest) first, on the main stream
-        if (sp.tcount[t]) used[nu++] = t;
     cudaStream_t ts[NTIER] = {st, st, st, st, st};
-    if (nu > 1) {
-        PLV_CUDA(cudaEventRecord(fork, st));
-        for (int u = 1; u < nu; u++) {
-            PLV_CUDA(cudaStreamWaitEvent(side[u - 1], fork, 0));
-            ts[used[u]] = side[u - 1];
-        }
+    bool forked = false;
+    for (int t = 0; t < NTIER - 1; t++) {
+        if (!sp.tcount[t]) continue;
+        if (!forked) PLV_CUDA(cudaEventRecord(fork, st));
+        forked = true;
+        PLV_CUDA(cudaStreamWaitEvent(side[t], fork, 0));
+        ts[t] = side[t];
     }
     launch_decide_tiers(P, a, A, ts);
-    for (int u = 1; u < nu; u++) {
-        PLV_CUDA(cudaEventRecord(join[u - 1], side[u - 1]));
-        PLV_CUDA(cudaStreamWaitEvent(st, join[u - 1], 0));
+    for (int t = 0; t < NTIER - 1; t++) {
+        if (!sp.tcount[t]) continue;
+        PLV_CUDA(cudaEventRecord(join[t], side[t]));
+        PLV_CUDA(cudaStreamWaitEvent(st, join[t], 0));
     }
 }
 
@@ -1430,7 +1430,7 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
     // few vertices (a late colour class): one wide block each, so a vertex's
     // latency-bound rounds shrink; many: narrow blocks, more vertices per SM
     if (sp.tcount[2] > T2_WIDE_MAX) {
-        k_decide_t2<T2A_TS, T2A_MAXD, 128><<<grid_for(sp.tcount[2], 1, 148 * 8), 128,
+        k_decide_t2<T2A_TS, T2A_MAXD, 128><<<grid_for(sp.tcount[2], 1, 1 << 30), 128,
                                              t2_smem(T2A_TS), ts[2]>>>(
             A, P.tier_list + sp.tstart[2], sp.tcount[2]);
         PLV_LAUNCH_CHECK();
@@ -1440,7 +1440,7 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
         PLV_LAUNCH_CHECK();
     }
     if (sp.tcount[3] > T2_WIDE_MAX) {
-        k_decide_t2<T2_TS, T2_MAXD, BLK><<<grid_for(sp.tcount[3], 1, 148 * 3), BLK,
+        k_decide_t2<T2_TS, T2_MAXD, BLK><<<grid_for(sp.tcount[3], 1, 1 << 30), BLK,
                                            t2_smem(T2_TS), ts[3]>>>(
             A, P.tier_list + sp.tstart[3], sp.tcount[3]);
         PLV_LAUNCH_CHECK();

@@ -143,14 +143,20 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
             P->ev.resize(2 * nst);
             for (auto &e : P->ev) PLV_CUDA(cudaEventCreate(&e));
         }
+        int prio_lo = 0, prio_hi = 0;
+        PLV_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
         for (int t = 0; t < NTIER - 1; t++) {
-            PLV_CUDA(cudaStreamCreateWithFlags(&P->side[t], cudaStreamNonBlocking));
+            // the hub chain (capture stream) first, then the block tiers (their
+            // per-vertex latency is long), the warp / thread tiers last
+            int pr = prio_hi + (NTIER - 1 - t);
+            if (pr > prio_lo) pr = prio_lo;
+            PLV_CUDA(cudaStreamCreateWithPriority(&P->side[t], cudaStreamNonBlocking, pr));
             PLV_CUDA(cudaEventCreateWithFlags(&P->join[t], cudaEventDisableTiming));
         }
         PLV_CUDA(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming));
         PLV_CUDA(cudaStreamSynchronize(s));
         cudaStream_t cs;
-        PLV_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        PLV_CUDA(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, prio_hi));
         PLV_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
         try {
             record_iteration(*P, cs);
@@ -163,7 +169,7 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
         }
         PLV_CUDA(cudaStreamEndCapture(cs, &P->graph));
         PLV_CUDA(cudaStreamDestroy(cs));
-        PLV_CUDA(cudaGraphInstantiate(&P->exec, P->graph, 0));
+        PLV_CUDA(cudaGraphInstantiate(&P->exec, P->graph, cudaGraphInstantiateFlagUseNodePriority));
     } catch (...) {
         cudaStreamSynchronize(s);
         P->release();
