@@ -868,8 +868,8 @@ __global__ void __launch_bounds__(NT) k_decide_t2(DecideArgs A, const int32_t *l
 
 // ------------------------------------------------------------ tier 4 (hubs)
 
-constexpr int HSB = 256;            // threads per hub pass block
-constexpr int HSU = 8;              // table slots per thread in a pass block
+constexpr int HSB = 1024;           // threads per hub pass block
+constexpr int HSU = 2;              // table slots per thread in a pass block
 constexpr int HTSL = HSB * HSU;     // table slots per pass block
 constexpr int HCPAD = 32;           // per-hub counters one 128-byte line apart
 
@@ -982,6 +982,7 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int64_t *e
     const int32_t l_old = so >= 0 ? hcnt[base + so] : 0;
     const double ki = A.k[i], a_old_excl = dsub(A.a_tot[c_old], ki);
     const double inv_m = 1.0 / A.m;
+    TR_MARK
     int32_t c[HSU];
     double F[HSU], g[HSU];
     int32_t L[HSU];
@@ -994,25 +995,34 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int64_t *e
         F[u] = s < cap ? hvals[base + s] : 0.0;
         L[u] = s < cap ? hcnt[base + s] : 0;
     }
+    TR_MARK
     Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
     unsigned long long nc = 0;
+    double at[HSU];
+#pragma unroll
+    for (int u = 0; u < HSU; u++) {  // every gather in flight before any store
+        nc += c[u] >= 0;
+        if (c[u] == c_old) c[u] = -1;  // not a candidate (its slot stays)
+        at[u] = c[u] >= 0 ? __ldg(A.a_tot + c[u]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < HSU; u++) {
+        if (c[u] < 0) continue;
+        g[u] = gain_of(F[u], f_old, A.m, ki, a_old_excl, at[u], A.four_m_sq);
+        sl[u] = __double2float_ru(gain_slack_r(F[u], L[u], f_old, l_old, inv_m, g[u]));
+        consider(b, g[u], LBL(A.labels, c[u]), c[u], F[u], L[u]);
+    }
 #pragma unroll
     for (int u = 0; u < HSU; u++) {
         const int64_t s = s0 + u * HSB;
         if (c[u] < 0) continue;
-        nc++;
-        if (c[u] == c_old) {
-            c[u] = -1;  // not a candidate
-            continue;
-        }
-        g[u] = gain_of(F[u], f_old, A.m, ki, a_old_excl, A.a_tot[c[u]], A.four_m_sq);
-        sl[u] = __double2float_ru(gain_slack_r(F[u], L[u], f_old, l_old, inv_m, g[u]));
-        consider(b, g[u], LBL(A.labels, c[u]), c[u], F[u], L[u]);
         hkeys[base + s] = -1;
         hvals[base + s] = 0.0;
         hcnt[base + s] = 0;
     }
+    TR_MARK
     b = block_best<HSB>(bs, b);
+    TR_MARK
     if (!A.integral) {
         const double thr = b.g - slack_max(ki, eoff[q + 1] - eoff[q], inv_m);
 #pragma unroll
@@ -1055,62 +1065,69 @@ __global__ void __launch_bounds__(HBLK) k_hub_decide(DecideArgs A, const int32_t
         const int32_t c_old = A.assign[i];
         const double ki = A.k[i];
         const int64_t base = toff[q];
-        Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
-        for (int64_t t = H.poff[q] + tid; t < H.poff[q + 1]; t += HBLK) {
-            const Best o = H.part[t];
-            consider(b, o.g, o.l, o.c, o.e, o.n);
-        }
-        b = block_best<HBLK>(S.bs, b);
-        const int32_t so = H.sold[q];
-        const double f_old = so >= 0 ? hvals[base + so] : 0.0;
-        const int32_t l_old = so >= 0 ? hcnt[base + so] : 0;
-        const int na = H.ncnt[q * HCPAD], nb = H.ncnt[q * HCPAD + 1];
-        if (tid == 0) {
-            const bool stay_best = b.c == c_old;
+        // warp 0: the hub's best from the partials and the overlap test on the
+        // near candidates (one per lane); the block waits once
+        if (tid < 32) {
+            const int lane = tid;
+            Best bw{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
+            for (int64_t t = H.poff[q] + lane; t < H.poff[q + 1]; t += 32) {
+                const Best o = H.part[t];
+                consider(bw, o.g, o.l, o.c, o.e, o.n);
+            }
+            warp_best(bw);
+            const int32_t so = H.sold[q];
+            const double f_old = so >= 0 ? hvals[base + so] : 0.0;
+            const int32_t l_old = so >= 0 ? hcnt[base + so] : 0;
+            const int na = H.ncnt[q * HCPAD], nb = H.ncnt[q * HCPAD + 1];
+            const bool stay_best = bw.c == c_old;
             const double slack_b =
-                stay_best ? 0.0 : gain_slack_r(b.e, b.n, f_old, l_old, 1.0 / A.m, b.g);
-            const double lower = stay_best ? 0.0 : b.g - slack_b;
-            int nS = 0, flag = 0;
+                stay_best ? 0.0 : gain_slack_r(bw.e, bw.n, f_old, l_old, 1.0 / A.m, bw.g);
+            const double lower = stay_best ? 0.0 : bw.g - slack_b;
+            int flag = 0;
+            bool pa = false, pb = false;
+            int32_t ca = -1, cb = -1;
             if (!A.integral) {
                 if (na > MAXS || (slack_b > 0.0 && nb > MAXS)) flag |= 2;
-                for (int t = 0; t < na && t < MAXS && !(flag & 2); t++) {
-                    const NearCand o = H.nearA[q * MAXS + t];
-                    if (o.c != b.c && o.g + (double)o.sl >= lower) {
-                        if (nS < MAXS)
-                            S.N[2 + nS++] = o.c;
-                        else
-                            flag |= 2;
-                    }
+                if (lane < na && lane < MAXS) {
+                    const NearCand o = H.nearA[q * MAXS + lane];
+                    pa = o.c != bw.c && o.g + (double)o.sl >= lower;
+                    ca = o.c;
                 }
-                if (slack_b > 0.0)
-                    for (int t = 0; t < nb && t < MAXS && !(flag & 2); t++) {
-                        const NearCand o = H.nearB[q * MAXS + t];
-                        if (o.c != b.c && o.g >= lower) {
-                            if (nS < MAXS)
-                                S.N[2 + nS++] = o.c;
-                            else
-                                flag |= 2;
-                        }
-                    }
+                if (slack_b > 0.0 && lane < nb && lane < MAXS) {
+                    const NearCand o = H.nearB[q * MAXS + lane];
+                    pb = o.c != bw.c && o.g >= lower;
+                    cb = o.c;
+                }
                 if (!stay_best && slack_b > 0.0 && lower <= 0.0) flag |= 1;  // "stay" overlaps
             }
-            S.nS = nS;
-            S.flag = flag;
-            S.f_old = f_old;
-            S.l_old = l_old;
+            const unsigned ma = __ballot_sync(FULL, pa), mb = __ballot_sync(FULL, pb);
+            const unsigned below = (1u << lane) - 1;
+            const int nA = __popc(ma), nS = nA + __popc(mb);
+            if (nS > MAXS) flag |= 2;
+            if (pa && !(flag & 2)) S.N[2 + __popc(ma & below)] = ca;
+            if (pb && !(flag & 2)) S.N[2 + nA + __popc(mb & below)] = cb;
+            if (lane == 0) {
+                S.bs.out = bw;
+                S.nS = nS;
+                S.flag = flag;
+                S.f_old = f_old;
+                S.l_old = l_old;
+                // back to idle: c_old's slot, the counters
+                if (so >= 0) {
+                    hkeys[base + so] = -1;
+                    hvals[base + so] = 0.0;
+                    hcnt[base + so] = 0;
+                }
+                H.sold[q] = -1;
+                H.ncnt[q * HCPAD] = 0;
+                H.ncnt[q * HCPAD + 1] = 0;
+            }
         }
         __syncthreads();
         const int nS = S.nS, flag = S.flag;
-        if (tid == 0) {  // back to idle: c_old's slot, the counters
-            if (so >= 0) {
-                hkeys[base + so] = -1;
-                hvals[base + so] = 0.0;
-                hcnt[base + so] = 0;
-            }
-            H.sold[q] = -1;
-            H.ncnt[q * HCPAD] = 0;
-            H.ncnt[q * HCPAD + 1] = 0;
-        }
+        const Best b = S.bs.out;
+        const double f_old = S.f_old;
+        const int32_t l_old = S.l_old;
         bool done = false;
         if (A.integral) {
             if (tid == 0) finish_vertex(A, x, c_old, f_old, b.g, b.c, b.e);
