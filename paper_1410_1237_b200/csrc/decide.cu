@@ -68,7 +68,6 @@ struct Trace {
         tr.mark();     \
         tr.flush(kid); \
     }
-constexpr int HBLK = 1024;                         // threads per hub block
 
 __device__ __forceinline__ int64_t LBL(const int32_t *labels, int32_t c) {
     return labels ? (int64_t)labels[c] : (int64_t)c;
@@ -958,19 +957,172 @@ __device__ __forceinline__ double slack_max(double ki, int64_t d, double inv_m) 
     return 1.1 * (1.02 * (2.0 * se * inv_m) + 8.0 * U_RND * (3.01 * ki * inv_m)) + 1e-300;
 }
 
+// The decision for hub q, by the block that completed its last pass item:
+// the hub's best from the partials, the overlap test on the listed near
+// candidates, then the decision.  Certain non-moves (and integral graphs)
+// finish at once; otherwise the overlapping communities are folded exactly
+// (or, past MAXS of them, the whole row through the hub's clean table slice)
+// and the decision is taken on exact values.  Resets the hub's state.
+__device__ __forceinline__ Best ldcg_best(const Best *p) {
+    Best b;
+    b.g = __ldcg(&p->g);
+    b.l = __ldcg(&p->l);
+    b.c = __ldcg(&p->c);
+    b.e = __ldcg(&p->e);
+    b.n = __ldcg(&p->n);
+    return b;
+}
+__device__ __forceinline__ NearCand ldcg_near(const NearCand *p) {
+    return NearCand{__ldcg(&p->c), __ldcg(&p->sl), __ldcg(&p->g)};
+}
+
+template <int NT>
+__device__ void hub_decide_one(const DecideArgs &A, const int32_t *list, const int64_t *toff,
+                               int32_t *hkeys, double *hvals, int32_t *hcnt, const HubScratch &H,
+                               int64_t q, CertSmem<NT> &S) {
+    const int tid = threadIdx.x;
+    const int64_t x = list[q];
+    const int32_t i = H.vid[q];
+    const int32_t c_old = A.assign[i];
+    const double ki = A.k[i];
+    const int64_t base = toff[q];
+    // warp 0: the hub's best from the partials and the overlap test on the
+    // near candidates (one per lane); the block waits once
+    if (tid < 32) {
+        const int lane = tid;
+        Best bw{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
+        for (int64_t t = H.poff[q] + lane; t < H.poff[q + 1]; t += 32) {
+            const Best o = ldcg_best(H.part + t);
+            consider(bw, o.g, o.l, o.c, o.e, o.n);
+        }
+        warp_best(bw);
+        const int32_t so = H.sold[q];
+        const double f_old = so >= 0 ? hvals[base + so] : 0.0;
+        const int32_t l_old = so >= 0 ? hcnt[base + so] : 0;
+        const int na = __ldcg(H.ncnt + q * HCPAD), nb = __ldcg(H.ncnt + q * HCPAD + 1);
+        const bool stay_best = bw.c == c_old;
+        const double slack_b =
+            stay_best ? 0.0 : gain_slack_r(bw.e, bw.n, f_old, l_old, 1.0 / A.m, bw.g);
+        const double lower = stay_best ? 0.0 : bw.g - slack_b;
+        int flag = 0;
+        bool pa = false, pb = false;
+        int32_t ca = -1, cb = -1;
+        if (!A.integral) {
+            if (na > MAXS || (slack_b > 0.0 && nb > MAXS)) flag |= 2;
+            if (lane < na && lane < MAXS) {
+                const NearCand o = ldcg_near(H.nearA + q * MAXS + lane);
+                pa = o.c != bw.c && o.g + (double)o.sl >= lower;
+                ca = o.c;
+            }
+            if (slack_b > 0.0 && lane < nb && lane < MAXS) {
+                const NearCand o = ldcg_near(H.nearB + q * MAXS + lane);
+                pb = o.c != bw.c && o.g >= lower;
+                cb = o.c;
+            }
+            if (!stay_best && slack_b > 0.0 && lower <= 0.0) flag |= 1;  // "stay" overlaps
+        }
+        const unsigned ma = __ballot_sync(FULL, pa), mb = __ballot_sync(FULL, pb);
+        const unsigned below = (1u << lane) - 1;
+        const int nA = __popc(ma), nS = nA + __popc(mb);
+        if (nS > MAXS) flag |= 2;
+        if (pa && !(flag & 2)) S.N[2 + __popc(ma & below)] = ca;
+        if (pb && !(flag & 2)) S.N[2 + nA + __popc(mb & below)] = cb;
+        if (lane == 0) {
+            S.bs.out = bw;
+            S.nS = nS;
+            S.flag = flag;
+            S.f_old = f_old;
+            S.l_old = l_old;
+            // back to idle: c_old's slot, the counters
+            if (so >= 0) {
+                hkeys[base + so] = -1;
+                hvals[base + so] = 0.0;
+                hcnt[base + so] = 0;
+            }
+            H.sold[q] = -1;
+            H.ncnt[q * HCPAD] = 0;
+            H.ncnt[q * HCPAD + 1] = 0;
+            H.ncnt[q * HCPAD + 2] = 0;  // the pass-item ticket
+        }
+    }
+    __syncthreads();
+    const int nS = S.nS, flag = S.flag;
+    const Best b = S.bs.out;
+    const double f_old = S.f_old;
+    const int32_t l_old = S.l_old;
+    bool done = false;
+    if (A.integral) {
+        if (tid == 0) finish_vertex(A, x, c_old, f_old, b.g, b.c, b.e);
+        done = true;
+    } else if (nS == 0 && !flag) {
+        bool moved = b.c != c_old && b.g > 0.0;  // certain: the exact best
+        if (moved && A.sizes[c_old] == 1 && A.sizes[b.c] == 1 &&
+            LBL(A.labels, b.c) > LBL(A.labels, c_old))
+            moved = false;
+        if (!moved || (b.n <= 2 && l_old <= 2)) {  // exact sums: no refold
+            if (tid == 0) {
+                if (moved)
+                    finish_vertex(A, x, c_old, f_old, b.g, b.c, b.e);
+                else
+                    finish_vertex(A, x, c_old, f_old, 0.0, c_old, 0.0);
+            }
+            done = true;
+        }
+    }
+    if (done) {
+        __syncthreads();
+        return;
+    }
+    if (!(flag & 2)) {
+        if (tid == 0) {
+            S.N[0] = c_old;
+            int nn = 1;
+            if (b.c != c_old) S.N[nn++] = b.c;
+            for (int t = 0; t < nS; t++) S.N[nn++] = S.N[2 + t];
+            S.nn = nn;
+        }
+        __syncthreads();
+        exact_folds<NT, 1>(A, i, S);
+        if (tid == 0) {
+            double a_old_excl = dsub(A.a_tot[c_old], ki);
+            Best e{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
+            for (int t = 1; t < S.nn; t++) {
+                int32_t c = S.N[t];
+                consider(e,
+                         gain_of(S.acc[t], S.acc[0], A.m, ki, a_old_excl, A.a_tot[c],
+                                 A.four_m_sq),
+                         LBL(A.labels, c), c, S.acc[t], 0);
+            }
+            finish_vertex(A, x, c_old, S.acc[0], e.g, e.c, e.e);
+        }
+        __syncthreads();
+        return;
+    }
+    // overflow: ordered folds of the whole row through the (clean) slice
+    __syncthreads();
+    table_exact<NT>(A, x, i, c_old, ki, hkeys + base, hvals + base,
+                      PowTab{(uint32_t)(toff[q + 1] - base - 1)}, S);
+}
+
 // Pass block (hub q, table slice y): gains and slack of the slice's entries
 // on the any-order sums, the slice's best (incl. "stay"), and every entry
 // within slack_max of it -- a superset of the entries that can overlap the
 // hub's best -- listed for the decision.  Clears the slice (c_old's slot is
 // cleared by the decision, which reads it).
-__global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int64_t *eoff,
-                                                 const int64_t *toff, int32_t *hkeys,
-                                                 double *hvals, int32_t *hcnt, HubScratch H) {
+__global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *list,
+                                                 const int64_t *eoff, const int64_t *toff,
+                                                 int32_t *hkeys, double *hvals, int32_t *hcnt,
+                                                 HubScratch H) {
     TR_BEGIN
-    __shared__ BestSmem<HSB> bs;
-    typedef cub::BlockReduce<unsigned long long, HSB> BR;
-    __shared__ typename BR::TempStorage red;
+    __shared__ CertSmem<HSB> S;
+    __shared__ int32_t cidx[HSB];
+    __shared__ double cw[HSB];
+    __shared__ int s_last;
     const int tid = threadIdx.x;
+    if (tid == 0) {
+        S.cidx = cidx;
+        S.cw = cw;
+    }
     const int64_t pk = H.blk[blockIdx.x];
     const int64_t q = pk >> 32, y = pk & 0xffffffffll;
     const int32_t i = H.vid[q];
@@ -1021,7 +1173,7 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int64_t *e
         hcnt[base + s] = 0;
     }
     TR_MARK
-    b = block_best<HSB>(bs, b);
+    b = block_best<HSB>(S.bs, b);
     TR_MARK
     if (!A.integral) {
         const double thr = b.g - slack_max(ki, eoff[q + 1] - eoff[q], inv_m);
@@ -1033,156 +1185,26 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int64_t *e
             if (k < MAXS) (cat ? H.nearB : H.nearA)[q * MAXS + k] = NearCand{c[u], sl[u], g[u]};
         }
     }
-    const unsigned long long tot = BR(red).Sum(nc);
+    const unsigned long long tot = cub::BlockReduce<unsigned long long, HSB>(S.red).Sum(nc);
     if (tid == 0) {
         H.part[H.poff[q] + y] = b;
         if (A.cand && tot) atomicAdd(A.cand, tot);
     }
+    // the block finishing the hub's last item decides it (every writer
+    // releases its partial / near-list stores, one ticket, acquire)
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        const int nsl = (int)(H.poff[q + 1] - H.poff[q]);
+        s_last = atomicAdd(H.ncnt + q * HCPAD + 2, 1) == nsl - 1;
+        if (s_last) __threadfence();
+    }
+    __syncthreads();
+    TR_MARK
+    if (s_last) hub_decide_one<HSB>(A, list, toff, hkeys, hvals, hcnt, H, q, S);
     TR_END(2)
 }
 
-// Block per hub: the hub's best from the partials, the overlap test on the
-// listed near candidates, then the decision.  Certain non-moves (and integral
-// graphs) finish at once; otherwise the overlapping communities are folded
-// exactly (or, past MAXS of them, the whole row through the hub's clean table
-// slice) and the decision is taken on exact values.  Resets the hub's state.
-__global__ void __launch_bounds__(HBLK) k_hub_decide(DecideArgs A, const int32_t *list,
-                                                    const int64_t *toff, int32_t *hkeys,
-                                                    double *hvals, int32_t *hcnt, HubScratch H) {
-    TR_BEGIN
-    __shared__ CertSmem<HBLK> S;
-    __shared__ int32_t cidx[HBLK];
-    __shared__ double cw[HBLK];
-    const int tid = threadIdx.x;
-    if (tid == 0) {
-        S.cidx = cidx;
-        S.cw = cw;
-    }
-    __syncthreads();
-    for (int64_t q = blockIdx.x; q < H.nh; q += gridDim.x) {
-        const int64_t x = list[q];
-        const int32_t i = H.vid[q];
-        const int32_t c_old = A.assign[i];
-        const double ki = A.k[i];
-        const int64_t base = toff[q];
-        // warp 0: the hub's best from the partials and the overlap test on the
-        // near candidates (one per lane); the block waits once
-        if (tid < 32) {
-            const int lane = tid;
-            Best bw{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
-            for (int64_t t = H.poff[q] + lane; t < H.poff[q + 1]; t += 32) {
-                const Best o = H.part[t];
-                consider(bw, o.g, o.l, o.c, o.e, o.n);
-            }
-            warp_best(bw);
-            const int32_t so = H.sold[q];
-            const double f_old = so >= 0 ? hvals[base + so] : 0.0;
-            const int32_t l_old = so >= 0 ? hcnt[base + so] : 0;
-            const int na = H.ncnt[q * HCPAD], nb = H.ncnt[q * HCPAD + 1];
-            const bool stay_best = bw.c == c_old;
-            const double slack_b =
-                stay_best ? 0.0 : gain_slack_r(bw.e, bw.n, f_old, l_old, 1.0 / A.m, bw.g);
-            const double lower = stay_best ? 0.0 : bw.g - slack_b;
-            int flag = 0;
-            bool pa = false, pb = false;
-            int32_t ca = -1, cb = -1;
-            if (!A.integral) {
-                if (na > MAXS || (slack_b > 0.0 && nb > MAXS)) flag |= 2;
-                if (lane < na && lane < MAXS) {
-                    const NearCand o = H.nearA[q * MAXS + lane];
-                    pa = o.c != bw.c && o.g + (double)o.sl >= lower;
-                    ca = o.c;
-                }
-                if (slack_b > 0.0 && lane < nb && lane < MAXS) {
-                    const NearCand o = H.nearB[q * MAXS + lane];
-                    pb = o.c != bw.c && o.g >= lower;
-                    cb = o.c;
-                }
-                if (!stay_best && slack_b > 0.0 && lower <= 0.0) flag |= 1;  // "stay" overlaps
-            }
-            const unsigned ma = __ballot_sync(FULL, pa), mb = __ballot_sync(FULL, pb);
-            const unsigned below = (1u << lane) - 1;
-            const int nA = __popc(ma), nS = nA + __popc(mb);
-            if (nS > MAXS) flag |= 2;
-            if (pa && !(flag & 2)) S.N[2 + __popc(ma & below)] = ca;
-            if (pb && !(flag & 2)) S.N[2 + nA + __popc(mb & below)] = cb;
-            if (lane == 0) {
-                S.bs.out = bw;
-                S.nS = nS;
-                S.flag = flag;
-                S.f_old = f_old;
-                S.l_old = l_old;
-                // back to idle: c_old's slot, the counters
-                if (so >= 0) {
-                    hkeys[base + so] = -1;
-                    hvals[base + so] = 0.0;
-                    hcnt[base + so] = 0;
-                }
-                H.sold[q] = -1;
-                H.ncnt[q * HCPAD] = 0;
-                H.ncnt[q * HCPAD + 1] = 0;
-            }
-        }
-        __syncthreads();
-        const int nS = S.nS, flag = S.flag;
-        const Best b = S.bs.out;
-        const double f_old = S.f_old;
-        const int32_t l_old = S.l_old;
-        bool done = false;
-        if (A.integral) {
-            if (tid == 0) finish_vertex(A, x, c_old, f_old, b.g, b.c, b.e);
-            done = true;
-        } else if (nS == 0 && !flag) {
-            bool moved = b.c != c_old && b.g > 0.0;  // certain: the exact best
-            if (moved && A.sizes[c_old] == 1 && A.sizes[b.c] == 1 &&
-                LBL(A.labels, b.c) > LBL(A.labels, c_old))
-                moved = false;
-            if (!moved || (b.n <= 2 && l_old <= 2)) {  // exact sums: no refold
-                if (tid == 0) {
-                    if (moved)
-                        finish_vertex(A, x, c_old, f_old, b.g, b.c, b.e);
-                    else
-                        finish_vertex(A, x, c_old, f_old, 0.0, c_old, 0.0);
-                }
-                done = true;
-            }
-        }
-        if (done) {
-            __syncthreads();
-            continue;
-        }
-        if (!(flag & 2)) {
-            if (tid == 0) {
-                S.N[0] = c_old;
-                int nn = 1;
-                if (b.c != c_old) S.N[nn++] = b.c;
-                for (int t = 0; t < nS; t++) S.N[nn++] = S.N[2 + t];
-                S.nn = nn;
-            }
-            __syncthreads();
-            exact_folds<HBLK, 1>(A, i, S);
-            if (tid == 0) {
-                double a_old_excl = dsub(A.a_tot[c_old], ki);
-                Best e{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
-                for (int t = 1; t < S.nn; t++) {
-                    int32_t c = S.N[t];
-                    consider(e,
-                             gain_of(S.acc[t], S.acc[0], A.m, ki, a_old_excl, A.a_tot[c],
-                                     A.four_m_sq),
-                             LBL(A.labels, c), c, S.acc[t], 0);
-                }
-                finish_vertex(A, x, c_old, S.acc[0], e.g, e.c, e.e);
-            }
-            __syncthreads();
-            continue;
-        }
-        // overflow: ordered folds of the whole row through the (clean) slice
-        __syncthreads();
-        table_exact<HBLK>(A, x, i, c_old, ki, hkeys + base, hvals + base,
-                          PowTab{(uint32_t)(toff[q + 1] - base - 1)}, S);
-    }
-    TR_END(4)
-}
 
 // ================================================================ planning
 
@@ -1482,10 +1504,7 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
                                                       P.hcnt, H);
         PLV_LAUNCH_CHECK();
         unsigned g2 = (unsigned)sp.hub_nblk;
-        k_hub_pass<<<g2, HSB, 0, st>>>(A, eoff, toff, P.hkeys, P.hvals, P.hcnt, H);
-        PLV_LAUNCH_CHECK();
-        k_hub_decide<<<(unsigned)(nh < 148 * 2 ? nh : 148 * 2), HBLK, 0, st>>>(
-            A, list, toff, P.hkeys, P.hvals, P.hcnt, H);
+        k_hub_pass<<<g2, HSB, 0, st>>>(A, list, eoff, toff, P.hkeys, P.hvals, P.hcnt, H);
         PLV_LAUNCH_CHECK();
     }
 }
