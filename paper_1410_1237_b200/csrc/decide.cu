@@ -271,27 +271,44 @@ __device__ __forceinline__ Best block_best(BestSmem<NT> &S, Best b) {
     return r;
 }
 
+// A tier's vertices: stage-local index x (outputs), vertex i, row [row, end),
+// laid out by the plan so a kernel's first loads are coalesced and independent.
+struct TierRef {
+    const int32_t *x;
+    const int32_t *vid;
+    const int64_t *row, *end;
+};
+
 // ------------------------------------------------------------ tier 0
 
-__global__ void __launch_bounds__(256) k_decide_t0(DecideArgs A, const int32_t *list, int64_t cnt) {
+__global__ void __launch_bounds__(256) k_decide_t0(DecideArgs A, TierRef L, int64_t cnt) {
     unsigned long long my_cand = 0;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < cnt;
          q += (int64_t)gridDim.x * blockDim.x) {
-        int64_t x = list[q];
-        int32_t i = A.subset[x];
-        int32_t c_old = A.assign[i];
-        int64_t e0 = A.off[i];
-        int deg = (int)(A.off[i + 1] - e0);
+        const int64_t x = L.x[q];
+        const int32_t i = L.vid[q];
+        const int64_t e0 = L.row[q];
+        const int deg = (int)(L.end[q] - e0);
+        const int32_t c_old = A.assign[i];
+        // all row loads, then all community loads, in flight together
+        int32_t jj[T0_MAXD], cc[T0_MAXD];
+        double ww[T0_MAXD];
+#pragma unroll
+        for (int t = 0; t < T0_MAXD; t++) {
+            jj[t] = t < deg ? A.nbr[e0 + t] : i;
+            ww[t] = t < deg ? A.wts[e0 + t] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < T0_MAXD; t++) cc[t] = jj[t] != i ? A.assign[jj[t]] : -1;
         int32_t keys[T0_MAXD];
         double vals[T0_MAXD];
         int nc = 0;
 #pragma unroll
         for (int t = 0; t < T0_MAXD; t++) {
             if (t < deg) {
-                int32_t j = A.nbr[e0 + t];
-                if (j != i) {
-                    int32_t c = A.assign[j];
-                    double w = A.wts[e0 + t];
+                if (cc[t] >= 0) {
+                    const int32_t c = cc[t];
+                    const double w = ww[t];
                     bool found = false;
 #pragma unroll
                     for (int s = 0; s < T0_MAXD; s++) {
@@ -354,7 +371,7 @@ __device__ __forceinline__ void fold_chunk(int32_t *keys, double *vals, Tab T, i
 
 // ------------------------------------------------------------ tier 1
 
-__global__ void __launch_bounds__(T1_WARPS * 32) k_decide_t1(DecideArgs A, const int32_t *list,
+__global__ void __launch_bounds__(T1_WARPS * 32) k_decide_t1(DecideArgs A, TierRef L,
                                                               int64_t cnt) {
     __shared__ int32_t skeys[T1_WARPS][T1_TS];
     __shared__ double svals[T1_WARPS][T1_TS];
@@ -366,10 +383,10 @@ __global__ void __launch_bounds__(T1_WARPS * 32) k_decide_t1(DecideArgs A, const
     unsigned long long my_cand = 0;
     for (int64_t q = blockIdx.x * (int64_t)T1_WARPS + wid; q < cnt;
          q += (int64_t)gridDim.x * T1_WARPS) {
-        int64_t x = list[q];
-        int32_t i = A.subset[x];
-        int32_t c_old = A.assign[i];
-        int64_t e0 = A.off[i], e1 = A.off[i + 1];
+        const int64_t x = L.x[q];
+        const int32_t i = L.vid[q];
+        const int64_t e0 = L.row[q], e1 = L.end[q];
+        const int32_t c_old = A.assign[i];
         int deg = (int)(e1 - e0);
         uint32_t ts = 32;
         while (ts < (uint32_t)(deg + deg / 2 + 2)) ts <<= 1;
@@ -785,13 +802,12 @@ __device__ void table_exact(const DecideArgs &A, int64_t x, int32_t i, int32_t c
 // any-order accumulation of the row (U entries per thread in flight), the
 // certification passes, then the exact resolution when needed.
 template <int NT, int U, int FU, class Tab, class CL>
-__device__ __forceinline__ void block_decide(const DecideArgs &A, int64_t x, Tab T, int32_t *keys,
-                                             double *vals, int32_t *cntt, CL *clist, int *ncl,
-                                             CertSmem<NT> &S, unsigned long long &my_cand) {
+__device__ __forceinline__ void block_decide(const DecideArgs &A, int64_t x, int32_t i, int64_t e0,
+                                             int64_t e1, Tab T, int32_t *keys, double *vals,
+                                             int32_t *cntt, CL *clist, int *ncl, CertSmem<NT> &S,
+                                             unsigned long long &my_cand) {
     const int tid = threadIdx.x, lane = tid & 31;
-    const int32_t i = A.subset[x];
     const int32_t c_old = A.assign[i];
-    const int64_t e0 = A.off[i], e1 = A.off[i + 1];
     const double ki = A.k[i];
     if (tid == 0) *ncl = 0;
     __syncthreads();
@@ -833,7 +849,7 @@ constexpr int T2_WIDE_MAX = 148;  // tiers 2-3 with at most this many vertices: 
 // Tiers 2 and 3: block per vertex, the table (TS slots) in dynamic shared
 // memory; tier 2's small tables let 3x more vertices be in flight per SM.
 template <int TS, int MAXD, int NT>
-__global__ void __launch_bounds__(NT) k_decide_t2(DecideArgs A, const int32_t *list, int64_t cnt) {
+__global__ void __launch_bounds__(NT) k_decide_t2(DecideArgs A, TierRef L, int64_t cnt) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ CertSmem<NT> S;
     __shared__ int32_t cidx[NT * T2_FU];
@@ -855,12 +871,12 @@ __global__ void __launch_bounds__(NT) k_decide_t2(DecideArgs A, const int32_t *l
         cntt[s] = 0;
     }
     for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
-        const int64_t x = list[q];
-        const int32_t i = A.subset[x];
-        const int64_t deg = A.off[i + 1] - A.off[i];
+        const int64_t e0 = L.row[q], e1 = L.end[q];
+        const int64_t deg = e1 - e0;
         uint32_t ts = 64;
         while (ts < (uint64_t)(deg + deg / 2 + 2)) ts <<= 1;
-        block_decide<NT, 1, T2_FU>(A, x, PowTab{ts - 1}, keys, vals, cntt, clist, &ncl, S, my_cand);
+        block_decide<NT, 1, T2_FU>(A, L.x[q], L.vid[q], e0, e1, PowTab{ts - 1}, keys, vals, cntt,
+                                   clist, &ncl, S, my_cand);
     }
     if (A.cand && tid == 0 && my_cand) atomicAdd(A.cand, my_cand);
 }
@@ -1234,10 +1250,16 @@ __global__ void k_tier_keys(const int64_t *off, const int32_t *vtx, const int64_
 }
 
 __global__ void k_tier_local(const uint32_t *skey, const int32_t *sidx, const int64_t *stage_off,
-                             int64_t total, int32_t *local) {
+                             int64_t total, const int64_t *off, const int32_t *vtx, int32_t *local,
+                             int32_t *vid, int64_t *row, int64_t *end) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < total;
-         p += (int64_t)gridDim.x * blockDim.x)
+         p += (int64_t)gridDim.x * blockDim.x) {
         local[p] = (int32_t)(sidx[p] - stage_off[skey[p] / NTIER]);
+        const int32_t i = vtx[sidx[p]];
+        vid[p] = i;
+        row[p] = off[i];
+        end[p] = off[i + 1];
+    }
 }
 
 __global__ void k_hub_degrees(const int64_t *off, const int32_t *vtx, const int64_t *stage_off,
@@ -1259,11 +1281,13 @@ __global__ void k_fill_i32_d(int32_t *p, int64_t n, int32_t v) {
 }
 
 void Plan::release() {
-    void *ps[] = {tier_list, hub_eoff, hub_toff, hub_poff, hub_blk, hub_row, hub_vid, hkeys,
+    void *ps[] = {tier_list, tier_vid, tier_row, tier_end, hub_eoff, hub_toff, hub_poff, hub_blk, hub_row, hub_vid, hkeys,
                   hvals,     hcnt,     hsold,    hncnt,    hnear,   hpart};
     for (void *p : ps)
         if (p) cudaFree(p);
     tier_list = nullptr;
+    tier_vid = nullptr;
+    tier_row = tier_end = nullptr;
     hub_eoff = hub_toff = hub_poff = hub_blk = hub_row = nullptr;
     hub_vid = nullptr;
     hkeys = hcnt = hsold = hncnt = nullptr;
@@ -1294,7 +1318,12 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
     PLV_LAUNCH_CHECK();
     iota_i32(gidx, total, s);
     sort_pairs<uint32_t, int32_t>(key, skey, gidx, sidx, total, 0, bits_for(NTIER * nst + NTIER), s);
-    k_tier_local<<<grid_for(total, 256), 256, 0, s>>>(skey, sidx, d_soff, total, P.tier_list);
+    P.tier_vid = dalloc<int32_t>(total);
+    P.tier_row = dalloc<int64_t>(total);
+    P.tier_end = dalloc<int64_t>(total);
+    k_tier_local<<<grid_for(total, 256), 256, 0, s>>>(skey, sidx, d_soff, total, off, vtx,
+                                                      P.tier_list, P.tier_vid, P.tier_row,
+                                                      P.tier_end);
     PLV_LAUNCH_CHECK();
     std::vector<unsigned long long> h(NTIER * nst);
     PLV_CUDA(cudaMemcpyAsync(h.data(), hist.get(), sizeof(unsigned long long) * NTIER * nst,
@@ -1454,16 +1483,21 @@ void launch_decide_par(const Plan &P, int64_t a, DecideArgs A, cudaStream_t st,
     }
 }
 
+static TierRef tier_ref(const Plan &P, const StagePlan &sp, int t) {
+    const int64_t o = sp.tstart[t];
+    return TierRef{P.tier_list + o, P.tier_vid + o, P.tier_row + o, P.tier_end + o};
+}
+
 void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStream_t *ts) {
     const StagePlan &sp = P.st[a];
     if (sp.tcount[0]) {
-        k_decide_t0<<<grid_for(sp.tcount[0], 256), 256, 0, ts[0]>>>(A, P.tier_list + sp.tstart[0],
+        k_decide_t0<<<grid_for(sp.tcount[0], 256), 256, 0, ts[0]>>>(A, tier_ref(P, sp, 0),
                                                                     sp.tcount[0]);
         PLV_LAUNCH_CHECK();
     }
     if (sp.tcount[1]) {
         k_decide_t1<<<grid_for(sp.tcount[1], T1_WARPS), T1_WARPS * 32, 0, ts[1]>>>(
-            A, P.tier_list + sp.tstart[1], sp.tcount[1]);
+            A, tier_ref(P, sp, 1), sp.tcount[1]);
         PLV_LAUNCH_CHECK();
     }
     // few vertices (a late colour class): one wide block each, so a vertex's
@@ -1471,21 +1505,21 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
     if (sp.tcount[2] > T2_WIDE_MAX) {
         k_decide_t2<T2A_TS, T2A_MAXD, 128><<<grid_for(sp.tcount[2], 1, 1 << 30), 128,
                                              t2_smem(T2A_TS), ts[2]>>>(
-            A, P.tier_list + sp.tstart[2], sp.tcount[2]);
+            A, tier_ref(P, sp, 2), sp.tcount[2]);
         PLV_LAUNCH_CHECK();
     } else if (sp.tcount[2]) {
         k_decide_t2<T2A_TS, T2A_MAXD, 512><<<(unsigned)sp.tcount[2], 512, t2_smem(T2A_TS), ts[2]>>>(
-            A, P.tier_list + sp.tstart[2], sp.tcount[2]);
+            A, tier_ref(P, sp, 2), sp.tcount[2]);
         PLV_LAUNCH_CHECK();
     }
     if (sp.tcount[3] > T2_WIDE_MAX) {
         k_decide_t2<T2_TS, T2_MAXD, BLK><<<grid_for(sp.tcount[3], 1, 1 << 30), BLK,
                                            t2_smem(T2_TS), ts[3]>>>(
-            A, P.tier_list + sp.tstart[3], sp.tcount[3]);
+            A, tier_ref(P, sp, 3), sp.tcount[3]);
         PLV_LAUNCH_CHECK();
     } else if (sp.tcount[3]) {
         k_decide_t2<T2_TS, T2_MAXD, 1024><<<(unsigned)sp.tcount[3], 1024, t2_smem(T2_TS), ts[3]>>>(
-            A, P.tier_list + sp.tstart[3], sp.tcount[3]);
+            A, tier_ref(P, sp, 3), sp.tcount[3]);
         PLV_LAUNCH_CHECK();
     }
     cudaStream_t st = ts[4];

@@ -80,6 +80,9 @@ constexpr int MAXS = 32;  // overlapping candidates resolved exactly per vertex
 struct Plan {
     std::vector<StagePlan> st;
     int32_t *tier_list = nullptr;  // stage-local indices grouped by (stage, tier)
+    int32_t *tier_vid = nullptr;   // the vertex of each tier-list entry
+    int64_t *tier_row = nullptr;   // its row [row, end)
+    int64_t *tier_end = nullptr;
     int64_t *hub_eoff = nullptr;   // per stage: nh+1 entry offsets (from 0)
     int64_t *hub_toff = nullptr;   // per stage: nh+1 table offsets (from 0, pow2 sizes)
     int64_t *hub_poff = nullptr;   // per stage: nh+1 partial-best offsets (slices)
