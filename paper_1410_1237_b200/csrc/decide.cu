@@ -887,6 +887,7 @@ constexpr int HSB = 1024;           // threads per hub pass block
 constexpr int HSU = 2;              // table slots per thread in a pass block
 constexpr int HTSL = HSB * HSU;     // table slots per pass block
 constexpr int HCPAD = 32;           // per-hub counters one 128-byte line apart
+constexpr int HUB_DENSE_K = 16;     // stages with at most this many hubs use dense arrays
 
 // A candidate near its slice's best: community, gain, slack (rounded up).
 struct NearCand {
@@ -908,6 +909,12 @@ struct HubScratch {
     const int64_t *blk;  // pass blocks of the stage: (hub << 32) | slice
     const int64_t *poff; // [nh + 1] first partial of each hub
     int64_t nh;
+    // dense mode (few hubs): per-hub arrays indexed by community, no claims
+    double *dval;        // [HUB_DENSE_K * dn] any-order sums (0 idle)
+    int32_t *dcnt;       // [HUB_DENSE_K * dn] term counts (0 idle)
+    int32_t *dmk;        // [HUB_DENSE_K * dn] first row position per community (INT_MAX idle)
+    int32_t *cbuf;       // [entries] community of every hub entry (-1: self loop)
+    int64_t dn;
 };
 
 // Largest hub q with eoff[q] <= t.
@@ -926,6 +933,7 @@ __device__ __forceinline__ int64_t hub_of(const int64_t *eoff, int64_t nh, int64
 // Every entry of every hub of the stage: any-order sums into the hub's slice
 // of the global table (warp-aggregated per (hub, community)); the inserter of
 // c_old records its slot.
+template <bool DENSE>
 __global__ void k_hub_accum(DecideArgs A, const int64_t *eoff, const int64_t *toff, int64_t nh,
                             int64_t E, int32_t *hkeys, double *hvals, int32_t *hcnt, HubScratch H) {
     TR_BEGIN
@@ -950,10 +958,18 @@ __global__ void k_hub_accum(DecideArgs A, const int64_t *eoff, const int64_t *to
         }
         TR_MARK
         // group lanes by (hub, community)
+        if (DENSE && t < E) H.cbuf[t] = c;
         const uint64_t key = c >= 0 ? (((uint64_t)q << 32) | (uint32_t)c) : ~0ull;
         const unsigned grp = __match_any_sync(FULL, key);
         const double v = group_sum(grp, w);
-        if (c >= 0 && lane == __ffs(grp) - 1) {
+        if (DENSE && c >= 0 && lane == __ffs(grp) - 1) {
+            // dense: plain reductions into the hub's community arrays; the
+            // group leader holds the group's first row position
+            const int64_t d = q * H.dn + c;
+            atomicAdd(H.dval + d, v);
+            atomicAdd(H.dcnt + d, __popc(grp));
+            atomicMin(H.dmk + d, (int32_t)(t - eoff[q]));
+        } else if (c >= 0 && lane == __ffs(grp) - 1) {
             const int64_t base = toff[q];
             const uint32_t mask = (uint32_t)(toff[q + 1] - base - 1);
             bool fresh;
@@ -992,7 +1008,7 @@ __device__ __forceinline__ NearCand ldcg_near(const NearCand *p) {
     return NearCand{__ldcg(&p->c), __ldcg(&p->sl), __ldcg(&p->g)};
 }
 
-template <int NT>
+template <int NT, bool DENSE>
 __device__ void hub_decide_one(const DecideArgs &A, const int32_t *list, const int64_t *toff,
                                int32_t *hkeys, double *hvals, int32_t *hcnt, const HubScratch &H,
                                int64_t q, CertSmem<NT> &S) {
@@ -1012,9 +1028,10 @@ __device__ void hub_decide_one(const DecideArgs &A, const int32_t *list, const i
             consider(bw, o.g, o.l, o.c, o.e, o.n);
         }
         warp_best(bw);
-        const int32_t so = H.sold[q];
-        const double f_old = so >= 0 ? hvals[base + so] : 0.0;
-        const int32_t l_old = so >= 0 ? hcnt[base + so] : 0;
+        const int64_t dq = q * H.dn;
+        const int32_t so = DENSE ? 0 : H.sold[q];
+        const double f_old = DENSE ? H.dval[dq + c_old] : so >= 0 ? hvals[base + so] : 0.0;
+        const int32_t l_old = DENSE ? H.dcnt[dq + c_old] : so >= 0 ? hcnt[base + so] : 0;
         const int na = __ldcg(H.ncnt + q * HCPAD), nb = __ldcg(H.ncnt + q * HCPAD + 1);
         const bool stay_best = bw.c == c_old;
         const double slack_b =
@@ -1049,13 +1066,19 @@ __device__ void hub_decide_one(const DecideArgs &A, const int32_t *list, const i
             S.flag = flag;
             S.f_old = f_old;
             S.l_old = l_old;
-            // back to idle: c_old's slot, the counters
-            if (so >= 0) {
-                hkeys[base + so] = -1;
-                hvals[base + so] = 0.0;
-                hcnt[base + so] = 0;
+            // back to idle: c_old's slot / entries, the counters
+            if (DENSE) {
+                H.dval[dq + c_old] = 0.0;
+                H.dcnt[dq + c_old] = 0;
+                H.dmk[dq + c_old] = INT_MAX;
+            } else {
+                if (so >= 0) {
+                    hkeys[base + so] = -1;
+                    hvals[base + so] = 0.0;
+                    hcnt[base + so] = 0;
+                }
+                H.sold[q] = -1;
             }
-            H.sold[q] = -1;
             H.ncnt[q * HCPAD] = 0;
             H.ncnt[q * HCPAD + 1] = 0;
             H.ncnt[q * HCPAD + 2] = 0;  // the pass-item ticket
@@ -1125,6 +1148,7 @@ __device__ void hub_decide_one(const DecideArgs &A, const int32_t *list, const i
 // within slack_max of it -- a superset of the entries that can overlap the
 // hub's best -- listed for the decision.  Clears the slice (c_old's slot is
 // cleared by the decision, which reads it).
+template <bool DENSE>
 __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *list,
                                                  const int64_t *eoff, const int64_t *toff,
                                                  int32_t *hkeys, double *hvals, int32_t *hcnt,
@@ -1134,6 +1158,8 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *l
     __shared__ int32_t cidx[HSB];
     __shared__ double cw[HSB];
     __shared__ int s_last;
+    constexpr int PU = DENSE ? 1 : HSU;  // items per thread
+    constexpr int PTSL = HSB * PU;        // positions / slots per pass block
     const int tid = threadIdx.x;
     if (tid == 0) {
         S.cidx = cidx;
@@ -1145,70 +1171,104 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *l
     const int32_t c_old = A.assign[i];
     const int64_t base = toff[q];
     const int64_t cap = toff[q + 1] - base;
-    const int32_t so = H.sold[q];
-    const double f_old = so >= 0 ? hvals[base + so] : 0.0;
-    const int32_t l_old = so >= 0 ? hcnt[base + so] : 0;
+    const int64_t dq = q * H.dn, deg = eoff[q + 1] - eoff[q];
+    const int32_t so = DENSE ? 0 : H.sold[q];
+    const double f_old = DENSE ? H.dval[dq + c_old] : so >= 0 ? hvals[base + so] : 0.0;
+    const int32_t l_old = DENSE ? H.dcnt[dq + c_old] : so >= 0 ? hcnt[base + so] : 0;
     const double ki = A.k[i], a_old_excl = dsub(A.a_tot[c_old], ki);
     const double inv_m = 1.0 / A.m;
     TR_MARK
-    int32_t c[HSU];
-    double F[HSU], g[HSU];
-    int32_t L[HSU];
-    float sl[HSU];
-    const int64_t s0 = y * HTSL + tid;
+    int32_t c[PU];
+    double F[PU], g[PU];
+    int32_t L[PU];
+    float sl[PU];
+    const int64_t s0 = y * PTSL + tid;
+    double at[PU];
+    if (DENSE) {
+        // items are row positions; the first position of each community owns
+        // it (every load of a position is issued at once, owner or not)
+        int32_t cc[PU], mk[PU];
 #pragma unroll
-    for (int u = 0; u < HSU; u++) {
-        const int64_t s = s0 + u * HSB;
-        c[u] = s < cap ? hkeys[base + s] : -1;
-        F[u] = s < cap ? hvals[base + s] : 0.0;
-        L[u] = s < cap ? hcnt[base + s] : 0;
+        for (int u = 0; u < PU; u++) {
+            const int64_t t = s0 + u * HSB;
+            cc[u] = t < deg ? H.cbuf[eoff[q] + t] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < PU; u++) {
+            const bool ok = cc[u] >= 0;
+            mk[u] = ok ? H.dmk[dq + cc[u]] : -1;
+            F[u] = ok ? H.dval[dq + cc[u]] : 0.0;
+            L[u] = ok ? H.dcnt[dq + cc[u]] : 0;
+            at[u] = ok ? __ldg(A.a_tot + cc[u]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < PU; u++) c[u] = mk[u] == (int32_t)(s0 + u * HSB) ? cc[u] : -1;
+    } else {
+#pragma unroll
+        for (int u = 0; u < PU; u++) {
+            const int64_t s = s0 + u * HSB;
+            c[u] = s < cap ? hkeys[base + s] : -1;
+            F[u] = s < cap ? hvals[base + s] : 0.0;
+            L[u] = s < cap ? hcnt[base + s] : 0;
+        }
     }
     TR_MARK
     Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
     unsigned long long nc = 0;
-    double at[HSU];
 #pragma unroll
-    for (int u = 0; u < HSU; u++) {  // every gather in flight before any store
+    for (int u = 0; u < PU; u++) {  // every gather in flight before any store
         nc += c[u] >= 0;
         if (c[u] == c_old) c[u] = -1;  // not a candidate (its slot stays)
-        at[u] = c[u] >= 0 ? __ldg(A.a_tot + c[u]) : 0.0;
+        if (!DENSE) at[u] = c[u] >= 0 ? __ldg(A.a_tot + c[u]) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < HSU; u++) {
+    for (int u = 0; u < PU; u++) {
         if (c[u] < 0) continue;
         g[u] = gain_of(F[u], f_old, A.m, ki, a_old_excl, at[u], A.four_m_sq);
         sl[u] = __double2float_ru(gain_slack_r(F[u], L[u], f_old, l_old, inv_m, g[u]));
         consider(b, g[u], LBL(A.labels, c[u]), c[u], F[u], L[u]);
     }
 #pragma unroll
-    for (int u = 0; u < HSU; u++) {
+    for (int u = 0; u < PU; u++) {
         const int64_t s = s0 + u * HSB;
         if (c[u] < 0) continue;
-        hkeys[base + s] = -1;
-        hvals[base + s] = 0.0;
-        hcnt[base + s] = 0;
+        if (DENSE) {
+            H.dval[dq + c[u]] = 0.0;
+            H.dcnt[dq + c[u]] = 0;
+            H.dmk[dq + c[u]] = INT_MAX;
+        } else {
+            hkeys[base + s] = -1;
+            hvals[base + s] = 0.0;
+            hcnt[base + s] = 0;
+        }
     }
     TR_MARK
     b = block_best<HSB>(S.bs, b);
     TR_MARK
+    bool wrote = false;
     if (!A.integral) {
         const double thr = b.g - slack_max(ki, eoff[q + 1] - eoff[q], inv_m);
 #pragma unroll
-        for (int u = 0; u < HSU; u++) {
+        for (int u = 0; u < PU; u++) {
             if (c[u] < 0 || g[u] + (double)sl[u] < thr) continue;
             const int cat = sl[u] > 0.0f ? 0 : 1;
             const int k = atomicAdd(H.ncnt + q * HCPAD + cat, 1);
             if (k < MAXS) (cat ? H.nearB : H.nearA)[q * MAXS + k] = NearCand{c[u], sl[u], g[u]};
+            wrote = true;
         }
     }
-    const unsigned long long tot = cub::BlockReduce<unsigned long long, HSB>(S.red).Sum(nc);
+    if (A.cand) {  // candidate statistic: one atomic per warp
+        unsigned long long w = nc;
+        for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(FULL, w, o);
+        if ((tid & 31) == 0 && w) atomicAdd(A.cand, w);
+    }
     if (tid == 0) {
         H.part[H.poff[q] + y] = b;
-        if (A.cand && tot) atomicAdd(A.cand, tot);
+        wrote = true;
     }
-    // the block finishing the hub's last item decides it (every writer
-    // releases its partial / near-list stores, one ticket, acquire)
-    __threadfence();
+    // the block finishing the hub's last item decides it (the writers
+    // release their partial / near-list stores, one ticket, acquire)
+    if (wrote) __threadfence();
     __syncthreads();
     if (tid == 0) {
         const int nsl = (int)(H.poff[q + 1] - H.poff[q]);
@@ -1217,7 +1277,7 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *l
     }
     __syncthreads();
     TR_MARK
-    if (s_last) hub_decide_one<HSB>(A, list, toff, hkeys, hvals, hcnt, H, q, S);
+    if (s_last) hub_decide_one<HSB, DENSE>(A, list, toff, hkeys, hvals, hcnt, H, q, S);
     TR_END(2)
 }
 
@@ -1282,7 +1342,8 @@ __global__ void k_fill_i32_d(int32_t *p, int64_t n, int32_t v) {
 
 void Plan::release() {
     void *ps[] = {tier_list, tier_vid, tier_row, tier_end, hub_eoff, hub_toff, hub_poff, hub_blk, hub_row, hub_vid, hkeys,
-                  hvals,     hcnt,     hsold,    hncnt,    hnear,   hpart};
+                  hvals,     hcnt,     hsold,    hncnt,    hnear,   hpart,
+                  dval,      dcnt,     dmk,      cbuf};
     for (void *p : ps)
         if (p) cudaFree(p);
     tier_list = nullptr;
@@ -1294,11 +1355,12 @@ void Plan::release() {
     hvals = nullptr;
     hnear = nullptr;
     hpart = nullptr;
+    dval = nullptr;
+    dcnt = dmk = cbuf = nullptr;
 }
 
 void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *stage_off_h,
                 int64_t nst, int64_t n, cudaStream_t s) {
-    (void)n;
     int64_t total = stage_off_h[nst];
     P.st.assign(nst, StagePlan{});
     for (int64_t a = 0; a < nst; a++) {
@@ -1364,6 +1426,8 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
     PLV_CUDA(cudaStreamSynchronize(s));
     std::vector<int64_t> eoff, toff, poff, blk, hrow;
     std::vector<int32_t> hvid;
+    // dense hub arrays cost 16 B x HUB_DENSE_K x n; keep them under 4 GB
+    const bool dense_ok = n > 0 && (double)n * HUB_DENSE_K * 16.0 <= 4e9;
     int64_t h0 = 0, max_parts = 1;
     for (int64_t a = 0; a < nst; a++) {
         StagePlan &sp = P.st[a];
@@ -1373,11 +1437,14 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
         eoff.push_back(0);
         toff.push_back(0);
         poff.push_back(0);
+        // few hubs: dense per-hub community arrays (no claims), items are row
+        // positions; else hash tables, items are table slices
+        sp.hub_dense = sp.tcount[4] > 0 && sp.tcount[4] <= HUB_DENSE_K && dense_ok;
         for (int64_t z = 0; z < sp.tcount[4]; z++) {
             int64_t d = deg[h0 + z];
             int64_t cap = 64;
             while (cap < 2 * d + 2) cap <<= 1;
-            int64_t sl = (cap + HTSL - 1) / HTSL;  // table slices
+            int64_t sl = sp.hub_dense ? (d + HSB - 1) / HSB : (cap + HTSL - 1) / HTSL;
             for (int64_t y = 0; y < sl; y++) blk.push_back((z << 32) | y);
             acc += d;
             tacc += cap;
@@ -1395,6 +1462,7 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
         sp.hub_nblk = pacc;
         max_parts = pacc > max_parts ? pacc : max_parts;
         P.max_hub_entries = acc > P.max_hub_entries ? acc : P.max_hub_entries;
+        if (sp.hub_dense) P.max_dense_entries = acc > P.max_dense_entries ? acc : P.max_dense_entries;
         P.max_hubs = sp.tcount[4] > P.max_hubs ? sp.tcount[4] : P.max_hubs;
         P.max_table = tacc > P.max_table ? tacc : P.max_table;
     }
@@ -1431,6 +1499,18 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
     P.hncnt = dalloc<int32_t>(HCPAD * H);
     PLV_CUDA(cudaMemsetAsync(P.hncnt, 0, sizeof(int32_t) * HCPAD * H, s));
     P.hnear = dalloc<NearCand>(2 * H * MAXS);
+    if (P.max_dense_entries) {
+        P.dn = n;
+        const int64_t D = (int64_t)HUB_DENSE_K * n;
+        P.dval = dalloc<double>(D);
+        P.dcnt = dalloc<int32_t>(D);
+        P.dmk = dalloc<int32_t>(D);
+        P.cbuf = dalloc<int32_t>(P.max_dense_entries);
+        PLV_CUDA(cudaMemsetAsync(P.dval, 0, sizeof(double) * D, s));
+        PLV_CUDA(cudaMemsetAsync(P.dcnt, 0, sizeof(int32_t) * D, s));
+        k_fill_i32_d<<<grid_for(D, 256), 256, 0, s>>>(P.dmk, D, INT_MAX);
+        PLV_LAUNCH_CHECK();
+    }
     P.hpart = dalloc<Best>(max_parts);
     PLV_CUDA(cudaStreamSynchronize(s));
 }
@@ -1529,17 +1609,35 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
         const int64_t *toff = P.hub_toff + sp.hub_base;
         int64_t nh = sp.tcount[4], E = sp.hub_entries;
         const int64_t Hm = P.max_hubs;
-        HubScratch H{P.hub_row + sp.hub_base, P.hub_vid + sp.hub_base,
-                     P.hsold,  P.hncnt,
-                     (NearCand *)P.hnear, (NearCand *)P.hnear + Hm * MAXS,
-                     P.hpart,  P.hub_blk + sp.hub_blk_base,    P.hub_poff + sp.hub_base,
-                     nh};
-        k_hub_accum<<<grid_for(E, 256), 256, 0, st>>>(A, eoff, toff, nh, E, P.hkeys, P.hvals,
-                                                      P.hcnt, H);
-        PLV_LAUNCH_CHECK();
+        HubScratch H{P.hub_row + sp.hub_base,
+                     P.hub_vid + sp.hub_base,
+                     P.hsold,
+                     P.hncnt,
+                     (NearCand *)P.hnear,
+                     (NearCand *)P.hnear + Hm * MAXS,
+                     P.hpart,
+                     P.hub_blk + sp.hub_blk_base,
+                     P.hub_poff + sp.hub_base,
+                     nh,
+                     P.dval,
+                     P.dcnt,
+                     P.dmk,
+                     P.cbuf,
+                     P.dn};
         unsigned g2 = (unsigned)sp.hub_nblk;
-        k_hub_pass<<<g2, HSB, 0, st>>>(A, list, eoff, toff, P.hkeys, P.hvals, P.hcnt, H);
-        PLV_LAUNCH_CHECK();
+        if (sp.hub_dense) {
+            k_hub_accum<true><<<grid_for(E, 256), 256, 0, st>>>(A, eoff, toff, nh, E, P.hkeys,
+                                                                P.hvals, P.hcnt, H);
+            PLV_LAUNCH_CHECK();
+            k_hub_pass<true><<<g2, HSB, 0, st>>>(A, list, eoff, toff, P.hkeys, P.hvals, P.hcnt, H);
+            PLV_LAUNCH_CHECK();
+        } else {
+            k_hub_accum<false><<<grid_for(E, 256), 256, 0, st>>>(A, eoff, toff, nh, E, P.hkeys,
+                                                                 P.hvals, P.hcnt, H);
+            PLV_LAUNCH_CHECK();
+            k_hub_pass<false><<<g2, HSB, 0, st>>>(A, list, eoff, toff, P.hkeys, P.hvals, P.hcnt, H);
+            PLV_LAUNCH_CHECK();
+        }
     }
 }
 

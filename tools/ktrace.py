@@ -55,7 +55,7 @@ for k, nm in names.items():
         continue
     t = r[m, 1:7]
     ns = r[m, 7]
-    nmk = int(ns.max())
+    nmk = min(int(ns.max()), 6)
     segs = [np.mean(t[:, i + 1] - t[:, i]) / 1e3 for i in range(min(nmk, 6) - 1)]
     print(f"{nm:11s} blocks {m.sum():6d}  mean per-block segments (us): " +
           " / ".join(f"{x:.2f}" for x in segs) +
