@@ -883,11 +883,12 @@ __global__ void __launch_bounds__(NT) k_decide_t2(DecideArgs A, TierRef L, int64
 
 // ------------------------------------------------------------ tier 4 (hubs)
 
-constexpr int HSB = 1024;           // threads per hub pass block
+constexpr int HSB = 512;            // threads per hub pass block
 constexpr int HSU = 2;              // table slots per thread in a pass block
 constexpr int HTSL = HSB * HSU;     // table slots per pass block
 constexpr int HCPAD = 32;           // per-hub counters one 128-byte line apart
 constexpr int HUB_DENSE_K = 16;     // stages with at most this many hubs use dense arrays
+constexpr int HFU = 4;              // row entries per thread per exact-fold chunk (hubs)
 
 // A candidate near its slice's best: community, gain, slack (rounded up).
 struct NearCand {
@@ -1121,7 +1122,7 @@ __device__ void hub_decide_one(const DecideArgs &A, const int32_t *list, const i
             S.nn = nn;
         }
         __syncthreads();
-        exact_folds<NT, 1>(A, i, S);
+        exact_folds<NT, HFU>(A, i, S);
         if (tid == 0) {
             double a_old_excl = dsub(A.a_tot[c_old], ki);
             Best e{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
@@ -1155,8 +1156,8 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *l
                                                  HubScratch H) {
     TR_BEGIN
     __shared__ CertSmem<HSB> S;
-    __shared__ int32_t cidx[HSB];
-    __shared__ double cw[HSB];
+    __shared__ int32_t cidx[HSB * HFU];
+    __shared__ double cw[HSB * HFU];
     __shared__ int s_last;
     constexpr int PU = DENSE ? 1 : HSU;  // items per thread
     constexpr int PTSL = HSB * PU;        // positions / slots per pass block
