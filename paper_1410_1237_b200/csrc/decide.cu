@@ -805,7 +805,7 @@ template <int NT, int U, int FU, class Tab, class CL>
 __device__ __forceinline__ void block_decide(const DecideArgs &A, int64_t x, int32_t i, int64_t e0,
                                              int64_t e1, Tab T, int32_t *keys, double *vals,
                                              int32_t *cntt, CL *clist, int *ncl, CertSmem<NT> &S,
-                                             unsigned long long &my_cand) {
+                                             unsigned long long &my_cand, Trace *trp = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31;
     const int32_t c_old = A.assign[i];
     const double ki = A.k[i];
@@ -827,11 +827,18 @@ __device__ __forceinline__ void block_decide(const DecideArgs &A, int64_t x, int
             c[u] = ok ? A.assign[j[u]] : -1;
             w[u] = ok ? A.wts[e] : 0.0;
         }
+        if (trp && b0 == e0) {
+            volatile int32_t sink = c[0];  // wait for the loads
+            (void)sink;
+            trp->mark();
+        }
 #pragma unroll
         for (int u = 0; u < U; u++) accum_entry(keys, vals, cntt, T, c[u], w[u], lane, clist, ncl);
     }
     __syncthreads();
+    if (trp) trp->mark();
     Best b = certify_table<NT>(A, c_old, ki, keys, vals, cntt, T, clist, *ncl, S, true);
+    if (trp) trp->mark();
     my_cand += tid == 0 ? S.ncand : 0;
     if (A.integral) {
         // exact in any order: the plain argmax is the reference's
@@ -870,15 +877,17 @@ __global__ void __launch_bounds__(NT) k_decide_t2(DecideArgs A, TierRef L, int64
         vals[s] = 0.0;
         cntt[s] = 0;
     }
+    TR_BEGIN
     for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
         const int64_t e0 = L.row[q], e1 = L.end[q];
         const int64_t deg = e1 - e0;
         uint32_t ts = 64;
         while (ts < (uint64_t)(deg + deg / 2 + 2)) ts <<= 1;
         block_decide<NT, 1, T2_FU>(A, L.x[q], L.vid[q], e0, e1, PowTab{ts - 1}, keys, vals, cntt,
-                                   clist, &ncl, S, my_cand);
+                                   clist, &ncl, S, my_cand, tr_on && tr.n < 2 ? &tr : nullptr);
     }
     if (A.cand && tid == 0 && my_cand) atomicAdd(A.cand, my_cand);
+    TR_END(NT == 1024 ? 5 : NT == 512 ? 6 : 7)
 }
 
 // ------------------------------------------------------------ tier 4 (hubs)

@@ -47,7 +47,7 @@ cl.plv_debug_trace_read(buf.ctypes.data, 1 << 18, ctypes.byref(n))
 cl.plv_debug_trace(0)
 r = buf[: 8 * n.value].reshape(-1, 8).astype(np.int64)
 kid = r[:, 0] >> 32
-names = {1: "hub_accum", 2: "hub_pass"}
+names = {1: "hub_accum", 2: "hub_pass", 5: "t2b_wide", 6: "t2a_wide", 7: "t2_narrow"}
 print(f"records {len(r)}")
 for k, nm in names.items():
     m = kid == k
