@@ -17,3 +17,8 @@ done
 timeout 900 ncu --profile-from-start off -k regex:k_decide_t2 -c 1 --set full --import-source on \
   --clock-control none -f -o gpurun_out/t2_full python tools/profile_iter.py --mode uncolored \
   > gpurun_out/t2_full.log 2>&1
+timeout 900 ncu --profile-from-start off -k regex:k_hub_pass -s 100 -c 1 --set full --import-source on \
+  --clock-control none -f -o gpurun_out/hubpass_full python tools/profile_iter.py --mode colored \
+  > gpurun_out/hubpass_full.log 2>&1
+timeout 600 python tools/timeline.py --dump gpurun_out/tl_c.tsv > gpurun_out/tl_c.txt 2>&1
+timeout 600 python tools/timeline.py --mode uncolored --dump gpurun_out/tl_u.tsv > gpurun_out/tl_u.txt 2>&1
