@@ -277,6 +277,30 @@ def test_hub_tiers_match_oracle(orc, cutoff):
     assert h.final_modularity == oh.final_modularity
 
 
+@pytest.mark.parametrize("cutoff", [0, 100_000])
+def test_many_hubs_hash_tier_matches_oracle(orc, cutoff):
+    """Two dozen hubs in one stage (uncoloured, and colour 0 since no two hubs
+    are adjacent): more hubs than the dense per-hub arrays take (16), so the
+    hash-table hub path runs (the dense path is covered by the tests above)."""
+    rng = np.random.default_rng(11)
+    n = 40000
+    u = [rng.integers(0, n, 120000)]
+    v = [rng.integers(0, n, 120000)]
+    for h in range(24):
+        d = int(rng.integers(2100, 9000))
+        u.append(np.full(d, h))
+        v.append(rng.choice(np.arange(100, n), d, replace=False))
+    u, v = np.concatenate(u), np.concatenate(v)
+    w = rng.uniform(1.0, 10.0, len(u))
+    og = orc.from_edges(u, v, w, num_vertices=n)
+    g = pl.Graph.from_edges(u, v, w, num_vertices=n)
+    assert (np.diff(g.adjacency_offsets) > 2048).sum() >= 24
+    oh = orc.run(og, color_cutoff=cutoff, max_iterations=30)
+    h = pl.run(g, pl.RunConfig(color_cutoff=cutoff, max_iterations_per_phase=30))
+    assert np.array_equal(h.final_assignment, oh.final_assignment)
+    assert h.final_modularity == oh.final_modularity
+
+
 def test_distributed_iteration_single_rank_cuda(orc):
     """The multi-GPU driver with the CUDA callbacks (world 1) equals the
     phase engine's coloured iteration and the oracle."""
