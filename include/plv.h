@@ -226,6 +226,17 @@ int plv_gen_grid(uint64_t seed, int64_t side, double keep, int64_t pendants, dou
 int plv_gen_chung_lu(uint64_t seed, const double *cdf, int64_t n, int64_t records, int32_t *u,
                      int32_t *v, double *w, int64_t cap, int64_t *count_h, void *stream);
 
+/* ------------------------------------------------------------ diagnostics */
+
+/* Per-block timeline of the decide kernels (tools/ktrace.py): plv_debug_trace(1)
+ * starts recording globaltimer stamps (thread 0 of each block) and clears the
+ * buffer, plv_debug_trace(0) stops (and clears); plv_debug_trace_read copies up
+ * to max_records records of 8 u64 [kernel id << 32 | block, stamps t0..t5,
+ * number of stamps] and returns their count in n_h.  No reference counterpart
+ * (profiling aid). */
+int plv_debug_trace(int on);
+int plv_debug_trace_read(unsigned long long *out_h, int64_t max_records, int64_t *n_h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -40,6 +40,8 @@ _SIGS = {
     "plv_last_error": [],
     "plv_device_ok": [],
     "plv_launch_count": [],
+    "plv_debug_trace": [ctypes.c_int],
+    "plv_debug_trace_read": [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p],
     "plv_sum": [_P, _I64, _P, _P],
     "plv_modularity": [_P, _P, _I64, _D, _P, _P],
     "plv_csr_build": [_P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P],
