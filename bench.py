@@ -436,7 +436,7 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (CSR %.0f MB)" % (nnz * 12 / 1e6)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic(args.mode, scale),
-                         "traffic_unit": "bytes per iteration (ncu, cold caches)",
+                         "traffic_unit": "bytes per iteration (ncu, warm caches)",
                          "peak_kind": peak_kind,
                          "kernel": "decide (tiers 0-4)",
                          "bytes_per_iter": decide_bytes, "ms_per_iter": decide_ms},
