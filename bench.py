@@ -57,7 +57,10 @@ def _args():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--scale", type=int, default=CONFIG["scale"])
+    p.add_argument("--scale", type=int, default=CONFIG["scale"], help="R-MAT scale (c2 config)")
+    p.add_argument("--config", default="c2_rmat20",
+                   choices=["c1_sbm", "c2_rmat20", "c3_grid", "c4_chung_lu"],
+                   help="BASELINE config to run (default: config 2, the headline)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-louvain", action="store_true", help="skip the full run() timing")
     p.add_argument("--mode", choices=["colored", "uncolored"], default="colored")
@@ -137,10 +140,10 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def _traffic(mode: str, scale: int):
+def _traffic(mode: str, scale: int, config: str = "c2_rmat20"):
     """DRAM bytes per iteration of the decide kernels, from the committed ncu
     capture (profiles/r01_traffic.json; C2 only), else None."""
-    if scale != CONFIG["scale"]:
+    if scale != CONFIG["scale"] or config != "c2_rmat20":
         return None
     try:
         with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
@@ -217,14 +220,24 @@ def _csr_to_records(off, nbr, wts, selfw):
     return src[keep], nbr[keep].astype(np.int64), wts[keep]
 
 
-def host_phase1_inputs(scale: int):
+def _config_desc(args):
+    return f"c2_rmat{args.scale}" if args.config == "c2_rmat20" else args.config
+
+
+def host_phase1_inputs(scale: int, config: str = "c2_rmat20"):
     """numpy generator + CPU oracle (pinned to the reference) -> the VF'd
     phase-1 graph and its colour classes, without touching the GPU."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as orc
     from paper_1410_1237_b200 import synthetic as syn
-    u, v, w = syn.rmat_records(scale, CONFIG["edge_factor"], seed=CONFIG["seed"])
-    g = orc.from_edges(u, v, w, num_vertices=1 << scale)
+    if config == "c2_rmat20":
+        u, v, w = syn.rmat_records(scale, CONFIG["edge_factor"], seed=CONFIG["seed"])
+        n = 1 << scale
+    else:
+        host, _, params = syn.CONFIGS[config]
+        u, v, w = host(seed=CONFIG["seed"], **params)
+        n = syn.config_num_vertices(config)
+    g = orc.from_edges(u, v, w, num_vertices=n)
     vf = orc.vf_compact(g)
     col = orc.color_graph(vf.graph)
     gg = vf.graph
@@ -236,7 +249,7 @@ def run_reference(args):
     if rank != 0:
         return
     scale = args.scale
-    gg, classes, ncol = host_phase1_inputs(scale)
+    gg, classes, ncol = host_phase1_inputs(scale, args.config)
     if args.mode == "uncolored":
         classes = [np.arange(gg.num_vertices, dtype=np.int64)]
     times, kind, cores, M = cpu_iteration_rate(gg.adjacency_offsets, gg.neighbors, gg.weights,
@@ -245,13 +258,13 @@ def run_reference(args):
     t = float(np.mean(times))
     val = M / t
     sample = (f"{len(times)} phase-1 {'coloured (' + str(ncol) + ' stages)' if args.mode == 'colored' else 'uncoloured'} "
-              f"local-move iterations of R-MAT s{scale} after VF, singleton start")
+              f"local-move iterations of {_config_desc(args)} after VF, singleton start")
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (counter-based R-MAT, numpy generator)",
-        "config": {"workload": f"c2_rmat{scale} phase-1 {args.mode} local-move iteration",
+        "config": {"workload": f"{_config_desc(args)} phase-1 {args.mode} local-move iteration",
                    "graph": {"n": gg.num_vertices, "M": M, "nnz": int(len(gg.neighbors))}},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": sample},
@@ -277,9 +290,12 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     scale = args.scale
     # ---- setup (untimed): generate, build, VF, colour -- all on device
-    u, v, w, n0 = syn.rmat_device(scale, CONFIG["edge_factor"], seed=CONFIG["seed"])
-    g0 = pl.Graph.from_device_records(u, v, w, n0)
-    del u, v, w
+    if args.config == "c2_rmat20":
+        u, v, w, n0 = syn.rmat_device(scale, CONFIG["edge_factor"], seed=CONFIG["seed"])
+        g0 = pl.Graph.from_device_records(u, v, w, n0)
+        del u, v, w
+    else:
+        g0 = syn.config_graph(args.config, seed=CONFIG["seed"])
     vf = pl.vf_compact(g0)
     g = vf.graph
     n = g.num_vertices
@@ -398,9 +414,12 @@ def run_ours(args):
     if not args.no_louvain:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        uu, vv, ww, nn = syn.rmat_device(scale, CONFIG["edge_factor"], seed=CONFIG["seed"])
-        gg = pl.Graph.from_device_records(uu, vv, ww, nn)
-        h = pl.run(gg, pl.RunConfig())
+        if args.config == "c2_rmat20":
+            uu, vv, ww, nn = syn.rmat_device(scale, CONFIG["edge_factor"], seed=CONFIG["seed"])
+            gg = pl.Graph.from_device_records(uu, vv, ww, nn)
+        else:
+            gg = syn.config_graph(args.config, seed=CONFIG["seed"])
+        h = pl.run(gg, pl.RunConfig(color_cutoff=0 if args.config == "c1_sbm" else 100_000))
         torch.cuda.synchronize()
         louv = {"seconds": time.perf_counter() - t0, "final_modularity": h.final_modularity,
                 "phases": len(h.phases), "communities": h.num_communities,
@@ -428,14 +447,14 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (counter-based R-MAT, generated on device)",
-            "config": {"workload": f"c2_rmat{scale} phase-1 {args.mode} local-move iteration",
+            "data": "synthetic (counter-based generator of the BASELINE config, on device)",
+            "config": {"workload": f"{_config_desc(args)} phase-1 {args.mode} local-move iteration",
                        "graph": {"n": n, "M": M, "nnz": nnz, "colours": ncol,
                                  "integral": g.integral},
                        "parallelism": "replicas" if ws > 1 else "single",
                        "l2": "inputs larger than L2 (CSR %.0f MB)" % (nnz * 12 / 1e6)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": _traffic(args.mode, scale),
+                         "frac": achieved / peak, "traffic": _traffic(args.mode, scale, args.config),
                          "traffic_unit": "bytes per iteration (ncu, warm caches)",
                          "peak_kind": peak_kind,
                          "kernel": "decide (tiers 0-4)",
