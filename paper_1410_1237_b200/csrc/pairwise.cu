@@ -20,6 +20,68 @@ __global__ void k_pw_nodes(const double *__restrict__ a, int64_t n, int d0, doub
     }
 }
 
+// The same node values with a warp per node: a node of <= 256 elements is a
+// leaf, two leaves, or a leaf plus a split right half (two leaves); each leaf
+// goes to an octet of lanes, lane k of the octet owning accumulator r_k
+// (elements k, k+8, ... below the multiple of 8), the accumulators combined
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by xor-shuffles -- numpy's operation
+// order -- then the tail added by the octet's first lane.
+template <class F>
+__device__ __forceinline__ double pw_leaf_octet(const double *a, int64_t n, F f, int k) {
+    double r = 0.0;
+    const int64_t lim = n >= 8 ? n - (n % 8) : 0;
+    if (lim) {
+        r = f(a[k]);
+        for (int64_t i = 8 + k; i < lim; i += 8) r = __dadd_rn(r, f(a[i]));
+    }
+    double t = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+    t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 2));
+    t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 4));
+    if (k == 0) {
+        double res = lim ? t : 0.0;
+        for (int64_t i = lim; i < n; i++) res = __dadd_rn(res, f(a[i]));
+        t = res;
+    }
+    return t;  // valid in the octet's first lane
+}
+
+template <class F>
+__global__ void k_pw_nodes_warp(const double *__restrict__ a, int64_t n, int d0, double *vals,
+                                F f) {
+    const int lane = threadIdx.x & 31, oct = lane >> 3, k = lane & 7;
+    const uint64_t cnt = 1ull << d0;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < cnt; t += nw) {
+        int64_t lo, len;
+        pw_node(n, d0, t, &lo, &len);
+        // the node's leaves: [len] or [L, R] or [L, [RL, RR]]
+        int64_t off[3] = {0, 0, 0}, ln[3] = {len, 0, 0};
+        int nleaf = 1;
+        if (len > 128) {
+            const int64_t n2 = pw_split(len);
+            ln[0] = n2;
+            off[1] = n2;
+            ln[1] = len - n2;
+            nleaf = 2;
+            if (ln[1] > 128) {
+                const int64_t m2 = pw_split(ln[1]);
+                off[2] = off[1] + m2;
+                ln[2] = ln[1] - m2;
+                ln[1] = m2;
+                nleaf = 3;
+            }
+        }
+        const int o = oct < 3 ? oct : 2;
+        const int64_t my_len = oct < nleaf ? ln[o] : 0;
+        const double v = pw_leaf_octet(a + lo + off[o], my_len, f, k);
+        const double vL = __shfl_sync(0xffffffffu, v, 0);
+        const double vR = __shfl_sync(0xffffffffu, v, 8);
+        const double vRR = __shfl_sync(0xffffffffu, v, 16);
+        if (lane == 0)
+            vals[t] = nleaf == 1 ? vL : nleaf == 2 ? __dadd_rn(vL, vR) : __dadd_rn(vL, __dadd_rn(vR, vRR));
+    }
+}
+
 // Reduce groups of 2^kb consecutive values (a perfect subtree each) to one
 // (ping-pong in shared memory). When `final` the single remaining value is
 // written as 0.0 + root.
@@ -66,7 +128,7 @@ static void pw_launch(const double *a, int64_t n, double *out_dev, cudaStream_t 
         scratch = own.get();
     }
     double *v0 = scratch, *v1 = scratch + cnt;
-    k_pw_nodes<<<grid_for(cnt, 256, 148 * 32), 256, 0, s>>>(a, n, d0, v0, f);
+    k_pw_nodes_warp<<<grid_for(cnt * 32, 256, 148 * 32), 256, 0, s>>>(a, n, d0, v0, f);
     PLV_LAUNCH_CHECK();
     // reduce the perfect top tree, 2^10 values per block per pass
     double *src = v0, *dst = v1;
