@@ -2,23 +2,12 @@
 //
 // Whole-array sum: the tree of n is cut at the first depth d0 where every
 // node has <= 256 elements.  Above d0 the tree is a perfect binary tree (no
-// node there is a leaf), so after one thread per depth-d0 node has computed
-// its subtree serially (<= 2 leaves), the remaining levels are an aligned
-// perfect pairwise reduction: value(level, p) = value(p0) + value(p1).
+// node there is a leaf), so after one warp per depth-d0 node has computed its
+// subtree (<= 3 leaves, an octet of lanes each), the remaining levels are an
+// aligned perfect pairwise reduction: value(level, p) = value(p0) + value(p1).
 #include "pairwise.cuh"
 
 namespace plv {
-
-template <class F>
-__global__ void k_pw_nodes(const double *__restrict__ a, int64_t n, int d0, double *vals, F f) {
-    uint64_t cnt = 1ull << d0;
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < cnt;
-         t += (uint64_t)gridDim.x * blockDim.x) {
-        int64_t lo, len;
-        pw_node(n, d0, t, &lo, &len);
-        vals[t] = pw_serial(a + lo, len, f);
-    }
-}
 
 // The same node values with a warp per node: a node of <= 256 elements is a
 // leaf, two leaves, or a leaf plus a split right half (two leaves); each leaf
