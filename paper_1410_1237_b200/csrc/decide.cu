@@ -896,7 +896,7 @@ constexpr int HSB = 512;            // threads per hub pass block
 constexpr int HSU = 2;              // table slots per thread in a pass block
 constexpr int HTSL = HSB * HSU;     // table slots per pass block
 constexpr int HCPAD = 32;           // per-hub counters one 128-byte line apart
-constexpr int HUB_DENSE_K = 16;     // stages with at most this many hubs use dense arrays
+constexpr int HUB_DENSE_KMAX = 64;  // stages with at most this many hubs may use dense arrays
 constexpr int HFU = 4;              // row entries per thread per exact-fold chunk (hubs)
 
 // A candidate near its slice's best: community, gain, slack (rounded up).
@@ -920,9 +920,9 @@ struct HubScratch {
     const int64_t *poff; // [nh + 1] first partial of each hub
     int64_t nh;
     // dense mode (few hubs): per-hub arrays indexed by community, no claims
-    double *dval;        // [HUB_DENSE_K * dn] any-order sums (0 idle)
-    int32_t *dcnt;       // [HUB_DENSE_K * dn] term counts (0 idle)
-    int32_t *dmk;        // [HUB_DENSE_K * dn] first row position per community (INT_MAX idle)
+    double *dval;        // [dense_k * dn] any-order sums (0 idle)
+    int32_t *dcnt;       // [dense_k * dn] term counts (0 idle)
+    int32_t *dmk;        // [dense_k * dn] first row position per community (INT_MAX idle)
     int32_t *cbuf;       // [entries] community of every hub entry (-1: self loop)
     int64_t dn;
 };
@@ -1401,19 +1401,32 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
     PLV_CUDA(cudaMemcpyAsync(h.data(), hist.get(), sizeof(unsigned long long) * NTIER * nst,
                              cudaMemcpyDeviceToHost, s));
     PLV_CUDA(cudaStreamSynchronize(s));
+    // dense hub arrays: as many per-stage slots as 4 GB allows, at most HUB_DENSE_KMAX
+    P.dense_k = n > 0 ? (int64_t)(4e9 / (16.0 * (double)n)) : 0;
+    if (P.dense_k > HUB_DENSE_KMAX) P.dense_k = HUB_DENSE_KMAX;
     int64_t pos = 0;
     std::vector<int64_t> hub_pos, hub_stage;
-    for (int64_t a = 0; a < nst; a++)
+    for (int64_t a = 0; a < nst; a++) {
+        StagePlan &sp = P.st[a];
         for (int t = 0; t < NTIER; t++) {
-            P.st[a].tstart[t] = pos;
-            P.st[a].tcount[t] = (int64_t)h[NTIER * a + t];
-            if (t == 4)
-                for (int64_t z = 0; z < P.st[a].tcount[4]; z++) {
-                    hub_pos.push_back(pos + z);
-                    hub_stage.push_back(a);
-                }
-            pos += (int64_t)h[NTIER * a + t];
+            sp.tstart[t] = pos;
+            sp.tcount[t] = (int64_t)h[NTIER * a + t];
+            pos += sp.tcount[t];
         }
+        // a small colour class with hubs: its block-tier vertices join the
+        // hub tier (their lists directly precede it) -- one vertex per block
+        // is a long serial chain, the hub tier spreads every row over the GPU
+        const int64_t nb = sp.tcount[2] + sp.tcount[3];
+        if (sp.tcount[4] && nb && nb + sp.tcount[4] <= P.dense_k) {
+            sp.tstart[4] = sp.tstart[2];
+            sp.tcount[4] += nb;
+            sp.tcount[2] = sp.tcount[3] = 0;
+        }
+        for (int64_t z = 0; z < sp.tcount[4]; z++) {
+            hub_pos.push_back(sp.tstart[4] + z);
+            hub_stage.push_back(a);
+        }
+    }
     int64_t nh = (int64_t)hub_pos.size();
     if (nh == 0) return;
     Buf<int64_t> d_hpos(nh, s), d_hst(nh, s), d_deg(nh, s), d_row(nh, s);
@@ -1436,8 +1449,6 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
     PLV_CUDA(cudaStreamSynchronize(s));
     std::vector<int64_t> eoff, toff, poff, blk, hrow;
     std::vector<int32_t> hvid;
-    // dense hub arrays cost 16 B x HUB_DENSE_K x n; keep them under 4 GB
-    const bool dense_ok = n > 0 && (double)n * HUB_DENSE_K * 16.0 <= 4e9;
     int64_t h0 = 0, max_parts = 1;
     for (int64_t a = 0; a < nst; a++) {
         StagePlan &sp = P.st[a];
@@ -1449,7 +1460,7 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
         poff.push_back(0);
         // few hubs: dense per-hub community arrays (no claims), items are row
         // positions; else hash tables, items are table slices
-        sp.hub_dense = sp.tcount[4] > 0 && sp.tcount[4] <= HUB_DENSE_K && dense_ok;
+        sp.hub_dense = sp.tcount[4] > 0 && sp.tcount[4] <= P.dense_k;
         for (int64_t z = 0; z < sp.tcount[4]; z++) {
             int64_t d = deg[h0 + z];
             int64_t cap = 64;
@@ -1511,7 +1522,7 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
     P.hnear = dalloc<NearCand>(2 * H * MAXS);
     if (P.max_dense_entries) {
         P.dn = n;
-        const int64_t D = (int64_t)HUB_DENSE_K * n;
+        const int64_t D = P.dense_k * n;
         P.dval = dalloc<double>(D);
         P.dcnt = dalloc<int32_t>(D);
         P.dmk = dalloc<int32_t>(D);

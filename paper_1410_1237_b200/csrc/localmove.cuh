@@ -98,10 +98,10 @@ struct Plan {
     int32_t *hncnt = nullptr;   // per hub: near-candidate counters (0 idle)
     void *hnear = nullptr;      // per hub: 2 * MAXS near candidates
     Best *hpart = nullptr;      // pass partial bests
-    double *dval = nullptr;     // dense hub arrays [HUB_DENSE_K * n] (idle: 0 / 0 / INT_MAX)
+    double *dval = nullptr;     // dense hub arrays [dense_k * n] (idle: 0 / 0 / INT_MAX)
     int32_t *dcnt = nullptr, *dmk = nullptr;
     int32_t *cbuf = nullptr;    // communities of a dense stage's hub entries
-    int64_t dn = 0, max_dense_entries = 0;
+    int64_t dn = 0, max_dense_entries = 0, dense_k = 0;
     int64_t max_slices = 1;
     void release();
 };
