@@ -180,6 +180,42 @@ int plv_phase_iterate(void *handle, double *q_h, int64_t *moves_h, int64_t *cand
  * (capacity max_iters); result_h = {iterations, total_moves, hit_cap}. */
 int plv_phase_run(void *handle, double theta, int64_t max_iters, double *q_trace_h,
                   int64_t *moves_trace_h, double *ms_trace_h, int64_t *result_h, void *stream);
+/*
+ * Partitioned phase (multi-GPU; the reference has no distributed mode -- new
+ * design of SURVEY.md 8e, no reference interface replaced).  Rank `rank` of
+ * `world` owns vertices [bounds_h[rank], bounds_h[rank+1]) (bounds_h: world+1
+ * ascending host values from 0 to n) and decides only its slice of every
+ * stage; the decided slices are exchanged with NCCL in-place broadcasts over
+ * `comm` (an ncclComm_t from plv_nccl_comm_init), captured in the iteration
+ * graph, and every rank applies whole stages, so the replicated state stays
+ * bit-identical to plv_phase_create's.  comm NULL with world > 1: no graph;
+ * the caller steps the stages (plv_phase_step) and moves the slices between
+ * ranks' decide outputs itself.  out_* (device, capacity stage_off_h[nstages];
+ * all four or none) are the decide outputs at global stage positions; NULL =
+ * allocated by the library.
+ */
+int plv_phase_create_part(const int64_t *off, const int32_t *nbr, const double *wts,
+                          const double *k, const double *selfw, int64_t n, double m, int flags,
+                          const int32_t *labels, const int64_t *stage_off_h,
+                          const int32_t *stage_vtx, int64_t nstages, int32_t *assign,
+                          double *a_tot, double *w_int, int32_t *sizes, int64_t rank,
+                          int64_t world, const int64_t *bounds_h, void *comm, int32_t *out_target,
+                          uint8_t *out_moved, double *out_e_old, double *out_e_best,
+                          void **handle_h, void *stream);
+#define PLV_STEP_DECIDE 0 /* decide this rank's slice of `stage`              */
+#define PLV_STEP_APPLY 1  /* exact apply of the whole of `stage`               */
+#define PLV_STEP_FINISH 2 /* modularity; q_h / moves_h of the stepped iteration */
+int plv_phase_step(void *handle, int64_t stage, int op, double *q_h, int64_t *moves_h,
+                   void *stream);
+/* Slice bounds of every stage (nstages * (world+1), relative to the stage). */
+int plv_phase_slices(void *handle, int64_t *slices_h);
+
+/* NCCL communicator for plv_phase_create_part (NCCL is bound at run time). */
+#define PLV_NCCL_ID_BYTES 128
+int plv_nccl_unique_id(uint8_t *id_h);
+int plv_nccl_comm_init(int64_t rank, int64_t world, const uint8_t *id_h, void **comm_h);
+int plv_nccl_comm_destroy(void *comm);
+
 /* Sum over stages of the decide time of the last iteration (timing handles). */
 int plv_phase_decide_ms(void *handle, double *ms_h);
 int plv_phase_destroy(void *handle);

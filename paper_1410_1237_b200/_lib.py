@@ -28,6 +28,11 @@ F_INDEPENDENT = 1
 F_INTEGRAL = 2
 F_IDENTITY = 4
 
+STEP_DECIDE = 0
+STEP_APPLY = 1
+STEP_FINISH = 2
+NCCL_ID_BYTES = 128
+
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _U64 = ctypes.c_uint64
@@ -59,6 +64,13 @@ _SIGS = {
                   _P],
     "plv_phase_create": [_P, _P, _P, _P, _P, _I64, _D, _INT, _P, _P, _P, _I64, _P, _P, _P, _P,
                          _INT, _P, _P],
+    "plv_phase_create_part": [_P, _P, _P, _P, _P, _I64, _D, _INT, _P, _P, _P, _I64, _P, _P, _P,
+                              _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P],
+    "plv_phase_step": [_P, _I64, _INT, _P, _P, _P],
+    "plv_phase_slices": [_P, _P],
+    "plv_nccl_unique_id": [_P],
+    "plv_nccl_comm_init": [_I64, _I64, _P, _P],
+    "plv_nccl_comm_destroy": [_P],
     "plv_phase_iterate": [_P, _P, _P, _P, _P],
     "plv_phase_run": [_P, _D, _I64, _P, _P, _P, _P, _P],
     "plv_phase_decide_ms": [_P, _P],

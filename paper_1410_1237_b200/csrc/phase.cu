@@ -7,7 +7,21 @@
 // decide + exact apply, the move counter, the modularity reduction and a
 // 24-byte read-back) is captured into a CUDA graph.  An iteration is then one
 // graph launch plus one host synchronisation for the theta test.
+//
+// Partitioned mode (multi-GPU): rank r of W owns the vertex
+// range [bounds[r], bounds[r+1]).  Stages list their vertices in ascending
+// id, so a rank's share of a stage is one contiguous slice and rank order is
+// subset order.  Per stage, every rank decides its slice only (the decide
+// plan covers the rank's slices), the slices' (target, moved, e_old, e_best)
+// are exchanged by one NCCL group of in-place broadcasts (root r sends slice
+// r), and every rank replays the whole stage's exact apply -- the replicated
+// assignment / a_tot / w_internal / sizes stay bit-identical on every rank and
+// to the single-GPU run.  The broadcasts are captured into the iteration's
+// graph with the kernels.  Without a communicator (world > 1, comm NULL) the
+// stages are stepped from the host (plv_phase_step) and the caller moves the
+// slices (the single-GPU test of the partitioned plan).
 #include "localmove.cuh"
+#include "nccl_dyn.cuh"
 #include "pairwise.cuh"
 #include <chrono>
 #include <cmath>
@@ -29,7 +43,13 @@ struct Phase {
     double *a_tot;
     double *w_int;
     int32_t *sizes;
-    const int32_t *vtx;
+    const int32_t *vtx;       // all stages' vertices (apply)
+    int32_t *lvtx = nullptr;  // this rank's slices, stage after stage (decide plan)
+    std::vector<int64_t> goff;  // global stage offsets into vtx (nst + 1)
+    std::vector<int64_t> slo;   // per stage: W + 1 slice bounds, relative to the stage
+    int64_t rank = 0, world = 1;
+    void *comm = nullptr;       // ncclComm_t (partitioned, captured exchange)
+    bool own_out = true;        // decide outputs allocated here (else the caller's)
     Plan plan;
     ApplyBuffers ab;
     int32_t *target = nullptr;
@@ -63,49 +83,118 @@ struct Phase {
         fork = nullptr;
         plan.release();
         ab.release();
-        void *ps[] = {target, moved, e_old, e_best, counters, q, mod_scratch};
+        void *ps[] = {counters, q, mod_scratch, lvtx};
         for (void *p : ps)
             if (p) cudaFree(p);
+        if (own_out) {
+            void *po[] = {target, moved, e_old, e_best};
+            for (void *p : po)
+                if (p) cudaFree(p);
+        }
+        lvtx = nullptr;
+        target = nullptr;
+        moved = nullptr;
+        e_old = e_best = nullptr;
+        counters = nullptr;
+        q = mod_scratch = nullptr;
         if (h_out) cudaFreeHost(h_out);
         h_out = nullptr;
     }
 };
 
-static void record_iteration(Phase &P, cudaStream_t st) {
-    PLV_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 2, st));
-    for (size_t a = 0; a < P.plan.st.size(); a++) {
-        const StagePlan &sp = P.plan.st[a];
-        if (!sp.ns) continue;
-        DecideArgs A = make_decide_args(P.off, P.nbr, P.wts, P.k, P.labels, P.vtx + sp.off,
-                                        P.assign, P.a_tot, P.sizes, P.m,
-                                        (P.flags & PLV_F_INTEGRAL) ? 1 : 0, P.target + sp.off,
-                                        P.moved + sp.off, P.e_old + sp.off, P.e_best + sp.off,
-                                        P.counters + 1);
-        if (P.timing)
-            PLV_CUDA(cudaEventRecordWithFlags(P.ev[2 * a], st, cudaEventRecordExternal));
-        if (P.timing)
-            launch_decide(P.plan, (int64_t)a, A, st);  // serial, so the events bracket all tiers
-        else
-            launch_decide_par(P.plan, (int64_t)a, A, st, P.side, P.fork, P.join);
-        if (P.timing)
-            PLV_CUDA(cudaEventRecordWithFlags(P.ev[2 * a + 1], st, cudaEventRecordExternal));
-        StageArgs S{P.off, P.nbr, P.wts, P.k, P.selfw, P.vtx + sp.off, sp.ns, P.target + sp.off,
-                    P.moved + sp.off, P.e_old + sp.off, P.e_best + sp.off, nullptr, P.flags,
-                    P.assign, P.a_tot, P.w_int, P.sizes, P.ab.ta + sp.off, P.ab.tb + sp.off,
-                    nullptr, nullptr, P.counters};
-        launch_apply(S, P.ab, st);
+// Stage a's decide over this rank's slice (outputs at their global positions).
+static void record_decide(Phase &P, size_t a, cudaStream_t st) {
+    const StagePlan &sp = P.plan.st[a];
+    if (!sp.ns) return;
+    const int64_t o = P.goff[a] + P.slo[a * (P.world + 1) + P.rank];
+    DecideArgs A = make_decide_args(P.off, P.nbr, P.wts, P.k, P.labels, P.lvtx + sp.off, P.assign,
+                                    P.a_tot, P.sizes, P.m, (P.flags & PLV_F_INTEGRAL) ? 1 : 0,
+                                    P.target + o, P.moved + o, P.e_old + o, P.e_best + o,
+                                    P.counters + 1);
+    if (P.timing) PLV_CUDA(cudaEventRecordWithFlags(P.ev[2 * a], st, cudaEventRecordExternal));
+    if (P.timing)
+        launch_decide(P.plan, (int64_t)a, A, st);  // serial, so the events bracket all tiers
+    else
+        launch_decide_par(P.plan, (int64_t)a, A, st, P.side, P.fork, P.join);
+    if (P.timing)
+        PLV_CUDA(cudaEventRecordWithFlags(P.ev[2 * a + 1], st, cudaEventRecordExternal));
+}
+
+// Every rank's slice of stage a to every rank: one group of in-place
+// broadcasts per decide output (root r owns slice r).
+static void record_exchange(Phase &P, size_t a, cudaStream_t st) {
+    if (!P.comm) return;  // (a 1-rank communicator still runs: the capture path)
+    const int64_t *sl = P.slo.data() + a * (P.world + 1);
+    const int64_t g = P.goff[a];
+    nccl_group_start();
+    for (int64_t r = 0; r < P.world; r++) {
+        const int64_t o = g + sl[r], c = sl[r + 1] - sl[r];
+        if (!c) continue;
+        nccl_bcast_inplace(P.target + o, c, ncclInt32, (int)r, P.comm, st);
+        nccl_bcast_inplace(P.moved + o, c, ncclUint8, (int)r, P.comm, st);
+        nccl_bcast_inplace(P.e_old + o, c, ncclFloat64, (int)r, P.comm, st);
+        nccl_bcast_inplace(P.e_best + o, c, ncclFloat64, (int)r, P.comm, st);
     }
+    nccl_group_end();
+}
+
+// Stage a's exact apply over the whole stage (replicated on every rank).
+static void record_apply(Phase &P, size_t a, cudaStream_t st) {
+    const int64_t g = P.goff[a], ns = P.goff[a + 1] - g;
+    StageArgs S{P.off, P.nbr, P.wts, P.k, P.selfw, P.vtx + g, ns, P.target + g,
+                P.moved + g, P.e_old + g, P.e_best + g, nullptr, P.flags,
+                P.assign, P.a_tot, P.w_int, P.sizes, P.ab.ta + g, P.ab.tb + g,
+                nullptr, nullptr, P.counters};
+    launch_apply(S, P.ab, st);
+}
+
+static void record_finish(Phase &P, cudaStream_t st) {
     modularity_async(P.w_int, P.a_tot, P.n, P.m, P.q, P.mod_scratch, st);
     PLV_CUDA(cudaMemcpyAsync(P.h_out, P.q, sizeof(double), cudaMemcpyDeviceToHost, st));
     PLV_CUDA(cudaMemcpyAsync(P.h_out + 1, P.counters, 2 * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, st));
 }
 
+static void record_iteration(Phase &P, cudaStream_t st) {
+    PLV_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 2, st));
+    for (size_t a = 0; a + 1 < P.goff.size(); a++) {
+        if (P.goff[a + 1] == P.goff[a]) continue;
+        record_decide(P, a, st);
+        record_exchange(P, a, st);
+        record_apply(P, a, st);
+    }
+    record_finish(P, st);
+}
+
+// Slice bounds of every stage for every rank boundary: sl[a * (W + 1) + r] =
+// lower_bound(stage a, bounds[r]) - stage start (stages ascending).
+__global__ void k_stage_slices(const int32_t *vtx, const int64_t *goff, int64_t nst,
+                               const int64_t *bounds, int64_t W, int64_t *sl) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nst * (W + 1);
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = t / (W + 1), r = t % (W + 1);
+        const int64_t b0 = goff[a], b1 = goff[a + 1];
+        const int64_t key = bounds[r];
+        int64_t lo = b0, hi = b1;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)vtx[mid] < key)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        sl[t] = lo - b0;
+    }
+}
+
 static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double *wts,
                            const double *k, const double *selfw, int64_t n, double m, int flags,
                            const int32_t *labels, const int64_t *stage_off_h, const int32_t *vtx,
                            int64_t nst, int32_t *assign, double *a_tot, double *w_int,
-                           int32_t *sizes, int timing, cudaStream_t s) {
+                           int32_t *sizes, int timing, int64_t rank, int64_t world,
+                           const int64_t *bounds_h, void *comm, int32_t *out_target,
+                           uint8_t *out_moved, double *out_e_old, double *out_e_best,
+                           cudaStream_t s) {
     Phase *P = new Phase();
     try {
         P->off = off;
@@ -123,19 +212,72 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
         P->sizes = sizes;
         P->vtx = vtx;
         P->timing = timing != 0;
+        P->rank = rank;
+        P->world = world;
+        P->comm = comm;
+        P->goff.assign(stage_off_h, stage_off_h + nst + 1);
         ensure_decide_attrs();
-        plan_build(P->plan, off, vtx, stage_off_h, nst, n, s);
         int64_t total = stage_off_h[nst];
+        // this rank's slice of every stage
+        P->slo.assign(nst * (world + 1), 0);
+        std::vector<int64_t> loff(nst + 1, 0);
+        if (world == 1) {
+            for (int64_t a = 0; a < nst; a++) P->slo[2 * a + 1] = stage_off_h[a + 1] - stage_off_h[a];
+            loff = P->goff;
+            PLV_CUDA(cudaMalloc((void **)&P->lvtx, sizeof(int32_t) * (total ? total : 1)));
+            if (total)
+                PLV_CUDA(cudaMemcpyAsync(P->lvtx, vtx, sizeof(int32_t) * total,
+                                         cudaMemcpyDeviceToDevice, s));
+        } else {
+            Buf<int64_t> d_goff(nst + 1, s), d_bounds(world + 1, s), d_sl(nst * (world + 1), s);
+            PLV_CUDA(cudaMemcpyAsync(d_goff.get(), stage_off_h, sizeof(int64_t) * (nst + 1),
+                                     cudaMemcpyHostToDevice, s));
+            PLV_CUDA(cudaMemcpyAsync(d_bounds.get(), bounds_h, sizeof(int64_t) * (world + 1),
+                                     cudaMemcpyHostToDevice, s));
+            if (nst) {
+                k_stage_slices<<<grid_for(nst * (world + 1), 256), 256, 0, s>>>(
+                    vtx, d_goff, nst, d_bounds, world, d_sl);
+                PLV_LAUNCH_CHECK();
+                PLV_CUDA(cudaMemcpyAsync(P->slo.data(), d_sl.get(),
+                                         sizeof(int64_t) * nst * (world + 1),
+                                         cudaMemcpyDeviceToHost, s));
+            }
+            PLV_CUDA(cudaStreamSynchronize(s));
+            for (int64_t a = 0; a < nst; a++) {
+                const int64_t *sl = P->slo.data() + a * (world + 1);
+                loff[a + 1] = loff[a] + (sl[rank + 1] - sl[rank]);
+            }
+            PLV_CUDA(cudaMalloc((void **)&P->lvtx, sizeof(int32_t) * (loff[nst] ? loff[nst] : 1)));
+            for (int64_t a = 0; a < nst; a++) {
+                const int64_t c = loff[a + 1] - loff[a];
+                if (c)
+                    PLV_CUDA(cudaMemcpyAsync(P->lvtx + loff[a],
+                                             vtx + stage_off_h[a] + P->slo[a * (world + 1) + rank],
+                                             sizeof(int32_t) * c, cudaMemcpyDeviceToDevice, s));
+            }
+        }
+        plan_build(P->plan, off, P->lvtx, loff.data(), nst, n, s);
         int64_t max_large = 0;
-        for (auto &sp : P->plan.st)
-            if (!((flags & PLV_F_INDEPENDENT) && sp.ns <= SMALL_APPLY_MAX))
-                max_large = sp.ns > max_large ? sp.ns : max_large;
+        for (int64_t a = 0; a < nst; a++) {
+            const int64_t ns = stage_off_h[a + 1] - stage_off_h[a];
+            if (!((flags & PLV_F_INDEPENDENT) && ns <= SMALL_APPLY_MAX))
+                max_large = ns > max_large ? ns : max_large;
+        }
         P->ab.alloc(total, max_large, n, s);
-        P->target = dalloc<int32_t>(total);
-        P->moved = dalloc<uint8_t>(total);
-        P->e_old = dalloc<double>(total);
-        P->e_best = dalloc<double>(total);
+        P->own_out = !out_target;
+        if (P->own_out) {
+            P->target = dalloc<int32_t>(total);
+            P->moved = dalloc<uint8_t>(total);
+            P->e_old = dalloc<double>(total);
+            P->e_best = dalloc<double>(total);
+        } else {
+            P->target = out_target;
+            P->moved = out_moved;
+            P->e_old = out_e_old;
+            P->e_best = out_e_best;
+        }
         P->counters = dalloc<unsigned long long>(2);
+        PLV_CUDA(cudaMemsetAsync(P->counters, 0, 2 * sizeof(unsigned long long), s));
         P->q = dalloc<double>(1);
         P->mod_scratch = dalloc<double>(modularity_scratch_doubles(n));
         PLV_CUDA(cudaMallocHost((void **)&P->h_out, 4 * sizeof(double)));
@@ -155,6 +297,7 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
         }
         PLV_CUDA(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming));
         PLV_CUDA(cudaStreamSynchronize(s));
+        if (world > 1 && !comm) return P;  // host-stepped (plv_phase_step)
         cudaStream_t cs;
         PLV_CUDA(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, prio_hi));
         PLV_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
@@ -180,6 +323,7 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
 }
 
 static void phase_iterate(Phase *P, cudaStream_t s, double *q, int64_t *moves, int64_t *cand) {
+    if (!P->exec) PLV_FAIL(PLV_EINVAL, "host-stepped partition: use plv_phase_step");
     PLV_CUDA(cudaGraphLaunch(P->exec, s));
     PLV_CUDA(cudaStreamSynchronize(s));
     *q = P->h_out[0];
@@ -206,9 +350,71 @@ extern "C" int plv_phase_create(const int64_t *off, const int32_t *nbr, const do
                                 void **handle_h, void *stream) {
     PLV_ENTRY
     if (!(m > 0.0)) PLV_FAIL(PLV_EINVAL, "modularity undefined for edgeless graph");
+    int64_t b[2] = {0, n};
     *handle_h = plv::phase_create(off, nbr, wts, k, selfw, n, m, flags, labels, stage_off_h,
-                                  stage_vtx, nstages, assign, a_tot, w_int, sizes, timing,
+                                  stage_vtx, nstages, assign, a_tot, w_int, sizes, timing, 0, 1, b,
+                                  nullptr, nullptr, nullptr, nullptr, nullptr, plv::S(stream));
+    PLV_EXIT
+}
+
+extern "C" int plv_phase_create_part(const int64_t *off, const int32_t *nbr, const double *wts,
+                                     const double *k, const double *selfw, int64_t n, double m,
+                                     int flags, const int32_t *labels, const int64_t *stage_off_h,
+                                     const int32_t *stage_vtx, int64_t nstages, int32_t *assign,
+                                     double *a_tot, double *w_int, int32_t *sizes, int64_t rank,
+                                     int64_t world, const int64_t *bounds_h, void *comm,
+                                     int32_t *out_target, uint8_t *out_moved, double *out_e_old,
+                                     double *out_e_best, void **handle_h, void *stream) {
+    PLV_ENTRY
+    if (!(m > 0.0)) PLV_FAIL(PLV_EINVAL, "modularity undefined for edgeless graph");
+    if (world < 1 || rank < 0 || rank >= world) PLV_FAIL(PLV_EINVAL, "bad rank/world");
+    if (bounds_h[0] != 0 || bounds_h[world] != n)
+        PLV_FAIL(PLV_EINVAL, "partition bounds must run from 0 to n");
+    for (int64_t r = 0; r < world; r++)
+        if (bounds_h[r + 1] < bounds_h[r]) PLV_FAIL(PLV_EINVAL, "partition bounds must ascend");
+    if ((out_target == nullptr) != (out_e_best == nullptr) ||
+        (out_target == nullptr) != (out_moved == nullptr) ||
+        (out_target == nullptr) != (out_e_old == nullptr))
+        PLV_FAIL(PLV_EINVAL, "decide outputs: all four or none");
+    *handle_h = plv::phase_create(off, nbr, wts, k, selfw, n, m, flags, labels, stage_off_h,
+                                  stage_vtx, nstages, assign, a_tot, w_int, sizes, 0, rank, world,
+                                  bounds_h, comm, out_target, out_moved, out_e_old, out_e_best,
                                   plv::S(stream));
+    PLV_EXIT
+}
+
+extern "C" int plv_phase_step(void *handle, int64_t stage, int op, double *q_h, int64_t *moves_h,
+                              void *stream) {
+    PLV_ENTRY
+    plv::Phase *P = (plv::Phase *)handle;
+    cudaStream_t s = plv::S(stream);
+    const int64_t nst = (int64_t)P->goff.size() - 1;
+    if (op == PLV_STEP_FINISH) {
+        plv::record_finish(*P, s);
+        PLV_CUDA(cudaStreamSynchronize(s));
+        *q_h = P->h_out[0];
+        unsigned long long c[2];
+        memcpy(c, P->h_out + 1, sizeof(c));
+        *moves_h = (int64_t)c[0];
+        PLV_CUDA(cudaMemsetAsync(P->counters, 0, sizeof(unsigned long long) * 2, s));
+    } else {
+        if (stage < 0 || stage >= nst) PLV_FAIL(PLV_ERANGE, "stage out of range");
+        if (P->goff[stage + 1] > P->goff[stage]) {
+            if (op == PLV_STEP_DECIDE)
+                plv::record_decide(*P, (size_t)stage, s);
+            else if (op == PLV_STEP_APPLY)
+                plv::record_apply(*P, (size_t)stage, s);
+            else
+                PLV_FAIL(PLV_EINVAL, "unknown step op");
+        }
+    }
+    PLV_EXIT
+}
+
+extern "C" int plv_phase_slices(void *handle, int64_t *slices_h) {
+    PLV_ENTRY
+    plv::Phase *P = (plv::Phase *)handle;
+    memcpy(slices_h, P->slo.data(), sizeof(int64_t) * P->slo.size());
     PLV_EXIT
 }
 

@@ -18,8 +18,10 @@ order is subset order.  Per stage:
 Modularity needs no communication (replicated aggregates).  Uncoloured
 iterations gather (target, moved) and replay the apply with the live rule on
 every rank.  The compute steps are callbacks, so the same driver runs the CUDA
-kernels (`CudaStageOps`) on GPUs over NCCL and a CPU checker over gloo in the
-tests.
+kernels (`CudaStageOps`, slice-level C-ABI calls) and a CPU checker over gloo
+in the tests.  The production multi-GPU path is `PartitionedPhaseEngine`
+(plv_phase_create_part): the same per-stage decide / exchange / replicated
+apply, with the NCCL broadcasts captured inside the iteration's CUDA graph.
 """
 
 from __future__ import annotations
@@ -96,6 +98,148 @@ class DistributedIteration:
                 d = DecideSlice(t, m, eo, eb)
             moves += self.ops.apply(a, d)
         return moves, self.ops.modularity()
+
+
+def nccl_communicator(rank: int, world: int, group=None):
+    """NCCL communicator for PartitionedPhaseEngine (libplv binds NCCL at run
+    time): rank 0 draws the unique id, torch.distributed broadcasts it."""
+    import ctypes
+    from . import _lib
+    L = _lib.lib()
+    idbuf = (ctypes.c_uint8 * _lib.NCCL_ID_BYTES)()
+    if rank == 0:
+        _lib.check(L.nccl_unique_id(ctypes.addressof(idbuf)), "nccl_unique_id")
+    if world > 1:
+        import torch.distributed as dist
+        obj = [bytes(idbuf)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        ctypes.memmove(idbuf, obj[0], _lib.NCCL_ID_BYTES)
+    comm = ctypes.c_void_p()
+    _lib.check(L.nccl_comm_init(rank, world, ctypes.addressof(idbuf), ctypes.byref(comm)),
+               "nccl_comm_init")
+    return comm
+
+
+def destroy_communicator(comm):
+    from . import _lib
+    if comm is not None and comm.value:
+        _lib.check(_lib.lib().nccl_comm_destroy(comm), "nccl_comm_destroy")
+
+
+class PartitionedPhaseEngine:
+    """The phase engine on one rank of a 1D vertex partition (plv_phase_create_part).
+
+    Rank `rank` decides its slice of every stage; with a communicator the
+    slices are exchanged by NCCL broadcasts inside the iteration's CUDA graph
+    and `iterate()` is one graph launch, as on one GPU.  Without one
+    (world > 1), the caller steps the stages: `step(a, STEP_DECIDE)`, move
+    the slices between ranks' `outputs`, `step(a, STEP_APPLY)`, then
+    `finish()` (the single-GPU test of the partitioned plan)."""
+
+    def __init__(self, g, s, coloring, rank: int, world: int, bounds=None, comm=None,
+                 outputs=None):
+        import ctypes
+        import torch
+        from . import _lib
+        self._lib = _lib
+        d = s.device()
+        dev = d["assignment"].device
+        n = g.num_vertices
+        self.g, self.s, self.d, self.rank, self.world = g, s, d, rank, world
+        if coloring is not None:
+            class_off, class_vtx = coloring.device_classes()
+            self.stage_off = np.ascontiguousarray(class_off, dtype=np.int64)
+            self.vtx = class_vtx
+            flags = _lib.F_INDEPENDENT
+        else:
+            self.stage_off = np.array([0, n], dtype=np.int64)
+            self.vtx = torch.arange(n, dtype=torch.int32, device=dev)
+            flags = _lib.F_IDENTITY
+        if g.integral:
+            flags |= _lib.F_INTEGRAL
+        self.nstages = len(self.stage_off) - 1
+        if bounds is None:
+            bounds = partition_bounds(g.adjacency_offsets, world)
+        self.bounds = np.ascontiguousarray(bounds, dtype=np.int64)
+        total = int(self.stage_off[-1])
+        if outputs is None and comm is None and world > 1:
+            outputs = {
+                "target": torch.empty(max(total, 1), dtype=torch.int32, device=dev),
+                "moved": torch.empty(max(total, 1), dtype=torch.uint8, device=dev),
+                "e_old": torch.empty(max(total, 1), dtype=torch.float64, device=dev),
+                "e_best": torch.empty(max(total, 1), dtype=torch.float64, device=dev)}
+        self.outputs = outputs
+        o = outputs or {}
+        self.handle = ctypes.c_void_p()
+        _lib.check(_lib.lib().phase_create_part(
+            _lib.ptr(g.d_off), _lib.ptr(g.d_nbr), _lib.ptr(g.d_w), _lib.ptr(g.d_k),
+            _lib.ptr(g.d_selfw), n, g.total_weight, flags, _lib.ptr(d["labels"]),
+            self.stage_off.ctypes.data, _lib.ptr(self.vtx), self.nstages,
+            _lib.ptr(d["assignment"]), _lib.ptr(d["a_tot"]), _lib.ptr(d["w_internal"]),
+            _lib.ptr(d["sizes"]), rank, world, self.bounds.ctypes.data, comm,
+            _lib.ptr(o.get("target")), _lib.ptr(o.get("moved")), _lib.ptr(o.get("e_old")),
+            _lib.ptr(o.get("e_best")), ctypes.byref(self.handle), _lib.stream()),
+            "phase_create_part")
+        self._q = _lib.f64_host(1)
+        self._mv = _lib.i64_host(1)
+        self._cand = _lib.i64_host(1)
+
+    def slices(self) -> np.ndarray:
+        out = np.empty(self.nstages * (self.world + 1), np.int64)
+        self._lib.check(self._lib.lib().phase_slices(self.handle, out.ctypes.data), "slices")
+        return out.reshape(self.nstages, self.world + 1)
+
+    def iterate(self):
+        _lib = self._lib
+        _lib.check(_lib.lib().phase_iterate(self.handle, _lib.hp(self._q), _lib.hp(self._mv),
+                                            _lib.hp(self._cand), _lib.stream()), "phase_iterate")
+        return float(self._q[0]), int(self._mv[0]), int(self._cand[0])
+
+    def step(self, stage: int, op: int):
+        _lib = self._lib
+        _lib.check(_lib.lib().phase_step(self.handle, stage, op, _lib.hp(self._q),
+                                         _lib.hp(self._mv), _lib.stream()), "phase_step")
+
+    def finish(self):
+        self.step(0, self._lib.STEP_FINISH)
+        return float(self._q[0]), int(self._mv[0])
+
+    def close(self):
+        if self.handle:
+            self._lib.lib().phase_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def stepped_iteration(engines):
+    """One iteration of W host-stepped partitioned engines (one per virtual
+    rank, same device): decide per rank, copy every slice to every other
+    rank (the exchange), apply.  Returns [(q, moves)] per rank."""
+    from . import _lib
+    sl = [e.slices() for e in engines]
+    off = engines[0].stage_off
+    W = len(engines)
+    for a in range(engines[0].nstages):
+        if off[a + 1] == off[a]:
+            continue
+        for e in engines:
+            e.step(a, _lib.STEP_DECIDE)
+        for r in range(W):
+            lo, hi = int(off[a] + sl[r][a][r]), int(off[a] + sl[r][a][r + 1])
+            if hi == lo:
+                continue
+            for q in range(W):
+                if q != r:
+                    for key in ("target", "moved", "e_old", "e_best"):
+                        engines[q].outputs[key][lo:hi].copy_(engines[r].outputs[key][lo:hi])
+        for e in engines:
+            e.step(a, _lib.STEP_APPLY)
+    return [e.finish() for e in engines]
 
 
 class CudaStageOps:

@@ -43,3 +43,12 @@ for rep in range(a.repeat):
     print(f"rep {rep}: n={g.num_vertices} M={g.num_edges} build={t1 - t0:.3f}s run={t2 - t1:.3f}s "
           f"Q={h.final_modularity!r} communities={h.num_communities} iterations={its} "
           f"stages_ms={ {k: round(v, 1) for k, v in by.items()} }", flush=True)
+    per = {}
+    for r in trace:
+        key = (r.phase, r.stage)
+        c, ms = per.get(key, (0, 0.0))
+        per[key] = (c + 1, ms + r.millis)
+    if rep == a.repeat - 1:
+        print("   phase graph sizes (n per phase input):", [len(p_.assignment) for p_ in h.phases], flush=True)
+        for (ph, stg), (c, ms) in sorted(per.items()):
+            print(f"   phase {ph} {stg:10s} n={c:6d} ms={ms:10.1f}", flush=True)
