@@ -176,8 +176,12 @@ int plv_phase_create(const int64_t *off, const int32_t *nbr, const double *wts, 
  * cand_h (nullable) = sum of distinct candidate communities over all deciders. */
 int plv_phase_iterate(void *handle, double *q_h, int64_t *moves_h, int64_t *cand_h, void *stream);
 /* The phase loop with the reference's stopping rule (PL/engine.py:203-212):
- * per-iteration Q / moves / host milliseconds into the *_trace_h arrays
- * (capacity max_iters); result_h = {iterations, total_moves, hit_cap}. */
+ * per-iteration Q / moves / milliseconds into the *_trace_h arrays (capacity
+ * max_iters); result_h = {iterations, total_moves, hit_cap, device_loop}.
+ * Single-GPU engines run the loop on the device (one CUDA graph: the
+ * iteration inside a WHILE conditional node, stopping rule and trace in a
+ * control kernel; milliseconds from the GPU global timer, device_loop = 1);
+ * otherwise one graph launch + host test per iteration (device_loop = 0). */
 int plv_phase_run(void *handle, double theta, int64_t max_iters, double *q_trace_h,
                   int64_t *moves_trace_h, double *ms_trace_h, int64_t *result_h, void *stream);
 /*
@@ -207,8 +211,10 @@ int plv_phase_create_part(const int64_t *off, const int32_t *nbr, const double *
 #define PLV_STEP_FINISH 2 /* modularity; q_h / moves_h of the stepped iteration */
 int plv_phase_step(void *handle, int64_t stage, int op, double *q_h, int64_t *moves_h,
                    void *stream);
-/* Slice bounds of every stage (nstages * (world+1), relative to the stage). */
-int plv_phase_slices(void *handle, int64_t *slices_h);
+/* The engine's stage offsets (nstages+1; stage lists keep only vertices with
+ * a non-self neighbour -- the others never move) and the slice bounds of
+ * every stage (nstages * (world+1), relative to the stage). */
+int plv_phase_slices(void *handle, int64_t *stage_off_h, int64_t *slices_h);
 
 /* NCCL communicator for plv_phase_create_part (NCCL is bound at run time). */
 #define PLV_NCCL_ID_BYTES 128

@@ -67,7 +67,7 @@ _SIGS = {
     "plv_phase_create_part": [_P, _P, _P, _P, _P, _I64, _D, _INT, _P, _P, _P, _I64, _P, _P, _P,
                               _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P],
     "plv_phase_step": [_P, _I64, _INT, _P, _P, _P],
-    "plv_phase_slices": [_P, _P],
+    "plv_phase_slices": [_P, _P, _P],
     "plv_nccl_unique_id": [_P],
     "plv_nccl_comm_init": [_I64, _I64, _P, _P],
     "plv_nccl_comm_destroy": [_P],

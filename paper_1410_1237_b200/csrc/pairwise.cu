@@ -149,11 +149,123 @@ __global__ void k_mod_finish(const double *sw, const double *sq, double two_m, d
     out[0] = __dsub_rn(__ddiv_rn(sw[0], two_m), sq[0]);
 }
 
-int64_t modularity_scratch_doubles(int64_t n) { return 2 * pw_scratch_doubles(n) + 2; }
+// Modularity in one launch (trees of <= MODF_MAX_NODES depth-d0 nodes): warps
+// compute the depth-d0 node values of both arrays, the last block to finish
+// (threadfence + ticket) reduces the two perfect top trees in shared memory
+// -- the same additions as k_pw_tree2 -- and writes Q.  The ticket resets
+// itself, so the scratch needs zeroing once (modularity_scratch_init).
+constexpr int64_t MODF_MAX_NODES = 8192;
+constexpr int MODF_THREADS = 512;
+
+template <class F>
+__device__ __forceinline__ double pw_node_warp(const double *a, int64_t n, int d0, uint64_t t,
+                                               F f) {
+    const int lane = threadIdx.x & 31, oct = lane >> 3, k = lane & 7;
+    int64_t lo, len;
+    pw_node(n, d0, t, &lo, &len);
+    int64_t off[3] = {0, 0, 0}, ln[3] = {len, 0, 0};
+    int nleaf = 1;
+    if (len > 128) {
+        const int64_t n2 = pw_split(len);
+        ln[0] = n2;
+        off[1] = n2;
+        ln[1] = len - n2;
+        nleaf = 2;
+        if (ln[1] > 128) {
+            const int64_t m2 = pw_split(ln[1]);
+            off[2] = off[1] + m2;
+            ln[2] = ln[1] - m2;
+            ln[1] = m2;
+            nleaf = 3;
+        }
+    }
+    const int o = oct < 3 ? oct : 2;
+    const int64_t my_len = oct < nleaf ? ln[o] : 0;
+    const double v = pw_leaf_octet(a + lo + off[o], my_len, f, k);
+    const double vL = __shfl_sync(0xffffffffu, v, 0);
+    const double vR = __shfl_sync(0xffffffffu, v, 8);
+    const double vRR = __shfl_sync(0xffffffffu, v, 16);
+    return nleaf == 1 ? vL : nleaf == 2 ? __dadd_rn(vL, vR) : __dadd_rn(vL, __dadd_rn(vR, vRR));
+}
+
+__global__ void __launch_bounds__(MODF_THREADS) k_mod_fused(const double *__restrict__ w_int,
+                                                            const double *__restrict__ a_tot,
+                                                            int64_t n, int d0, double two_m,
+                                                            double *vals, unsigned int *ticket,
+                                                            double *out) {
+    extern __shared__ double sm[];  // 2 * cnt
+    __shared__ bool s_last;
+    const uint64_t cnt = 1ull << d0;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < 2 * cnt;
+         t += nw) {
+        const double v = t < cnt ? pw_node_warp(w_int, n, d0, t, Ident{})
+                                 : pw_node_warp(a_tot, n, d0, t - cnt, SqScaled{two_m});
+        if ((threadIdx.x & 31) == 0) vals[t] = v;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (uint64_t i = threadIdx.x; i < 2 * cnt; i += blockDim.x) sm[i] = __ldcg(vals + i);
+    __syncthreads();
+    // both perfect trees level by level: pair (2i, 2i+1) of each half
+    for (uint64_t width = cnt; width > 1; width >>= 1) {
+        const uint64_t half = width >> 1;
+        double r[2 * MODF_MAX_NODES / MODF_THREADS];
+        int c = 0;
+        for (uint64_t i = threadIdx.x; i < 2 * half; i += blockDim.x) {
+            const uint64_t h = i / half, j = i % half;
+            r[c++] = __dadd_rn(sm[h * cnt + 2 * j], sm[h * cnt + 2 * j + 1]);
+        }
+        __syncthreads();
+        c = 0;
+        for (uint64_t i = threadIdx.x; i < 2 * half; i += blockDim.x) {
+            const uint64_t h = i / half, j = i % half;
+            sm[h * cnt + j] = r[c++];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double sw = __dadd_rn(0.0, sm[0]), sq = __dadd_rn(0.0, sm[cnt]);
+        out[0] = __dsub_rn(__ddiv_rn(sw, two_m), sq);
+        *ticket = 0u;
+    }
+}
+
+int64_t modularity_scratch_doubles(int64_t n) { return 2 * pw_scratch_doubles(n) + 4; }
+
+void modularity_scratch_init(double *scratch, cudaStream_t s) {
+    PLV_CUDA(cudaMemsetAsync(scratch, 0, sizeof(double), s));
+}
 
 void modularity_async(const double *w_int, const double *a_tot, int64_t n, double m, double *out,
                       double *scratch, cudaStream_t s) {
     double two_m = 2.0 * m;
+    unsigned int *ticket = (unsigned int *)scratch;
+    scratch += 2;
+    if (n > 0) {
+        const int d0 = pw_depth(n);
+        const int64_t cnt = 1ll << d0;
+        if (cnt <= MODF_MAX_NODES) {
+            static int attr_dev = -1;
+            int dev;
+            PLV_CUDA(cudaGetDevice(&dev));
+            if (attr_dev != dev) {
+                PLV_CUDA(cudaFuncSetAttribute(k_mod_fused,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)(2 * MODF_MAX_NODES * sizeof(double))));
+                attr_dev = dev;
+            }
+            k_mod_fused<<<grid_for(2 * cnt * 32, MODF_THREADS, 148 * 4), MODF_THREADS,
+                          2 * cnt * sizeof(double), s>>>(w_int, a_tot, n, d0, two_m, scratch,
+                                                         ticket, out);
+            PLV_LAUNCH_CHECK();
+            return;
+        }
+    }
     int64_t ps = pw_scratch_doubles(n);
     double *tmp = scratch + 2 * ps;
     pw_launch(w_int, n, tmp, s, Ident{}, scratch);
@@ -237,6 +349,7 @@ extern "C" int plv_modularity(const double *w_int, const double *a_tot, int64_t 
     cudaStream_t s = plv::S(stream);
     if (!(m > 0.0)) PLV_FAIL(PLV_EINVAL, "modularity undefined for edgeless graph");
     plv::Buf<double> scratch(plv::modularity_scratch_doubles(n), s);
+    plv::modularity_scratch_init(scratch.get(), s);
     plv::modularity_async(w_int, a_tot, n, m, out, scratch.get(), s);
     PLV_EXIT
 }

@@ -158,6 +158,8 @@ void pw_sum_sq_async(const double *a, int64_t n, double two_m, double *out_dev, 
 // list starts[0..M) (segment t ends at starts[t+1], the last at R).
 int64_t pw_scratch_doubles(int64_t n);
 int64_t modularity_scratch_doubles(int64_t n);
+// Zero the scratch's ticket once after allocating it (it resets itself).
+void modularity_scratch_init(double *scratch, cudaStream_t s);
 // q = pairwise(w_int)/2m - pairwise((a_tot/2m)^2); scratch: modularity_scratch_doubles(n).
 void modularity_async(const double *w_int, const double *a_tot, int64_t n, double m, double *out,
                       double *scratch, cudaStream_t s);

@@ -23,11 +23,22 @@
 #include "localmove.cuh"
 #include "nccl_dyn.cuh"
 #include "pairwise.cuh"
+#include <cub/cub.cuh>
 #include <chrono>
 #include <cmath>
 #include <cstring>
 
 namespace plv {
+
+// Device state of the phase loop (PL/engine.py:203-212 on device).
+struct RunCtl {
+    double theta;
+    int64_t max_iters;
+    int64_t it, total, hit;
+    double q_prev;
+    int64_t have_prev;
+    unsigned long long t0;
+};
 
 struct Phase {
     const int64_t *off;
@@ -43,7 +54,9 @@ struct Phase {
     double *a_tot;
     double *w_int;
     int32_t *sizes;
-    const int32_t *vtx;       // all stages' vertices (apply)
+    const int32_t *vtx;       // all stages' active vertices (apply)
+    int32_t *fvtx = nullptr;  // the filtered stage lists when some vertex was inactive
+    int32_t *pos = nullptr;   // filtered uncoloured stage: subset position per vertex
     int32_t *lvtx = nullptr;  // this rank's slices, stage after stage (decide plan)
     std::vector<int64_t> goff;  // global stage offsets into vtx (nst + 1)
     std::vector<int64_t> slo;   // per stage: W + 1 slice bounds, relative to the stage
@@ -65,8 +78,30 @@ struct Phase {
     cudaEvent_t fork = nullptr, join[NTIER - 1] = {};
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    // whole-phase graph: the iteration inside a device-side WHILE loop
+    cudaGraph_t rgraph = nullptr;
+    cudaGraphExec_t rexec = nullptr;
+    RunCtl *ctl = nullptr;         // device loop state
+    double *tr_q = nullptr;        // per-iteration trace (capacity tr_cap)
+    unsigned long long *tr_mv = nullptr, *tr_t = nullptr;
+    int64_t tr_cap = 0;
+    bool run_graph_failed = false;
 
+    void release_run() {
+        if (rexec) cudaGraphExecDestroy(rexec);
+        if (rgraph) cudaGraphDestroy(rgraph);
+        rexec = nullptr;
+        rgraph = nullptr;
+        void *pr[] = {ctl, tr_q, tr_mv, tr_t};
+        for (void *p : pr)
+            if (p) cudaFree(p);
+        ctl = nullptr;
+        tr_q = nullptr;
+        tr_mv = tr_t = nullptr;
+        tr_cap = 0;
+    }
     void release() {
+        release_run();
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
         exec = nullptr;
@@ -83,7 +118,7 @@ struct Phase {
         fork = nullptr;
         plan.release();
         ab.release();
-        void *ps[] = {counters, q, mod_scratch, lvtx};
+        void *ps[] = {counters, q, mod_scratch, lvtx, fvtx, pos};
         for (void *p : ps)
             if (p) cudaFree(p);
         if (own_out) {
@@ -91,7 +126,7 @@ struct Phase {
             for (void *p : po)
                 if (p) cudaFree(p);
         }
-        lvtx = nullptr;
+        lvtx = fvtx = pos = nullptr;
         target = nullptr;
         moved = nullptr;
         e_old = e_best = nullptr;
@@ -142,7 +177,7 @@ static void record_exchange(Phase &P, size_t a, cudaStream_t st) {
 static void record_apply(Phase &P, size_t a, cudaStream_t st) {
     const int64_t g = P.goff[a], ns = P.goff[a + 1] - g;
     StageArgs S{P.off, P.nbr, P.wts, P.k, P.selfw, P.vtx + g, ns, P.target + g,
-                P.moved + g, P.e_old + g, P.e_best + g, nullptr, P.flags,
+                P.moved + g, P.e_old + g, P.e_best + g, P.pos, P.flags,
                 P.assign, P.a_tot, P.w_int, P.sizes, P.ab.ta + g, P.ab.tb + g,
                 nullptr, nullptr, P.counters};
     launch_apply(S, P.ab, st);
@@ -187,6 +222,80 @@ __global__ void k_stage_slices(const int32_t *vtx, const int64_t *goff, int64_t 
     }
 }
 
+// A vertex whose row holds nothing but (at most) its self loop has no
+// candidate community: decide keeps it (PL/_kernels.pyx:77-95 with an empty
+// e_to) and apply has nothing to do, so stage lists keep only the others.
+__global__ void k_active_flags(const int64_t *off, const double *selfw, const int32_t *vtx,
+                               int64_t total, int32_t *flag) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t i = vtx[g];
+        const int64_t d = off[i + 1] - off[i] - (selfw[i] != 0.0 ? 1 : 0);
+        flag[g] = d > 0 ? 1 : 0;
+    }
+}
+
+__global__ void k_active_compact(const int32_t *vtx, const int32_t *flag, const int32_t *scan,
+                                 int64_t total, int32_t *out) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+         g += (int64_t)gridDim.x * blockDim.x)
+        if (flag[g]) out[scan[g]] = vtx[g];
+}
+
+__global__ void k_gather_offsets(const int32_t *scan, const int32_t *flag, const int64_t *goff,
+                                 int64_t nst, int64_t total, int64_t *out) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a <= nst;
+         a += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = goff[a];
+        out[a] = g < total ? (int64_t)scan[g] : (int64_t)scan[total - 1] + flag[total - 1];
+    }
+}
+
+__global__ void k_positions(const int32_t *sub, int64_t ns, int32_t *pos) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < ns;
+         x += (int64_t)gridDim.x * blockDim.x)
+        pos[sub[x]] = (int32_t)x;
+}
+
+// Drop inactive vertices from the stage lists (order kept); updates P.vtx,
+// P.goff and, for an uncoloured stage, the flags and the position table.
+static void filter_active(Phase &P, const int32_t *vtx, int64_t nst, cudaStream_t s) {
+    P.vtx = vtx;
+    const int64_t total = P.goff[nst];
+    if (!total) return;
+    Buf<int32_t> flag(total, s), scan(total, s);
+    k_active_flags<<<grid_for(total, 256), 256, 0, s>>>(P.off, P.selfw, vtx, total, flag);
+    PLV_LAUNCH_CHECK();
+    size_t tb = 0;
+    PLV_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag.get(), scan.get(), total, s));
+    Buf<char> tmp(tb, s);
+    PLV_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, flag.get(), scan.get(), total, s));
+    Buf<int64_t> d_goff(nst + 1, s), d_new(nst + 1, s);
+    PLV_CUDA(cudaMemcpyAsync(d_goff.get(), P.goff.data(), sizeof(int64_t) * (nst + 1),
+                             cudaMemcpyHostToDevice, s));
+    k_gather_offsets<<<grid_for(nst + 1, 256), 256, 0, s>>>(scan, flag, d_goff, nst, total, d_new);
+    PLV_LAUNCH_CHECK();
+    std::vector<int64_t> nw(nst + 1);
+    PLV_CUDA(cudaMemcpyAsync(nw.data(), d_new.get(), sizeof(int64_t) * (nst + 1),
+                             cudaMemcpyDeviceToHost, s));
+    PLV_CUDA(cudaStreamSynchronize(s));
+    if (nw[nst] == total) return;  // every listed vertex is active
+    P.fvtx = dalloc<int32_t>(nw[nst]);
+    k_active_compact<<<grid_for(total, 256), 256, 0, s>>>(vtx, flag, scan, total, P.fvtx);
+    PLV_LAUNCH_CHECK();
+    P.vtx = P.fvtx;
+    P.goff = nw;
+    if (P.flags & PLV_F_IDENTITY) {
+        // the stage is no longer arange(n): apply's live rule looks positions up
+        P.flags &= ~PLV_F_IDENTITY;
+        P.pos = dalloc<int32_t>(P.n);
+        PLV_CUDA(cudaMemsetAsync(P.pos, 0xff, sizeof(int32_t) * P.n, s));
+        k_positions<<<grid_for(nw[nst], 256), 256, 0, s>>>(P.fvtx, nw[nst], P.pos);
+        PLV_LAUNCH_CHECK();
+    }
+    PLV_CUDA(cudaStreamSynchronize(s));
+}
+
 static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double *wts,
                            const double *k, const double *selfw, int64_t n, double m, int flags,
                            const int32_t *labels, const int64_t *stage_off_h, const int32_t *vtx,
@@ -210,13 +319,16 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
         P->a_tot = a_tot;
         P->w_int = w_int;
         P->sizes = sizes;
-        P->vtx = vtx;
         P->timing = timing != 0;
         P->rank = rank;
         P->world = world;
         P->comm = comm;
         P->goff.assign(stage_off_h, stage_off_h + nst + 1);
         ensure_decide_attrs();
+        filter_active(*P, vtx, nst, s);
+        vtx = P->vtx;
+        flags = P->flags;
+        stage_off_h = P->goff.data();
         int64_t total = stage_off_h[nst];
         // this rank's slice of every stage
         P->slo.assign(nst * (world + 1), 0);
@@ -280,6 +392,7 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
         PLV_CUDA(cudaMemsetAsync(P->counters, 0, 2 * sizeof(unsigned long long), s));
         P->q = dalloc<double>(1);
         P->mod_scratch = dalloc<double>(modularity_scratch_doubles(n));
+        modularity_scratch_init(P->mod_scratch, s);
         PLV_CUDA(cudaMallocHost((void **)&P->h_out, 4 * sizeof(double)));
         if (P->timing) {
             P->ev.resize(2 * nst);
@@ -334,6 +447,148 @@ static void phase_iterate(Phase *P, cudaStream_t s, double *q, int64_t *moves, i
 }
 
 static const double ZERO_GUARD = 1e-15;  // PL/engine.py:28
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void k_run_start(RunCtl *c) { c->t0 = gtimer(); }
+
+// End of one loop iteration: trace row, the reference's stopping rule
+// (PL/engine.py:203-212, _iteration_converged :134-137), loop condition.
+__global__ void k_run_ctl(RunCtl *c, const double *q, const unsigned long long *counters,
+                          double *tr_q, unsigned long long *tr_mv, unsigned long long *tr_t,
+                          cudaGraphConditionalHandle h) {
+    const double q_cur = *q;
+    const unsigned long long moves = counters[0];
+    const int64_t it = c->it;
+    tr_q[it] = q_cur;
+    tr_mv[it] = moves;
+    tr_t[it] = gtimer();
+    c->it = it + 1;
+    c->total += (int64_t)moves;
+    bool stop = false;
+    if (moves == 0) {
+        stop = true;
+    } else if (c->have_prev) {
+        const double qp = c->q_prev;
+        const bool conv = fabs(qp) < ZERO_GUARD ? fabs(q_cur - qp) < c->theta
+                                                : fabs(q_cur - qp) / fabs(qp) < c->theta;
+        stop = conv;
+    }
+    if (!stop && it + 1 >= c->max_iters) {
+        c->hit = 1;
+        stop = true;
+    }
+    c->q_prev = q_cur;
+    c->have_prev = 1;
+    cudaGraphSetConditional(h, stop ? 0u : 1u);
+}
+
+// Capture the whole phase: k_run_start, then WHILE (condition) { iteration;
+// k_run_ctl }.  The per-iteration read-back of the single-iteration graph is
+// replaced by the device trace; the host synchronises once per phase.
+static void build_run_graph(Phase &P, int64_t cap, cudaStream_t s) {
+    P.release_run();
+    P.ctl = dalloc<RunCtl>(1);
+    P.tr_q = dalloc<double>(cap);
+    P.tr_mv = dalloc<unsigned long long>(cap);
+    P.tr_t = dalloc<unsigned long long>(cap);
+    P.tr_cap = cap;
+    PLV_CUDA(cudaGraphCreate(&P.rgraph, 0));
+    cudaGraphConditionalHandle h;
+    PLV_CUDA(cudaGraphConditionalHandleCreate(&h, P.rgraph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNode_t start;
+    {
+        cudaKernelNodeParams kp = {};
+        void *args[] = {(void *)&P.ctl};
+        kp.func = (void *)k_run_start;
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(1);
+        kp.kernelParams = args;
+        PLV_CUDA(cudaGraphAddKernelNode(&start, P.rgraph, nullptr, 0, &kp));
+        count_launch();
+    }
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t loop;
+    PLV_CUDA(cudaGraphAddNode(&loop, P.rgraph, &start, 1, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    int prio_lo = 0, prio_hi = 0;
+    PLV_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    cudaStream_t cs;
+    PLV_CUDA(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, prio_hi));
+    PLV_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
+    try {
+        PLV_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 2, cs));
+        for (size_t a = 0; a + 1 < P.goff.size(); a++) {
+            if (P.goff[a + 1] == P.goff[a]) continue;
+            record_decide(P, a, cs);
+            record_apply(P, a, cs);
+        }
+        modularity_async(P.w_int, P.a_tot, P.n, P.m, P.q, P.mod_scratch, cs);
+        k_run_ctl<<<1, 1, 0, cs>>>(P.ctl, P.q, P.counters, P.tr_q, P.tr_mv, P.tr_t, h);
+        PLV_LAUNCH_CHECK();
+    } catch (...) {
+        cudaGraph_t g2 = nullptr;
+        cudaStreamEndCapture(cs, &g2);
+        cudaStreamDestroy(cs);
+        throw;
+    }
+    cudaGraph_t got = nullptr;
+    PLV_CUDA(cudaStreamEndCapture(cs, &got));
+    PLV_CUDA(cudaStreamDestroy(cs));
+    PLV_CUDA(cudaGraphInstantiate(&P.rexec, P.rgraph, cudaGraphInstantiateFlagUseNodePriority));
+}
+
+// The phase loop on device: returns false when the loop graph is unavailable
+// (then the caller runs the host loop).
+static bool phase_run_device(Phase &P, double theta, int64_t max_iters, double *q_h,
+                             int64_t *mv_h, double *ms_h, int64_t *res_h, cudaStream_t s) {
+    if (P.world > 1 || P.comm || P.timing || P.run_graph_failed) return false;
+    if (!P.rexec || P.tr_cap < max_iters) {
+        try {
+            build_run_graph(P, max_iters, s);
+        } catch (Fail &) {
+            cudaGetLastError();
+            P.release_run();
+            P.run_graph_failed = true;
+            return false;
+        }
+    }
+    RunCtl c0 = {theta, max_iters, 0, 0, 0, 0.0, 0, 0ull};
+    PLV_CUDA(cudaMemcpyAsync(P.ctl, &c0, sizeof(c0), cudaMemcpyHostToDevice, s));
+    PLV_CUDA(cudaGraphLaunch(P.rexec, s));
+    RunCtl c;
+    PLV_CUDA(cudaMemcpyAsync(&c, P.ctl, sizeof(c), cudaMemcpyDeviceToHost, s));
+    PLV_CUDA(cudaStreamSynchronize(s));
+    const int64_t it = c.it;
+    std::vector<unsigned long long> mv(it), tt(it);
+    PLV_CUDA(cudaMemcpyAsync(q_h, P.tr_q, sizeof(double) * it, cudaMemcpyDeviceToHost, s));
+    PLV_CUDA(cudaMemcpyAsync(mv.data(), P.tr_mv, sizeof(unsigned long long) * it,
+                             cudaMemcpyDeviceToHost, s));
+    PLV_CUDA(cudaMemcpyAsync(tt.data(), P.tr_t, sizeof(unsigned long long) * it,
+                             cudaMemcpyDeviceToHost, s));
+    PLV_CUDA(cudaStreamSynchronize(s));
+    unsigned long long prev = c.t0;
+    for (int64_t i = 0; i < it; i++) {
+        mv_h[i] = (int64_t)mv[i];
+        ms_h[i] = (double)(tt[i] - prev) / 1e6;
+        prev = tt[i];
+    }
+    res_h[0] = it;
+    res_h[1] = c.total;
+    res_h[2] = c.hit;
+    res_h[3] = 1;
+    return true;
+}
+
 
 static bool converged(double q_cur, double q_prev, double theta) {  // PL/engine.py:134-137
     if (fabs(q_prev) < ZERO_GUARD) return fabs(q_cur - q_prev) < theta;
@@ -411,9 +666,10 @@ extern "C" int plv_phase_step(void *handle, int64_t stage, int op, double *q_h, 
     PLV_EXIT
 }
 
-extern "C" int plv_phase_slices(void *handle, int64_t *slices_h) {
+extern "C" int plv_phase_slices(void *handle, int64_t *stage_off_h, int64_t *slices_h) {
     PLV_ENTRY
     plv::Phase *P = (plv::Phase *)handle;
+    memcpy(stage_off_h, P->goff.data(), sizeof(int64_t) * P->goff.size());
     memcpy(slices_h, P->slo.data(), sizeof(int64_t) * P->slo.size());
     PLV_EXIT
 }
@@ -431,6 +687,10 @@ extern "C" int plv_phase_run(void *handle, double theta, int64_t max_iters, doub
     PLV_ENTRY
     plv::Phase *P = (plv::Phase *)handle;
     cudaStream_t s = plv::S(stream);
+    if (max_iters < 1) PLV_FAIL(PLV_EINVAL, "max_iters must be >= 1");
+    if (plv::phase_run_device(*P, theta, max_iters, q_trace_h, moves_trace_h, ms_trace_h,
+                              result_h, s))
+        return PLV_OK;
     int64_t it = 0, total = 0, hit = 0;
     bool have_prev = false;
     double q_prev = 0.0, q_cur = 0.0;
@@ -456,6 +716,7 @@ extern "C" int plv_phase_run(void *handle, double theta, int64_t max_iters, doub
     result_h[0] = it;
     result_h[1] = total;
     result_h[2] = hit;
+    result_h[3] = 0;
     PLV_EXIT
 }
 

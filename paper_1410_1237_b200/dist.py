@@ -185,9 +185,19 @@ class PartitionedPhaseEngine:
         self._cand = _lib.i64_host(1)
 
     def slices(self) -> np.ndarray:
+        """Per stage, the W + 1 slice bounds (relative to the stage start)."""
+        return self._stages()[1]
+
+    def engine_stage_off(self) -> np.ndarray:
+        """Stage offsets into the engine's (active-vertex) stage lists."""
+        return self._stages()[0]
+
+    def _stages(self):
+        so = np.empty(self.nstages + 1, np.int64)
         out = np.empty(self.nstages * (self.world + 1), np.int64)
-        self._lib.check(self._lib.lib().phase_slices(self.handle, out.ctypes.data), "slices")
-        return out.reshape(self.nstages, self.world + 1)
+        self._lib.check(self._lib.lib().phase_slices(self.handle, so.ctypes.data,
+                                                     out.ctypes.data), "slices")
+        return so, out.reshape(self.nstages, self.world + 1)
 
     def iterate(self):
         _lib = self._lib
@@ -222,7 +232,7 @@ def stepped_iteration(engines):
     rank (the exchange), apply.  Returns [(q, moves)] per rank."""
     from . import _lib
     sl = [e.slices() for e in engines]
-    off = engines[0].stage_off
+    off = engines[0].engine_stage_off()
     W = len(engines)
     for a in range(engines[0].nstages):
         if off[a + 1] == off[a]:

@@ -62,7 +62,7 @@ def test_virtual_ranks_match_single_gpu(kind, colored, world):
         engines.append(pdist.PartitionedPhaseEngine(g, s, col, r, world))
         states.append(st)
     sl = engines[0].slices()
-    assert (sl[:, 0] == 0).all() and (sl[:, -1] == np.diff(engines[0].stage_off)).all()
+    assert (sl[:, 0] == 0).all() and (sl[:, -1] == np.diff(engines[0].engine_stage_off())).all()
     for _ in range(3):
         q1, m1, _ = ref.iterate()
         outs = pdist.stepped_iteration(engines)

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_phase_loop.py tests/test_partitioned.py tests/test_gpu_parity.py -x -q > gpurun_out/loop_tests.log 2>&1; echo "rc=$?" >> gpurun_out/loop_tests.log
+timeout 600 python tools/run_trace.py c3_grid --repeat 2 > gpurun_out/rt_c3.txt 2>&1
+timeout 600 python tools/run_trace.py c4_chung_lu --repeat 1 > gpurun_out/rt_c4.txt 2>&1
+timeout 300 python tools/run_trace.py c2_rmat20 --repeat 2 > gpurun_out/rt_c2.txt 2>&1
