@@ -17,6 +17,38 @@ void set_error(const char *fmt, ...) {
     va_end(ap);
 }
 
+static thread_local cudaStream_t g_alloc_stream[64] = {};
+
+static void pool_setup(int dev) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = 64ull << 30;  // keep up to 64 GB mapped between phases
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+}
+
+static cudaStream_t alloc_stream() {
+    int dev = 0;
+    PLV_CUDA(cudaGetDevice(&dev));
+    if (!g_alloc_stream[dev & 63])
+        PLV_CUDA(cudaStreamCreateWithFlags(&g_alloc_stream[dev & 63], cudaStreamNonBlocking));
+    return g_alloc_stream[dev & 63];
+}
+
+void *pool_alloc(size_t bytes) {
+    cudaStream_t s = alloc_stream();
+    void *p = nullptr;
+    PLV_CUDA(cudaMallocAsync(&p, bytes ? bytes : 1, s));
+    PLV_CUDA(cudaStreamSynchronize(s));
+    return p;
+}
+
+void pool_free(void *p) {
+    if (!p) return;
+    if (cudaFreeAsync(p, alloc_stream()) != cudaSuccess) cudaGetLastError();
+}
+
 void check_device() {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -34,6 +66,11 @@ void check_device() {
         set_error("libplv is built for sm_100a; device %d has compute capability major %d", dev,
                   major);
         throw Fail{PLV_ENODEV};
+    }
+    static int pooled[64] = {};
+    if (!pooled[dev & 63]) {
+        pool_setup(dev);
+        pooled[dev & 63] = 1;
     }
     checked_dev = dev;
 }

@@ -16,6 +16,7 @@
 // Stages of colour classes with <= 2048 vertices run steps 1-3 in one CTA.
 #include "localmove.cuh"
 #include "csr.cuh"
+#include "pairwise.cuh"
 #include <cub/cub.cuh>
 
 namespace plv {
@@ -93,7 +94,11 @@ __global__ void __launch_bounds__(256) k_stage_big(StageArgs A) {
 // One block per huge mover (> APPLY_HUGE entries): the row's entries whose
 // live community is a or b are compacted in order (block scan), then thread 0
 // folds them -- the chain is only the matching entries, the scan is parallel.
-constexpr int64_t APPLY_HUGE = 2048;
+constexpr int64_t APPLY_HUGE = 128;
+// Movers with longer rows fold their live e_a / e_b with a whole warp: a
+// thread's fold is a chain of dependent loads per entry (neighbour, position,
+// live community), a warp's is one round per 32 entries.
+constexpr int64_t APPLY_THREAD_MAX = 8;
 
 __global__ void __launch_bounds__(256) k_stage_huge(StageArgs A) {
     typedef cub::BlockScan<int, 256> Scan;
@@ -174,16 +179,28 @@ __global__ void __launch_bounds__(256) k_stage_prep(StageArgs A) {
                 e_b = A.e_best[x];
             } else {
                 int64_t e0 = A.off[i], e1 = A.off[i + 1];
-                big = (e1 - e0) > 32;
+                const int deg = (int)(e1 - e0);
+                big = deg > APPLY_THREAD_MAX;
                 if (!big) {
-                    for (int64_t e = e0; e < e1; e++) {
-                        int32_t j = A.nbr[e];
-                        if (j == i) continue;
-                        int32_t c = live_comm(A, j, x);
-                        if (c == a)
-                            e_a = dadd(e_a, A.wts[e]);
-                        else if (c == b)
-                            e_b = dadd(e_b, A.wts[e]);
+                    // every load of a level in flight together (row, then
+                    // positions, then live communities); the fold stays in order
+                    int32_t jj[APPLY_THREAD_MAX], cc[APPLY_THREAD_MAX];
+                    double ww[APPLY_THREAD_MAX];
+#pragma unroll
+                    for (int t = 0; t < APPLY_THREAD_MAX; t++) {
+                        jj[t] = t < deg ? A.nbr[e0 + t] : i;
+                        ww[t] = t < deg ? A.wts[e0 + t] : 0.0;
+                    }
+#pragma unroll
+                    for (int t = 0; t < APPLY_THREAD_MAX; t++)
+                        cc[t] = jj[t] != i ? live_comm(A, jj[t], x) : -1;
+#pragma unroll
+                    for (int t = 0; t < APPLY_THREAD_MAX; t++) {
+                        if (cc[t] < 0) continue;
+                        if (cc[t] == a)
+                            e_a = dadd(e_a, ww[t]);
+                        else if (cc[t] == b)
+                            e_b = dadd(e_b, ww[t]);
                     }
                 }
             }
@@ -197,6 +214,10 @@ __global__ void __launch_bounds__(256) k_stage_prep(StageArgs A) {
                 A.big[atomicAdd(A.nbig, 1ull)] = (int32_t)x;
         }
         if (mover && !big) mover_deltas(A, x, i, a, b, e_a, e_b, integral);
+        if (mover && A.dirty) {
+            A.dirty[pw_node_of(A.tree_n, A.tree_d0, a)] = 1;
+            A.dirty[pw_node_of(A.tree_n, A.tree_d0, b)] = 1;
+        }
         // independent stages: no stage vertex reads another's assignment, so
         // the scatter can happen here
         if (indep && mover) A.assign[i] = b;
@@ -505,7 +526,7 @@ void ApplyBuffers::alloc(int64_t ta_len, int64_t max_ns, int64_t n, cudaStream_t
     lcnt = dalloc<unsigned long long>(1);
     nb = bits_for(n + 1);  // SENTINEL's low nb bits exceed every community id
     PLV_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, ekey, ekey2, eval, eval2, ne, 0, nb, s));
-    PLV_CUDA(cudaMalloc(&tmp, bytes ? bytes : 1));
+    tmp = pool_alloc(bytes);
     static int dev_done = -1;
     int dev;
     PLV_CUDA(cudaGetDevice(&dev));
@@ -518,9 +539,10 @@ void ApplyBuffers::alloc(int64_t ta_len, int64_t max_ns, int64_t n, cudaStream_t
 }
 
 void ApplyBuffers::release() {
+    cudaDeviceSynchronize();  // buffers go back to the pool idle
     void *ps[] = {ta, tb, ekey, ekey2, eval, eval2, tmp, dW, dA, lrun, lcnt, big, nbig};
     for (void *p : ps)
-        if (p) cudaFree(p);
+        pool_free(p);
     big = nullptr;
     nbig = nullptr;
     dW = dA = nullptr;
@@ -565,7 +587,7 @@ void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {
     if (!indep) {
         k_stage_big<<<148 * 8, 256, 0, st>>>(S);
         PLV_LAUNCH_CHECK();
-        k_stage_huge<<<148 * 2, 256, 0, st>>>(S);
+        k_stage_huge<<<148 * 4, 256, 0, st>>>(S);
         PLV_LAUNCH_CHECK();
     }
     if (!integral) {

@@ -65,6 +65,15 @@ void count_launch();
 
 inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Long-lived device buffers (phase plans, engine state) come from the
+// device's default memory pool, which keeps freed memory mapped (release
+// threshold raised at first use of a device, api_util.cu): phases allocate
+// and free hundreds of MB each, and cudaMalloc / cudaFree of fresh pages
+// cost milliseconds and synchronise the device.  pool_free needs the buffer
+// idle (callers synchronise first).
+void *pool_alloc(size_t bytes);
+void pool_free(void *p);
+
 // Stream-ordered scratch buffer (cudaMallocAsync pool); freed on scope exit.
 template <class T>
 struct Buf {

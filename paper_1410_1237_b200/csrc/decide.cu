@@ -396,20 +396,26 @@ __global__ void __launch_bounds__(T1_WARPS * 32) k_decide_t1(DecideArgs A, TierR
             vals[s] = 0.0;
         }
         __syncwarp();
-        for (int64_t base = e0; base < e1; base += 32) {
-            int64_t e = base + lane;
-            int32_t c = -1;
-            double w = 0.0;
-            if (e < e1) {
-                int32_t j = A.nbr[e];
-                if (j != i) {
-                    c = A.assign[j];
-                    w = A.wts[e];
-                }
-            }
-            wb[lane] = w;
+        // all (<= 4) chunks' loads first -- rows, then communities -- so the
+        // warp waits for two round trips, not two per chunk; then the chunks
+        // fold in adjacency order
+        constexpr int NCH = (T1_MAXD + 31) / 32;
+        int32_t jv[NCH], cv[NCH];
+        double wv[NCH];
+#pragma unroll
+        for (int u = 0; u < NCH; u++) {
+            const int64_t e = e0 + 32 * u + lane;
+            jv[u] = e < e1 ? A.nbr[e] : i;
+            wv[u] = e < e1 ? A.wts[e] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < NCH; u++) cv[u] = jv[u] != i ? A.assign[jv[u]] : -1;
+#pragma unroll
+        for (int u = 0; u < NCH; u++) {
+            if (e0 + 32 * u >= e1) break;
+            wb[lane] = cv[u] >= 0 ? wv[u] : 0.0;
             __syncwarp();
-            fold_chunk(keys, vals, PowTab{mask}, c, wb, lane);
+            fold_chunk(keys, vals, PowTab{mask}, cv[u], wb, lane);
             __syncwarp();
         }
         double e_old = 0.0;
@@ -1351,11 +1357,12 @@ __global__ void k_fill_i32_d(int32_t *p, int64_t n, int32_t v) {
 }
 
 void Plan::release() {
+    cudaDeviceSynchronize();  // buffers go back to the pool idle
     void *ps[] = {tier_list, tier_vid, tier_row, tier_end, hub_eoff, hub_toff, hub_poff, hub_blk, hub_row, hub_vid, hkeys,
                   hvals,     hcnt,     hsold,    hncnt,    hnear,   hpart,
                   dval,      dcnt,     dmk,      cbuf};
     for (void *p : ps)
-        if (p) cudaFree(p);
+        pool_free(p);
     tier_list = nullptr;
     tier_vid = nullptr;
     tier_row = tier_end = nullptr;

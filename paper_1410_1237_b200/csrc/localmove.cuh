@@ -145,6 +145,11 @@ struct StageArgs {
     unsigned long long *nbig = nullptr;
     int32_t *huge = nullptr;  // huge movers (live folds by whole blocks)
     unsigned long long *nhuge = nullptr;
+    // incremental modularity (pairwise.cuh): mark the depth-d0 tree nodes of
+    // both communities of every mover (nullptr: off)
+    uint8_t *dirty = nullptr;
+    int64_t tree_n = 0;
+    int tree_d0 = 0;
 };
 
 // Event / sort scratch for stages of up to max_ns vertices.
@@ -171,7 +176,7 @@ void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st);
 template <class T>
 T *dalloc(size_t count) {
     T *p = nullptr;
-    PLV_CUDA(cudaMalloc((void **)&p, sizeof(T) * (count ? count : 1)));
+    p = (T *)pool_alloc(sizeof(T) * (count ? count : 1));
     return p;
 }
 

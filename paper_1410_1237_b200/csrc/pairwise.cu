@@ -17,18 +17,37 @@ namespace plv {
 // order -- then the tail added by the octet's first lane.
 template <class F>
 __device__ __forceinline__ double pw_leaf_octet(const double *a, int64_t n, F f, int k) {
+    // n <= 128: lane k's accumulator takes elements k, k+8, ... (< lim); all
+    // of its loads are issued before the first addition (independent of the
+    // chain), then the additions run in numpy's order
     double r = 0.0;
     const int64_t lim = n >= 8 ? n - (n % 8) : 0;
+    double buf[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+        const int64_t i = k + 8 * u;
+        buf[u] = i < lim ? a[i] : 0.0;
+    }
+    double tail[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+        const int64_t i = lim + u;
+        tail[u] = (k == 0 && i < n) ? a[i] : 0.0;
+    }
     if (lim) {
-        r = f(a[k]);
-        for (int64_t i = 8 + k; i < lim; i += 8) r = __dadd_rn(r, f(a[i]));
+        r = f(buf[0]);
+#pragma unroll
+        for (int u = 1; u < 16; u++)
+            if (k + 8 * u < lim) r = __dadd_rn(r, f(buf[u]));
     }
     double t = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
     t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 2));
     t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 4));
     if (k == 0) {
         double res = lim ? t : 0.0;
-        for (int64_t i = lim; i < n; i++) res = __dadd_rn(res, f(a[i]));
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+            if (lim + u < n) res = __dadd_rn(res, f(tail[u]));
         t = res;
     }
     return t;  // valid in the octet's first lane
@@ -156,6 +175,7 @@ __global__ void k_mod_finish(const double *sw, const double *sq, double two_m, d
 // itself, so the scratch needs zeroing once (modularity_scratch_init).
 constexpr int64_t MODF_MAX_NODES = 8192;
 constexpr int MODF_THREADS = 512;
+constexpr unsigned FULLW = 0xffffffffu;
 
 template <class F>
 __device__ __forceinline__ double pw_node_warp(const double *a, int64_t n, int d0, uint64_t t,
@@ -192,16 +212,20 @@ __global__ void __launch_bounds__(MODF_THREADS) k_mod_fused(const double *__rest
                                                             const double *__restrict__ a_tot,
                                                             int64_t n, int d0, double two_m,
                                                             double *vals, unsigned int *ticket,
-                                                            double *out) {
-    extern __shared__ double sm[];  // 2 * cnt
+                                                            double *out, uint8_t *dirty,
+                                                            const int64_t *full_if_zero) {
+    __shared__ double sA[2 * MODF_MAX_NODES / 32], sB[2 * MODF_MAX_NODES / 32 / 32 + 2];
     __shared__ bool s_last;
     const uint64_t cnt = 1ull << d0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const bool full = !dirty || *full_if_zero == 0;
     for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < 2 * cnt;
          t += nw) {
+        if (!full && !dirty[t < cnt ? t : t - cnt]) continue;  // value kept from last call
         const double v = t < cnt ? pw_node_warp(w_int, n, d0, t, Ident{})
                                  : pw_node_warp(a_tot, n, d0, t - cnt, SqScaled{two_m});
-        if ((threadIdx.x & 31) == 0) vals[t] = v;
+        if (lane == 0) vals[t] = v;
     }
     __threadfence();
     __syncthreads();
@@ -209,27 +233,35 @@ __global__ void __launch_bounds__(MODF_THREADS) k_mod_fused(const double *__rest
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    for (uint64_t i = threadIdx.x; i < 2 * cnt; i += blockDim.x) sm[i] = __ldcg(vals + i);
-    __syncthreads();
-    // both perfect trees level by level: pair (2i, 2i+1) of each half
-    for (uint64_t width = cnt; width > 1; width >>= 1) {
-        const uint64_t half = width >> 1;
-        double r[2 * MODF_MAX_NODES / MODF_THREADS];
-        int c = 0;
-        for (uint64_t i = threadIdx.x; i < 2 * half; i += blockDim.x) {
-            const uint64_t h = i / half, j = i % half;
-            r[c++] = __dadd_rn(sm[h * cnt + 2 * j], sm[h * cnt + 2 * j + 1]);
+    // The two perfect top trees (cnt leaves each), 32 consecutive values per
+    // warp and round: xor-butterflies add (2i, 2i+1), then pairs of those, ...
+    // -- the tree's own additions (lane 0 always holds the left operand).
+    const double *src = vals;
+    double *dst = sA;
+    bool global_src = true;
+    uint64_t w = cnt;
+    while (w > 1) {
+        const uint64_t g = w < 32 ? w : 32, gpa = w / g;
+        for (uint64_t gi = warp; gi < 2 * gpa; gi += nwarps) {
+            const uint64_t h = gi >= gpa ? 1 : 0, k = gi - h * gpa;
+            const uint64_t idx = h * w + k * g + lane;
+            double v = 0.0;
+            if ((uint64_t)lane < g) v = global_src ? __ldcg(src + idx) : src[idx];
+            for (uint64_t o = 1; o < g; o <<= 1) v = __dadd_rn(v, __shfl_xor_sync(FULLW, v, (int)o));
+            if (lane == 0) dst[h * gpa + k] = v;
         }
         __syncthreads();
-        c = 0;
-        for (uint64_t i = threadIdx.x; i < 2 * half; i += blockDim.x) {
-            const uint64_t h = i / half, j = i % half;
-            sm[h * cnt + j] = r[c++];
-        }
-        __syncthreads();
+        w = gpa;
+        src = dst;
+        global_src = false;
+        dst = dst == sA ? sB : sA;
     }
+    if (dirty)
+        for (uint64_t t = threadIdx.x; t < cnt; t += blockDim.x) dirty[t] = 0;
     if (threadIdx.x == 0) {
-        const double sw = __dadd_rn(0.0, sm[0]), sq = __dadd_rn(0.0, sm[cnt]);
+        const double r0 = global_src ? __ldcg(src) : src[0];
+        const double r1 = global_src ? __ldcg(src + 1) : src[1];
+        const double sw = __dadd_rn(0.0, r0), sq = __dadd_rn(0.0, r1);
         out[0] = __dsub_rn(__ddiv_rn(sw, two_m), sq);
         *ticket = 0u;
     }
@@ -250,18 +282,8 @@ void modularity_async(const double *w_int, const double *a_tot, int64_t n, doubl
         const int d0 = pw_depth(n);
         const int64_t cnt = 1ll << d0;
         if (cnt <= MODF_MAX_NODES) {
-            static int attr_dev = -1;
-            int dev;
-            PLV_CUDA(cudaGetDevice(&dev));
-            if (attr_dev != dev) {
-                PLV_CUDA(cudaFuncSetAttribute(k_mod_fused,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)(2 * MODF_MAX_NODES * sizeof(double))));
-                attr_dev = dev;
-            }
-            k_mod_fused<<<grid_for(2 * cnt * 32, MODF_THREADS, 148 * 4), MODF_THREADS,
-                          2 * cnt * sizeof(double), s>>>(w_int, a_tot, n, d0, two_m, scratch,
-                                                         ticket, out);
+            k_mod_fused<<<grid_for(2 * cnt * 32, MODF_THREADS, 148 * 8), MODF_THREADS, 0, s>>>(
+                w_int, a_tot, n, d0, two_m, scratch, ticket, out, nullptr, nullptr);
             PLV_LAUNCH_CHECK();
             return;
         }
@@ -271,6 +293,24 @@ void modularity_async(const double *w_int, const double *a_tot, int64_t n, doubl
     pw_launch(w_int, n, tmp, s, Ident{}, scratch);
     pw_launch(a_tot, n, tmp + 1, s, SqScaled{two_m}, scratch + ps);
     k_mod_finish<<<1, 1, 0, s>>>(tmp, tmp + 1, two_m, out);
+    PLV_LAUNCH_CHECK();
+}
+
+bool modularity_inc_supported(int64_t n, int *d0) {
+    if (n <= 0) return false;
+    *d0 = pw_depth(n);
+    return (1ll << *d0) <= MODF_MAX_NODES;
+}
+
+void modularity_async_inc(const double *w_int, const double *a_tot, int64_t n, double m,
+                          double *out, double *scratch, uint8_t *dirty,
+                          const int64_t *full_if_zero, cudaStream_t s) {
+    int d0 = 0;
+    if (!modularity_inc_supported(n, &d0)) PLV_FAIL(PLV_EINVAL, "incremental modularity: tree too large");
+    const int64_t cnt = 1ll << d0;
+    k_mod_fused<<<grid_for(2 * cnt * 32, MODF_THREADS, 148 * 8), MODF_THREADS, 0, s>>>(
+        w_int, a_tot, n, d0, 2.0 * m, scratch + 2, (unsigned int *)scratch, out, dirty,
+        full_if_zero);
     PLV_LAUNCH_CHECK();
 }
 

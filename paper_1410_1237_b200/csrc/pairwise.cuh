@@ -120,6 +120,23 @@ __host__ __device__ __forceinline__ void pw_node(int64_t n, int d, uint64_t path
     *len = s;
 }
 
+// Index of the depth-d node of the tree of n that holds element c.
+__host__ __device__ __forceinline__ uint64_t pw_node_of(int64_t n, int d, int64_t c) {
+    int64_t o = 0, s = n;
+    uint64_t path = 0;
+    for (int b = d - 1; b >= 0; b--) {
+        const int64_t n2 = pw_split(s);
+        if (c - o >= n2) {
+            o += n2;
+            s -= n2;
+            path |= 1ull << b;
+        } else {
+            s = n2;
+        }
+    }
+    return path;
+}
+
 // Smallest depth at which every node of the tree of n has <= `cap` elements
 // (cap >= 256 guarantees no leaf sits above that depth, so the top of the
 // tree is a perfect binary tree of 2^d nodes).
@@ -163,6 +180,15 @@ void modularity_scratch_init(double *scratch, cudaStream_t s);
 // q = pairwise(w_int)/2m - pairwise((a_tot/2m)^2); scratch: modularity_scratch_doubles(n).
 void modularity_async(const double *w_int, const double *a_tot, int64_t n, double m, double *out,
                       double *scratch, cudaStream_t s);
+// Incremental variant (same bits): only the depth-d0 nodes flagged in
+// `dirty` (cnt bytes, cleared here) are recomputed, the others keep their
+// value from the previous call on the same scratch -- unless *full_if_zero
+// is 0 (the first iteration of a device loop), then all are.  Returns false
+// (nothing launched) when the tree is too large for the one-launch kernel.
+bool modularity_inc_supported(int64_t n, int *d0);
+void modularity_async_inc(const double *w_int, const double *a_tot, int64_t n, double m,
+                          double *out, double *scratch, uint8_t *dirty,
+                          const int64_t *full_if_zero, cudaStream_t s);
 void reduceat_async(const double *w, const int64_t *starts, int64_t M, int64_t R, double *out,
                     cudaStream_t s);
 

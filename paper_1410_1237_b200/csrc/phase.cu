@@ -86,16 +86,20 @@ struct Phase {
     unsigned long long *tr_mv = nullptr, *tr_t = nullptr;
     int64_t tr_cap = 0;
     bool run_graph_failed = false;
+    uint8_t *dirty = nullptr;  // incremental modularity in the device loop (one stage)
+    int mod_d0 = 0;
 
     void release_run() {
+        cudaDeviceSynchronize();  // buffers go back to the pool idle
         if (rexec) cudaGraphExecDestroy(rexec);
         if (rgraph) cudaGraphDestroy(rgraph);
         rexec = nullptr;
         rgraph = nullptr;
-        void *pr[] = {ctl, tr_q, tr_mv, tr_t};
+        void *pr[] = {ctl, tr_q, tr_mv, tr_t, dirty};
         for (void *p : pr)
-            if (p) cudaFree(p);
+            pool_free(p);
         ctl = nullptr;
+        dirty = nullptr;
         tr_q = nullptr;
         tr_mv = tr_t = nullptr;
         tr_cap = 0;
@@ -120,11 +124,11 @@ struct Phase {
         ab.release();
         void *ps[] = {counters, q, mod_scratch, lvtx, fvtx, pos};
         for (void *p : ps)
-            if (p) cudaFree(p);
+            pool_free(p);
         if (own_out) {
             void *po[] = {target, moved, e_old, e_best};
             for (void *p : po)
-                if (p) cudaFree(p);
+                pool_free(p);
         }
         lvtx = fvtx = pos = nullptr;
         target = nullptr;
@@ -174,12 +178,15 @@ static void record_exchange(Phase &P, size_t a, cudaStream_t st) {
 }
 
 // Stage a's exact apply over the whole stage (replicated on every rank).
-static void record_apply(Phase &P, size_t a, cudaStream_t st) {
+static void record_apply(Phase &P, size_t a, cudaStream_t st, uint8_t *dirty = nullptr) {
     const int64_t g = P.goff[a], ns = P.goff[a + 1] - g;
     StageArgs S{P.off, P.nbr, P.wts, P.k, P.selfw, P.vtx + g, ns, P.target + g,
                 P.moved + g, P.e_old + g, P.e_best + g, P.pos, P.flags,
                 P.assign, P.a_tot, P.w_int, P.sizes, P.ab.ta + g, P.ab.tb + g,
                 nullptr, nullptr, P.counters};
+    S.dirty = dirty;
+    S.tree_n = P.n;
+    S.tree_d0 = P.mod_d0;
     launch_apply(S, P.ab, st);
 }
 
@@ -336,7 +343,7 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
         if (world == 1) {
             for (int64_t a = 0; a < nst; a++) P->slo[2 * a + 1] = stage_off_h[a + 1] - stage_off_h[a];
             loff = P->goff;
-            PLV_CUDA(cudaMalloc((void **)&P->lvtx, sizeof(int32_t) * (total ? total : 1)));
+            P->lvtx = dalloc<int32_t>(total);
             if (total)
                 PLV_CUDA(cudaMemcpyAsync(P->lvtx, vtx, sizeof(int32_t) * total,
                                          cudaMemcpyDeviceToDevice, s));
@@ -359,7 +366,7 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
                 const int64_t *sl = P->slo.data() + a * (world + 1);
                 loff[a + 1] = loff[a] + (sl[rank + 1] - sl[rank]);
             }
-            PLV_CUDA(cudaMalloc((void **)&P->lvtx, sizeof(int32_t) * (loff[nst] ? loff[nst] : 1)));
+            P->lvtx = dalloc<int32_t>(loff[nst]);
             for (int64_t a = 0; a < nst; a++) {
                 const int64_t c = loff[a + 1] - loff[a];
                 if (c)
@@ -497,6 +504,16 @@ static void build_run_graph(Phase &P, int64_t cap, cudaStream_t s) {
     P.tr_mv = dalloc<unsigned long long>(cap);
     P.tr_t = dalloc<unsigned long long>(cap);
     P.tr_cap = cap;
+    // one uncoloured stage (the long, capped phases): the apply marks the tree
+    // nodes its movers touch and Q recomputes only those (full on iteration 0);
+    // the apply of a one-stage phase always runs k_stage_prep (non-independent)
+    int64_t nonempty = 0;
+    for (size_t a = 0; a + 1 < P.goff.size(); a++) nonempty += P.goff[a + 1] > P.goff[a];
+    if (nonempty == 1 && !(P.flags & PLV_F_INDEPENDENT) &&
+        modularity_inc_supported(P.n, &P.mod_d0)) {
+        P.dirty = dalloc<uint8_t>((size_t)1 << P.mod_d0);
+        PLV_CUDA(cudaMemsetAsync(P.dirty, 0, (size_t)1 << P.mod_d0, s));
+    }
     PLV_CUDA(cudaGraphCreate(&P.rgraph, 0));
     cudaGraphConditionalHandle h;
     PLV_CUDA(cudaGraphConditionalHandleCreate(&h, P.rgraph, 1, cudaGraphCondAssignDefault));
@@ -530,9 +547,13 @@ static void build_run_graph(Phase &P, int64_t cap, cudaStream_t s) {
         for (size_t a = 0; a + 1 < P.goff.size(); a++) {
             if (P.goff[a + 1] == P.goff[a]) continue;
             record_decide(P, a, cs);
-            record_apply(P, a, cs);
+            record_apply(P, a, cs, P.dirty);
         }
-        modularity_async(P.w_int, P.a_tot, P.n, P.m, P.q, P.mod_scratch, cs);
+        if (P.dirty)
+            modularity_async_inc(P.w_int, P.a_tot, P.n, P.m, P.q, P.mod_scratch, P.dirty,
+                                 &P.ctl->it, cs);
+        else
+            modularity_async(P.w_int, P.a_tot, P.n, P.m, P.q, P.mod_scratch, cs);
         k_run_ctl<<<1, 1, 0, cs>>>(P.ctl, P.q, P.counters, P.tr_q, P.tr_mv, P.tr_t, h);
         PLV_LAUNCH_CHECK();
     } catch (...) {

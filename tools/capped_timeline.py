@@ -59,7 +59,7 @@ t0 = time.perf_counter()
 for _ in range(100):
     eng.iterate()
 t1 = time.perf_counter()
-print(f"host wall per iteration {(t1 - t0) * 10:.1f} us; moves last warm iters {mv[-6:]}")
+print(f"host wall per iteration {(t1 - t0) * 1e4:.1f} us; moves last warm iters {mv[-6:]}")
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(a.iters):
         eng.iterate()
