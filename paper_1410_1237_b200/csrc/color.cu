@@ -12,8 +12,9 @@
 // "used" mask per window of 64 colours.  Higher-degree vertices are pushed to
 // a worklist and handled one block each: the block marks the colours of the
 // row in a shared-memory bitmap (windows of 4096 colours) and finds the first
-// free bit, or scans the lower-id prefix of the row for a clash.  No host
-// synchronisation inside a round except the rejected count.
+// free bit, or scans the lower-id prefix of the row for a clash.  The round
+// loop runs on the device (a CUDA graph WHILE node, see color()): no host
+// synchronisation until the colouring is complete.
 #include "common.cuh"
 #include "csr.cuh"
 #include <cub/cub.cuh>
@@ -24,6 +25,24 @@ constexpr int COLOR_THREAD_MAXD = 32;
 constexpr int CB = 256;             // threads per block, big-vertex kernels
 constexpr int CWIN = 4096;          // colours per bitmap window
 constexpr int CBIG_GRID = 148 * 4;  // blocks of the big-vertex kernels
+
+// The active list of a round: a host-driven call passes (a0, na); the device
+// loop passes both ping-pong buffers and its control words (ctl[0] = active
+// count, ctl[1] = rounds done: round r reads buffer r & 1, writes the other).
+struct ActiveRef {
+    const int32_t *a0, *a1;
+    const int64_t *ctl;
+    int64_t na;
+    __device__ __forceinline__ const int32_t *act() const {
+        return ctl ? ((ctl[1] & 1) ? a1 : a0) : a0;
+    }
+    __device__ __forceinline__ int32_t *next() const {
+        return const_cast<int32_t *>((ctl[1] & 1) ? a0 : a1);
+    }
+    __device__ __forceinline__ int64_t count() const { return ctl ? ctl[0] : na; }
+};
+
+inline ActiveRef host_active(const int32_t *a, int64_t na) { return ActiveRef{a, nullptr, nullptr, na}; }
 
 __device__ __forceinline__ int first_free_thread(const int64_t *off, const int32_t *nbr,
                                                  const int32_t *colors, int32_t i) {
@@ -44,10 +63,12 @@ __device__ __forceinline__ int first_free_thread(const int64_t *off, const int32
 // (one block each) or, above CHUGE entries, to `huge` (split over blocks).
 constexpr int64_t CHUGE = 4096;
 
-__global__ void k_color_assign_small(const int64_t *off, const int32_t *nbr,
-                                     const int32_t *active, int64_t na, const int32_t *colors,
-                                     int32_t *out, int32_t *big, unsigned long long *nbig,
-                                     int32_t *huge, unsigned long long *nhuge) {
+__global__ void k_color_assign_small(const int64_t *off, const int32_t *nbr, ActiveRef R,
+                                     const int32_t *colors, int32_t *out, int32_t *big,
+                                     unsigned long long *nbig, int32_t *huge,
+                                     unsigned long long *nhuge) {
+    const int32_t *active = R.act();
+    const int64_t na = R.count();
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < na;
          x += (int64_t)gridDim.x * blockDim.x) {
         int32_t i = active[x];
@@ -64,15 +85,17 @@ __global__ void k_color_assign_small(const int64_t *off, const int32_t *nbr,
 // Huge rows: block (q, chunk) ORs the colours of CHUGE entries into the
 // global bitmap of huge item q (first window of CWIN colours).
 __global__ void __launch_bounds__(CB) k_color_assign_huge(const int64_t *off, const int32_t *nbr,
-                                                          const int32_t *active,
+                                                          ActiveRef R,
                                                           const int32_t *colors,
                                                           const int32_t *huge,
                                                           const unsigned long long *nhuge,
-                                                          uint32_t *hbits) {
-    const int64_t cnt = (int64_t)*nhuge;
-    for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
+                                                          uint32_t *hbits, int64_t chunks) {
+    const int32_t *active = R.act();
+    const int64_t cnt = (int64_t)*nhuge * chunks;  // (item, chunk) pairs
+    for (int64_t w = blockIdx.x; w < cnt; w += gridDim.x) {
+        const int64_t q = w / chunks, ch = w % chunks;
         int32_t i = active[huge[q]];
-        int64_t e0 = off[i] + (int64_t)blockIdx.y * CHUGE, e1 = off[i + 1];
+        int64_t e0 = off[i] + ch * CHUGE, e1 = off[i + 1];
         int64_t ee = e0 + CHUGE < e1 ? e0 + CHUGE : e1;
         uint32_t *bits = hbits + q * (CWIN / 32);
         for (int64_t e = e0 + threadIdx.x; e < ee; e += CB) {
@@ -87,12 +110,13 @@ __global__ void __launch_bounds__(CB) k_color_assign_huge(const int64_t *off, co
 // First free colour of every huge item from its bitmap (block per item); a
 // row whose first CWIN colours are all taken falls back to windowed scans.
 __global__ void __launch_bounds__(CB) k_color_huge_final(const int64_t *off, const int32_t *nbr,
-                                                         const int32_t *active,
+                                                         ActiveRef R,
                                                          const int32_t *colors,
                                                          const int32_t *huge,
                                                          const unsigned long long *nhuge,
                                                          const uint32_t *hbits, int32_t *out,
                                                          uint8_t *keep) {
+    const int32_t *active = R.act();
     __shared__ uint32_t bits[CWIN / 32];
     __shared__ int s_found;
     const int tid = threadIdx.x;
@@ -138,17 +162,19 @@ __global__ void __launch_bounds__(CB) k_color_huge_final(const int64_t *off, con
 // Huge rows: block (q, chunk) scans its entries of the j < i prefix.
 __global__ void __launch_bounds__(CB) k_color_conflicts_huge(const int64_t *off,
                                                              const int32_t *nbr,
-                                                             const int32_t *active,
+                                                             ActiveRef R,
                                                              const int32_t *colors,
                                                              const int32_t *huge,
                                                              const unsigned long long *nhuge,
-                                                             uint8_t *keep) {
-    const int64_t cnt = (int64_t)*nhuge;
-    for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
+                                                             uint8_t *keep, int64_t chunks) {
+    const int32_t *active = R.act();
+    const int64_t cnt = (int64_t)*nhuge * chunks;  // (item, chunk) pairs
+    for (int64_t w = blockIdx.x; w < cnt; w += gridDim.x) {
+        const int64_t q = w / chunks, ch = w % chunks;
         int64_t x = huge[q];
         int32_t i = active[x];
         int32_t ci = colors[i];
-        int64_t e0 = off[i] + (int64_t)blockIdx.y * CHUGE, e1 = off[i + 1];
+        int64_t e0 = off[i] + ch * CHUGE, e1 = off[i + 1];
         int64_t ee = e0 + CHUGE < e1 ? e0 + CHUGE : e1;
         bool clash = false;
         for (int64_t e = e0 + threadIdx.x; e < ee; e += CB) {
@@ -161,9 +187,10 @@ __global__ void __launch_bounds__(CB) k_color_conflicts_huge(const int64_t *off,
 
 // One block per high-degree active vertex: bitmap of neighbour colours.
 __global__ void __launch_bounds__(CB) k_color_assign_big(const int64_t *off, const int32_t *nbr,
-                                                         const int32_t *active, const int32_t *colors,
+                                                         ActiveRef R, const int32_t *colors,
                                                          int32_t *out, const int32_t *big,
                                                          const unsigned long long *nbig) {
+    const int32_t *active = R.act();
     __shared__ uint32_t bits[CWIN / 32];
     __shared__ int s_found;
     const int tid = threadIdx.x;
@@ -199,9 +226,10 @@ __global__ void __launch_bounds__(CB) k_color_assign_big(const int64_t *off, con
 }
 
 // keep[x] = no lower-id neighbour shares colors[active[x]] (low degree).
-__global__ void k_color_conflicts_small(const int64_t *off, const int32_t *nbr,
-                                        const int32_t *active, int64_t na, const int32_t *colors,
-                                        uint8_t *keep) {
+__global__ void k_color_conflicts_small(const int64_t *off, const int32_t *nbr, ActiveRef R,
+                                        const int32_t *colors, uint8_t *keep) {
+    const int32_t *active = R.act();
+    const int64_t na = R.count();
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < na;
          x += (int64_t)gridDim.x * blockDim.x) {
         int32_t i = active[x];
@@ -222,10 +250,11 @@ __global__ void k_color_conflicts_small(const int64_t *off, const int32_t *nbr,
 }
 
 __global__ void __launch_bounds__(CB) k_color_conflicts_big(const int64_t *off, const int32_t *nbr,
-                                                            const int32_t *active,
+                                                            ActiveRef R,
                                                             const int32_t *colors, uint8_t *keep,
                                                             const int32_t *big,
                                                             const unsigned long long *nbig) {
+    const int32_t *active = R.act();
     const int tid = threadIdx.x;
     const int64_t cnt = (int64_t)*nbig;
     for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
@@ -268,23 +297,12 @@ __global__ void k_color_init(int32_t *colors, int32_t *active, int64_t n) {
     }
 }
 
-__global__ void k_color_commit(const int32_t *active, int64_t na, const int32_t *tent,
-                               int32_t *colors) {
+__global__ void k_color_commit(ActiveRef R, const int32_t *tent, int32_t *colors) {
+    const int32_t *active = R.act();
+    const int64_t na = R.count();
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < na;
          x += (int64_t)gridDim.x * blockDim.x)
         colors[active[x]] = tent[x];
-}
-
-__global__ void k_reject_flags(const uint8_t *keep, int64_t na, uint8_t *rej) {
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < na;
-         x += (int64_t)gridDim.x * blockDim.x)
-        rej[x] = !keep[x];
-}
-
-__global__ void k_uncolor(const int32_t *rejected, int64_t nr, int32_t *colors) {
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nr;
-         x += (int64_t)gridDim.x * blockDim.x)
-        colors[rejected[x]] = -1;
 }
 
 __global__ void k_max_color(const int32_t *colors, int64_t n, int *mx) {
@@ -298,45 +316,131 @@ __global__ void k_max_color(const int32_t *colors, int64_t n, int *mx) {
     if (threadIdx.x == 0) atomicMax(mx, b);
 }
 
-// One speculative round over active[0..na): tentative colours, commit, keep flags.
+// One speculative round over the active list: tentative colours, commit, keep flags.
 struct ColorScratch {
     int32_t *big, *huge;
-    unsigned long long *cnt;  // [0] big, [1] huge
+    unsigned long long *cnt;  // [0] big, [1] huge (zero at the start of a round)
     uint32_t *hbits;          // nhuge_max * CWIN / 32 words
     int64_t nhuge_max;
     unsigned huge_chunks;     // ceil(max_degree / CHUGE)
 };
 
-static void color_round(const int64_t *off, const int32_t *nbr, const int32_t *active, int64_t na,
+static void color_round(const int64_t *off, const int32_t *nbr, ActiveRef R, int64_t na_max,
                         int32_t *colors, int32_t *tent, uint8_t *keep, const ColorScratch &C,
                         cudaStream_t s) {
-    PLV_CUDA(cudaMemsetAsync(C.cnt, 0, 2 * sizeof(unsigned long long), s));
     bool huge = C.nhuge_max > 0;
-    k_color_assign_small<<<grid_for(na, 256), 256, 0, s>>>(
-        off, nbr, active, na, colors, tent, C.big, C.cnt, huge ? C.huge : nullptr, C.cnt + 1);
+    const unsigned g = grid_for(na_max, 256, 148 * 8);
+    k_color_assign_small<<<g, 256, 0, s>>>(off, nbr, R, colors, tent, C.big, C.cnt,
+                                           huge ? C.huge : nullptr, C.cnt + 1);
     PLV_LAUNCH_CHECK();
-    k_color_assign_big<<<CBIG_GRID, CB, 0, s>>>(off, nbr, active, colors, tent, C.big, C.cnt);
+    k_color_assign_big<<<CBIG_GRID, CB, 0, s>>>(off, nbr, R, colors, tent, C.big, C.cnt);
     PLV_LAUNCH_CHECK();
     if (huge) {
         PLV_CUDA(cudaMemsetAsync(C.hbits, 0, sizeof(uint32_t) * C.nhuge_max * (CWIN / 32), s));
-        dim3 g(148, C.huge_chunks);
-        k_color_assign_huge<<<g, CB, 0, s>>>(off, nbr, active, colors, C.huge, C.cnt + 1, C.hbits);
+        k_color_assign_huge<<<148 * C.huge_chunks, CB, 0, s>>>(off, nbr, R, colors, C.huge,
+                                                               C.cnt + 1, C.hbits, C.huge_chunks);
         PLV_LAUNCH_CHECK();
-        k_color_huge_final<<<148, CB, 0, s>>>(off, nbr, active, colors, C.huge, C.cnt + 1, C.hbits,
+        k_color_huge_final<<<148, CB, 0, s>>>(off, nbr, R, colors, C.huge, C.cnt + 1, C.hbits,
                                               tent, keep);
         PLV_LAUNCH_CHECK();
     }
-    k_color_commit<<<grid_for(na, 256), 256, 0, s>>>(active, na, tent, colors);
+    k_color_commit<<<g, 256, 0, s>>>(R, tent, colors);
     PLV_LAUNCH_CHECK();
-    k_color_conflicts_small<<<grid_for(na, 256), 256, 0, s>>>(off, nbr, active, na, colors, keep);
+    k_color_conflicts_small<<<g, 256, 0, s>>>(off, nbr, R, colors, keep);
     PLV_LAUNCH_CHECK();
-    k_color_conflicts_big<<<CBIG_GRID, CB, 0, s>>>(off, nbr, active, colors, keep, C.big, C.cnt);
+    k_color_conflicts_big<<<CBIG_GRID, CB, 0, s>>>(off, nbr, R, colors, keep, C.big, C.cnt);
     PLV_LAUNCH_CHECK();
     if (huge) {
-        dim3 g(148, C.huge_chunks);
-        k_color_conflicts_huge<<<g, CB, 0, s>>>(off, nbr, active, colors, C.huge, C.cnt + 1, keep);
+        k_color_conflicts_huge<<<148 * C.huge_chunks, CB, 0, s>>>(off, nbr, R, colors, C.huge,
+                                                                  C.cnt + 1, keep, C.huge_chunks);
         PLV_LAUNCH_CHECK();
     }
+}
+
+// Stable compaction of the rejected (keep == 0) active vertices into the
+// other buffer, which they leave uncoloured (PL/heuristics.py:113-115):
+// per-tile counts, one-block scan of the tile counts, ordered scatter.
+constexpr int RT = 256, RI = 4, RTILE = RT * RI;
+
+__global__ void __launch_bounds__(RT) k_rej_tiles(ActiveRef R, const uint8_t *keep,
+                                                  int64_t *tsum) {
+    typedef cub::BlockReduce<int, RT> BR;
+    __shared__ typename BR::TempStorage tmp;
+    const int64_t na = R.count(), nt = (na + RTILE - 1) / RTILE;
+    for (int64_t t = blockIdx.x; t < nt; t += gridDim.x) {
+        int c = 0;
+#pragma unroll
+        for (int u = 0; u < RI; u++) {
+            const int64_t x = t * RTILE + threadIdx.x * RI + u;
+            c += (x < na && !keep[x]) ? 1 : 0;
+        }
+        const int tot = BR(tmp).Sum(c);
+        if (threadIdx.x == 0) tsum[t] = tot;
+        __syncthreads();
+    }
+}
+
+constexpr int RS = 1024;
+__global__ void __launch_bounds__(RS) k_rej_scan(int64_t *ctl, int64_t *tsum) {
+    typedef cub::BlockScan<int64_t, RS> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    const int64_t na = ctl[0], nt = (na + RTILE - 1) / RTILE;
+    const int64_t per = (nt + RS - 1) / RS, t0 = threadIdx.x * per;
+    int64_t loc = 0;
+    for (int64_t t = t0; t < t0 + per && t < nt; t++) loc += tsum[t];
+    int64_t base, total;
+    Scan(tmp).ExclusiveSum(loc, base, total);
+    for (int64_t t = t0; t < t0 + per && t < nt; t++) {
+        const int64_t v = tsum[t];
+        tsum[t] = base;
+        base += v;
+    }
+    if (threadIdx.x == 0) ctl[2] = total;
+}
+
+__global__ void __launch_bounds__(RT) k_rej_scatter(ActiveRef R, const uint8_t *keep,
+                                                    const int64_t *tsum, int32_t *colors) {
+    typedef cub::BlockScan<int, RT> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    const int32_t *A = R.act();
+    int32_t *N = R.next();
+    const int64_t na = R.count(), nt = (na + RTILE - 1) / RTILE;
+    for (int64_t t = blockIdx.x; t < nt; t += gridDim.x) {
+        int f[RI], c = 0;
+#pragma unroll
+        for (int u = 0; u < RI; u++) {
+            const int64_t x = t * RTILE + threadIdx.x * RI + u;
+            f[u] = (x < na && !keep[x]) ? 1 : 0;
+            c += f[u];
+        }
+        int pos;
+        Scan(tmp).ExclusiveSum(c, pos);
+        int64_t o = tsum[t] + pos;
+#pragma unroll
+        for (int u = 0; u < RI; u++) {
+            if (!f[u]) continue;
+            const int32_t i = A[t * RTILE + threadIdx.x * RI + u];
+            N[o++] = i;
+            colors[i] = -1;
+        }
+        __syncthreads();
+    }
+}
+
+// End of a round: the rejected become the active list; loop while any.
+__global__ void k_color_step(int64_t *ctl, unsigned long long *cnt, cudaGraphConditionalHandle h) {
+    const int64_t nr = ctl[2];
+    ctl[0] = nr;
+    ctl[1] += 1;
+    cnt[0] = cnt[1] = 0ull;
+    cudaGraphSetConditional(h, nr > 0 ? 1u : 0u);
+}
+
+__global__ void k_color_init_ctl(int64_t *ctl, int64_t n, unsigned long long *cnt) {
+    ctl[0] = n;
+    ctl[1] = 0;
+    ctl[2] = 0;
+    cnt[0] = cnt[1] = 0ull;
 }
 
 __global__ void k_count_huge(const int64_t *off, int64_t n, unsigned long long *cnt,
@@ -359,6 +463,9 @@ __global__ void k_count_huge(const int64_t *off, int64_t n, unsigned long long *
     }
 }
 
+// The whole colouring as one CUDA graph: init, then WHILE (active) { round;
+// compaction; step }.  Rounds repeat until no vertex is rejected, exactly as
+// the host loop of PL/heuristics.py:100-116, with no host round trip per round.
 void color(const int64_t *off, const int32_t *nbr, int64_t n, int32_t *colors, int64_t *info_h,
            cudaStream_t s) {
     if (n <= 0) {
@@ -367,8 +474,8 @@ void color(const int64_t *off, const int32_t *nbr, int64_t n, int32_t *colors, i
         return;
     }
     Buf<int32_t> act0(n, s), act1(n, s), tent(n, s), big(n, s);
-    Buf<uint8_t> keep(n, s), rej(n, s);
-    Buf<int64_t> cnt(1, s);
+    Buf<uint8_t> keep(n, s);
+    Buf<int64_t> ctl(4, s), tsum((n + RTILE - 1) / RTILE + 1, s);
     Buf<unsigned long long> cnts(4, s);
     PLV_CUDA(cudaMemsetAsync(cnts.get(), 0, 4 * sizeof(unsigned long long), s));
     k_count_huge<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(off, n, cnts.get() + 2, cnts.get() + 3);
@@ -382,34 +489,66 @@ void color(const int64_t *off, const int32_t *nbr, int64_t n, int32_t *colors, i
                    (unsigned)((hc[1] + CHUGE - 1) / CHUGE)};
     k_color_init<<<grid_for(n, 256), 256, 0, s>>>(colors, act0, n);
     PLV_LAUNCH_CHECK();
-    int32_t *active = act0.get(), *next = act1.get();
-    int64_t na = n, rounds = 0;
-    size_t bytes = 0;
-    PLV_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, active, rej.get(), next, cnt.get(), n, s));
-    Buf<char> tmp(bytes, s);
-    while (na > 0) {
-        rounds++;
-        color_round(off, nbr, active, na, colors, tent, keep, C, s);
-        k_reject_flags<<<grid_for(na, 256), 256, 0, s>>>(keep, na, rej);
-        PLV_LAUNCH_CHECK();
-        size_t b2 = bytes;
-        PLV_CUDA(cub::DeviceSelect::Flagged(tmp.get(), b2, active, rej.get(), next, cnt.get(), na, s));
-        int64_t nr = d2h(cnt.get(), s);
-        if (nr > 0) {
-            k_uncolor<<<grid_for(nr, 256), 256, 0, s>>>(next, nr, colors);
+    k_color_init_ctl<<<1, 1, 0, s>>>(ctl, n, cnts);
+    PLV_LAUNCH_CHECK();
+    PLV_CUDA(cudaStreamSynchronize(s));
+    ActiveRef R{act0.get(), act1.get(), ctl.get(), 0};
+    cudaGraph_t graph = nullptr, body = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaStream_t cs = nullptr;
+    try {
+        PLV_CUDA(cudaGraphCreate(&graph, 0));
+        cudaGraphConditionalHandle h;
+        PLV_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t loop;
+        PLV_CUDA(cudaGraphAddNode(&loop, graph, nullptr, 0, &cp));
+        body = cp.conditional.phGraph_out[0];
+        PLV_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        PLV_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
+                                               cudaStreamCaptureModeThreadLocal));
+        try {
+            color_round(off, nbr, R, n, colors, tent, keep, C, cs);
+            const unsigned gt = grid_for((n + RTILE - 1) / RTILE, 1, 148 * 8);
+            k_rej_tiles<<<gt, RT, 0, cs>>>(R, keep, tsum);
             PLV_LAUNCH_CHECK();
+            k_rej_scan<<<1, RS, 0, cs>>>(ctl, tsum);
+            PLV_LAUNCH_CHECK();
+            k_rej_scatter<<<gt, RT, 0, cs>>>(R, keep, tsum, colors);
+            PLV_LAUNCH_CHECK();
+            k_color_step<<<1, 1, 0, cs>>>(ctl, cnts, h);
+            PLV_LAUNCH_CHECK();
+        } catch (...) {
+            cudaGraph_t g2 = nullptr;
+            cudaStreamEndCapture(cs, &g2);
+            throw;
         }
-        int32_t *t = active;
-        active = next;
-        next = t;
-        na = nr;
+        cudaGraph_t got = nullptr;
+        PLV_CUDA(cudaStreamEndCapture(cs, &got));
+        PLV_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        PLV_CUDA(cudaGraphLaunch(exec, s));
+        PLV_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        if (cs) cudaStreamDestroy(cs);
+        throw;
     }
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    cudaStreamDestroy(cs);
+    int64_t c[2];
+    PLV_CUDA(cudaMemcpyAsync(c, ctl.get(), sizeof(c), cudaMemcpyDeviceToHost, s));
     Buf<int> mx(1, s);
     PLV_CUDA(cudaMemsetAsync(mx.get(), 0xff, sizeof(int), s));
     k_max_color<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(colors, n, mx);
     PLV_LAUNCH_CHECK();
     info_h[0] = (int64_t)d2h(mx.get(), s) + 1;
-    info_h[1] = rounds;
+    info_h[1] = c[1];
 }
 
 __global__ void k_class_count(const int32_t *colors, int64_t n, int32_t *cnt) {
@@ -455,10 +594,10 @@ extern "C" int plv_color_assign(const int64_t *off, const int32_t *nbr, const in
         plv::Buf<unsigned long long> nbig(1, s);
         PLV_CUDA(cudaMemsetAsync(nbig.get(), 0, sizeof(unsigned long long), s));
         plv::k_color_assign_small<<<plv::grid_for(na, 256), 256, 0, s>>>(
-            off, nbr, active, na, colors, out_colors, big, nbig, nullptr, nullptr);
+            off, nbr, plv::host_active(active, na), colors, out_colors, big, nbig, nullptr, nullptr);
         PLV_LAUNCH_CHECK();
-        plv::k_color_assign_big<<<plv::CBIG_GRID, plv::CB, 0, s>>>(off, nbr, active, colors,
-                                                                  out_colors, big, nbig);
+        plv::k_color_assign_big<<<plv::CBIG_GRID, plv::CB, 0, s>>>(
+            off, nbr, plv::host_active(active, na), colors, out_colors, big, nbig);
         PLV_LAUNCH_CHECK();
         PLV_CUDA(cudaStreamSynchronize(s));
     }
@@ -474,13 +613,13 @@ extern "C" int plv_color_conflicts(const int64_t *off, const int32_t *nbr, const
         plv::Buf<int32_t> big(na, s);
         plv::Buf<unsigned long long> nbig(1, s);
         PLV_CUDA(cudaMemsetAsync(nbig.get(), 0, sizeof(unsigned long long), s));
-        plv::k_color_conflicts_small<<<plv::grid_for(na, 256), 256, 0, s>>>(off, nbr, active, na,
-                                                                           colors, out_keep);
+        plv::k_color_conflicts_small<<<plv::grid_for(na, 256), 256, 0, s>>>(
+            off, nbr, plv::host_active(active, na), colors, out_keep);
         PLV_LAUNCH_CHECK();
         plv::k_big_list<<<plv::grid_for(na, 256), 256, 0, s>>>(off, active, na, big, nbig);
         PLV_LAUNCH_CHECK();
-        plv::k_color_conflicts_big<<<plv::CBIG_GRID, plv::CB, 0, s>>>(off, nbr, active, colors,
-                                                                     out_keep, big, nbig);
+        plv::k_color_conflicts_big<<<plv::CBIG_GRID, plv::CB, 0, s>>>(
+            off, nbr, plv::host_active(active, na), colors, out_keep, big, nbig);
         PLV_LAUNCH_CHECK();
         PLV_CUDA(cudaStreamSynchronize(s));
     }
