@@ -250,6 +250,24 @@ int plv_csr_from_sorted(const int32_t *a, const int32_t *b, const double *w, int
 int plv_compose(const int32_t *map, const int32_t *assign, const int32_t *renumber, int64_t n,
                 int32_t *out, void *stream);
 
+/* ---------------------------------------------------------------- ingest */
+
+/*
+ * load_graph's edge-list branch (PL/graph.py:245-288) on
+ * device: `text` (device, len bytes) is the file; record lines `u v [w]`
+ * become u / v (int32, dense ids kept as in the file) and w (f64) in file
+ * order, capacity cap.  info_h = {records, n}.  Returns PLV_INGEST_HOST
+ * (> 0) when the file needs the host parser's rules: characters other than
+ * ASCII digits, signs, '.', 'e' and blanks; a malformed line; a weight that
+ * is not a plain decimal on Clinger's exact fast path or is not positive; ids
+ * that do not already form 0..n-1 (renumbering by first appearance); an
+ * empty file.  The host parser then reproduces the reference's result or its
+ * error with the line number.
+ */
+#define PLV_INGEST_HOST 1
+int plv_parse_edge_list(const uint8_t *text, int64_t len, int32_t *u, int32_t *v, double *w,
+                        int64_t cap, int64_t *info_h, void *stream);
+
 /* ------------------------------------------------------------ generators */
 
 /* Counter-based synthetic graphs (BASELINE.json configs), identical to the

@@ -32,6 +32,7 @@ STEP_DECIDE = 0
 STEP_APPLY = 1
 STEP_FINISH = 2
 NCCL_ID_BYTES = 128
+INGEST_HOST = 1
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -77,6 +78,7 @@ _SIGS = {
     "plv_phase_destroy": [_P],
     "plv_rebuild_records": [_P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P],
     "plv_compose": [_P, _P, _P, _I64, _P, _P],
+    "plv_parse_edge_list": [_P, _I64, _P, _P, _P, _I64, _P, _P],
     "plv_gen_rmat": [_U64, _INT, _I64, _D, _D, _D, _D, _D, _P, _P, _P, _I64, _P, _P],
     "plv_gen_sbm": [_U64, _I64, _I64, _D, _D, _P, _P, _P, _I64, _P, _P],
     "plv_gen_grid": [_U64, _I64, _D, _I64, _D, _P, _P, _P, _I64, _P, _P],
