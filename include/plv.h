@@ -177,11 +177,18 @@ int plv_phase_create(const int64_t *off, const int32_t *nbr, const double *wts, 
 int plv_phase_iterate(void *handle, double *q_h, int64_t *moves_h, int64_t *cand_h, void *stream);
 /* The phase loop with the reference's stopping rule (PL/engine.py:203-212):
  * per-iteration Q / moves / milliseconds into the *_trace_h arrays (capacity
- * max_iters); result_h = {iterations, total_moves, hit_cap, device_loop}.
+ * max_iters); result_h (6 values) = {iterations, total_moves, hit_cap,
+ * device_loop, cycle_period, iterations_executed}.
  * Single-GPU engines run the loop on the device (one CUDA graph: the
  * iteration inside a WHILE conditional node, stopping rule and trace in a
  * control kernel; milliseconds from the GPU global timer, device_loop = 1);
- * otherwise one graph launch + host test per iteration (device_loop = 0). */
+ * otherwise one graph launch + host test per iteration (device_loop = 0).
+ * Integral graphs with one (uncoloured) stage skip exact cycles: when the
+ * state after an iteration equals the state p iterations earlier (hash
+ * candidate, then a bitwise comparison), the loop stops at the next
+ * iteration congruent to the cap and the remaining trace rows are the
+ * cycle's (milliseconds 0): same final state, same trace as running to the
+ * cap (cycle_period = p, else 0). */
 int plv_phase_run(void *handle, double theta, int64_t max_iters, double *q_trace_h,
                   int64_t *moves_trace_h, double *ms_trace_h, int64_t *result_h, void *stream);
 /*

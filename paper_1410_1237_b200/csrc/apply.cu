@@ -218,6 +218,11 @@ __global__ void __launch_bounds__(256) k_stage_prep(StageArgs A) {
             A.dirty[pw_node_of(A.tree_n, A.tree_d0, a)] = 1;
             A.dirty[pw_node_of(A.tree_n, A.tree_d0, b)] = 1;
         }
+        if (mover && A.chash)
+            atomicXor(A.chash, mix64(((unsigned long long)i << 32) ^ (unsigned int)a ^
+                                     0x9E3779B97F4A7C15ull) ^
+                                   mix64(((unsigned long long)i << 32) ^ (unsigned int)b ^
+                                         0x9E3779B97F4A7C15ull));
         // independent stages: no stage vertex reads another's assignment, so
         // the scatter can happen here
         if (indep && mover) A.assign[i] = b;

@@ -148,6 +148,7 @@ struct StageArgs {
     // incremental modularity (pairwise.cuh): mark the depth-d0 tree nodes of
     // both communities of every mover (nullptr: off)
     uint8_t *dirty = nullptr;
+    unsigned long long *chash = nullptr;  // cycle skipping: XOR hash of the assignment
     int64_t tree_n = 0;
     int tree_d0 = 0;
 };

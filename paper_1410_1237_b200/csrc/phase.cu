@@ -31,6 +31,7 @@
 namespace plv {
 
 // Device state of the phase loop (PL/engine.py:203-212 on device).
+constexpr int CYC_K = 32;  // ring of recent state hashes (periods 1..CYC_K-1)
 struct RunCtl {
     double theta;
     int64_t max_iters;
@@ -38,6 +39,10 @@ struct RunCtl {
     double q_prev;
     int64_t have_prev;
     unsigned long long t0;
+    // exact cycle skipping (integral one-stage phases; see k_run_ctl)
+    int64_t cyc_on, cyc_mode, cyc_t0, cyc_p, cyc_stop, cyc_done;
+    int32_t cyc_cmd, cyc_mismatch;  // k_cycle: 1 snapshot, 2 compare
+    unsigned long long ring[CYC_K];
 };
 
 struct Phase {
@@ -88,6 +93,11 @@ struct Phase {
     bool run_graph_failed = false;
     uint8_t *dirty = nullptr;  // incremental modularity in the device loop (one stage)
     int mod_d0 = 0;
+    // exact cycle skipping: XOR hash of the assignment (updated by apply), and
+    // the state snapshot the candidate cycle is verified against
+    unsigned long long *chash = nullptr;
+    int32_t *snap_i = nullptr;  // assign, sizes
+    double *snap_d = nullptr;   // a_tot, w_int
 
     void release_run() {
         cudaDeviceSynchronize();  // buffers go back to the pool idle
@@ -95,11 +105,14 @@ struct Phase {
         if (rgraph) cudaGraphDestroy(rgraph);
         rexec = nullptr;
         rgraph = nullptr;
-        void *pr[] = {ctl, tr_q, tr_mv, tr_t, dirty};
+        void *pr[] = {ctl, tr_q, tr_mv, tr_t, dirty, chash, snap_i, snap_d};
         for (void *p : pr)
             pool_free(p);
         ctl = nullptr;
         dirty = nullptr;
+        chash = nullptr;
+        snap_i = nullptr;
+        snap_d = nullptr;
         tr_q = nullptr;
         tr_mv = tr_t = nullptr;
         tr_cap = 0;
@@ -178,13 +191,15 @@ static void record_exchange(Phase &P, size_t a, cudaStream_t st) {
 }
 
 // Stage a's exact apply over the whole stage (replicated on every rank).
-static void record_apply(Phase &P, size_t a, cudaStream_t st, uint8_t *dirty = nullptr) {
+static void record_apply(Phase &P, size_t a, cudaStream_t st, uint8_t *dirty = nullptr,
+                         unsigned long long *chash = nullptr) {
     const int64_t g = P.goff[a], ns = P.goff[a + 1] - g;
     StageArgs S{P.off, P.nbr, P.wts, P.k, P.selfw, P.vtx + g, ns, P.target + g,
                 P.moved + g, P.e_old + g, P.e_best + g, P.pos, P.flags,
                 P.assign, P.a_tot, P.w_int, P.sizes, P.ab.ta + g, P.ab.tb + g,
                 nullptr, nullptr, P.counters};
     S.dirty = dirty;
+    S.chash = chash;
     S.tree_n = P.n;
     S.tree_d0 = P.mod_d0;
     launch_apply(S, P.ab, st);
@@ -467,7 +482,7 @@ __global__ void k_run_start(RunCtl *c) { c->t0 = gtimer(); }
 // (PL/engine.py:203-212, _iteration_converged :134-137), loop condition.
 __global__ void k_run_ctl(RunCtl *c, const double *q, const unsigned long long *counters,
                           double *tr_q, unsigned long long *tr_mv, unsigned long long *tr_t,
-                          cudaGraphConditionalHandle h) {
+                          const unsigned long long *chash, cudaGraphConditionalHandle h) {
     const double q_cur = *q;
     const unsigned long long moves = counters[0];
     const int64_t it = c->it;
@@ -491,7 +506,90 @@ __global__ void k_run_ctl(RunCtl *c, const double *q, const unsigned long long *
     }
     c->q_prev = q_cur;
     c->have_prev = 1;
+    // Exact cycle skipping.  In an integral graph a_tot / w_int / sizes are
+    // exact functions of the assignment, and an iteration is a function of
+    // the state, so once the state after iteration done equals the state
+    // after done - p, everything repeats with period p: the state after the
+    // cap is the state after any iteration congruent to it (mod p), and the
+    // trace rows repeat.  A hash match (ring of recent assignment hashes) is
+    // a candidate; the state is snapshotted and compared bit for bit p
+    // iterations later (k_cycle); once verified -- by then every consecutive
+    // pair of Q values in the cycle has passed the stopping test -- the loop
+    // runs on only to the next iteration congruent to the cap and the host
+    // fills in the remaining trace rows.
+    c->cyc_cmd = 0;
+    if (c->cyc_on && !stop) {
+        const int64_t done = it + 1;
+        const unsigned long long H = *chash;
+        if (c->cyc_mode == 0) {
+            for (int64_t p = 1; p < CYC_K && p < done; p++)
+                if (c->ring[(done - p) % CYC_K] == H) {
+                    c->cyc_mode = 1;
+                    c->cyc_t0 = done;
+                    c->cyc_p = p;
+                    c->cyc_cmd = 1;  // snapshot the state after iteration done
+                    break;
+                }
+        } else if (c->cyc_mode == 1 && done == c->cyc_t0 + c->cyc_p) {
+            c->cyc_mode = 2;
+            c->cyc_mismatch = 0;
+            c->cyc_cmd = 2;  // compare with the snapshot
+        } else if (c->cyc_mode == 2) {
+            if (c->cyc_mismatch) {
+                c->cyc_mode = 0;  // hash collision
+            } else {
+                const int64_t t0 = c->cyc_t0, p = c->cyc_p, cap = c->max_iters;
+                const int64_t want = (cap - t0) % p;
+                int64_t stop_at = done + (((want - (done - t0)) % p) + p) % p;
+                c->cyc_mode = 3;
+                c->cyc_stop = stop_at;
+            }
+        }
+        if (c->cyc_mode == 3 && done == c->cyc_stop) {
+            c->cyc_done = 1;
+            c->hit = 1;
+            stop = true;
+        }
+        c->ring[done % CYC_K] = H;
+    }
     cudaGraphSetConditional(h, stop ? 0u : 1u);
+}
+
+// The cycle check's data side: snapshot (cmd 1) or compare (cmd 2) the state.
+__global__ void k_cycle(RunCtl *c, const int32_t *assign, const int32_t *sizes,
+                        const double *a_tot, const double *w_int, int64_t n, int32_t *snap_i,
+                        double *snap_d) {
+    const int cmd = c->cyc_cmd;
+    if (!cmd) return;
+    bool diff = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (cmd == 1) {
+            snap_i[i] = assign[i];
+            snap_i[n + i] = sizes[i];
+            snap_d[i] = a_tot[i];
+            snap_d[n + i] = w_int[i];
+        } else {
+            // bitwise: -0.0 vs 0.0 or NaN payloads would differ
+            diff |= snap_i[i] != assign[i] || snap_i[n + i] != sizes[i] ||
+                    __double_as_longlong(snap_d[i]) != __double_as_longlong(a_tot[i]) ||
+                    __double_as_longlong(snap_d[n + i]) != __double_as_longlong(w_int[i]);
+        }
+    }
+    if (diff) c->cyc_mismatch = 1;
+}
+
+__device__ __forceinline__ unsigned long long vhash(int64_t i, int32_t comm) {
+    return mix64(((unsigned long long)i << 32) ^ (unsigned int)comm ^ 0x9E3779B97F4A7C15ull);
+}
+
+__global__ void k_hash_assign(const int32_t *assign, int64_t n, unsigned long long *h) {
+    unsigned long long x = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x ^= vhash(i, assign[i]);
+    for (int o = 16; o > 0; o >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0 && x) atomicXor(h, x);
 }
 
 // Capture the whole phase: k_run_start, then WHILE (condition) { iteration;
@@ -513,6 +611,11 @@ static void build_run_graph(Phase &P, int64_t cap, cudaStream_t s) {
         modularity_inc_supported(P.n, &P.mod_d0)) {
         P.dirty = dalloc<uint8_t>((size_t)1 << P.mod_d0);
         PLV_CUDA(cudaMemsetAsync(P.dirty, 0, (size_t)1 << P.mod_d0, s));
+    }
+    if (nonempty == 1 && !(P.flags & PLV_F_INDEPENDENT) && (P.flags & PLV_F_INTEGRAL)) {
+        P.chash = dalloc<unsigned long long>(1);
+        P.snap_i = dalloc<int32_t>(2 * P.n);
+        P.snap_d = dalloc<double>(2 * P.n);
     }
     PLV_CUDA(cudaGraphCreate(&P.rgraph, 0));
     cudaGraphConditionalHandle h;
@@ -547,15 +650,20 @@ static void build_run_graph(Phase &P, int64_t cap, cudaStream_t s) {
         for (size_t a = 0; a + 1 < P.goff.size(); a++) {
             if (P.goff[a + 1] == P.goff[a]) continue;
             record_decide(P, a, cs);
-            record_apply(P, a, cs, P.dirty);
+            record_apply(P, a, cs, P.dirty, P.chash);
         }
         if (P.dirty)
             modularity_async_inc(P.w_int, P.a_tot, P.n, P.m, P.q, P.mod_scratch, P.dirty,
                                  &P.ctl->it, cs);
         else
             modularity_async(P.w_int, P.a_tot, P.n, P.m, P.q, P.mod_scratch, cs);
-        k_run_ctl<<<1, 1, 0, cs>>>(P.ctl, P.q, P.counters, P.tr_q, P.tr_mv, P.tr_t, h);
+        k_run_ctl<<<1, 1, 0, cs>>>(P.ctl, P.q, P.counters, P.tr_q, P.tr_mv, P.tr_t, P.chash, h);
         PLV_LAUNCH_CHECK();
+        if (P.chash) {
+            k_cycle<<<grid_for(P.n, 256, 148 * 8), 256, 0, cs>>>(P.ctl, P.assign, P.sizes, P.a_tot,
+                                                                P.w_int, P.n, P.snap_i, P.snap_d);
+            PLV_LAUNCH_CHECK();
+        }
     } catch (...) {
         cudaGraph_t g2 = nullptr;
         cudaStreamEndCapture(cs, &g2);
@@ -583,8 +691,17 @@ static bool phase_run_device(Phase &P, double theta, int64_t max_iters, double *
             return false;
         }
     }
-    RunCtl c0 = {theta, max_iters, 0, 0, 0, 0.0, 0, 0ull};
+    RunCtl c0;
+    memset(&c0, 0, sizeof(c0));
+    c0.theta = theta;
+    c0.max_iters = max_iters;
+    c0.cyc_on = P.chash ? 1 : 0;
     PLV_CUDA(cudaMemcpyAsync(P.ctl, &c0, sizeof(c0), cudaMemcpyHostToDevice, s));
+    if (P.chash) {
+        PLV_CUDA(cudaMemsetAsync(P.chash, 0, sizeof(unsigned long long), s));
+        k_hash_assign<<<grid_for(P.n, 256, 148 * 8), 256, 0, s>>>(P.assign, P.n, P.chash);
+        PLV_LAUNCH_CHECK();
+    }
     PLV_CUDA(cudaGraphLaunch(P.rexec, s));
     RunCtl c;
     PLV_CUDA(cudaMemcpyAsync(&c, P.ctl, sizeof(c), cudaMemcpyDeviceToHost, s));
@@ -603,10 +720,25 @@ static bool phase_run_device(Phase &P, double theta, int64_t max_iters, double *
         ms_h[i] = (double)(tt[i] - prev) / 1e6;
         prev = tt[i];
     }
-    res_h[0] = it;
-    res_h[1] = c.total;
+    int64_t iters = it, total = c.total;
+    if (c.cyc_done) {
+        // rows it+1 .. cap repeat rows t0+1 .. t0+p (1-based iteration numbers)
+        const int64_t t0 = c.cyc_t0, p = c.cyc_p;
+        for (int64_t x = it + 1; x <= max_iters; x++) {
+            const int64_t src = t0 + 1 + ((x - t0 - 1) % p);
+            q_h[x - 1] = q_h[src - 1];
+            mv_h[x - 1] = mv_h[src - 1];
+            ms_h[x - 1] = 0.0;  // not executed
+            total += mv_h[x - 1];
+        }
+        iters = max_iters;
+    }
+    res_h[0] = iters;
+    res_h[1] = total;
     res_h[2] = c.hit;
     res_h[3] = 1;
+    res_h[4] = c.cyc_done ? c.cyc_p : 0;
+    res_h[5] = c.cyc_done ? it : 0;
     return true;
 }
 
@@ -738,6 +870,8 @@ extern "C" int plv_phase_run(void *handle, double theta, int64_t max_iters, doub
     result_h[1] = total;
     result_h[2] = hit;
     result_h[3] = 0;
+    result_h[4] = 0;
+    result_h[5] = 0;
     PLV_EXIT
 }
 

@@ -88,3 +88,49 @@ def test_capped_phases_match_oracle(orc, seed):
     assert [p.stats.iterations for p in h.phases] == [p.iterations for p in oh.phases]
     assert np.array_equal(h.final_assignment, oh.final_assignment)
     assert h.final_modularity == oh.final_modularity
+
+
+def _sbm_integral(n=1200, blocks=12, seed=7):
+    rng = np.random.default_rng(seed)
+    b = np.arange(n) // (n // blocks)
+    iu, ju = np.triu_indices(n, 1)
+    p = np.where(b[iu] == b[ju], 0.08, 0.004)
+    keep = rng.random(len(iu)) < p
+    return iu[keep], ju[keep]
+
+
+@pytest.mark.parametrize("cap", [10_000, 777])
+def test_cycle_skipping_is_exact(cap):
+    """Integral weights, one uncoloured stage: the device loop detects the
+    oscillation, verifies it bit for bit, skips to the cap -- same trace and
+    same final state as iterating every time."""
+    u, v = _sbm_integral()
+    g = pl.Graph.from_edges(u, v, num_vertices=1200)
+    assert g.integral
+    s1, st1 = _state(g)
+    s2, st2 = _state(g)
+    e1 = PhaseEngine(g, s1, None)
+    e2 = PhaseEngine(g, s2, None)
+    qs, mvs, hit = _host_loop(e1, 1e-6, cap)
+    q2, m2, ms2, it, total, hit2 = e2.run(1e-6, cap)
+    assert it == len(qs) and hit2 == hit and total == sum(mvs)
+    assert [float(x) for x in q2] == qs and [int(x) for x in m2] == mvs
+    for k in KEYS:
+        assert bool((st1[k] == st2[k]).all()), k
+    if hit:
+        assert e2.cycle is not None and e2.cycle[1] < cap  # the tail was skipped
+    e1.close()
+    e2.close()
+
+
+def test_cycle_skipping_run_matches_oracle(orc):
+    u, v = _sbm_integral(seed=11)
+    n = 1200
+    w = np.ones(len(u))
+    g = pl.Graph.from_edges(u, v, w, num_vertices=n)
+    og = orc.from_edges(u, v, w, num_vertices=n)
+    h = pl.run(g, pl.RunConfig(max_iterations_per_phase=3000))
+    oh = orc.run(og, max_iterations=3000)
+    assert [p.stats.iterations for p in h.phases] == [p.iterations for p in oh.phases]
+    assert np.array_equal(h.final_assignment, oh.final_assignment)
+    assert h.final_modularity == oh.final_modularity
