@@ -62,11 +62,13 @@ __device__ __forceinline__ int first_free_thread(const int64_t *off, const int32
 // Tentative colours of low-degree active vertices; the others go to `big`
 // (one block each) or, above CHUGE entries, to `huge` (split over blocks).
 constexpr int64_t CHUGE = 4096;
+constexpr int64_t CMID_MAXD = 512;  // warp per vertex up to here, then a block
 
 __global__ void k_color_assign_small(const int64_t *off, const int32_t *nbr, ActiveRef R,
                                      const int32_t *colors, int32_t *out, int32_t *big,
                                      unsigned long long *nbig, int32_t *huge,
-                                     unsigned long long *nhuge) {
+                                     unsigned long long *nhuge, int32_t *mid = nullptr,
+                                     unsigned long long *nmid = nullptr) {
     const int32_t *active = R.act();
     const int64_t na = R.count();
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < na;
@@ -75,8 +77,10 @@ __global__ void k_color_assign_small(const int64_t *off, const int32_t *nbr, Act
         int64_t d = off[i + 1] - off[i];
         if (d <= COLOR_THREAD_MAXD)
             out[x] = first_free_thread(off, nbr, colors, i);
-        else if (d <= CHUGE || !huge)
+        else if (d <= CMID_MAXD || !mid)
             big[atomicAdd(nbig, 1ull)] = (int32_t)x;
+        else if (d <= CHUGE || !huge)
+            mid[atomicAdd(nmid, 1ull)] = (int32_t)x;
         else
             huge[atomicAdd(nhuge, 1ull)] = (int32_t)x;
     }
@@ -90,20 +94,29 @@ __global__ void __launch_bounds__(CB) k_color_assign_huge(const int64_t *off, co
                                                           const int32_t *huge,
                                                           const unsigned long long *nhuge,
                                                           uint32_t *hbits, int64_t chunks) {
+    // colours cluster in a few words: OR into a shared bitmap first, then
+    // publish only its non-zero words (global atomics on one word serialise)
+    __shared__ uint32_t sb[CWIN / 32];
     const int32_t *active = R.act();
     const int64_t cnt = (int64_t)*nhuge * chunks;  // (item, chunk) pairs
-    for (int64_t w = blockIdx.x; w < cnt; w += gridDim.x) {
-        const int64_t q = w / chunks, ch = w % chunks;
+    for (int64_t w0 = blockIdx.x; w0 < cnt; w0 += gridDim.x) {
+        const int64_t q = w0 / chunks, ch = w0 % chunks;
+        for (int w = threadIdx.x; w < CWIN / 32; w += CB) sb[w] = 0u;
+        __syncthreads();
         int32_t i = active[huge[q]];
         int64_t e0 = off[i] + ch * CHUGE, e1 = off[i + 1];
         int64_t ee = e0 + CHUGE < e1 ? e0 + CHUGE : e1;
-        uint32_t *bits = hbits + q * (CWIN / 32);
         for (int64_t e = e0 + threadIdx.x; e < ee; e += CB) {
             int32_t j = nbr[e];
             if (j == i) continue;
             int32_t cj = colors[j];
-            if (cj >= 0 && cj < CWIN) atomicOr(bits + (cj >> 5), 1u << (cj & 31));
+            if (cj >= 0 && cj < CWIN) atomicOr(sb + (cj >> 5), 1u << (cj & 31));
         }
+        __syncthreads();
+        uint32_t *bits = hbits + q * (CWIN / 32);
+        for (int w = threadIdx.x; w < CWIN / 32; w += CB)
+            if (sb[w]) atomicOr(bits + w, sb[w]);
+        __syncthreads();
     }
 }
 
@@ -185,8 +198,50 @@ __global__ void __launch_bounds__(CB) k_color_conflicts_huge(const int64_t *off,
     }
 }
 
-// One block per high-degree active vertex: bitmap of neighbour colours.
+// One warp per active vertex of COLOR_THREAD_MAXD < degree <= CMID_MAXD: a 1024-colour bitmap per warp in shared memory, windows of 1024
+// colours until one has a free bit.
+constexpr int WWIN = 1024;
+
 __global__ void __launch_bounds__(CB) k_color_assign_big(const int64_t *off, const int32_t *nbr,
+                                                         ActiveRef R, const int32_t *colors,
+                                                         int32_t *out, const int32_t *big,
+                                                         const unsigned long long *nbig) {
+    __shared__ uint32_t bits[CB / 32][WWIN / 32];
+    const int32_t *active = R.act();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t *wb = bits[wid];
+    const int64_t cnt = (int64_t)*nbig;
+    for (int64_t q = blockIdx.x * (int64_t)(CB / 32) + wid; q < cnt;
+         q += (int64_t)gridDim.x * (CB / 32)) {
+        const int64_t x = big[q];
+        const int32_t i = active[x];
+        const int64_t e0 = off[i], e1 = off[i + 1];
+        for (int base = 0;; base += WWIN) {
+            wb[lane] = 0u;
+            __syncwarp();
+            for (int64_t e = e0 + lane; e < e1; e += 32) {
+                const int32_t j = nbr[e];
+                if (j == i) continue;
+                const int32_t cj = colors[j] - base;
+                if (cj >= 0 && cj < WWIN) atomicOr(wb + (cj >> 5), 1u << (cj & 31));
+            }
+            __syncwarp();
+            const uint32_t fr = ~wb[lane];  // lane l owns colours [32 l, 32 l + 32)
+            const unsigned any = __ballot_sync(0xffffffffu, fr != 0u);
+            __syncwarp();
+            if (any) {
+                const int l = __ffs(any) - 1;
+                const uint32_t frl = __shfl_sync(0xffffffffu, fr, l);
+                if (lane == 0) out[x] = base + l * 32 + __ffs(frl) - 1;
+                break;
+            }
+        }
+    }
+}
+
+// One block per active vertex of CMID_MAXD < degree <= CHUGE: bitmap of
+// neighbour colours in shared memory.
+__global__ void __launch_bounds__(CB) k_color_assign_mid(const int64_t *off, const int32_t *nbr,
                                                          ActiveRef R, const int32_t *colors,
                                                          int32_t *out, const int32_t *big,
                                                          const unsigned long long *nbig) {
@@ -255,6 +310,36 @@ __global__ void __launch_bounds__(CB) k_color_conflicts_big(const int64_t *off, 
                                                             const int32_t *big,
                                                             const unsigned long long *nbig) {
     const int32_t *active = R.act();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t cnt = (int64_t)*nbig;
+    for (int64_t q = blockIdx.x * (int64_t)(CB / 32) + wid; q < cnt;
+         q += (int64_t)gridDim.x * (CB / 32)) {
+        const int64_t x = big[q];
+        const int32_t i = active[x];
+        const int32_t ci = colors[i];
+        const int64_t e0 = off[i], e1 = off[i + 1];
+        bool clash = false;
+        for (int64_t c0 = e0; c0 < e1; c0 += 32) {
+            const int64_t e = c0 + lane;
+            bool past = true;
+            if (e < e1) {
+                const int32_t j = nbr[e];
+                past = j >= i;  // rows are sorted: only the prefix j < i matters
+                if (!past && colors[j] == ci) clash = true;
+            }
+            if (__any_sync(0xffffffffu, clash || past)) break;
+        }
+        clash = __any_sync(0xffffffffu, clash);
+        if (lane == 0) keep[x] = clash ? 0 : 1;
+    }
+}
+
+__global__ void __launch_bounds__(CB) k_color_conflicts_mid(const int64_t *off, const int32_t *nbr,
+                                                            ActiveRef R,
+                                                            const int32_t *colors, uint8_t *keep,
+                                                            const int32_t *big,
+                                                            const unsigned long long *nbig) {
+    const int32_t *active = R.act();
     const int tid = threadIdx.x;
     const int64_t cnt = (int64_t)*nbig;
     for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
@@ -318,8 +403,8 @@ __global__ void k_max_color(const int32_t *colors, int64_t n, int *mx) {
 
 // One speculative round over the active list: tentative colours, commit, keep flags.
 struct ColorScratch {
-    int32_t *big, *huge;
-    unsigned long long *cnt;  // [0] big, [1] huge (zero at the start of a round)
+    int32_t *big, *huge, *mid;
+    unsigned long long *cnt;  // [0] big, [1] huge, [2] mid (zero at the start of a round)
     uint32_t *hbits;          // nhuge_max * CWIN / 32 words
     int64_t nhuge_max;
     unsigned huge_chunks;     // ceil(max_degree / CHUGE)
@@ -331,9 +416,11 @@ static void color_round(const int64_t *off, const int32_t *nbr, ActiveRef R, int
     bool huge = C.nhuge_max > 0;
     const unsigned g = grid_for(na_max, 256, 148 * 8);
     k_color_assign_small<<<g, 256, 0, s>>>(off, nbr, R, colors, tent, C.big, C.cnt,
-                                           huge ? C.huge : nullptr, C.cnt + 1);
+                                           huge ? C.huge : nullptr, C.cnt + 1, C.mid, C.cnt + 2);
     PLV_LAUNCH_CHECK();
     k_color_assign_big<<<CBIG_GRID, CB, 0, s>>>(off, nbr, R, colors, tent, C.big, C.cnt);
+    PLV_LAUNCH_CHECK();
+    k_color_assign_mid<<<CBIG_GRID, CB, 0, s>>>(off, nbr, R, colors, tent, C.mid, C.cnt + 2);
     PLV_LAUNCH_CHECK();
     if (huge) {
         PLV_CUDA(cudaMemsetAsync(C.hbits, 0, sizeof(uint32_t) * C.nhuge_max * (CWIN / 32), s));
@@ -349,6 +436,8 @@ static void color_round(const int64_t *off, const int32_t *nbr, ActiveRef R, int
     k_color_conflicts_small<<<g, 256, 0, s>>>(off, nbr, R, colors, keep);
     PLV_LAUNCH_CHECK();
     k_color_conflicts_big<<<CBIG_GRID, CB, 0, s>>>(off, nbr, R, colors, keep, C.big, C.cnt);
+    PLV_LAUNCH_CHECK();
+    k_color_conflicts_mid<<<CBIG_GRID, CB, 0, s>>>(off, nbr, R, colors, keep, C.mid, C.cnt + 2);
     PLV_LAUNCH_CHECK();
     if (huge) {
         k_color_conflicts_huge<<<148 * C.huge_chunks, CB, 0, s>>>(off, nbr, R, colors, C.huge,
@@ -432,7 +521,7 @@ __global__ void k_color_step(int64_t *ctl, unsigned long long *cnt, cudaGraphCon
     const int64_t nr = ctl[2];
     ctl[0] = nr;
     ctl[1] += 1;
-    cnt[0] = cnt[1] = 0ull;
+    cnt[0] = cnt[1] = cnt[2] = 0ull;
     cudaGraphSetConditional(h, nr > 0 ? 1u : 0u);
 }
 
@@ -440,7 +529,7 @@ __global__ void k_color_init_ctl(int64_t *ctl, int64_t n, unsigned long long *cn
     ctl[0] = n;
     ctl[1] = 0;
     ctl[2] = 0;
-    cnt[0] = cnt[1] = 0ull;
+    cnt[0] = cnt[1] = cnt[2] = 0ull;
 }
 
 __global__ void k_count_huge(const int64_t *off, int64_t n, unsigned long long *cnt,
@@ -473,19 +562,19 @@ void color(const int64_t *off, const int32_t *nbr, int64_t n, int32_t *colors, i
         info_h[1] = 0;
         return;
     }
-    Buf<int32_t> act0(n, s), act1(n, s), tent(n, s), big(n, s);
+    Buf<int32_t> act0(n, s), act1(n, s), tent(n, s), big(n, s), mid(n, s);
     Buf<uint8_t> keep(n, s);
     Buf<int64_t> ctl(4, s), tsum((n + RTILE - 1) / RTILE + 1, s);
-    Buf<unsigned long long> cnts(4, s);
-    PLV_CUDA(cudaMemsetAsync(cnts.get(), 0, 4 * sizeof(unsigned long long), s));
-    k_count_huge<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(off, n, cnts.get() + 2, cnts.get() + 3);
+    Buf<unsigned long long> cnts(6, s);
+    PLV_CUDA(cudaMemsetAsync(cnts.get(), 0, 6 * sizeof(unsigned long long), s));
+    k_count_huge<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(off, n, cnts.get() + 4, cnts.get() + 5);
     PLV_LAUNCH_CHECK();
     unsigned long long hc[2];
-    PLV_CUDA(cudaMemcpyAsync(hc, cnts.get() + 2, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    PLV_CUDA(cudaMemcpyAsync(hc, cnts.get() + 4, sizeof(hc), cudaMemcpyDeviceToHost, s));
     PLV_CUDA(cudaStreamSynchronize(s));
     Buf<int32_t> huge(hc[0] ? hc[0] : 1, s);
     Buf<uint32_t> hbits((hc[0] ? hc[0] : 1) * (CWIN / 32), s);
-    ColorScratch C{big.get(), huge.get(), cnts.get(), hbits.get(), (int64_t)hc[0],
+    ColorScratch C{big.get(), huge.get(), mid.get(), cnts.get(), hbits.get(), (int64_t)hc[0],
                    (unsigned)((hc[1] + CHUGE - 1) / CHUGE)};
     k_color_init<<<grid_for(n, 256), 256, 0, s>>>(colors, act0, n);
     PLV_LAUNCH_CHECK();
