@@ -58,10 +58,8 @@ __device__ __forceinline__ void mover_deltas(const StageArgs &A, int64_t x, int3
 
 // One warp per high-degree mover: live e_a / e_b as ordered folds (the
 // matching lanes of each 32-entry chunk are added in lane order).
-__global__ void __launch_bounds__(256) k_stage_big(StageArgs A) {
+__device__ __forceinline__ void stage_big_warps(const StageArgs &A, int64_t gw, int64_t nw) {
     const int lane = threadIdx.x & 31;
-    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t cnt = (int64_t)*A.nbig;
     const bool integral = A.flags & PLV_F_INTEGRAL;
     for (int64_t q = gw; q < cnt; q += nw) {
@@ -100,7 +98,7 @@ constexpr int64_t APPLY_HUGE = 128;
 // live community), a warp's is one round per 32 entries.
 constexpr int64_t APPLY_THREAD_MAX = 8;
 
-__global__ void __launch_bounds__(256) k_stage_huge(StageArgs A) {
+__device__ __forceinline__ void stage_huge_block(const StageArgs &A, int64_t b0, int64_t nb) {
     typedef cub::BlockScan<int, 256> Scan;
     __shared__ typename Scan::TempStorage scan;
     __shared__ int8_t sidx[256];
@@ -108,7 +106,7 @@ __global__ void __launch_bounds__(256) k_stage_huge(StageArgs A) {
     const int tid = threadIdx.x;
     const int64_t cnt = (int64_t)*A.nhuge;
     const bool integral = A.flags & PLV_F_INTEGRAL;
-    for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
+    for (int64_t q = b0; q < cnt; q += nb) {
         const int64_t x = A.huge[q];
         const int32_t i = A.subset[x], b = A.target[x], a = A.assign[i];
         const int64_t e0 = A.off[i], e1 = A.off[i + 1];
@@ -145,10 +143,27 @@ __global__ void __launch_bounds__(256) k_stage_huge(StageArgs A) {
     }
 }
 
+// Live e_a / e_b of the movers k_stage_prep deferred: the first APPLY_HB
+// blocks take the huge ones (a block each), the others the big ones (a warp
+// each) -- one launch for both.
+constexpr int APPLY_HB = 148 * 4;
+constexpr int APPLY_BB = 148 * 8;
+
+__global__ void __launch_bounds__(256) k_stage_live(StageArgs A) {
+    if (blockIdx.x < APPLY_HB) {
+        stage_huge_block(A, blockIdx.x, APPLY_HB);
+    } else {
+        const int64_t b = blockIdx.x - APPLY_HB;
+        stage_big_warps(A, (b * blockDim.x + threadIdx.x) >> 5,
+                        ((int64_t)(gridDim.x - APPLY_HB) * blockDim.x) >> 5);
+    }
+}
+
 // Per subset index x: events + deltas (+ sizes, moves, and the assignment
 // scatter for independent stages).  Low-degree movers fold their live
 // e_a / e_b here; high-degree ones go to the k_stage_big worklist.
 __global__ void __launch_bounds__(256) k_stage_prep(StageArgs A) {
+    if (A.lcnt && blockIdx.x == 0 && threadIdx.x == 0) *A.lcnt = 0ull;  // long runs of this stage
     const bool indep = A.flags & PLV_F_INDEPENDENT;
     const bool integral = A.flags & PLV_F_INTEGRAL;
     int lane = threadIdx.x & 31;
@@ -247,22 +262,11 @@ __device__ __forceinline__ void event_delta(const StageArgs &A, int32_t v, doubl
     }
 }
 
-__global__ void k_stage_deltas(StageArgs A, const uint32_t *key, const int32_t *val, int64_t ne,
-                               double *dW, double *dA) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ne;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        if (key[p] == SENTINEL) continue;
-        double dw, da;
-        event_delta(A, val[p], dw, da);
-        dW[p] = dw;
-        dA[p] = da;
-    }
-}
-
-// Sequential fold of the run of community c starting at p from contiguous
-// deltas (loads batched so only the additions are serial).
-__device__ __forceinline__ void fold_deltas(const uint32_t *key, const double *dW,
-                                            const double *dA, int64_t p, int64_t ne, double &W,
+// Sequential fold of the run of community c starting at p; the deltas come
+// straight from the sorted event ids (loads batched so only the additions
+// are serial).
+__device__ __forceinline__ void fold_events(const StageArgs &A, const uint32_t *key,
+                                            const int32_t *val, int64_t p, int64_t ne, double &W,
                                             double &At) {
     const uint32_t c = key[p];
     while (true) {
@@ -272,8 +276,9 @@ __device__ __forceinline__ void fold_deltas(const uint32_t *key, const double *d
         for (int u = 0; u < 8; u++) {
             int64_t q = p + u;
             ok[u] = q < ne && key[q] == c;
-            w[u] = ok[u] ? dW[q] : 0.0;
-            a[u] = ok[u] ? dA[q] : 0.0;
+            w[u] = 0.0;
+            a[u] = 0.0;
+            if (ok[u]) event_delta(A, val[q], w[u], a[u]);
         }
 #pragma unroll
         for (int u = 0; u < 8; u++) {
@@ -287,8 +292,9 @@ __device__ __forceinline__ void fold_deltas(const uint32_t *key, const double *d
 
 constexpr int SHORT_EVENTS = 32;  // longer community runs are folded by a whole block
 
-__global__ void k_stage_fold(StageArgs A, const uint32_t *key, int64_t ne, const double *dW,
-                             const double *dA, int64_t *lrun, unsigned long long *lcnt) {
+__global__ void k_stage_fold(StageArgs A, const uint32_t *key, const int32_t *val, int64_t ne,
+                             int64_t *lrun, unsigned long long *lcnt) {
+    const bool indep = A.flags & PLV_F_INDEPENDENT;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ne;
          p += (int64_t)gridDim.x * blockDim.x) {
         uint32_t c = key[p];
@@ -299,17 +305,23 @@ __global__ void k_stage_fold(StageArgs A, const uint32_t *key, int64_t ne, const
             continue;
         }
         double W = A.w_int[c], At = A.a_tot[c];
-        fold_deltas(key, dW, dA, p, ne, W, At);
+        fold_events(A, key, val, p, ne, W, At);
         A.w_int[c] = W;
         A.a_tot[c] = At;
     }
+    // every live fold has read the assignment by now: scatter the moves
+    if (!indep)
+        for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < A.ns;
+             x += (int64_t)gridDim.x * blockDim.x)
+            if (A.moved[x]) A.assign[A.subset[x]] = A.target[x];
+    if (blockIdx.x == 0 && threadIdx.x == 0 && A.nbig) A.nbig[0] = A.nbig[1] = 0ull;  // next stage
 }
 
 // Long community runs: one block each, block-staged ordered folds.
 __global__ void __launch_bounds__(256) k_stage_fold_long(StageArgs A, const uint32_t *key,
-                                                        int64_t ne, const double *dW,
-                                                        const double *dA, const int64_t *lrun,
-                                                        const unsigned long long *lcnt) {
+                                                        const int32_t *val, int64_t ne,
+                                                        const int64_t *lrun,
+                                                        unsigned long long *lcnt) {
     __shared__ double sb[4 * FOLD_CH];
     __shared__ int64_t s_end;
     const int64_t cnt = (int64_t)*lcnt;
@@ -330,10 +342,7 @@ __global__ void __launch_bounds__(256) k_stage_fold_long(StageArgs A, const uint
         __syncthreads();
         double W = A.w_int[c], At = A.a_tot[c];
         block_fold2(
-            [=] __device__(int64_t t, double &x, double &y) {
-                x = dW[p + t];
-                y = dA[p + t];
-            },
+            [=] __device__(int64_t t, double &x, double &y) { event_delta(A, val[p + t], x, y); },
             s_end - p, W, At, sb);
         if (threadIdx.x == 0) {
             A.w_int[c] = W;
@@ -347,6 +356,7 @@ __global__ void k_stage_scatter(StageArgs A) {
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < A.ns;
          x += (int64_t)gridDim.x * blockDim.x)
         if (A.moved[x]) A.assign[A.subset[x]] = A.target[x];
+    if (blockIdx.x == 0 && threadIdx.x == 0 && A.nbig) A.nbig[0] = A.nbig[1] = 0ull;  // next stage
 }
 
 // One CTA applies a small independent stage: event keys in registers, block
@@ -522,13 +532,13 @@ void ApplyBuffers::alloc(int64_t ta_len, int64_t max_ns, int64_t n, cudaStream_t
     ekey2 = dalloc<uint32_t>(ne);
     eval = dalloc<int32_t>(ne);
     eval2 = dalloc<int32_t>(ne);
-    dW = dalloc<double>(ne);
-    dA = dalloc<double>(ne);
     big_cap = max_ns ? max_ns : 1;
     big = dalloc<int32_t>(2 * big_cap);  // big movers, then huge movers
     nbig = dalloc<unsigned long long>(2);
+    PLV_CUDA(cudaMemsetAsync(nbig, 0, 2 * sizeof(unsigned long long), s));
     lrun = dalloc<int64_t>(ne);
     lcnt = dalloc<unsigned long long>(1);
+    PLV_CUDA(cudaMemsetAsync(lcnt, 0, sizeof(unsigned long long), s));
     nb = bits_for(n + 1);  // SENTINEL's low nb bits exceed every community id
     PLV_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, ekey, ekey2, eval, eval2, ne, 0, nb, s));
     tmp = pool_alloc(bytes);
@@ -545,12 +555,11 @@ void ApplyBuffers::alloc(int64_t ta_len, int64_t max_ns, int64_t n, cudaStream_t
 
 void ApplyBuffers::release() {
     cudaDeviceSynchronize();  // buffers go back to the pool idle
-    void *ps[] = {ta, tb, ekey, ekey2, eval, eval2, tmp, dW, dA, lrun, lcnt, big, nbig};
+    void *ps[] = {ta, tb, ekey, ekey2, eval, eval2, tmp, lrun, lcnt, big, nbig};
     for (void *p : ps)
         pool_free(p);
     big = nullptr;
     nbig = nullptr;
-    dW = dA = nullptr;
     lrun = nullptr;
     lcnt = nullptr;
     ta = tb = nullptr;
@@ -586,13 +595,13 @@ void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {
     S.nbig = B.nbig;
     S.huge = B.big + B.big_cap;
     S.nhuge = B.nbig + 1;
-    if (!indep) PLV_CUDA(cudaMemsetAsync(B.nbig, 0, 2 * sizeof(unsigned long long), st));
+    S.lcnt = B.lcnt;
+    // worklist counters are zero on entry: allocation clears them, and the
+    // apply that used them last cleared them after its last reader
     k_stage_prep<<<grid_for((S.ns + 31) / 32 * 32, 256, 148 * 16), 256, 0, st>>>(S);
     PLV_LAUNCH_CHECK();
     if (!indep) {
-        k_stage_big<<<148 * 8, 256, 0, st>>>(S);
-        PLV_LAUNCH_CHECK();
-        k_stage_huge<<<148 * 4, 256, 0, st>>>(S);
+        k_stage_live<<<APPLY_HB + APPLY_BB, 256, 0, st>>>(S);
         PLV_LAUNCH_CHECK();
     }
     if (!integral) {
@@ -600,15 +609,13 @@ void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {
         size_t bytes = B.bytes;
         PLV_CUDA(cub::DeviceRadixSort::SortPairs(B.tmp, bytes, B.ekey, B.ekey2, B.eval, B.eval2, ne,
                                                  0, B.nb, st));
-        k_stage_deltas<<<grid_for(ne, 256), 256, 0, st>>>(S, B.ekey2, B.eval2, ne, B.dW, B.dA);
+        // folds of short community runs + the scatter; long runs next
+        k_stage_fold<<<grid_for(ne > S.ns ? ne : S.ns, 256), 256, 0, st>>>(S, B.ekey2, B.eval2, ne,
+                                                                          B.lrun, B.lcnt);
         PLV_LAUNCH_CHECK();
-        PLV_CUDA(cudaMemsetAsync(B.lcnt, 0, sizeof(unsigned long long), st));
-        k_stage_fold<<<grid_for(ne, 256), 256, 0, st>>>(S, B.ekey2, ne, B.dW, B.dA, B.lrun, B.lcnt);
+        k_stage_fold_long<<<148 * 2, 256, 0, st>>>(S, B.ekey2, B.eval2, ne, B.lrun, B.lcnt);
         PLV_LAUNCH_CHECK();
-        k_stage_fold_long<<<148 * 2, 256, 0, st>>>(S, B.ekey2, ne, B.dW, B.dA, B.lrun, B.lcnt);
-        PLV_LAUNCH_CHECK();
-    }
-    if (!indep) {
+    } else if (!indep) {
         k_stage_scatter<<<grid_for(S.ns, 256), 256, 0, st>>>(S);
         PLV_LAUNCH_CHECK();
     }

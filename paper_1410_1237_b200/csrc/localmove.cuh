@@ -145,6 +145,7 @@ struct StageArgs {
     unsigned long long *nbig = nullptr;
     int32_t *huge = nullptr;  // huge movers (live folds by whole blocks)
     unsigned long long *nhuge = nullptr;
+    unsigned long long *lcnt = nullptr;  // long community runs of the fold (reset by prep)
     // incremental modularity (pairwise.cuh): mark the depth-d0 tree nodes of
     // both communities of every mover (nullptr: off)
     uint8_t *dirty = nullptr;
@@ -160,7 +161,6 @@ struct ApplyBuffers {
     int32_t *eval = nullptr, *eval2 = nullptr;
     void *tmp = nullptr;
     size_t bytes = 0;
-    double *dW = nullptr, *dA = nullptr;  // sorted event deltas
     int64_t *lrun = nullptr;              // heads of long community runs
     unsigned long long *lcnt = nullptr;
     int32_t *big = nullptr;               // high-degree movers, then huge movers
