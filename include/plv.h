@@ -275,6 +275,19 @@ int plv_compose(const int32_t *map, const int32_t *assign, const int32_t *renumb
 int plv_parse_edge_list(const uint8_t *text, int64_t len, int32_t *u, int32_t *v, double *w,
                         int64_t cap, int64_t *info_h, void *stream);
 
+/* ------------------------------------------------------- post-processing */
+
+/* write_assignment's file body (PL/engine.py:318-322): "i c\n" per vertex,
+ * decimal, from a device assignment of int32 (elem_bytes 4) or int64 (8).
+ * len_h = the byte length; the text is written to out (device) only when it
+ * fits cap. */
+int plv_format_assignment(const void *assign, int elem_bytes, int64_t n, uint8_t *out,
+                          int64_t cap, int64_t *len_h, void *stream);
+/* compare_partitions' contingency counts (PL/evaluation.py:68-86) for int64
+ * labelings s, p of n vertices: out_h = {sum over (s,p) cells of C(cell,2),
+ * sum over classes of s of C(class,2), same for p}. */
+int plv_pair_counts(const int64_t *s, const int64_t *p, int64_t n, int64_t *out_h, void *stream);
+
 /* ------------------------------------------------------------ generators */
 
 /* Counter-based synthetic graphs (BASELINE.json configs), identical to the

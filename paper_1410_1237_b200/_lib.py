@@ -79,6 +79,8 @@ _SIGS = {
     "plv_rebuild_records": [_P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P],
     "plv_compose": [_P, _P, _P, _I64, _P, _P],
     "plv_parse_edge_list": [_P, _I64, _P, _P, _P, _I64, _P, _P],
+    "plv_format_assignment": [_P, _INT, _I64, _P, _I64, _P, _P],
+    "plv_pair_counts": [_P, _P, _I64, _P, _P],
     "plv_gen_rmat": [_U64, _INT, _I64, _D, _D, _D, _D, _D, _P, _P, _P, _I64, _P, _P],
     "plv_gen_sbm": [_U64, _I64, _I64, _D, _D, _P, _P, _P, _I64, _P, _P],
     "plv_gen_grid": [_U64, _I64, _D, _I64, _D, _P, _P, _P, _I64, _P, _P],
