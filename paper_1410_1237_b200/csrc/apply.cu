@@ -67,23 +67,31 @@ __device__ __forceinline__ void stage_big_warps(const StageArgs &A, int64_t gw, 
         const int32_t i = A.subset[x], b = A.target[x], a = A.assign[i];
         const int64_t e0 = A.off[i], e1 = A.off[i + 1];
         double fa = 0.0, fb = 0.0;
-        for (int64_t c0 = e0; c0 < e1; c0 += 32) {
-            int64_t e = c0 + lane;
-            int32_t c = -1;
-            double w = 0.0;
-            if (e < e1) {
-                int32_t j = A.nbr[e];
-                if (j != i) {
-                    c = live_comm(A, j, x);
-                    w = A.wts[e];
-                }
+        // four 32-entry chunks per round: their loads (row, then live
+        // community) are in flight together; the folds stay in entry order
+        constexpr int G = 4;
+        for (int64_t g0 = e0; g0 < e1; g0 += 32 * G) {
+            int32_t jj[G], cc[G];
+            double ww[G];
+#pragma unroll
+            for (int u = 0; u < G; u++) {
+                const int64_t e = g0 + 32 * u + lane;
+                jj[u] = e < e1 ? A.nbr[e] : i;
+                ww[u] = e < e1 ? A.wts[e] : 0.0;
             }
-            unsigned ma = __ballot_sync(FULL, c == a);
-            unsigned mb = __ballot_sync(FULL, c == b && c != a);
-            for (unsigned mm = ma; mm; mm &= mm - 1)
-                fa = dadd(fa, __shfl_sync(FULL, w, __ffs(mm) - 1));
-            for (unsigned mm = mb; mm; mm &= mm - 1)
-                fb = dadd(fb, __shfl_sync(FULL, w, __ffs(mm) - 1));
+#pragma unroll
+            for (int u = 0; u < G; u++) cc[u] = jj[u] != i ? live_comm(A, jj[u], x) : -1;
+#pragma unroll
+            for (int u = 0; u < G; u++) {
+                const int32_t c = cc[u];
+                const double w = ww[u];
+                unsigned ma = __ballot_sync(FULL, c == a);
+                unsigned mb = __ballot_sync(FULL, c == b && c != a);
+                for (unsigned mm = ma; mm; mm &= mm - 1)
+                    fa = dadd(fa, __shfl_sync(FULL, w, __ffs(mm) - 1));
+                for (unsigned mm = mb; mm; mm &= mm - 1)
+                    fb = dadd(fb, __shfl_sync(FULL, w, __ffs(mm) - 1));
+            }
         }
         if (lane == 0) mover_deltas(A, x, i, a, b, fa, fb, integral);
     }
@@ -92,7 +100,7 @@ __device__ __forceinline__ void stage_big_warps(const StageArgs &A, int64_t gw, 
 // One block per huge mover (> APPLY_HUGE entries): the row's entries whose
 // live community is a or b are compacted in order (block scan), then thread 0
 // folds them -- the chain is only the matching entries, the scan is parallel.
-constexpr int64_t APPLY_HUGE = 128;
+constexpr int64_t APPLY_HUGE = 1024;
 // Movers with longer rows fold their live e_a / e_b with a whole warp: a
 // thread's fold is a chain of dependent loads per entry (neighbour, position,
 // live community), a warp's is one round per 32 entries.
@@ -110,6 +118,30 @@ __device__ __forceinline__ void stage_huge_block(const StageArgs &A, int64_t b0,
         const int64_t x = A.huge[q];
         const int32_t i = A.subset[x], b = A.target[x], a = A.assign[i];
         const int64_t e0 = A.off[i], e1 = A.off[i + 1];
+        // Fast path: if no neighbour that precedes i in the subset has moved,
+        // every live community is the snapshot one and decide's exact folds
+        // e_old / e_best are e_a / e_b.  Rows are sorted and the subset is
+        // ascending, so only the row prefix j < i can hold such neighbours --
+        // short for the low-id hubs of R-MAT graphs.
+        bool early = false;
+        for (int64_t base = e0; base < e1; base += 256) {
+            const int64_t e = base + tid;
+            bool past = true;
+            if (e < e1) {
+                const int32_t j = A.nbr[e];
+                past = j >= i;
+                if (!past) {
+                    const int64_t p =
+                        (A.flags & PLV_F_IDENTITY) ? (int64_t)j : (int64_t)A.pos[j];
+                    early |= p >= 0 && p < x && A.moved[p];
+                }
+            }
+            if (__syncthreads_or(early || past)) break;
+        }
+        if (!__syncthreads_or(early)) {
+            if (tid == 0) mover_deltas(A, x, i, a, b, A.e_old[x], A.e_best[x], integral);
+            continue;
+        }
         double fa = 0.0, fb = 0.0;  // thread 0's accumulators
         for (int64_t base = e0; base < e1; base += 256) {
             int64_t e = base + tid;
@@ -293,12 +325,18 @@ __device__ __forceinline__ void fold_events(const StageArgs &A, const uint32_t *
 constexpr int SHORT_EVENTS = 32;  // longer community runs are folded by a whole block
 
 __global__ void k_stage_fold(StageArgs A, const uint32_t *key, const int32_t *val, int64_t ne,
-                             int64_t *lrun, unsigned long long *lcnt) {
+                             int64_t *lrun, unsigned long long *lcnt, double *dW, double *dA) {
     const bool indep = A.flags & PLV_F_INDEPENDENT;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ne;
          p += (int64_t)gridDim.x * blockDim.x) {
         uint32_t c = key[p];
         if (c == SENTINEL) continue;
+        {  // every event's delta, in sorted order, for the long-run folds
+            double w, a;
+            event_delta(A, val[p], w, a);
+            dW[p] = w;
+            dA[p] = a;
+        }
         if (p > 0 && key[p - 1] == c) continue;
         if (p + SHORT_EVENTS < ne && key[p + SHORT_EVENTS] == c) {
             lrun[atomicAdd(lcnt, 1ull)] = p;
@@ -319,8 +357,8 @@ __global__ void k_stage_fold(StageArgs A, const uint32_t *key, const int32_t *va
 
 // Long community runs: one block each, block-staged ordered folds.
 __global__ void __launch_bounds__(256) k_stage_fold_long(StageArgs A, const uint32_t *key,
-                                                        const int32_t *val, int64_t ne,
-                                                        const int64_t *lrun,
+                                                        const double *dW, const double *dA,
+                                                        int64_t ne, const int64_t *lrun,
                                                         unsigned long long *lcnt) {
     __shared__ double sb[4 * FOLD_CH];
     __shared__ int64_t s_end;
@@ -342,7 +380,10 @@ __global__ void __launch_bounds__(256) k_stage_fold_long(StageArgs A, const uint
         __syncthreads();
         double W = A.w_int[c], At = A.a_tot[c];
         block_fold2(
-            [=] __device__(int64_t t, double &x, double &y) { event_delta(A, val[p + t], x, y); },
+            [=] __device__(int64_t t, double &x, double &y) {
+                x = dW[p + t];
+                y = dA[p + t];
+            },
             s_end - p, W, At, sb);
         if (threadIdx.x == 0) {
             A.w_int[c] = W;
@@ -532,6 +573,8 @@ void ApplyBuffers::alloc(int64_t ta_len, int64_t max_ns, int64_t n, cudaStream_t
     ekey2 = dalloc<uint32_t>(ne);
     eval = dalloc<int32_t>(ne);
     eval2 = dalloc<int32_t>(ne);
+    dW = dalloc<double>(ne);
+    dA = dalloc<double>(ne);
     big_cap = max_ns ? max_ns : 1;
     big = dalloc<int32_t>(2 * big_cap);  // big movers, then huge movers
     nbig = dalloc<unsigned long long>(2);
@@ -555,7 +598,7 @@ void ApplyBuffers::alloc(int64_t ta_len, int64_t max_ns, int64_t n, cudaStream_t
 
 void ApplyBuffers::release() {
     cudaDeviceSynchronize();  // buffers go back to the pool idle
-    void *ps[] = {ta, tb, ekey, ekey2, eval, eval2, tmp, lrun, lcnt, big, nbig};
+    void *ps[] = {ta, tb, ekey, ekey2, eval, eval2, tmp, dW, dA, lrun, lcnt, big, nbig};
     for (void *p : ps)
         pool_free(p);
     big = nullptr;
@@ -565,6 +608,7 @@ void ApplyBuffers::release() {
     ta = tb = nullptr;
     ekey = ekey2 = nullptr;
     eval = eval2 = nullptr;
+    dW = dA = nullptr;
     tmp = nullptr;
 }
 
@@ -610,10 +654,10 @@ void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {
         PLV_CUDA(cub::DeviceRadixSort::SortPairs(B.tmp, bytes, B.ekey, B.ekey2, B.eval, B.eval2, ne,
                                                  0, B.nb, st));
         // folds of short community runs + the scatter; long runs next
-        k_stage_fold<<<grid_for(ne > S.ns ? ne : S.ns, 256), 256, 0, st>>>(S, B.ekey2, B.eval2, ne,
-                                                                          B.lrun, B.lcnt);
+        k_stage_fold<<<grid_for(ne > S.ns ? ne : S.ns, 256), 256, 0, st>>>(
+            S, B.ekey2, B.eval2, ne, B.lrun, B.lcnt, B.dW, B.dA);
         PLV_LAUNCH_CHECK();
-        k_stage_fold_long<<<148 * 2, 256, 0, st>>>(S, B.ekey2, B.eval2, ne, B.lrun, B.lcnt);
+        k_stage_fold_long<<<148 * 2, 256, 0, st>>>(S, B.ekey2, B.dW, B.dA, ne, B.lrun, B.lcnt);
         PLV_LAUNCH_CHECK();
     } else if (!indep) {
         k_stage_scatter<<<grid_for(S.ns, 256), 256, 0, st>>>(S);

@@ -161,6 +161,7 @@ struct ApplyBuffers {
     int32_t *eval = nullptr, *eval2 = nullptr;
     void *tmp = nullptr;
     size_t bytes = 0;
+    double *dW = nullptr, *dA = nullptr;  // sorted event deltas (long-run folds)
     int64_t *lrun = nullptr;              // heads of long community runs
     unsigned long long *lcnt = nullptr;
     int32_t *big = nullptr;               // high-degree movers, then huge movers
