@@ -484,19 +484,20 @@ __device__ __forceinline__ double group_sum(unsigned grp, double w) {
     return v;
 }
 
-// Accumulate one entry (c, w) with warp aggregation: lanes with the same
-// community combine (any order) before one atomic per group.
+// Accumulate one entry (c, w) into the any-order table (sum and term count)
+// and list the slot when this call inserted it.
 template <class Tab, class CL>
 __device__ __forceinline__ void accum_entry(int32_t *keys, double *vals, int32_t *cnt, Tab T,
                                             int32_t c, double w, int lane, CL *clist, int *ncl) {
-    unsigned grp = __match_any_sync(FULL, c);
-    double v = group_sum(grp, w);
+    // every lane adds its own entry: shared-memory atomics serialise lanes
+    // that hit the same slot, which measured cheaper than grouping the warp's
+    // lanes by community first (match + group sums)
     bool fresh = false;
     uint32_t s = 0;
-    if (c >= 0 && lane == __ffs(grp) - 1) {
+    if (c >= 0) {
         s = probe_insert_f(keys, c, T, &fresh);
-        atomicAdd(vals + s, v);
-        atomicAdd(cnt + s, __popc(grp));
+        atomicAdd(vals + s, w);
+        atomicAdd(cnt + s, 1);
     }
     unsigned fm = __ballot_sync(FULL, fresh);  // one list append per warp
     if (fm) {
@@ -973,19 +974,21 @@ __global__ void k_hub_accum(DecideArgs A, const int64_t *eoff, const int64_t *to
             }
         }
         TR_MARK
-        // group lanes by (hub, community)
         if (DENSE && t < E) H.cbuf[t] = c;
+        if (DENSE) {  // every lane adds its own entry: plain reductions, no grouping
+            if (c >= 0) {
+                const int64_t d = q * H.dn + c;
+                atomicAdd(H.dval + d, w);
+                atomicAdd(H.dcnt + d, 1);
+                atomicMin(H.dmk + d, (int32_t)(t - eoff[q]));
+            }
+            continue;
+        }
+        // hash tables: group lanes by (hub, community), one claim per group
         const uint64_t key = c >= 0 ? (((uint64_t)q << 32) | (uint32_t)c) : ~0ull;
         const unsigned grp = __match_any_sync(FULL, key);
         const double v = group_sum(grp, w);
-        if (DENSE && c >= 0 && lane == __ffs(grp) - 1) {
-            // dense: plain reductions into the hub's community arrays; the
-            // group leader holds the group's first row position
-            const int64_t d = q * H.dn + c;
-            atomicAdd(H.dval + d, v);
-            atomicAdd(H.dcnt + d, __popc(grp));
-            atomicMin(H.dmk + d, (int32_t)(t - eoff[q]));
-        } else if (c >= 0 && lane == __ffs(grp) - 1) {
+        if (c >= 0 && lane == __ffs(grp) - 1) {
             const int64_t base = toff[q];
             const uint32_t mask = (uint32_t)(toff[q + 1] - base - 1);
             bool fresh;
