@@ -858,6 +858,7 @@ __device__ __forceinline__ void block_decide(const DecideArgs &A, int64_t x, int
 }
 
 constexpr int T2_FU = 1;
+constexpr int T2_U = 1;  // row entries per thread in flight during the accumulation (2 measured slower)
 constexpr int T2_WIDE_MAX = 148;  // tiers 2-3 with at most this many vertices: wide blocks  // row entries per thread per exact-fold chunk in tier 2
 
 // Tiers 2 and 3: block per vertex, the table (TS slots) in dynamic shared
@@ -890,7 +891,7 @@ __global__ void __launch_bounds__(NT) k_decide_t2(DecideArgs A, TierRef L, int64
         const int64_t deg = e1 - e0;
         uint32_t ts = 64;
         while (ts < (uint64_t)(deg + deg / 2 + 2)) ts <<= 1;
-        block_decide<NT, 1, T2_FU>(A, L.x[q], L.vid[q], e0, e1, PowTab{ts - 1}, keys, vals, cntt,
+        block_decide<NT, T2_U, T2_FU>(A, L.x[q], L.vid[q], e0, e1, PowTab{ts - 1}, keys, vals, cntt,
                                    clist, &ncl, S, my_cand, tr_on && tr.n < 2 ? &tr : nullptr);
     }
     if (A.cand && tid == 0 && my_cand) atomicAdd(A.cand, my_cand);
@@ -987,15 +988,20 @@ __global__ void k_hub_accum(DecideArgs A, const int64_t *eoff, const int64_t *to
         // hash tables: group lanes by (hub, community), one claim per group
         const uint64_t key = c >= 0 ? (((uint64_t)q << 32) | (uint32_t)c) : ~0ull;
         const unsigned grp = __match_any_sync(FULL, key);
-        const double v = group_sum(grp, w);
-        if (c >= 0 && lane == __ffs(grp) - 1) {
+        const int leader = __ffs(grp) - 1;
+        uint32_t s = 0;
+        if (c >= 0 && lane == leader) {
             const int64_t base = toff[q];
             const uint32_t mask = (uint32_t)(toff[q + 1] - base - 1);
             bool fresh;
-            const uint32_t s = probe_claim(hkeys + base, c, mask, &fresh);
-            atomicAdd(hvals + base + s, v);
-            atomicAdd(hcnt + base + s, __popc(grp));
+            s = probe_claim(hkeys + base, c, mask, &fresh);
             if (fresh && c == c_old) H.sold[q] = (int32_t)s;
+        }
+        s = __shfl_sync(FULL, s, leader);  // the group's slot; every lane adds its entry
+        if (c >= 0) {
+            const int64_t base = toff[q];
+            atomicAdd(hvals + base + s, w);
+            atomicAdd(hcnt + base + s, 1);
         }
     }
     TR_END(1)
