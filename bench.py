@@ -66,6 +66,8 @@ def _args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-louvain", action="store_true", help="skip the full run() timing")
     p.add_argument("--mode", choices=["colored", "uncolored"], default="colored")
+    p.add_argument("--partitioned", action="store_true",
+                   help="use the partitioned (NCCL) engine even on one rank (plumbing check)")
     return p.parse_args()
 
 
@@ -310,7 +312,7 @@ def run_ours(args):
                                           st["sizes"])
     coloring = col if args.mode == "colored" else None
     comm = None
-    if ws > 1:
+    if ws > 1 or args.partitioned:
         # 1D vertex partition: each rank decides its slice of every stage, NCCL
         # broadcasts of the decided slices inside the iteration graph, every
         # rank replays the exact apply
@@ -469,7 +471,7 @@ def run_ours(args):
                        "graph": {"n": n, "M": M, "nnz": nnz, "colours": ncol,
                                  "integral": g.integral},
                        "parallelism": f"vertex-partition{ws} (NCCL slice broadcasts per stage)"
-                       if ws > 1 else "single",
+                       if comm is not None else "single",
                        "l2": "inputs larger than L2 (CSR %.0f MB)" % (nnz * 12 / 1e6)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic(args.mode, scale, args.config),
@@ -489,10 +491,11 @@ def run_ours(args):
             "louvain": louv,
         }
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if comm is not None:
         eng.close()
         from paper_1410_1237_b200 import dist as pdist
         pdist.destroy_communicator(comm)
+    if ws > 1:
         dist.destroy_process_group()
 
 
