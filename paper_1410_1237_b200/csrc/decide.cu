@@ -858,6 +858,7 @@ __device__ __forceinline__ void block_decide(const DecideArgs &A, int64_t x, int
 }
 
 constexpr int T2_FU = 1;
+constexpr int T2A_NT = 128;  // threads per tier-2 block (64 and 256 measured slower)
 constexpr int T2_U = 1;  // row entries per thread in flight during the accumulation (2 measured slower)
 constexpr int T2_WIDE_MAX = 148;  // tiers 2-3 with at most this many vertices: wide blocks  // row entries per thread per exact-fold chunk in tier 2
 
@@ -1559,7 +1560,7 @@ void ensure_decide_attrs() {
     int dev;
     PLV_CUDA(cudaGetDevice(&dev));
     if (dev_done == dev) return;
-    PLV_CUDA(cudaFuncSetAttribute(k_decide_t2<T2A_TS, T2A_MAXD, 128>,
+    PLV_CUDA(cudaFuncSetAttribute(k_decide_t2<T2A_TS, T2A_MAXD, T2A_NT>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)t2_smem(T2A_TS)));
     PLV_CUDA(cudaFuncSetAttribute(k_decide_t2<T2_TS, T2_MAXD, BLK>,
@@ -1620,7 +1621,7 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
     // few vertices (a late colour class): one wide block each, so a vertex's
     // latency-bound rounds shrink; many: narrow blocks, more vertices per SM
     if (sp.tcount[2] > T2_WIDE_MAX) {
-        k_decide_t2<T2A_TS, T2A_MAXD, 128><<<grid_for(sp.tcount[2], 1, 1 << 30), 128,
+        k_decide_t2<T2A_TS, T2A_MAXD, T2A_NT><<<grid_for(sp.tcount[2], 1, 1 << 30), T2A_NT,
                                              t2_smem(T2A_TS), ts[2]>>>(
             A, tier_ref(P, sp, 2), sp.tcount[2]);
         PLV_LAUNCH_CHECK();
