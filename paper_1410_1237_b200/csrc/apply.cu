@@ -406,6 +406,7 @@ __global__ void k_stage_scatter(StageArgs A) {
 // (SA_ITEMS, the events per thread, shadows the namespace constant.)
 template <int SA_ITEMS>
 __global__ void __launch_bounds__(SA_THREADS) k_stage_apply_small(StageArgs A, int nb) {
+    static_assert(SA_ITEMS % 2 == 0, "two events (leave, join) per vertex per thread");
     typedef cub::BlockRadixSort<uint32_t, SA_THREADS, SA_ITEMS, int32_t> Sort;
     __shared__ union {
         typename Sort::TempStorage sort;
@@ -423,27 +424,44 @@ __global__ void __launch_bounds__(SA_THREADS) k_stage_apply_small(StageArgs A, i
     uint32_t keys[SA_ITEMS];
     int32_t vals[SA_ITEMS];
     unsigned long long mv = 0;
+    // this thread's SA_ITEMS / 2 vertices (events 2x, 2x + 1): every load of a
+    // level is issued before any is used (the stores below would otherwise
+    // order each vertex's loads after the previous vertex's stores)
+    constexpr int VPT = SA_ITEMS / 2;
+    const int64_t x0 = (int64_t)tid * VPT;
+    int32_t iv[VPT], bv[VPT], av[VPT];
+    bool mvr[VPT];
 #pragma unroll
-    for (int it = 0; it < SA_ITEMS; it++) {
-        int64_t e = (int64_t)tid * SA_ITEMS + it;
-        keys[it] = SENTINEL;
-        vals[it] = (int32_t)e;
-        if (e < ne) {
-            int64_t x = e >> 1;
-            int32_t i = A.subset[x];
-            int32_t b = A.target[x];
-            int32_t a = A.assign[i];
-            if (A.moved[x] && a != b) {
-                keys[it] = (e & 1) ? (uint32_t)b : (uint32_t)a;
-                if (!(e & 1)) {
-                    double sw = A.selfw[i];
-                    A.ta[x] = dadd(dmul(2.0, A.e_old[x]), dmul(2.0, sw));
-                    A.tb[x] = dadd(dmul(2.0, A.e_best[x]), dmul(2.0, sw));
-                    atomicSub(A.sizes + a, 1);
-                    atomicAdd(A.sizes + b, 1);
-                    mv++;
-                }
-            }
+    for (int k = 0; k < VPT; k++) {
+        const int64_t x = x0 + k;
+        const bool ok = x < A.ns;
+        iv[k] = ok ? A.subset[x] : 0;
+        bv[k] = ok ? A.target[x] : 0;
+        mvr[k] = ok && A.moved[x];
+    }
+#pragma unroll
+    for (int k = 0; k < VPT; k++) av[k] = mvr[k] ? A.assign[iv[k]] : 0;
+    double sw[VPT], eo[VPT], eb[VPT];
+#pragma unroll
+    for (int k = 0; k < VPT; k++) {
+        mvr[k] = mvr[k] && av[k] != bv[k];
+        sw[k] = mvr[k] ? A.selfw[iv[k]] : 0.0;
+        eo[k] = mvr[k] ? A.e_old[x0 + k] : 0.0;
+        eb[k] = mvr[k] ? A.e_best[x0 + k] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < VPT; k++) {
+        const int64_t x = x0 + k;
+        keys[2 * k] = mvr[k] ? (uint32_t)av[k] : SENTINEL;
+        keys[2 * k + 1] = mvr[k] ? (uint32_t)bv[k] : SENTINEL;
+        vals[2 * k] = (int32_t)(2 * x);
+        vals[2 * k + 1] = (int32_t)(2 * x + 1);
+        if (mvr[k]) {
+            A.ta[x] = dadd(dmul(2.0, eo[k]), dmul(2.0, sw[k]));
+            A.tb[x] = dadd(dmul(2.0, eb[k]), dmul(2.0, sw[k]));
+            atomicSub(A.sizes + av[k], 1);
+            atomicAdd(A.sizes + bv[k], 1);
+            mv++;
         }
     }
     Sort(sm.sort).Sort(keys, vals, 0, nb);
@@ -456,8 +474,30 @@ __global__ void __launch_bounds__(SA_THREADS) k_stage_apply_small(StageArgs A, i
     if (mv) atomicAdd(&s_moves, mv);
     __syncthreads();
     double *dW = sdel, *dA = sdel + SA_THREADS * SA_ITEMS;
-    for (int64_t p = tid; p < ne; p += SA_THREADS)
-        if (sm.s.key[p] != SENTINEL) event_delta(A, sm.s.val[p], dW[p], dA[p]);
+    {  // event deltas, every level's loads in flight together
+        int32_t ev[SA_ITEMS], vx[SA_ITEMS];
+#pragma unroll
+        for (int it = 0; it < SA_ITEMS; it++) {
+            const int64_t p = tid + (int64_t)it * SA_THREADS;
+            ev[it] = (p < ne && sm.s.key[p] != SENTINEL) ? sm.s.val[p] : -1;
+        }
+#pragma unroll
+        for (int it = 0; it < SA_ITEMS; it++) vx[it] = ev[it] >= 0 ? A.subset[ev[it] >> 1] : 0;
+        double kk[SA_ITEMS], tt[SA_ITEMS];
+#pragma unroll
+        for (int it = 0; it < SA_ITEMS; it++) {
+            kk[it] = ev[it] >= 0 ? A.k[vx[it]] : 0.0;
+            tt[it] = ev[it] >= 0 ? ((ev[it] & 1) ? A.tb[ev[it] >> 1] : A.ta[ev[it] >> 1]) : 0.0;
+        }
+#pragma unroll
+        for (int it = 0; it < SA_ITEMS; it++) {
+            if (ev[it] < 0) continue;
+            const int64_t p = tid + (int64_t)it * SA_THREADS;
+            // leaving a: -(2 e_a + 2 sw), -k_i; joining b: +(2 e_b + 2 sw), +k_i (event_delta)
+            dW[p] = (ev[it] & 1) ? tt[it] : -tt[it];
+            dA[p] = (ev[it] & 1) ? kk[it] : -kk[it];
+        }
+    }
     __syncthreads();
     for (int64_t p = tid; p < ne; p += SA_THREADS) {
         uint32_t c = sm.s.key[p];
@@ -625,8 +665,8 @@ void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {
     }
     if (indep && !integral && S.ns <= SMALL_APPLY_MAX) {
         // events per thread sized to the stage (2 events per vertex)
-        if (2 * S.ns <= SA_THREADS)
-            k_stage_apply_small<1><<<1, SA_THREADS, 2 * SA_THREADS * sizeof(double), st>>>(S, B.nb);
+        if (2 * S.ns <= 2 * SA_THREADS)
+            k_stage_apply_small<2><<<1, SA_THREADS, 4 * SA_THREADS * sizeof(double), st>>>(S, B.nb);
         else if (2 * S.ns <= 4 * SA_THREADS)
             k_stage_apply_small<4><<<1, SA_THREADS, 8 * SA_THREADS * sizeof(double), st>>>(S, B.nb);
         else
