@@ -406,6 +406,8 @@ __global__ void k_stage_scatter(StageArgs A) {
 // (SA_ITEMS, the events per thread, shadows the namespace constant.)
 template <int SA_ITEMS>
 __global__ void __launch_bounds__(SA_THREADS) k_stage_apply_small(StageArgs A, int nb) {
+
+    pdl_wait();  // the decide outputs
     static_assert(SA_ITEMS % 2 == 0, "two events (leave, join) per vertex per thread");
     typedef cub::BlockRadixSort<uint32_t, SA_THREADS, SA_ITEMS, int32_t> Sort;
     __shared__ union {
@@ -525,6 +527,8 @@ __global__ void __launch_bounds__(SA_THREADS) k_stage_apply_small(StageArgs A, i
 // of its barriers.
 template <int VPL>
 __global__ void __launch_bounds__(32) k_stage_apply_tiny(StageArgs A) {
+
+    pdl_wait();  // the decide outputs
     constexpr int NE = 64 * VPL;
     __shared__ unsigned long long sk[NE];
     __shared__ double sw[NE], sa[NE];
@@ -659,20 +663,20 @@ void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {
     bool indep = S.flags & PLV_F_INDEPENDENT;
     bool integral = S.flags & PLV_F_INTEGRAL;
     if (indep && !integral && S.ns <= 32) {  // (a second vertex per lane measured slower)
-        k_stage_apply_tiny<1><<<1, 32, 0, st>>>(S);
-        PLV_LAUNCH_CHECK();
+        launch_pdl(k_stage_apply_tiny<1>, 1, 32, 0, st, S);
         return;
     }
     if (indep && !integral && S.ns <= SMALL_APPLY_MAX) {
         // events per thread sized to the stage (2 events per vertex)
         if (2 * S.ns <= 2 * SA_THREADS)
-            k_stage_apply_small<2><<<1, SA_THREADS, 4 * SA_THREADS * sizeof(double), st>>>(S, B.nb);
+            launch_pdl(k_stage_apply_small<2>, 1, SA_THREADS, 4 * SA_THREADS * sizeof(double), st, S,
+                       B.nb);
         else if (2 * S.ns <= 4 * SA_THREADS)
-            k_stage_apply_small<4><<<1, SA_THREADS, 8 * SA_THREADS * sizeof(double), st>>>(S, B.nb);
+            launch_pdl(k_stage_apply_small<4>, 1, SA_THREADS, 8 * SA_THREADS * sizeof(double), st, S,
+                       B.nb);
         else
-            k_stage_apply_small<SA_ITEMS><<<1, SA_THREADS, 2 * SA_THREADS * SA_ITEMS * sizeof(double),
-                                            st>>>(S, B.nb);
-        PLV_LAUNCH_CHECK();
+            launch_pdl(k_stage_apply_small<SA_ITEMS>, 1, SA_THREADS,
+                       2 * SA_THREADS * SA_ITEMS * sizeof(double), st, S, B.nb);
         return;
     }
     S.big = B.big;

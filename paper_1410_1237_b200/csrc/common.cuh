@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <string>
 #include <stdexcept>
+#include <utility>
 
 #include "../../include/plv.h"
 
@@ -99,6 +100,32 @@ struct Buf {
     T *get() const { return p; }
     operator T *() const { return p; }
 };
+
+// Programmatic dependent launch (sm_90+).  A kernel launched with
+// launch_pdl may be scheduled while its predecessor in the stream is still
+// finishing; it must execute pdl_wait() before touching anything the
+// predecessor writes (the wait returns at once for ordinary launches).
+// pdl_trigger() lets the next PDL kernel start launching early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+void count_launch();
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    PLV_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+    count_launch();
+}
 
 inline unsigned grid_for(int64_t work, int block, int64_t cap = 148 * 64) {
     int64_t g = (work + block - 1) / block;

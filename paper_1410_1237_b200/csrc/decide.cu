@@ -955,24 +955,35 @@ __device__ __forceinline__ int64_t hub_of(const int64_t *eoff, int64_t nh, int64
 template <bool DENSE>
 __global__ void k_hub_accum(DecideArgs A, const int64_t *eoff, const int64_t *toff, int64_t nh,
                             int64_t E, int32_t *hkeys, double *hvals, int32_t *hcnt, HubScratch H) {
+
     TR_BEGIN
     const int lane = threadIdx.x & 31;
+    bool waited = false;
     // warp-uniform loop: the whole warp takes 32 consecutive entries per step
     for (int64_t w0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); w0 < E;
          w0 += (int64_t)gridDim.x * blockDim.x) {
         int64_t t = w0 + lane;
-        int32_t c = -1, c_old = -1;
-        double w = 0.0;
+        int32_t c = -1, c_old = -1, i = -1, j = -1;
+        double w = 0.0, wv = 0.0;
         int64_t q = 0;
-        if (t < E) {
+        if (t < E) {  // the static part of the entry (graph, plan)
             q = hub_of(eoff, nh, t);
-            const int32_t i = H.vid[q];
+            i = H.vid[q];
             const int64_t e = H.row[q] + (t - eoff[q]);
-            const int32_t j = A.nbr[e];
+            j = A.nbr[e];
+            wv = A.wts[e];
+        }
+        if (!waited) {
+            // launched programmatically: the loads above overlap the previous
+            // stage's apply; the assignment and the tables only after it
+            pdl_wait();
+            waited = true;
+        }
+        if (t < E) {
             c_old = A.assign[i];
             if (j != i) {
                 c = A.assign[j];
-                w = A.wts[e];
+                w = wv;
             }
         }
         TR_MARK
@@ -1179,6 +1190,8 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *l
                                                  const int64_t *eoff, const int64_t *toff,
                                                  int32_t *hkeys, double *hvals, int32_t *hcnt,
                                                  HubScratch H) {
+
+    pdl_wait();  // the accumulation's sums
     TR_BEGIN
     __shared__ CertSmem<HSB> S;
     __shared__ int32_t cidx[HSB * HFU];
@@ -1664,17 +1677,15 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
                      P.dn};
         unsigned g2 = (unsigned)sp.hub_nblk;
         if (sp.hub_dense) {
-            k_hub_accum<true><<<grid_for(E, 256), 256, 0, st>>>(A, eoff, toff, nh, E, P.hkeys,
-                                                                P.hvals, P.hcnt, H);
-            PLV_LAUNCH_CHECK();
-            k_hub_pass<true><<<g2, HSB, 0, st>>>(A, list, eoff, toff, P.hkeys, P.hvals, P.hcnt, H);
-            PLV_LAUNCH_CHECK();
+            launch_pdl(k_hub_accum<true>, grid_for(E, 256), 256, 0, st, A, eoff, toff, nh, E,
+                       P.hkeys, P.hvals, P.hcnt, H);
+            launch_pdl(k_hub_pass<true>, g2, HSB, 0, st, A, list, eoff, toff, P.hkeys, P.hvals,
+                       P.hcnt, H);
         } else {
-            k_hub_accum<false><<<grid_for(E, 256), 256, 0, st>>>(A, eoff, toff, nh, E, P.hkeys,
-                                                                 P.hvals, P.hcnt, H);
-            PLV_LAUNCH_CHECK();
-            k_hub_pass<false><<<g2, HSB, 0, st>>>(A, list, eoff, toff, P.hkeys, P.hvals, P.hcnt, H);
-            PLV_LAUNCH_CHECK();
+            launch_pdl(k_hub_accum<false>, grid_for(E, 256), 256, 0, st, A, eoff, toff, nh, E,
+                       P.hkeys, P.hvals, P.hcnt, H);
+            launch_pdl(k_hub_pass<false>, g2, HSB, 0, st, A, list, eoff, toff, P.hkeys, P.hvals,
+                       P.hcnt, H);
         }
     }
 }
