@@ -182,6 +182,7 @@ constexpr int APPLY_HB = 148 * 4;
 constexpr int APPLY_BB = 148 * 8;
 
 __global__ void __launch_bounds__(256) k_stage_live(StageArgs A) {
+    pdl_wait();  // launched programmatically after its predecessor
     if (blockIdx.x < APPLY_HB) {
         stage_huge_block(A, blockIdx.x, APPLY_HB);
     } else {
@@ -195,6 +196,7 @@ __global__ void __launch_bounds__(256) k_stage_live(StageArgs A) {
 // scatter for independent stages).  Low-degree movers fold their live
 // e_a / e_b here; high-degree ones go to the k_stage_big worklist.
 __global__ void __launch_bounds__(256) k_stage_prep(StageArgs A) {
+    pdl_wait();  // launched programmatically after its predecessor
     if (A.lcnt && blockIdx.x == 0 && threadIdx.x == 0) *A.lcnt = 0ull;  // long runs of this stage
     const bool indep = A.flags & PLV_F_INDEPENDENT;
     const bool integral = A.flags & PLV_F_INTEGRAL;
@@ -326,6 +328,7 @@ constexpr int SHORT_EVENTS = 32;  // longer community runs are folded by a whole
 
 __global__ void k_stage_fold(StageArgs A, const uint32_t *key, const int32_t *val, int64_t ne,
                              int64_t *lrun, unsigned long long *lcnt, double *dW, double *dA) {
+    pdl_wait();  // launched programmatically after its predecessor
     const bool indep = A.flags & PLV_F_INDEPENDENT;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ne;
          p += (int64_t)gridDim.x * blockDim.x) {
@@ -360,6 +363,7 @@ __global__ void __launch_bounds__(256) k_stage_fold_long(StageArgs A, const uint
                                                         const double *dW, const double *dA,
                                                         int64_t ne, const int64_t *lrun,
                                                         unsigned long long *lcnt) {
+    pdl_wait();  // launched programmatically after its predecessor
     __shared__ double sb[4 * FOLD_CH];
     __shared__ int64_t s_end;
     const int64_t cnt = (int64_t)*lcnt;
@@ -394,6 +398,7 @@ __global__ void __launch_bounds__(256) k_stage_fold_long(StageArgs A, const uint
 }
 
 __global__ void k_stage_scatter(StageArgs A) {
+    pdl_wait();  // launched programmatically after its predecessor
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < A.ns;
          x += (int64_t)gridDim.x * blockDim.x)
         if (A.moved[x]) A.assign[A.subset[x]] = A.target[x];
@@ -686,11 +691,9 @@ void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {
     S.lcnt = B.lcnt;
     // worklist counters are zero on entry: allocation clears them, and the
     // apply that used them last cleared them after its last reader
-    k_stage_prep<<<grid_for((S.ns + 31) / 32 * 32, 256, 148 * 16), 256, 0, st>>>(S);
-    PLV_LAUNCH_CHECK();
+    launch_pdl(k_stage_prep, grid_for((S.ns + 31) / 32 * 32, 256, 148 * 16), 256, 0, st, S);
     if (!indep) {
-        k_stage_live<<<APPLY_HB + APPLY_BB, 256, 0, st>>>(S);
-        PLV_LAUNCH_CHECK();
+        launch_pdl(k_stage_live, APPLY_HB + APPLY_BB, 256, 0, st, S);
     }
     if (!integral) {
         int64_t ne = 2 * S.ns;
@@ -698,14 +701,14 @@ void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {
         PLV_CUDA(cub::DeviceRadixSort::SortPairs(B.tmp, bytes, B.ekey, B.ekey2, B.eval, B.eval2, ne,
                                                  0, B.nb, st));
         // folds of short community runs + the scatter; long runs next
-        k_stage_fold<<<grid_for(ne > S.ns ? ne : S.ns, 256), 256, 0, st>>>(
-            S, B.ekey2, B.eval2, ne, B.lrun, B.lcnt, B.dW, B.dA);
-        PLV_LAUNCH_CHECK();
-        k_stage_fold_long<<<148 * 2, 256, 0, st>>>(S, B.ekey2, B.dW, B.dA, ne, B.lrun, B.lcnt);
-        PLV_LAUNCH_CHECK();
+        launch_pdl(k_stage_fold, grid_for(ne > S.ns ? ne : S.ns, 256), 256, 0, st, S,
+                   (const uint32_t *)B.ekey2, (const int32_t *)B.eval2, ne, B.lrun, B.lcnt, B.dW,
+                   B.dA);
+        launch_pdl(k_stage_fold_long, 148 * 2, 256, 0, st, S, (const uint32_t *)B.ekey2,
+                   (const double *)B.dW, (const double *)B.dA, ne, (const int64_t *)B.lrun,
+                   B.lcnt);
     } else if (!indep) {
-        k_stage_scatter<<<grid_for(S.ns, 256), 256, 0, st>>>(S);
-        PLV_LAUNCH_CHECK();
+        launch_pdl(k_stage_scatter, grid_for(S.ns, 256), 256, 0, st, S);
     }
 }
 

@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(MODF_THREADS) k_mod_fused(const double *__rest
                                                             double *vals, unsigned int *ticket,
                                                             double *out, uint8_t *dirty,
                                                             const int64_t *full_if_zero) {
+    pdl_wait();  // the apply's totals
     __shared__ double sA[2 * MODF_MAX_NODES / 32], sB[2 * MODF_MAX_NODES / 32 / 32 + 2];
     __shared__ bool s_last;
     const uint64_t cnt = 1ull << d0;
@@ -282,9 +283,9 @@ void modularity_async(const double *w_int, const double *a_tot, int64_t n, doubl
         const int d0 = pw_depth(n);
         const int64_t cnt = 1ll << d0;
         if (cnt <= MODF_MAX_NODES) {
-            k_mod_fused<<<grid_for(2 * cnt * 32, MODF_THREADS, 148 * 8), MODF_THREADS, 0, s>>>(
-                w_int, a_tot, n, d0, two_m, scratch, ticket, out, nullptr, nullptr);
-            PLV_LAUNCH_CHECK();
+            launch_pdl(k_mod_fused, grid_for(2 * cnt * 32, MODF_THREADS, 148 * 8), MODF_THREADS, 0,
+                       s, w_int, a_tot, n, d0, two_m, scratch, ticket, out, (uint8_t *)nullptr,
+                       (const int64_t *)nullptr);
             return;
         }
     }
@@ -308,10 +309,9 @@ void modularity_async_inc(const double *w_int, const double *a_tot, int64_t n, d
     int d0 = 0;
     if (!modularity_inc_supported(n, &d0)) PLV_FAIL(PLV_EINVAL, "incremental modularity: tree too large");
     const int64_t cnt = 1ll << d0;
-    k_mod_fused<<<grid_for(2 * cnt * 32, MODF_THREADS, 148 * 8), MODF_THREADS, 0, s>>>(
-        w_int, a_tot, n, d0, 2.0 * m, scratch + 2, (unsigned int *)scratch, out, dirty,
-        full_if_zero);
-    PLV_LAUNCH_CHECK();
+    launch_pdl(k_mod_fused, grid_for(2 * cnt * 32, MODF_THREADS, 148 * 8), MODF_THREADS, 0, s,
+               w_int, a_tot, n, d0, 2.0 * m, scratch + 2, (unsigned int *)scratch, out, dirty,
+               full_if_zero);
 }
 
 // ---------------------------------------------------------------- reduceat

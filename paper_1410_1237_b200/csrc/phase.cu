@@ -483,6 +483,7 @@ __global__ void k_run_start(RunCtl *c) { c->t0 = gtimer(); }
 __global__ void k_run_ctl(RunCtl *c, const double *q, const unsigned long long *counters,
                           double *tr_q, unsigned long long *tr_mv, unsigned long long *tr_t,
                           const unsigned long long *chash, cudaGraphConditionalHandle h) {
+    pdl_wait();  // Q and the move counter
     const double q_cur = *q;
     const unsigned long long moves = counters[0];
     const int64_t it = c->it;
@@ -657,8 +658,9 @@ static void build_run_graph(Phase &P, int64_t cap, cudaStream_t s) {
                                  &P.ctl->it, cs);
         else
             modularity_async(P.w_int, P.a_tot, P.n, P.m, P.q, P.mod_scratch, cs);
-        k_run_ctl<<<1, 1, 0, cs>>>(P.ctl, P.q, P.counters, P.tr_q, P.tr_mv, P.tr_t, P.chash, h);
-        PLV_LAUNCH_CHECK();
+        launch_pdl(k_run_ctl, 1, 1, 0, cs, P.ctl, (const double *)P.q,
+                   (const unsigned long long *)P.counters, P.tr_q, P.tr_mv, P.tr_t,
+                   (const unsigned long long *)P.chash, h);
         if (P.chash) {
             k_cycle<<<grid_for(P.n, 256, 148 * 8), 256, 0, cs>>>(P.ctl, P.assign, P.sizes, P.a_tot,
                                                                 P.w_int, P.n, P.snap_i, P.snap_d);
