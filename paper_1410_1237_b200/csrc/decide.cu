@@ -281,10 +281,12 @@ struct TierRef {
 
 // ------------------------------------------------------------ tier 0
 
-__global__ void __launch_bounds__(256) k_decide_t0(DecideArgs A, TierRef L, int64_t cnt) {
+// Tier 0 over blocks [b, b + nb) of the launch (a thread per vertex).
+__device__ __forceinline__ void decide_t0_body(const DecideArgs &A, const TierRef &L, int64_t cnt,
+                                               int64_t b, int64_t nb) {
     unsigned long long my_cand = 0;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < cnt;
-         q += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t q = b * (int64_t)blockDim.x + threadIdx.x; q < cnt;
+         q += nb * (int64_t)blockDim.x) {
         const int64_t x = L.x[q];
         const int32_t i = L.vid[q];
         const int64_t e0 = L.row[q];
@@ -355,6 +357,10 @@ __global__ void __launch_bounds__(256) k_decide_t0(DecideArgs A, TierRef L, int6
     }
 }
 
+__global__ void __launch_bounds__(256) k_decide_t0(DecideArgs A, TierRef L, int64_t cnt) {
+    decide_t0_body(A, L, cnt, blockIdx.x, gridDim.x);
+}
+
 // Fold one 32-entry chunk (c, w per lane; c = -1 for none) into a table in
 // adjacency order.  wb: the chunk's 32 weights staged in lane order.
 template <class Tab>
@@ -371,8 +377,9 @@ __device__ __forceinline__ void fold_chunk(int32_t *keys, double *vals, Tab T, i
 
 // ------------------------------------------------------------ tier 1
 
-__global__ void __launch_bounds__(T1_WARPS * 32) k_decide_t1(DecideArgs A, TierRef L,
-                                                              int64_t cnt) {
+// Tier 1 over blocks [b, b + nb) of the launch (a warp per vertex).
+__device__ __forceinline__ void decide_t1_body(const DecideArgs &A, const TierRef &L, int64_t cnt,
+                                               int64_t b, int64_t nb) {
     __shared__ int32_t skeys[T1_WARPS][T1_TS];
     __shared__ double svals[T1_WARPS][T1_TS];
     __shared__ double swb[T1_WARPS][32];
@@ -381,8 +388,7 @@ __global__ void __launch_bounds__(T1_WARPS * 32) k_decide_t1(DecideArgs A, TierR
     double *vals = svals[wid];
     double *wb = swb[wid];
     unsigned long long my_cand = 0;
-    for (int64_t q = blockIdx.x * (int64_t)T1_WARPS + wid; q < cnt;
-         q += (int64_t)gridDim.x * T1_WARPS) {
+    for (int64_t q = b * (int64_t)T1_WARPS + wid; q < cnt; q += nb * (int64_t)T1_WARPS) {
         const int64_t x = L.x[q];
         const int32_t i = L.vid[q];
         const int64_t e0 = L.row[q], e1 = L.end[q];
@@ -445,6 +451,24 @@ __global__ void __launch_bounds__(T1_WARPS * 32) k_decide_t1(DecideArgs A, TierR
         for (int o = 16; o > 0; o >>= 1) my_cand += __shfl_xor_sync(FULL, my_cand, o);
         if (lane == 0 && my_cand) atomicAdd(A.cand, my_cand);
     }
+}
+
+__global__ void __launch_bounds__(T1_WARPS * 32) k_decide_t1(DecideArgs A, TierRef L,
+                                                              int64_t cnt) {
+    decide_t1_body(A, L, cnt, blockIdx.x, gridDim.x);
+}
+
+// A small stage whose vertices all sit in tiers 0 and 1: both tiers in one
+// launch (the first nb0 blocks take tier 0), on the stage's own stream --
+// no fork / join around the tiers, and a programmatic launch after the
+// previous kernel.
+__global__ void __launch_bounds__(256) k_decide_t01(DecideArgs A, TierRef L0, int64_t cnt0,
+                                                    TierRef L1, int64_t cnt1, int nb0) {
+    pdl_wait();
+    if ((int)blockIdx.x < nb0)
+        decide_t0_body(A, L0, cnt0, blockIdx.x, nb0);
+    else
+        decide_t1_body(A, L1, cnt1, blockIdx.x - nb0, gridDim.x - nb0);
 }
 
 // ------------------------------------------------ certification machinery
@@ -1593,9 +1617,12 @@ void launch_decide(const Plan &P, int64_t a, DecideArgs A, cudaStream_t st) {
     launch_decide_tiers(P, a, A, ts);
 }
 
+static bool launch_small_t01(const Plan &P, int64_t a, const DecideArgs &A, cudaStream_t st);
+
 void launch_decide_par(const Plan &P, int64_t a, DecideArgs A, cudaStream_t st,
                        const cudaStream_t *side, cudaEvent_t fork, const cudaEvent_t *join) {
     // tier t < NTIER - 1 on its own stream side[t]; the hubs on `st`
+    if (launch_small_t01(P, a, A, st)) return;
     const StagePlan &sp = P.st[a];
     cudaStream_t ts[NTIER] = {st, st, st, st, st};
     bool forked = false;
@@ -1617,6 +1644,20 @@ void launch_decide_par(const Plan &P, int64_t a, DecideArgs A, cudaStream_t st,
 static TierRef tier_ref(const Plan &P, const StagePlan &sp, int t) {
     const int64_t o = sp.tstart[t];
     return TierRef{P.tier_list + o, P.tier_vid + o, P.tier_row + o, P.tier_end + o};
+}
+
+constexpr int64_t T01_FUSE_MAX = 65536;  // vertices of a stage decided by k_decide_t01
+
+static bool launch_small_t01(const Plan &P, int64_t a, const DecideArgs &A, cudaStream_t st) {
+    const StagePlan &sp = P.st[a];
+    if (sp.tcount[2] || sp.tcount[3] || sp.tcount[4]) return false;
+    const int64_t tot = sp.tcount[0] + sp.tcount[1];
+    if (!tot || tot > T01_FUSE_MAX) return false;
+    const int nb0 = sp.tcount[0] ? (int)grid_for(sp.tcount[0], 256) : 0;
+    const int nb1 = sp.tcount[1] ? (int)grid_for(sp.tcount[1], T1_WARPS) : 0;
+    launch_pdl(k_decide_t01, nb0 + nb1, 256, 0, st, A, tier_ref(P, sp, 0), sp.tcount[0],
+               tier_ref(P, sp, 1), sp.tcount[1], nb0);
+    return true;
 }
 
 void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStream_t *ts) {
