@@ -318,6 +318,26 @@ static void filter_active(Phase &P, const int32_t *vtx, int64_t nst, cudaStream_
     PLV_CUDA(cudaStreamSynchronize(s));
 }
 
+static void capture_iteration(Phase &P) {
+    int prio_lo = 0, prio_hi = 0;
+    PLV_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    cudaStream_t cs;
+    PLV_CUDA(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, prio_hi));
+    PLV_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    try {
+        record_iteration(P, cs);
+    } catch (...) {
+        cudaGraph_t g2 = nullptr;
+        cudaStreamEndCapture(cs, &g2);
+        if (g2) cudaGraphDestroy(g2);
+        cudaStreamDestroy(cs);
+        throw;
+    }
+    PLV_CUDA(cudaStreamEndCapture(cs, &P.graph));
+    PLV_CUDA(cudaStreamDestroy(cs));
+    PLV_CUDA(cudaGraphInstantiate(&P.exec, P.graph, cudaGraphInstantiateFlagUseNodePriority));
+}
+
 static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double *wts,
                            const double *k, const double *selfw, int64_t n, double m, int flags,
                            const int32_t *labels, const int64_t *stage_off_h, const int32_t *vtx,
@@ -432,22 +452,9 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
         }
         PLV_CUDA(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming));
         PLV_CUDA(cudaStreamSynchronize(s));
-        if (world > 1 && !comm) return P;  // host-stepped (plv_phase_step)
-        cudaStream_t cs;
-        PLV_CUDA(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, prio_hi));
-        PLV_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-        try {
-            record_iteration(*P, cs);
-        } catch (...) {
-            cudaGraph_t g2 = nullptr;
-            cudaStreamEndCapture(cs, &g2);
-            if (g2) cudaGraphDestroy(g2);
-            cudaStreamDestroy(cs);
-            throw;
-        }
-        PLV_CUDA(cudaStreamEndCapture(cs, &P->graph));
-        PLV_CUDA(cudaStreamDestroy(cs));
-        PLV_CUDA(cudaGraphInstantiate(&P->exec, P->graph, cudaGraphInstantiateFlagUseNodePriority));
+        // the single-iteration graph is captured on the first plv_phase_iterate
+        // (run() only needs the whole-phase graph; comm engines capture now)
+        if (comm) capture_iteration(*P);
     } catch (...) {
         cudaStreamSynchronize(s);
         P->release();
@@ -458,7 +465,10 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
 }
 
 static void phase_iterate(Phase *P, cudaStream_t s, double *q, int64_t *moves, int64_t *cand) {
-    if (!P->exec) PLV_FAIL(PLV_EINVAL, "host-stepped partition: use plv_phase_step");
+    if (!P->exec) {
+        if (P->world > 1 && !P->comm) PLV_FAIL(PLV_EINVAL, "host-stepped partition: use plv_phase_step");
+        capture_iteration(*P);
+    }
     PLV_CUDA(cudaGraphLaunch(P->exec, s));
     PLV_CUDA(cudaStreamSynchronize(s));
     *q = P->h_out[0];
