@@ -15,6 +15,7 @@
 //  3. sizes with integer atomics; the assignment is scattered last.
 // Stages of colour classes with <= 2048 vertices run steps 1-3 in one CTA.
 #include "localmove.cuh"
+#include "lm_device.cuh"
 #include "csr.cuh"
 #include "pairwise.cuh"
 #include <cub/cub.cuh>
@@ -27,34 +28,6 @@ __global__ void k_fill_i32_a(int32_t *p, int64_t n, int32_t v) {
         p[i] = v;
 }
 
-// Live community of neighbour j for the mover at subset index x.
-__device__ __forceinline__ int32_t live_comm(const StageArgs &A, int32_t j, int64_t x) {
-    int64_t p = (A.flags & PLV_F_IDENTITY) ? (int64_t)j : (int64_t)A.pos[j];
-    if (p >= 0 && p < x && A.moved[p]) return A.target[p];
-    return A.assign[j];
-}
-
-// Deltas of one mover: 2 e_a + 2 sw leaving a, 2 e_b + 2 sw joining b (the
-// reference's `w_int[a] -= 2.0 * e_a + 2.0 * sw`, PL/_kernels.pyx:137-142),
-// stored for the ordered fold, or added with atomics for integral graphs;
-// sizes are integers either way.
-__device__ __forceinline__ void mover_deltas(const StageArgs &A, int64_t x, int32_t i, int32_t a,
-                                             int32_t b, double e_a, double e_b, bool integral) {
-    double sw = A.selfw[i], ki = A.k[i];
-    double ta = dadd(dmul(2.0, e_a), dmul(2.0, sw));
-    double tb = dadd(dmul(2.0, e_b), dmul(2.0, sw));
-    if (integral) {
-        atomicAdd(A.w_int + a, -ta);
-        atomicAdd(A.w_int + b, tb);
-        atomicAdd(A.a_tot + a, -ki);
-        atomicAdd(A.a_tot + b, ki);
-    } else {
-        A.ta[x] = ta;
-        A.tb[x] = tb;
-    }
-    atomicSub(A.sizes + a, 1);
-    atomicAdd(A.sizes + b, 1);
-}
 
 // One warp per high-degree mover: live e_a / e_b as ordered folds (the
 // matching lanes of each 32-entry chunk are added in lane order).
@@ -280,21 +253,6 @@ __global__ void __launch_bounds__(256) k_stage_prep(StageArgs A) {
     if (lane == 0 && my_moves) atomicAdd(A.moves, my_moves);
 }
 
-// Event deltas in sorted order: leaving a (-(2 e_a + 2 sw), -k_i), joining b
-// (+(2 e_b + 2 sw), +k_i).  x - y and x + (-y) round identically, so folding
-// the signed deltas reproduces `w_int[a] -= ...; a_tot[a] -= ki` exactly.
-__device__ __forceinline__ void event_delta(const StageArgs &A, int32_t v, double &dw,
-                                            double &da) {
-    int64_t x = v >> 1;
-    double ki = A.k[A.subset[x]];
-    if (v & 1) {
-        dw = A.tb[x];
-        da = ki;
-    } else {
-        dw = -A.ta[x];
-        da = -ki;
-    }
-}
 
 // Sequential fold of the run of community c starting at p; the deltas come
 // straight from the sorted event ids (loads batched so only the additions

@@ -27,6 +27,7 @@
 // decision and the reference's e values, bit for bit.  Integral graphs (all
 // weights integers, 2m < 2^52) are exact in any order and skip the check.
 #include "localmove.cuh"
+#include "lm_device.cuh"
 #include "csr.cuh"
 #include <cub/cub.cuh>
 
@@ -69,23 +70,6 @@ struct Trace {
         tr.flush(kid); \
     }
 
-__device__ __forceinline__ int64_t LBL(const int32_t *labels, int32_t c) {
-    return labels ? (int64_t)labels[c] : (int64_t)c;
-}
-
-// (gain, label) lexicographic order of PL/_kernels.pyx:88.
-__device__ __forceinline__ bool better(double g1, int64_t l1, double g2, int64_t l2) {
-    return g1 > g2 || (g1 == g2 && l1 < l2);
-}
-
-// Eq. 4 gain, PL/_kernels.pyx:86-87, evaluated with one rounding per op.
-__device__ __forceinline__ double gain_of(double e_c, double e_old, double m, double ki,
-                                          double a_old_excl, double atot_c, double four_m_sq) {
-    double t2 = ddiv(dsub(e_c, e_old), m);
-    double tk = dmul(2.0, ki);
-    double t5 = dsub(dmul(tk, a_old_excl), dmul(tk, atot_c));
-    return dadd(t2, ddiv(t5, four_m_sq));
-}
 
 // |sequential - any-order| bound for a sum of L positive terms near F.
 // A sum of at most two positive terms is the same in every order (0 + a = a,
@@ -208,31 +192,6 @@ __device__ __forceinline__ uint32_t probe_claim(int32_t *keys, int32_t c, uint32
     }
 }
 
-// Final decision of PL/_kernels.pyx:92-98.
-__device__ __forceinline__ void finish_vertex(const DecideArgs &A, int64_t x, int32_t c_old,
-                                              double e_old, double bg, int32_t bc, double be) {
-    bool moved = bg > 0.0 && bc != c_old;
-    if (moved && A.sizes[c_old] == 1 && A.sizes[bc] == 1 &&
-        LBL(A.labels, bc) > LBL(A.labels, c_old))
-        moved = false;  // singleton-pair guard
-    A.out_target[x] = moved ? bc : c_old;
-    A.out_moved[x] = moved ? 1 : 0;
-    A.out_e_old[x] = e_old;
-    A.out_e_best[x] = moved ? be : e_old;
-}
-
-struct Best {
-    double g;
-    int64_t l;
-    int32_t c;
-    double e;
-    int32_t n;  // term count of e (certification)
-};
-
-__device__ __forceinline__ void consider(Best &b, double g, int64_t l, int32_t c, double e,
-                                         int32_t n) {
-    if (better(g, l, b.g, b.l)) b = Best{g, l, c, e, n};
-}
 
 __device__ __forceinline__ void warp_best(Best &b) {
 #pragma unroll
@@ -271,91 +230,9 @@ __device__ __forceinline__ Best block_best(BestSmem<NT> &S, Best b) {
     return r;
 }
 
-// A tier's vertices: stage-local index x (outputs), vertex i, row [row, end),
-// laid out by the plan so a kernel's first loads are coalesced and independent.
-struct TierRef {
-    const int32_t *x;
-    const int32_t *vid;
-    const int64_t *row, *end;
-};
 
 // ------------------------------------------------------------ tier 0
 
-// Tier 0 over blocks [b, b + nb) of the launch (a thread per vertex).
-__device__ __forceinline__ void decide_t0_body(const DecideArgs &A, const TierRef &L, int64_t cnt,
-                                               int64_t b, int64_t nb) {
-    unsigned long long my_cand = 0;
-    for (int64_t q = b * (int64_t)blockDim.x + threadIdx.x; q < cnt;
-         q += nb * (int64_t)blockDim.x) {
-        const int64_t x = L.x[q];
-        const int32_t i = L.vid[q];
-        const int64_t e0 = L.row[q];
-        const int deg = (int)(L.end[q] - e0);
-        const int32_t c_old = A.assign[i];
-        // all row loads, then all community loads, in flight together
-        int32_t jj[T0_MAXD], cc[T0_MAXD];
-        double ww[T0_MAXD];
-#pragma unroll
-        for (int t = 0; t < T0_MAXD; t++) {
-            jj[t] = t < deg ? A.nbr[e0 + t] : i;
-            ww[t] = t < deg ? A.wts[e0 + t] : 0.0;
-        }
-#pragma unroll
-        for (int t = 0; t < T0_MAXD; t++) cc[t] = jj[t] != i ? A.assign[jj[t]] : -1;
-        int32_t keys[T0_MAXD];
-        double vals[T0_MAXD];
-        int nc = 0;
-#pragma unroll
-        for (int t = 0; t < T0_MAXD; t++) {
-            if (t < deg) {
-                if (cc[t] >= 0) {
-                    const int32_t c = cc[t];
-                    const double w = ww[t];
-                    bool found = false;
-#pragma unroll
-                    for (int s = 0; s < T0_MAXD; s++) {
-                        if (s < nc && keys[s] == c) {
-                            vals[s] = dadd(vals[s], w);
-                            found = true;
-                        }
-                    }
-                    if (!found) {
-#pragma unroll
-                        for (int s = 0; s < T0_MAXD; s++)
-                            if (s == nc) {
-                                keys[s] = c;
-                                vals[s] = w;  // 0.0 + w
-                            }
-                        nc++;
-                    }
-                }
-            }
-        }
-        my_cand += nc;
-        double e_old = 0.0;
-#pragma unroll
-        for (int s = 0; s < T0_MAXD; s++)
-            if (s < nc && keys[s] == c_old) e_old = vals[s];
-        double ki = A.k[i];
-        double a_old_excl = dsub(A.a_tot[c_old], ki);
-        Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
-#pragma unroll
-        for (int s = 0; s < T0_MAXD; s++) {
-            if (s < nc && keys[s] != c_old) {
-                int32_t c = keys[s];
-                consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq),
-                         LBL(A.labels, c), c, vals[s], 0);
-            }
-        }
-        finish_vertex(A, x, c_old, e_old, b.g, b.c, b.e);
-    }
-    if (A.cand) {
-        typedef cub::BlockReduce<unsigned long long, 256> BR;
-        __shared__ typename BR::TempStorage tmp;
-        unsigned long long tot = BR(tmp).Sum(my_cand);
-        if (threadIdx.x == 0 && tot) atomicAdd(A.cand, tot);
-    }
-}
 
 __global__ void __launch_bounds__(256) k_decide_t0(DecideArgs A, TierRef L, int64_t cnt) {
     decide_t0_body(A, L, cnt, blockIdx.x, gridDim.x);

@@ -167,6 +167,81 @@ inline int pw_depth(int64_t n, int64_t cap = 256) {
     }
 }
 
+// The same node values with a warp per node: a node of <= 256 elements is a
+// leaf, two leaves, or a leaf plus a split right half (two leaves); each leaf
+// goes to an octet of lanes, lane k of the octet owning accumulator r_k
+// (elements k, k+8, ... below the multiple of 8), the accumulators combined
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by xor-shuffles -- numpy's operation
+// order -- then the tail added by the octet's first lane.
+template <class F>
+__device__ __forceinline__ double pw_leaf_octet(const double *a, int64_t n, F f, int k) {
+    // n <= 128: lane k's accumulator takes elements k, k+8, ... (< lim); all
+    // of its loads are issued before the first addition (independent of the
+    // chain), then the additions run in numpy's order
+    double r = 0.0;
+    const int64_t lim = n >= 8 ? n - (n % 8) : 0;
+    double buf[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+        const int64_t i = k + 8 * u;
+        buf[u] = i < lim ? a[i] : 0.0;
+    }
+    double tail[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+        const int64_t i = lim + u;
+        tail[u] = (k == 0 && i < n) ? a[i] : 0.0;
+    }
+    if (lim) {
+        r = f(buf[0]);
+#pragma unroll
+        for (int u = 1; u < 16; u++)
+            if (k + 8 * u < lim) r = __dadd_rn(r, f(buf[u]));
+    }
+    double t = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+    t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 2));
+    t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 4));
+    if (k == 0) {
+        double res = lim ? t : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+            if (lim + u < n) res = __dadd_rn(res, f(tail[u]));
+        t = res;
+    }
+    return t;  // valid in the octet's first lane
+}
+
+template <class F>
+__device__ __forceinline__ double pw_node_warp(const double *a, int64_t n, int d0, uint64_t t,
+                                               F f) {
+    const int lane = threadIdx.x & 31, oct = lane >> 3, k = lane & 7;
+    int64_t lo, len;
+    pw_node(n, d0, t, &lo, &len);
+    int64_t off[3] = {0, 0, 0}, ln[3] = {len, 0, 0};
+    int nleaf = 1;
+    if (len > 128) {
+        const int64_t n2 = pw_split(len);
+        ln[0] = n2;
+        off[1] = n2;
+        ln[1] = len - n2;
+        nleaf = 2;
+        if (ln[1] > 128) {
+            const int64_t m2 = pw_split(ln[1]);
+            off[2] = off[1] + m2;
+            ln[2] = ln[1] - m2;
+            ln[1] = m2;
+            nleaf = 3;
+        }
+    }
+    const int o = oct < 3 ? oct : 2;
+    const int64_t my_len = oct < nleaf ? ln[o] : 0;
+    const double v = pw_leaf_octet(a + lo + off[o], my_len, f, k);
+    const double vL = __shfl_sync(0xffffffffu, v, 0);
+    const double vR = __shfl_sync(0xffffffffu, v, 8);
+    const double vRR = __shfl_sync(0xffffffffu, v, 16);
+    return nleaf == 1 ? vL : nleaf == 2 ? __dadd_rn(vL, vR) : __dadd_rn(vL, __dadd_rn(vR, vRR));
+}
+
 // Host-side launchers (pairwise.cu).
 // out_dev[0] = 0.0 + pairwise(f(a[0:n))) ; f = Ident or SqScaled.
 void pw_sum_async(const double *a, int64_t n, double *out_dev, cudaStream_t s);

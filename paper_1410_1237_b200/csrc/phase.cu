@@ -191,8 +191,7 @@ static void record_exchange(Phase &P, size_t a, cudaStream_t st) {
 }
 
 // Stage a's exact apply over the whole stage (replicated on every rank).
-static void record_apply(Phase &P, size_t a, cudaStream_t st, uint8_t *dirty = nullptr,
-                         unsigned long long *chash = nullptr) {
+static StageArgs stage_args(const Phase &P, size_t a, uint8_t *dirty, unsigned long long *chash) {
     const int64_t g = P.goff[a], ns = P.goff[a + 1] - g;
     StageArgs S{P.off, P.nbr, P.wts, P.k, P.selfw, P.vtx + g, ns, P.target + g,
                 P.moved + g, P.e_old + g, P.e_best + g, P.pos, P.flags,
@@ -202,7 +201,12 @@ static void record_apply(Phase &P, size_t a, cudaStream_t st, uint8_t *dirty = n
     S.chash = chash;
     S.tree_n = P.n;
     S.tree_d0 = P.mod_d0;
-    launch_apply(S, P.ab, st);
+    return S;
+}
+
+static void record_apply(Phase &P, size_t a, cudaStream_t st, uint8_t *dirty = nullptr,
+                         unsigned long long *chash = nullptr) {
+    launch_apply(stage_args(P, a, dirty, chash), P.ab, st);
 }
 
 static void record_finish(Phase &P, cudaStream_t st) {
