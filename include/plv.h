@@ -229,6 +229,9 @@ int plv_nccl_unique_id(uint8_t *id_h);
 int plv_nccl_comm_init(int64_t rank, int64_t world, const uint8_t *id_h, void **comm_h);
 int plv_nccl_comm_destroy(void *comm);
 
+/* Kernel nodes in the engine's single-iteration CUDA graph (captured now if
+ * needed): the kernels one plv_phase_iterate launches. */
+int plv_phase_graph_kernels(void *handle, int64_t *n_h);
 /* Sum over stages of the decide time of the last iteration (timing handles). */
 int plv_phase_decide_ms(void *handle, double *ms_h);
 int plv_phase_destroy(void *handle);

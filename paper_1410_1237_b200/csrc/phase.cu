@@ -91,6 +91,7 @@ struct Phase {
     unsigned long long *tr_mv = nullptr, *tr_t = nullptr;
     int64_t tr_cap = 0;
     bool run_graph_failed = false;
+    int64_t graph_kernels = 0;  // kernel nodes in the single-iteration graph
     uint8_t *dirty = nullptr;  // incremental modularity in the device loop (one stage)
     int mod_d0 = 0;
     // exact cycle skipping: XOR hash of the assignment (updated by apply), and
@@ -340,6 +341,17 @@ static void capture_iteration(Phase &P) {
     PLV_CUDA(cudaStreamEndCapture(cs, &P.graph));
     PLV_CUDA(cudaStreamDestroy(cs));
     PLV_CUDA(cudaGraphInstantiate(&P.exec, P.graph, cudaGraphInstantiateFlagUseNodePriority));
+    // kernel nodes of one iteration (evidence of the native path for bench.py)
+    size_t nn = 0;
+    PLV_CUDA(cudaGraphGetNodes(P.graph, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    PLV_CUDA(cudaGraphGetNodes(P.graph, nodes.data(), &nn));
+    P.graph_kernels = 0;
+    for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        PLV_CUDA(cudaGraphNodeGetType(nd, &t));
+        P.graph_kernels += t == cudaGraphNodeTypeKernel;
+    }
 }
 
 static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double *wts,
@@ -888,6 +900,17 @@ extern "C" int plv_phase_run(void *handle, double theta, int64_t max_iters, doub
     result_h[3] = 0;
     result_h[4] = 0;
     result_h[5] = 0;
+    PLV_EXIT
+}
+
+extern "C" int plv_phase_graph_kernels(void *handle, int64_t *n_h) {
+    PLV_ENTRY
+    plv::Phase *P = (plv::Phase *)handle;
+    if (!P->exec) {
+        if (P->world > 1 && !P->comm) PLV_FAIL(PLV_EINVAL, "host-stepped partition has no graph");
+        plv::capture_iteration(*P);
+    }
+    *n_h = P->graph_kernels;
     PLV_EXIT
 }
 

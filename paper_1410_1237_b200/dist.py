@@ -26,6 +26,7 @@ apply, with the NCCL broadcasts captured inside the iteration's CUDA graph.
 
 from __future__ import annotations
 
+import contextlib
 from dataclasses import dataclass
 
 import numpy as np
@@ -100,6 +101,24 @@ class DistributedIteration:
         return moves, self.ops.modularity()
 
 
+@contextlib.contextmanager
+def stdout_to_stderr():
+    """Route file descriptor 1 to stderr: NCCL prints its version banner on
+    stdout at first use, and stdout may carry machine-read output (bench.py's
+    JSON line)."""
+    import os
+    import sys
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        yield
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
+
+
 def nccl_communicator(rank: int, world: int, group=None):
     """NCCL communicator for PartitionedPhaseEngine (libplv binds NCCL at run
     time): rank 0 draws the unique id, torch.distributed broadcasts it."""
@@ -107,16 +126,17 @@ def nccl_communicator(rank: int, world: int, group=None):
     from . import _lib
     L = _lib.lib()
     idbuf = (ctypes.c_uint8 * _lib.NCCL_ID_BYTES)()
-    if rank == 0:
-        _lib.check(L.nccl_unique_id(ctypes.addressof(idbuf)), "nccl_unique_id")
-    if world > 1:
-        import torch.distributed as dist
-        obj = [bytes(idbuf)]
-        dist.broadcast_object_list(obj, src=0, group=group)
-        ctypes.memmove(idbuf, obj[0], _lib.NCCL_ID_BYTES)
     comm = ctypes.c_void_p()
-    _lib.check(L.nccl_comm_init(rank, world, ctypes.addressof(idbuf), ctypes.byref(comm)),
-               "nccl_comm_init")
+    with stdout_to_stderr():
+        if rank == 0:
+            _lib.check(L.nccl_unique_id(ctypes.addressof(idbuf)), "nccl_unique_id")
+        if world > 1:
+            import torch.distributed as dist
+            obj = [bytes(idbuf)]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            ctypes.memmove(idbuf, obj[0], _lib.NCCL_ID_BYTES)
+        _lib.check(L.nccl_comm_init(rank, world, ctypes.addressof(idbuf), ctypes.byref(comm)),
+                   "nccl_comm_init")
     return comm
 
 
@@ -204,6 +224,13 @@ class PartitionedPhaseEngine:
         _lib.check(_lib.lib().phase_iterate(self.handle, _lib.hp(self._q), _lib.hp(self._mv),
                                             _lib.hp(self._cand), _lib.stream()), "phase_iterate")
         return float(self._q[0]), int(self._mv[0]), int(self._cand[0])
+
+    def graph_kernels(self) -> int:
+        """Kernel nodes of one iteration's CUDA graph (plv_phase_graph_kernels)."""
+        _lib = self._lib
+        out = _lib.i64_host(1)
+        _lib.check(_lib.lib().phase_graph_kernels(self.handle, _lib.hp(out)), "graph_kernels")
+        return int(out[0])
 
     def step(self, stage: int, op: int):
         _lib = self._lib
