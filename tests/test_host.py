@@ -169,3 +169,14 @@ def test_gnm_matches_reference_generator(ref):
         g = rsyn.gnm_random_graph(50, 120, seed=seed, weight_range=(0.0, 2.0))
         rg = ref.Graph.from_edges(u, v, w, num_vertices=50)
         assert rg.same_as(g)
+
+
+def test_stdout_to_stderr_routes_fd1(capfd):
+    """NCCL's stdout banner is diverted so bench.py's stdout is one JSON line."""
+    import os
+    from paper_1410_1237_b200.dist import stdout_to_stderr
+    with stdout_to_stderr():
+        os.write(1, b"banner\n")
+    os.write(1, b"json\n")
+    out, err = capfd.readouterr()
+    assert out == "json\n" and "banner" in err

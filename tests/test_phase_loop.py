@@ -134,3 +134,19 @@ def test_cycle_skipping_run_matches_oracle(orc):
     assert [p.stats.iterations for p in h.phases] == [p.iterations for p in oh.phases]
     assert np.array_equal(h.final_assignment, oh.final_assignment)
     assert h.final_modularity == oh.final_modularity
+
+
+def test_iteration_graph_kernel_count():
+    """The single-iteration graph is captured on demand and reports its kernel
+    nodes (bench.py's gpu_launches)."""
+    u, v, w = syn.rmat_records(11, 8, seed=5)
+    g = pl.Graph.from_edges(u, v, w, num_vertices=1 << 11)
+    s, _ = _state(g)
+    col = pl.color_graph(g)
+    e = PhaseEngine(g, s, col)
+    k = e.graph_kernels()
+    assert k >= col.num_colors  # at least one decide kernel per colour stage
+    q1 = e.iterate()
+    assert e.graph_kernels() == k
+    assert q1[1] >= 0
+    e.close()
