@@ -4,7 +4,7 @@
 // (a sequential left fold per community) and takes the argmax of the Eq. 4
 // gain under (gain desc, label asc), then applies the singleton-pair guard.
 // Vertices of a stage are degree-binned once per plan:
-//   tier 0  deg <= 16     thread per vertex, candidates in registers, folds
+//   tier 0  deg <= 12     thread per vertex, candidates in registers, folds
 //                         in adjacency order (exact by construction)
 //   tier 1  deg <= 128    warp per vertex, shared-memory hash table, 32-entry
 //                         chunks folded in lane order (exact by construction)

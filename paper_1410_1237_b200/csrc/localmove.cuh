@@ -19,7 +19,7 @@
 namespace plv {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int T0_MAXD = 16;
+constexpr int T0_MAXD = 12;
 constexpr int T1_MAXD = 128;
 constexpr int T2A_MAXD = 680;  // tier 2: 1024-slot tables (>= 1.5 * (680 + 1))
 constexpr int T2_MAXD = 2048;   // tier 3: 4096-slot tables
