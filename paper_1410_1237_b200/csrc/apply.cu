@@ -73,7 +73,7 @@ __device__ __forceinline__ void stage_big_warps(const StageArgs &A, int64_t gw, 
 // One block per huge mover (> APPLY_HUGE entries): the row's entries whose
 // live community is a or b are compacted in order (block scan), then thread 0
 // folds them -- the chain is only the matching entries, the scan is parallel.
-constexpr int64_t APPLY_HUGE = 1024;
+constexpr int64_t APPLY_HUGE = 2048;
 // Movers with longer rows fold their live e_a / e_b with a whole warp: a
 // thread's fold is a chain of dependent loads per entry (neighbour, position,
 // live community), a warp's is one round per 32 entries.
