@@ -255,17 +255,19 @@ __device__ __forceinline__ void fold_chunk(int32_t *keys, double *vals, Tab T, i
 // ------------------------------------------------------------ tier 1
 
 // Tier 1 over blocks [b, b + nb) of the launch (a warp per vertex).
+// NW: warps per block of the launching kernel.
+template <int NW>
 __device__ __forceinline__ void decide_t1_body(const DecideArgs &A, const TierRef &L, int64_t cnt,
                                                int64_t b, int64_t nb) {
-    __shared__ int32_t skeys[T1_WARPS][T1_TS];
-    __shared__ double svals[T1_WARPS][T1_TS];
-    __shared__ double swb[T1_WARPS][32];
+    __shared__ int32_t skeys[NW][T1_TS];
+    __shared__ double svals[NW][T1_TS];
+    __shared__ double swb[NW][32];
     int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int32_t *keys = skeys[wid];
     double *vals = svals[wid];
     double *wb = swb[wid];
     unsigned long long my_cand = 0;
-    for (int64_t q = b * (int64_t)T1_WARPS + wid; q < cnt; q += nb * (int64_t)T1_WARPS) {
+    for (int64_t q = b * (int64_t)NW + wid; q < cnt; q += nb * (int64_t)NW) {
         const int64_t x = L.x[q];
         const int32_t i = L.vid[q];
         const int64_t e0 = L.row[q], e1 = L.end[q];
@@ -332,7 +334,7 @@ __device__ __forceinline__ void decide_t1_body(const DecideArgs &A, const TierRe
 
 __global__ void __launch_bounds__(T1_WARPS * 32) k_decide_t1(DecideArgs A, TierRef L,
                                                               int64_t cnt) {
-    decide_t1_body(A, L, cnt, blockIdx.x, gridDim.x);
+    decide_t1_body<T1_WARPS>(A, L, cnt, blockIdx.x, gridDim.x);
 }
 
 // A small stage whose vertices all sit in tiers 0 and 1: both tiers in one
@@ -345,7 +347,7 @@ __global__ void __launch_bounds__(256) k_decide_t01(DecideArgs A, TierRef L0, in
     if ((int)blockIdx.x < nb0)
         decide_t0_body(A, L0, cnt0, blockIdx.x, nb0);
     else
-        decide_t1_body(A, L1, cnt1, blockIdx.x - nb0, gridDim.x - nb0);
+        decide_t1_body<8>(A, L1, cnt1, blockIdx.x - nb0, gridDim.x - nb0);
 }
 
 // ------------------------------------------------ certification machinery
@@ -761,7 +763,7 @@ __device__ __forceinline__ void block_decide(const DecideArgs &A, int64_t x, int
 constexpr int T2_FU = 1;
 constexpr int T2A_NT = 128;  // threads per tier-2 block (64 and 256 measured slower)
 constexpr int T2_U = 1;  // row entries per thread in flight during the accumulation (2 measured slower)
-constexpr int T2_WIDE_MAX = 148;  // tiers 2-3 with at most this many vertices: wide blocks  // row entries per thread per exact-fold chunk in tier 2
+constexpr int T2_WIDE_MAX = 600;  // tiers 2-3 with at most this many vertices: wide blocks (64-1000 measured)
 
 // Tiers 2 and 3: block per vertex, the table (TS slots) in dynamic shared
 // memory; tier 2's small tables let 3x more vertices be in flight per SM.
@@ -1531,7 +1533,7 @@ static bool launch_small_t01(const Plan &P, int64_t a, const DecideArgs &A, cuda
     const int64_t tot = sp.tcount[0] + sp.tcount[1];
     if (!tot || tot > T01_FUSE_MAX) return false;
     const int nb0 = sp.tcount[0] ? (int)grid_for(sp.tcount[0], 256) : 0;
-    const int nb1 = sp.tcount[1] ? (int)grid_for(sp.tcount[1], T1_WARPS) : 0;
+    const int nb1 = sp.tcount[1] ? (int)grid_for(sp.tcount[1], 8) : 0;  // 8 warps per block
     launch_pdl(k_decide_t01, nb0 + nb1, 256, 0, st, A, tier_ref(P, sp, 0), sp.tcount[0],
                tier_ref(P, sp, 1), sp.tcount[1], nb0);
     return true;
