@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(NT) k_decide_t2(DecideArgs A, TierRef L, int64
 // ------------------------------------------------------------ tier 4 (hubs)
 
 constexpr int HSB = 512;            // threads per hub pass block
-constexpr int HSU = 2;              // table slots per thread in a pass block
+constexpr int HSU = 8;              // table slots per thread in a pass block (2, 4, 8 measured)
 constexpr int HTSL = HSB * HSU;     // table slots per pass block
 constexpr int HCPAD = 32;           // per-hub counters one 128-byte line apart
 constexpr int HUB_DENSE_KMAX = 64;  // stages with at most this many hubs may use dense arrays

@@ -30,9 +30,9 @@ constexpr int T2_TS = 4096;   // smem slots for tier 2 (>= 1.5 * (2048 + 1))
 constexpr int T2A_TS = 1024;
 constexpr int NTIER = 5;  // t0, t1, t2 (block, small table), t3 (block), t4 (hubs)
 
-constexpr int SMALL_APPLY_MAX = 2048;  // stage size handled by the one-CTA apply
+constexpr int SMALL_APPLY_MAX = 1024;  // stage size handled by the one-CTA apply (2048 measured slower)
 constexpr int SA_THREADS = 256;
-constexpr int SA_ITEMS = 16;  // 256 * 16 = 4096 events = 2 * SMALL_APPLY_MAX
+constexpr int SA_ITEMS = 8;   // 256 * 8 = 2048 events = 2 * SMALL_APPLY_MAX
 constexpr uint32_t SENTINEL = 0xFFFFFFFFu;
 
 struct DecideArgs {

@@ -1,0 +1,18 @@
+mkdir -p gpurun_out
+run() {  # name
+  python -m paper_1410_1237_b200.build > gpurun_out/kn_$1.build 2>&1 || { echo "build failed $1" > gpurun_out/kn_$1.txt; return; }
+  for r in 1 2; do
+    timeout 300 python bench.py --no-cpu-baseline --no-louvain --steps 10 > gpurun_out/kn_$1_c2_$r.json 2>/dev/null
+  done
+  timeout 300 python bench.py --config c4_chung_lu --no-cpu-baseline --no-louvain --steps 5 > gpurun_out/kn_$1_c4.json 2>/dev/null
+  timeout 300 python bench.py --no-cpu-baseline --no-louvain --steps 10 --mode uncolored > gpurun_out/kn_$1_u.json 2>/dev/null
+}
+D=paper_1410_1237_b200/csrc/decide.cu
+L=paper_1410_1237_b200/csrc/localmove.cuh
+run base2
+sed -i 's/^constexpr int HFU = 4; /constexpr int HFU = 8; /' $D; run hfu8
+sed -i 's/^constexpr int HFU = 8; /constexpr int HFU = 2; /' $D; run hfu2
+sed -i 's/^constexpr int HFU = 2; /constexpr int HFU = 4; /' $D
+sed -i 's/^constexpr int T2_FU = 1;/constexpr int T2_FU = 2;/' $D; run t2fu2
+sed -i 's/^constexpr int T2_FU = 2;/constexpr int T2_FU = 1;/' $D
+sed -i 's/^constexpr int HSU = 2; /constexpr int HSU = 4; /' $D; run hsu4
