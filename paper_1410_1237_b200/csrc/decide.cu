@@ -808,7 +808,7 @@ constexpr int HSB = 512;            // threads per hub pass block
 constexpr int HSU = 8;              // table slots per thread in a pass block (2, 4, 8 measured)
 constexpr int HTSL = HSB * HSU;     // table slots per pass block
 constexpr int HCPAD = 32;           // per-hub counters one 128-byte line apart
-constexpr int HUB_DENSE_KMAX = 64;  // stages with at most this many hubs may use dense arrays
+constexpr int HUB_DENSE_KMAX = 32;  // stages with at most this many hubs may use dense arrays (16-128 measured)
 constexpr int HFU = 4;              // row entries per thread per exact-fold chunk (hubs)
 
 // A candidate near its slice's best: community, gain, slack (rounded up).
