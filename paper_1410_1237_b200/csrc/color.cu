@@ -410,17 +410,51 @@ struct ColorScratch {
     unsigned huge_chunks;     // ceil(max_degree / CHUGE)
 };
 
+// Side streams of a captured round: the big / mid / huge kernels of the
+// assignment and of the conflict test touch disjoint vertices, so each group
+// runs as parallel graph branches (fork / join events).
+struct RoundStreams {
+    cudaStream_t side[2] = {nullptr, nullptr};
+    cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
+    void create() {
+        for (int t = 0; t < 2; t++) {
+            PLV_CUDA(cudaStreamCreateWithFlags(&side[t], cudaStreamNonBlocking));
+            PLV_CUDA(cudaEventCreateWithFlags(&join[t], cudaEventDisableTiming));
+        }
+        PLV_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    }
+    void destroy() {
+        for (int t = 0; t < 2; t++) {
+            if (side[t]) cudaStreamDestroy(side[t]);
+            if (join[t]) cudaEventDestroy(join[t]);
+        }
+        if (fork) cudaEventDestroy(fork);
+    }
+    void split(cudaStream_t s) {
+        PLV_CUDA(cudaEventRecord(fork, s));
+        for (int t = 0; t < 2; t++) PLV_CUDA(cudaStreamWaitEvent(side[t], fork, 0));
+    }
+    void merge(cudaStream_t s) {
+        for (int t = 0; t < 2; t++) {
+            PLV_CUDA(cudaEventRecord(join[t], side[t]));
+            PLV_CUDA(cudaStreamWaitEvent(s, join[t], 0));
+        }
+    }
+};
+
 static void color_round(const int64_t *off, const int32_t *nbr, ActiveRef R, int64_t na_max,
                         int32_t *colors, int32_t *tent, uint8_t *keep, const ColorScratch &C,
-                        cudaStream_t s) {
+                        cudaStream_t s, RoundStreams *rs = nullptr) {
     bool huge = C.nhuge_max > 0;
     const unsigned g = grid_for(na_max, 256, 148 * 8);
+    cudaStream_t s1 = rs ? rs->side[0] : s, s2 = rs ? rs->side[1] : s;
     k_color_assign_small<<<g, 256, 0, s>>>(off, nbr, R, colors, tent, C.big, C.cnt,
                                            huge ? C.huge : nullptr, C.cnt + 1, C.mid, C.cnt + 2);
     PLV_LAUNCH_CHECK();
-    k_color_assign_big<<<CBIG_GRID, CB, 0, s>>>(off, nbr, R, colors, tent, C.big, C.cnt);
+    if (rs) rs->split(s);
+    k_color_assign_big<<<CBIG_GRID, CB, 0, s1>>>(off, nbr, R, colors, tent, C.big, C.cnt);
     PLV_LAUNCH_CHECK();
-    k_color_assign_mid<<<CBIG_GRID, CB, 0, s>>>(off, nbr, R, colors, tent, C.mid, C.cnt + 2);
+    k_color_assign_mid<<<CBIG_GRID, CB, 0, s2>>>(off, nbr, R, colors, tent, C.mid, C.cnt + 2);
     PLV_LAUNCH_CHECK();
     if (huge) {
         PLV_CUDA(cudaMemsetAsync(C.hbits, 0, sizeof(uint32_t) * C.nhuge_max * (CWIN / 32), s));
@@ -431,19 +465,22 @@ static void color_round(const int64_t *off, const int32_t *nbr, ActiveRef R, int
                                               tent, keep);
         PLV_LAUNCH_CHECK();
     }
+    if (rs) rs->merge(s);
     k_color_commit<<<g, 256, 0, s>>>(R, tent, colors);
     PLV_LAUNCH_CHECK();
+    if (rs) rs->split(s);
     k_color_conflicts_small<<<g, 256, 0, s>>>(off, nbr, R, colors, keep);
     PLV_LAUNCH_CHECK();
-    k_color_conflicts_big<<<CBIG_GRID, CB, 0, s>>>(off, nbr, R, colors, keep, C.big, C.cnt);
+    k_color_conflicts_big<<<CBIG_GRID, CB, 0, s1>>>(off, nbr, R, colors, keep, C.big, C.cnt);
     PLV_LAUNCH_CHECK();
-    k_color_conflicts_mid<<<CBIG_GRID, CB, 0, s>>>(off, nbr, R, colors, keep, C.mid, C.cnt + 2);
+    k_color_conflicts_mid<<<CBIG_GRID, CB, 0, s2>>>(off, nbr, R, colors, keep, C.mid, C.cnt + 2);
     PLV_LAUNCH_CHECK();
     if (huge) {
         k_color_conflicts_huge<<<148 * C.huge_chunks, CB, 0, s>>>(off, nbr, R, colors, C.huge,
                                                                   C.cnt + 1, keep, C.huge_chunks);
         PLV_LAUNCH_CHECK();
     }
+    if (rs) rs->merge(s);
 }
 
 // Stable compaction of the rejected (keep == 0) active vertices into the
@@ -585,6 +622,7 @@ void color(const int64_t *off, const int32_t *nbr, int64_t n, int32_t *colors, i
     cudaGraph_t graph = nullptr, body = nullptr;
     cudaGraphExec_t exec = nullptr;
     cudaStream_t cs = nullptr;
+    RoundStreams rs;
     try {
         PLV_CUDA(cudaGraphCreate(&graph, 0));
         cudaGraphConditionalHandle h;
@@ -598,10 +636,11 @@ void color(const int64_t *off, const int32_t *nbr, int64_t n, int32_t *colors, i
         PLV_CUDA(cudaGraphAddNode(&loop, graph, nullptr, 0, &cp));
         body = cp.conditional.phGraph_out[0];
         PLV_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        rs.create();
         PLV_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
                                                cudaStreamCaptureModeThreadLocal));
         try {
-            color_round(off, nbr, R, n, colors, tent, keep, C, cs);
+            color_round(off, nbr, R, n, colors, tent, keep, C, cs, &rs);
             const unsigned gt = grid_for((n + RTILE - 1) / RTILE, 1, 148 * 8);
             k_rej_tiles<<<gt, RT, 0, cs>>>(R, keep, tsum);
             PLV_LAUNCH_CHECK();
@@ -625,11 +664,13 @@ void color(const int64_t *off, const int32_t *nbr, int64_t n, int32_t *colors, i
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
         if (cs) cudaStreamDestroy(cs);
+        rs.destroy();
         throw;
     }
     cudaGraphExecDestroy(exec);
     cudaGraphDestroy(graph);
     cudaStreamDestroy(cs);
+    rs.destroy();
     int64_t c[2];
     PLV_CUDA(cudaMemcpyAsync(c, ctl.get(), sizeof(c), cudaMemcpyDeviceToHost, s));
     Buf<int> mx(1, s);
