@@ -488,10 +488,17 @@ static void color_round(const int64_t *off, const int32_t *nbr, ActiveRef R, int
 // per-tile counts, one-block scan of the tile counts, ordered scatter.
 constexpr int RT = 256, RI = 4, RTILE = RT * RI;
 
+// Per-tile rejected counts; the last block to finish (ticket ctl[3]) turns
+// them into exclusive tile offsets and the total ctl[2].
 __global__ void __launch_bounds__(RT) k_rej_tiles(ActiveRef R, const uint8_t *keep,
-                                                  int64_t *tsum) {
+                                                  int64_t *tsum, int64_t *ctl) {
     typedef cub::BlockReduce<int, RT> BR;
-    __shared__ typename BR::TempStorage tmp;
+    typedef cub::BlockScan<int64_t, RT> Scan;
+    __shared__ union {
+        typename BR::TempStorage red;
+        typename Scan::TempStorage scan;
+    } tmp;
+    __shared__ bool s_last;
     const int64_t na = R.count(), nt = (na + RTILE - 1) / RTILE;
     for (int64_t t = blockIdx.x; t < nt; t += gridDim.x) {
         int c = 0;
@@ -500,34 +507,43 @@ __global__ void __launch_bounds__(RT) k_rej_tiles(ActiveRef R, const uint8_t *ke
             const int64_t x = t * RTILE + threadIdx.x * RI + u;
             c += (x < na && !keep[x]) ? 1 : 0;
         }
-        const int tot = BR(tmp).Sum(c);
+        const int tot = BR(tmp.red).Sum(c);
         if (threadIdx.x == 0) tsum[t] = tot;
         __syncthreads();
     }
-}
-
-constexpr int RS = 1024;
-__global__ void __launch_bounds__(RS) k_rej_scan(int64_t *ctl, int64_t *tsum) {
-    typedef cub::BlockScan<int64_t, RS> Scan;
-    __shared__ typename Scan::TempStorage tmp;
-    const int64_t na = ctl[0], nt = (na + RTILE - 1) / RTILE;
-    const int64_t per = (nt + RS - 1) / RS, t0 = threadIdx.x * per;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0)
+        s_last = atomicAdd((unsigned long long *)(ctl + 3), 1ull) == (unsigned long long)gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int64_t per = (nt + RT - 1) / RT, t0 = threadIdx.x * per;
     int64_t loc = 0;
-    for (int64_t t = t0; t < t0 + per && t < nt; t++) loc += tsum[t];
+    for (int64_t t = t0; t < t0 + per && t < nt; t++) loc += __ldcg(tsum + t);
     int64_t base, total;
-    Scan(tmp).ExclusiveSum(loc, base, total);
+    Scan(tmp.scan).ExclusiveSum(loc, base, total);
     for (int64_t t = t0; t < t0 + per && t < nt; t++) {
-        const int64_t v = tsum[t];
+        const int64_t v = __ldcg(tsum + t);
         tsum[t] = base;
         base += v;
     }
-    if (threadIdx.x == 0) ctl[2] = total;
+    if (threadIdx.x == 0) {
+        ctl[2] = total;
+        ctl[3] = 0;
+    }
 }
 
+// Ordered scatter of the rejected into the other buffer (uncoloured); the
+// last block (ticket ctl[4]) ends the round: the rejected become the active
+// list, the worklist counters reset, and the loop continues while any.
 __global__ void __launch_bounds__(RT) k_rej_scatter(ActiveRef R, const uint8_t *keep,
-                                                    const int64_t *tsum, int32_t *colors) {
+                                                    const int64_t *tsum, int32_t *colors,
+                                                    int64_t *ctl, unsigned long long *cnt,
+                                                    cudaGraphConditionalHandle h) {
     typedef cub::BlockScan<int, RT> Scan;
     __shared__ typename Scan::TempStorage tmp;
+    __shared__ bool s_last;
     const int32_t *A = R.act();
     int32_t *N = R.next();
     const int64_t na = R.count(), nt = (na + RTILE - 1) / RTILE;
@@ -551,21 +567,28 @@ __global__ void __launch_bounds__(RT) k_rej_scatter(ActiveRef R, const uint8_t *
         }
         __syncthreads();
     }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        s_last = atomicAdd((unsigned long long *)(ctl + 4), 1ull) == (unsigned long long)gridDim.x - 1;
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        const int64_t nr = ctl[2];
+        ctl[0] = nr;
+        ctl[1] += 1;
+        ctl[4] = 0;
+        cnt[0] = cnt[1] = cnt[2] = 0ull;
+        cudaGraphSetConditional(h, nr > 0 ? 1u : 0u);
+    }
 }
 
-// End of a round: the rejected become the active list; loop while any.
-__global__ void k_color_step(int64_t *ctl, unsigned long long *cnt, cudaGraphConditionalHandle h) {
-    const int64_t nr = ctl[2];
-    ctl[0] = nr;
-    ctl[1] += 1;
-    cnt[0] = cnt[1] = cnt[2] = 0ull;
-    cudaGraphSetConditional(h, nr > 0 ? 1u : 0u);
-}
-
+// ctl: [0] active count, [1] rounds done, [2] rejected count, [3] / [4]
+// tickets of the compaction kernels' last blocks.
 __global__ void k_color_init_ctl(int64_t *ctl, int64_t n, unsigned long long *cnt) {
     ctl[0] = n;
     ctl[1] = 0;
     ctl[2] = 0;
+    ctl[3] = 0;
+    ctl[4] = 0;
     cnt[0] = cnt[1] = cnt[2] = 0ull;
 }
 
@@ -601,7 +624,7 @@ void color(const int64_t *off, const int32_t *nbr, int64_t n, int32_t *colors, i
     }
     Buf<int32_t> act0(n, s), act1(n, s), tent(n, s), big(n, s), mid(n, s);
     Buf<uint8_t> keep(n, s);
-    Buf<int64_t> ctl(4, s), tsum((n + RTILE - 1) / RTILE + 1, s);
+    Buf<int64_t> ctl(6, s), tsum((n + RTILE - 1) / RTILE + 1, s);
     Buf<unsigned long long> cnts(6, s);
     PLV_CUDA(cudaMemsetAsync(cnts.get(), 0, 6 * sizeof(unsigned long long), s));
     k_count_huge<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(off, n, cnts.get() + 4, cnts.get() + 5);
@@ -642,13 +665,9 @@ void color(const int64_t *off, const int32_t *nbr, int64_t n, int32_t *colors, i
         try {
             color_round(off, nbr, R, n, colors, tent, keep, C, cs, &rs);
             const unsigned gt = grid_for((n + RTILE - 1) / RTILE, 1, 148 * 8);
-            k_rej_tiles<<<gt, RT, 0, cs>>>(R, keep, tsum);
+            k_rej_tiles<<<gt, RT, 0, cs>>>(R, keep, tsum, ctl);
             PLV_LAUNCH_CHECK();
-            k_rej_scan<<<1, RS, 0, cs>>>(ctl, tsum);
-            PLV_LAUNCH_CHECK();
-            k_rej_scatter<<<gt, RT, 0, cs>>>(R, keep, tsum, colors);
-            PLV_LAUNCH_CHECK();
-            k_color_step<<<1, 1, 0, cs>>>(ctl, cnts, h);
+            k_rej_scatter<<<gt, RT, 0, cs>>>(R, keep, tsum, colors, ctl, cnts, h);
             PLV_LAUNCH_CHECK();
         } catch (...) {
             cudaGraph_t g2 = nullptr;
