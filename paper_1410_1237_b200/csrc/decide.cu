@@ -356,7 +356,6 @@ template <int NT>
 struct CertSmem {
     BestSmem<NT> bs;
     typename cub::BlockScan<int, NT>::TempStorage scan;
-    typename cub::BlockReduce<unsigned long long, NT>::TempStorage red;
     int32_t *cidx;  // [NT * FU] ordered compaction of matching entries (set by the kernel)
     double *cw;     // [NT * FU]
     int32_t N[MAXS + 2];  // communities to fold exactly (N[0] = c_old)
@@ -524,9 +523,11 @@ __device__ Best certify_table(const DecideArgs &A, int32_t c_old, double ki, int
         if (!stay_best && slack_b > 0.0 && lower <= 0.0) S.flag |= 1;
         S.ncand = 0;
     }
-    __syncthreads();
-    unsigned long long tot = cub::BlockReduce<unsigned long long, NT>(S.red).Sum(nc);
-    if (tid == 0) S.ncand = tot;
+    // the candidate statistic: one atomic per warp, no block-wide reduction
+    if (A.cand) {
+        for (int o = 16; o > 0; o >>= 1) nc += __shfl_xor_sync(FULL, nc, o);
+        if ((tid & 31) == 0 && nc) atomicAdd(A.cand, nc);
+    }
     __syncthreads();
     return b;
 }
@@ -749,7 +750,7 @@ __device__ __forceinline__ void block_decide(const DecideArgs &A, int64_t x, int
     if (trp) trp->mark();
     Best b = certify_table<NT>(A, c_old, ki, keys, vals, cntt, T, clist, *ncl, S, true);
     if (trp) trp->mark();
-    my_cand += tid == 0 ? S.ncand : 0;
+    (void)my_cand;  // counted per warp in certify_table
     if (A.integral) {
         // exact in any order: the plain argmax is the reference's
         if (tid == 0) finish_vertex(A, x, c_old, S.f_old, b.g, b.c, b.e);
