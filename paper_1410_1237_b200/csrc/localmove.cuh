@@ -25,7 +25,7 @@ constexpr int T2A_MAXD = 680;  // tier 2: 1024-slot tables (>= 1.5 * (680 + 1))
 constexpr int T2_MAXD = 2048;   // tier 3: 4096-slot tables
 constexpr int T1_WARPS = 2;   // warps per block in tier 1 (8, 4, 2, 1 measured; 2 best)
 constexpr int T1_TS = 256;    // slots per warp table (>= 1.5 * (128 + 1))
-constexpr int BLK = 256;      // threads per block in tiers 2/3
+constexpr int BLK = 512;      // threads per block in tier 3 (128/256/1024 measured slower)
 constexpr int T2_TS = 4096;   // smem slots for tier 2 (>= 1.5 * (2048 + 1))
 constexpr int T2A_TS = 1024;
 constexpr int NTIER = 5;  // t0, t1, t2 (block, small table), t3 (block), t4 (hubs)
