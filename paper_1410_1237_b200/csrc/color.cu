@@ -86,48 +86,131 @@ __global__ void k_color_assign_small(const int64_t *off, const int32_t *nbr, Act
     }
 }
 
-// Huge rows: block (q, chunk) ORs the colours of CHUGE entries into the
-// global bitmap of huge item q (first window of CWIN colours).
+constexpr int HPT = CHUGE / CB;  // entries per thread per chunk
+
+// Huge rows (> CHUGE entries) keep state across the rounds of a colouring,
+// per slot (hslot[i]): the bitmap of the colours of their committed
+// neighbours (first window of CWIN colours) and, per chunk of CHUGE row
+// entries, the sorted list of the chunk's neighbours still uncoloured at the
+// last assignment ("pending").  A neighbour that has a colour at an
+// assignment is committed -- active vertices carry -1 and committed colours
+// never change -- so the bitmap only grows, and round r reads the pending
+// lists of round r - 1 (round 0: the row) instead of the whole row.  After
+// round r's assignment the pending lists are exactly the neighbours active in
+// round r: the only ones a clash can come from.
+struct HugeState {
+    const int32_t *hslot;  // [n] slot of a huge vertex (only those entries are read)
+    const int64_t *hoff;   // [slots] first entry of the slot's region (a multiple of CHUGE)
+    int32_t *pend;         // [regions] pending lists, CHUGE entries per chunk
+    int32_t *pc;           // [regions / CHUGE] pending count per chunk
+    uint32_t *bits;        // [slots * CWIN / 32] colours of committed neighbours
+};
+
+__device__ __forceinline__ unsigned lanes_below() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Block (q, chunk): the chunk's pending entries (round 0: its row entries).
+// Coloured neighbours go into the slot's bitmap (shared-memory
+// pre-aggregation, then the non-zero words); the uncoloured ones are
+// compacted in place, in order.  A chunk where nothing was committed is left
+// as it is.
 __global__ void __launch_bounds__(CB) k_color_assign_huge(const int64_t *off, const int32_t *nbr,
                                                           ActiveRef R,
                                                           const int32_t *colors,
                                                           const int32_t *huge,
                                                           const unsigned long long *nhuge,
-                                                          uint32_t *hbits, int64_t chunks) {
-    // colours cluster in a few words: OR into a shared bitmap first, then
-    // publish only its non-zero words (global atomics on one word serialise)
+                                                          HugeState H, int64_t chunks) {
+    constexpr int NWC = CB / 32;
     __shared__ uint32_t sb[CWIN / 32];
+    __shared__ int wofs[HPT * NWC];  // pending per (u, warp), then their offsets
+    __shared__ int s_tot;
     const int32_t *active = R.act();
+    const int64_t r = R.ctl[1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t cnt = (int64_t)*nhuge * chunks;  // (item, chunk) pairs
     for (int64_t w0 = blockIdx.x; w0 < cnt; w0 += gridDim.x) {
         const int64_t q = w0 / chunks, ch = w0 % chunks;
+        const int32_t i = active[huge[q]];
+        const int64_t r0 = off[i] + ch * CHUGE, deg = off[i + 1] - off[i];
+        if (ch * CHUGE >= deg) continue;  // block-uniform
+        const int32_t sl = H.hslot[i];
+        const int64_t rb = H.hoff[sl] + ch * CHUGE;
+        int32_t *reg = H.pend + rb;
+        int32_t *pcnt = H.pc + rb / CHUGE;
+        const int32_t *src = r == 0 ? nbr + r0 : reg;
+        const int64_t len = r == 0 ? (deg - ch * CHUGE < CHUGE ? deg - ch * CHUGE : CHUGE) : *pcnt;
+        if (len == 0) continue;
         for (int w = threadIdx.x; w < CWIN / 32; w += CB) sb[w] = 0u;
         __syncthreads();
-        int32_t i = active[huge[q]];
-        int64_t e0 = off[i] + ch * CHUGE, e1 = off[i + 1];
-        int64_t ee = e0 + CHUGE < e1 ? e0 + CHUGE : e1;
-        for (int64_t e = e0 + threadIdx.x; e < ee; e += CB) {
-            int32_t j = nbr[e];
-            if (j == i) continue;
-            int32_t cj = colors[j];
-            if (cj >= 0 && cj < CWIN) atomicOr(sb + (cj >> 5), 1u << (cj & 31));
+        int32_t jj[HPT], cc[HPT];
+#pragma unroll
+        for (int u = 0; u < HPT; u++) {
+            const int64_t e = threadIdx.x + u * CB;
+            jj[u] = e < len ? src[e] : i;
+        }
+#pragma unroll
+        for (int u = 0; u < HPT; u++) cc[u] = jj[u] != i ? colors[jj[u]] : 0x7fffffff;
+        unsigned m[HPT];
+        bool done = false;
+#pragma unroll
+        for (int u = 0; u < HPT; u++) {
+            m[u] = __ballot_sync(0xffffffffu, cc[u] < 0);
+            if (lane == 0) wofs[u * NWC + wid] = __popc(m[u]);
+            if (cc[u] >= 0 && cc[u] != 0x7fffffff) {
+                done = true;
+                if (cc[u] < CWIN) atomicOr(sb + (cc[u] >> 5), 1u << (cc[u] & 31));
+            }
+        }
+        if (__syncthreads_or(done) || r == 0) {
+            if (wid == 0) {  // exclusive scan of the (u, warp) counts, in entry order
+                constexpr int PER = HPT * NWC / 32;
+                int v[PER], t = 0;
+#pragma unroll
+                for (int k = 0; k < PER; k++) {
+                    v[k] = wofs[lane * PER + k];
+                    t += v[k];
+                }
+                int incl = t;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                int base = incl - t;
+#pragma unroll
+                for (int k = 0; k < PER; k++) {
+                    wofs[lane * PER + k] = base;
+                    base += v[k];
+                }
+                if (lane == 31) s_tot = incl;
+            }
+            __syncthreads();
+            const unsigned lt = lanes_below();
+#pragma unroll
+            for (int u = 0; u < HPT; u++)
+                if (cc[u] < 0) reg[wofs[u * NWC + wid] + __popc(m[u] & lt)] = jj[u];
+            if (threadIdx.x == 0) *pcnt = s_tot;
         }
         __syncthreads();
-        uint32_t *bits = hbits + q * (CWIN / 32);
+        uint32_t *bits = H.bits + (int64_t)sl * (CWIN / 32);
         for (int w = threadIdx.x; w < CWIN / 32; w += CB)
             if (sb[w]) atomicOr(bits + w, sb[w]);
         __syncthreads();
     }
 }
 
-// First free colour of every huge item from its bitmap (block per item); a
-// row whose first CWIN colours are all taken falls back to windowed scans.
+// First free colour of every huge item from its slot's bitmap (block per
+// item); a row whose first CWIN colours are all taken falls back to windowed
+// scans of the row.
 __global__ void __launch_bounds__(CB) k_color_huge_final(const int64_t *off, const int32_t *nbr,
                                                          ActiveRef R,
                                                          const int32_t *colors,
                                                          const int32_t *huge,
                                                          const unsigned long long *nhuge,
-                                                         const uint32_t *hbits, int32_t *out,
+                                                         HugeState H, int32_t *out,
                                                          uint8_t *keep) {
     const int32_t *active = R.act();
     __shared__ uint32_t bits[CWIN / 32];
@@ -137,10 +220,11 @@ __global__ void __launch_bounds__(CB) k_color_huge_final(const int64_t *off, con
     for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
         int64_t x = huge[q];
         int32_t i = active[x];
+        const int32_t sl = H.hslot[i];
         if (tid == 0) s_found = INT32_MAX;
         __syncthreads();
         for (int w = tid; w < CWIN / 32; w += CB) {
-            uint32_t free = ~hbits[q * (CWIN / 32) + w];
+            uint32_t free = ~H.bits[(int64_t)sl * (CWIN / 32) + w];
             if (free) atomicMin(&s_found, w * 32 + __ffs(free) - 1);
         }
         __syncthreads();
@@ -172,28 +256,39 @@ __global__ void __launch_bounds__(CB) k_color_huge_final(const int64_t *off, con
     }
 }
 
-// Huge rows: block (q, chunk) scans its entries of the j < i prefix.
+// Huge rows: block (q, chunk) scans the chunk's neighbours active this
+// round (its pending list, sorted: the j < i prefix ends the scan) for a
+// lower id with the same tentative colour.
 __global__ void __launch_bounds__(CB) k_color_conflicts_huge(const int64_t *off,
                                                              const int32_t *nbr,
                                                              ActiveRef R,
                                                              const int32_t *colors,
                                                              const int32_t *huge,
                                                              const unsigned long long *nhuge,
-                                                             uint8_t *keep, int64_t chunks) {
+                                                             HugeState H, uint8_t *keep,
+                                                             int64_t chunks) {
     const int32_t *active = R.act();
     const int64_t cnt = (int64_t)*nhuge * chunks;  // (item, chunk) pairs
     for (int64_t w = blockIdx.x; w < cnt; w += gridDim.x) {
         const int64_t q = w / chunks, ch = w % chunks;
-        int64_t x = huge[q];
-        int32_t i = active[x];
-        int32_t ci = colors[i];
-        int64_t e0 = off[i] + ch * CHUGE, e1 = off[i + 1];
-        int64_t ee = e0 + CHUGE < e1 ? e0 + CHUGE : e1;
-        bool clash = false;
-        for (int64_t e = e0 + threadIdx.x; e < ee; e += CB) {
-            int32_t j = nbr[e];
-            if (j < i && colors[j] == ci) clash = true;
+        const int64_t x = huge[q];
+        const int32_t i = active[x];
+        if (ch * CHUGE >= off[i + 1] - off[i]) continue;  // block-uniform
+        const int64_t rb = H.hoff[H.hslot[i]] + ch * CHUGE;
+        const int32_t *src = H.pend + rb;
+        const int64_t len = H.pc[rb / CHUGE];
+        if (len == 0 || src[0] >= i) continue;
+        const int32_t ci = colors[i];
+        int32_t jj[HPT];
+#pragma unroll
+        for (int u = 0; u < HPT; u++) {
+            const int64_t e = threadIdx.x + u * CB;
+            jj[u] = e < len ? src[e] : i;
         }
+        bool clash = false;
+#pragma unroll
+        for (int u = 0; u < HPT; u++)
+            if (jj[u] < i && colors[jj[u]] == ci) clash = true;
         if (clash) keep[x] = 0;
     }
 }
@@ -405,7 +500,7 @@ __global__ void k_max_color(const int32_t *colors, int64_t n, int *mx) {
 struct ColorScratch {
     int32_t *big, *huge, *mid;
     unsigned long long *cnt;  // [0] big, [1] huge, [2] mid (zero at the start of a round)
-    uint32_t *hbits;          // nhuge_max * CWIN / 32 words
+    HugeState H;              // huge rows' state across rounds
     int64_t nhuge_max;
     unsigned huge_chunks;     // ceil(max_degree / CHUGE)
 };
@@ -457,11 +552,10 @@ static void color_round(const int64_t *off, const int32_t *nbr, ActiveRef R, int
     k_color_assign_mid<<<CBIG_GRID, CB, 0, s2>>>(off, nbr, R, colors, tent, C.mid, C.cnt + 2);
     PLV_LAUNCH_CHECK();
     if (huge) {
-        PLV_CUDA(cudaMemsetAsync(C.hbits, 0, sizeof(uint32_t) * C.nhuge_max * (CWIN / 32), s));
         k_color_assign_huge<<<148 * C.huge_chunks, CB, 0, s>>>(off, nbr, R, colors, C.huge,
-                                                               C.cnt + 1, C.hbits, C.huge_chunks);
+                                                               C.cnt + 1, C.H, C.huge_chunks);
         PLV_LAUNCH_CHECK();
-        k_color_huge_final<<<148, CB, 0, s>>>(off, nbr, R, colors, C.huge, C.cnt + 1, C.hbits,
+        k_color_huge_final<<<148, CB, 0, s>>>(off, nbr, R, colors, C.huge, C.cnt + 1, C.H,
                                               tent, keep);
         PLV_LAUNCH_CHECK();
     }
@@ -477,7 +571,8 @@ static void color_round(const int64_t *off, const int32_t *nbr, ActiveRef R, int
     PLV_LAUNCH_CHECK();
     if (huge) {
         k_color_conflicts_huge<<<148 * C.huge_chunks, CB, 0, s>>>(off, nbr, R, colors, C.huge,
-                                                                  C.cnt + 1, keep, C.huge_chunks);
+                                                                  C.cnt + 1, C.H, keep,
+                                                                  C.huge_chunks);
         PLV_LAUNCH_CHECK();
     }
     if (rs) rs->merge(s);
@@ -592,23 +687,40 @@ __global__ void k_color_init_ctl(int64_t *ctl, int64_t n, unsigned long long *cn
     cnt[0] = cnt[1] = cnt[2] = 0ull;
 }
 
-__global__ void k_count_huge(const int64_t *off, int64_t n, unsigned long long *cnt,
-                             unsigned long long *maxdeg) {
-    unsigned long long c = 0, md = 0;
+// cnt[0] huge rows, cnt[1] max degree, cnt[2] entries of the huge rows' regions.
+__global__ void k_count_huge(const int64_t *off, int64_t n, unsigned long long *cnt) {
+    unsigned long long c = 0, md = 0, te = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         unsigned long long d = (unsigned long long)(off[i + 1] - off[i]);
         c += d > (unsigned long long)CHUGE;
+        te += d > (unsigned long long)CHUGE ? (d + CHUGE - 1) / CHUGE * CHUGE : 0ull;
         md = d > md ? d : md;
     }
     typedef cub::BlockReduce<unsigned long long, 256> BR;
     __shared__ typename BR::TempStorage t1;
     unsigned long long tc = BR(t1).Sum(c);
     __syncthreads();
+    unsigned long long tt = BR(t1).Sum(te);
+    __syncthreads();
     unsigned long long tm = BR(t1).Reduce(md, cub::Max());
     if (threadIdx.x == 0) {
         if (tc) atomicAdd(cnt, tc);
-        atomicMax(maxdeg, tm);
+        if (tt) atomicAdd(cnt + 2, tt);
+        atomicMax(cnt + 1, tm);
+    }
+}
+
+// Slots of the huge rows (any order) and their pending-list offsets.
+__global__ void k_huge_slots(const int64_t *off, int64_t n, int32_t *hslot, int64_t *hoff,
+                             unsigned long long *ctr) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long d = (unsigned long long)(off[i + 1] - off[i]);
+        if (d <= (unsigned long long)CHUGE) continue;
+        const int32_t sl = (int32_t)atomicAdd(ctr, 1ull);
+        hslot[i] = sl;
+        hoff[sl] = (int64_t)atomicAdd(ctr + 1, (d + CHUGE - 1) / CHUGE * CHUGE);
     }
 }
 
@@ -625,16 +737,27 @@ void color(const int64_t *off, const int32_t *nbr, int64_t n, int32_t *colors, i
     Buf<int32_t> act0(n, s), act1(n, s), tent(n, s), big(n, s), mid(n, s);
     Buf<uint8_t> keep(n, s);
     Buf<int64_t> ctl(6, s), tsum((n + RTILE - 1) / RTILE + 1, s);
-    Buf<unsigned long long> cnts(6, s);
-    PLV_CUDA(cudaMemsetAsync(cnts.get(), 0, 6 * sizeof(unsigned long long), s));
-    k_count_huge<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(off, n, cnts.get() + 4, cnts.get() + 5);
+    Buf<unsigned long long> cnts(8, s);
+    PLV_CUDA(cudaMemsetAsync(cnts.get(), 0, 8 * sizeof(unsigned long long), s));
+    k_count_huge<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(off, n, cnts.get() + 4);
     PLV_LAUNCH_CHECK();
-    unsigned long long hc[2];
+    unsigned long long hc[3];
     PLV_CUDA(cudaMemcpyAsync(hc, cnts.get() + 4, sizeof(hc), cudaMemcpyDeviceToHost, s));
     PLV_CUDA(cudaStreamSynchronize(s));
-    Buf<int32_t> huge(hc[0] ? hc[0] : 1, s);
-    Buf<uint32_t> hbits((hc[0] ? hc[0] : 1) * (CWIN / 32), s);
-    ColorScratch C{big.get(), huge.get(), mid.get(), cnts.get(), hbits.get(), (int64_t)hc[0],
+    const int64_t nh = (int64_t)hc[0], nh1 = nh ? nh : 1, ne1 = hc[2] ? (int64_t)hc[2] : 1;
+    Buf<int32_t> huge(nh1, s), hslot(nh ? n : 1, s), pend(nh ? ne1 : 1, s),
+        hpc(nh ? ne1 / CHUGE : 1, s);
+    Buf<int64_t> hoff(nh1, s);
+    Buf<unsigned long long> hctr(2, s);
+    Buf<uint32_t> hbits(nh1 * (CWIN / 32), s);
+    if (nh) {
+        PLV_CUDA(cudaMemsetAsync(hctr.get(), 0, sizeof(unsigned long long) * 2, s));
+        PLV_CUDA(cudaMemsetAsync(hbits.get(), 0, sizeof(uint32_t) * nh1 * (CWIN / 32), s));
+        k_huge_slots<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(off, n, hslot, hoff, hctr);
+        PLV_LAUNCH_CHECK();
+    }
+    HugeState H{hslot.get(), hoff.get(), pend.get(), hpc.get(), hbits.get()};
+    ColorScratch C{big.get(), huge.get(), mid.get(), cnts.get(), H, nh,
                    (unsigned)((hc[1] + CHUGE - 1) / CHUGE)};
     k_color_init<<<grid_for(n, 256), 256, 0, s>>>(colors, act0, n);
     PLV_LAUNCH_CHECK();

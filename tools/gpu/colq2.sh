@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q -k "color or colour or full_size or parity" > gpurun_out/colq_tests.log 2>&1; echo "rc=$?" >> gpurun_out/colq_tests.log
+for c in c4_chung_lu c2_rmat20 c3_grid; do timeout 600 python tools/color_calls.py $c > gpurun_out/cc2_$c.txt 2>&1; done
+python tools/color_timeline_k.py c4_chung_lu 3 > gpurun_out/ctk_new.txt 2>&1
+python tools/color_timeline_k.py c4_chung_lu 1 > gpurun_out/ctk1_new.txt 2>&1
