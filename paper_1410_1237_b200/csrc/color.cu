@@ -104,6 +104,10 @@ struct HugeState {
     int32_t *pend;         // [regions] pending lists, CHUGE entries per chunk
     int32_t *pc;           // [regions / CHUGE] pending count per chunk
     uint32_t *bits;        // [slots * CWIN / 32] colours of committed neighbours
+    const int32_t *hvid;   // [slots] the slot's vertex
+    int32_t *xof;          // [slots] its position in this round's active list
+    int64_t *wl[2];        // chunks with pending entries, (slot << 32) | chunk, by round parity
+    unsigned long long *wc;  // [2] their counts
 };
 
 __device__ __forceinline__ unsigned lanes_below() {
@@ -130,13 +134,27 @@ __global__ void __launch_bounds__(CB) k_color_assign_huge(const int64_t *off, co
     const int32_t *active = R.act();
     const int64_t r = R.ctl[1];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t cnt = (int64_t)*nhuge * chunks;  // (item, chunk) pairs
+    const int cur = (int)(r & 1), nxt = cur ^ 1;
+    // round 0: every (item, chunk) pair; then the chunks left with pending
+    // entries (those of committed vertices are skipped)
+    const int64_t cnt = r == 0 ? (int64_t)*nhuge * chunks : (int64_t)H.wc[cur];
     for (int64_t w0 = blockIdx.x; w0 < cnt; w0 += gridDim.x) {
-        const int64_t q = w0 / chunks, ch = w0 % chunks;
-        const int32_t i = active[huge[q]];
-        const int64_t r0 = off[i] + ch * CHUGE, deg = off[i + 1] - off[i];
-        if (ch * CHUGE >= deg) continue;  // block-uniform
-        const int32_t sl = H.hslot[i];
+        int32_t i, sl;
+        int64_t ch, r0 = 0;
+        if (r == 0) {
+            ch = w0 % chunks;
+            i = active[huge[w0 / chunks]];
+            r0 = off[i] + ch * CHUGE;
+            if (r0 >= off[i + 1]) continue;  // block-uniform
+            sl = H.hslot[i];
+        } else {
+            const int64_t e = H.wl[cur][w0];
+            sl = (int32_t)(e >> 32);
+            ch = e & 0xffffffffll;
+            i = H.hvid[sl];
+            if (colors[i] >= 0) continue;  // committed
+        }
+        const int64_t deg = off[i + 1] - off[i];
         const int64_t rb = H.hoff[sl] + ch * CHUGE;
         int32_t *reg = H.pend + rb;
         int32_t *pcnt = H.pc + rb / CHUGE;
@@ -164,6 +182,7 @@ __global__ void __launch_bounds__(CB) k_color_assign_huge(const int64_t *off, co
                 if (cc[u] < CWIN) atomicOr(sb + (cc[u] >> 5), 1u << (cc[u] & 31));
             }
         }
+        int left = (int)len;
         if (__syncthreads_or(done) || r == 0) {
             if (wid == 0) {  // exclusive scan of the (u, warp) counts, in entry order
                 constexpr int PER = HPT * NWC / 32;
@@ -193,7 +212,10 @@ __global__ void __launch_bounds__(CB) k_color_assign_huge(const int64_t *off, co
             for (int u = 0; u < HPT; u++)
                 if (cc[u] < 0) reg[wofs[u * NWC + wid] + __popc(m[u] & lt)] = jj[u];
             if (threadIdx.x == 0) *pcnt = s_tot;
+            left = s_tot;  // read before the barrier below
         }
+        if (threadIdx.x == 0 && left > 0)
+            H.wl[nxt][atomicAdd(H.wc + nxt, 1ull)] = ((int64_t)sl << 32) | ch;
         __syncthreads();
         uint32_t *bits = H.bits + (int64_t)sl * (CWIN / 32);
         for (int w = threadIdx.x; w < CWIN / 32; w += CB)
@@ -217,11 +239,15 @@ __global__ void __launch_bounds__(CB) k_color_huge_final(const int64_t *off, con
     __shared__ int s_found;
     const int tid = threadIdx.x;
     const int64_t cnt = (int64_t)*nhuge;
+    if (blockIdx.x == 0 && tid == 0) H.wc[R.ctl[1] & 1] = 0ull;  // read by the assignment only
     for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
         int64_t x = huge[q];
         int32_t i = active[x];
         const int32_t sl = H.hslot[i];
-        if (tid == 0) s_found = INT32_MAX;
+        if (tid == 0) {
+            s_found = INT32_MAX;
+            H.xof[sl] = (int32_t)x;
+        }
         __syncthreads();
         for (int w = tid; w < CWIN / 32; w += CB) {
             uint32_t free = ~H.bits[(int64_t)sl * (CWIN / 32) + w];
@@ -256,40 +282,36 @@ __global__ void __launch_bounds__(CB) k_color_huge_final(const int64_t *off, con
     }
 }
 
-// Huge rows: block (q, chunk) scans the chunk's neighbours active this
-// round (its pending list, sorted: the j < i prefix ends the scan) for a
-// lower id with the same tentative colour.
-__global__ void __launch_bounds__(CB) k_color_conflicts_huge(const int64_t *off,
-                                                             const int32_t *nbr,
-                                                             ActiveRef R,
+// Huge rows: block per chunk with pending entries after this round's
+// assignment (the worklist it wrote) scans them -- the neighbours active this
+// round, sorted: the j < i prefix ends the scan -- for a lower id with the
+// same tentative colour.
+__global__ void __launch_bounds__(CB) k_color_conflicts_huge(ActiveRef R,
                                                              const int32_t *colors,
-                                                             const int32_t *huge,
-                                                             const unsigned long long *nhuge,
-                                                             HugeState H, uint8_t *keep,
-                                                             int64_t chunks) {
-    const int32_t *active = R.act();
-    const int64_t cnt = (int64_t)*nhuge * chunks;  // (item, chunk) pairs
+                                                             HugeState H, uint8_t *keep) {
+    const int nxt = (int)((R.ctl[1] + 1) & 1);
+    const int64_t cnt = (int64_t)H.wc[nxt];
     for (int64_t w = blockIdx.x; w < cnt; w += gridDim.x) {
-        const int64_t q = w / chunks, ch = w % chunks;
-        const int64_t x = huge[q];
-        const int32_t i = active[x];
-        if (ch * CHUGE >= off[i + 1] - off[i]) continue;  // block-uniform
-        const int64_t rb = H.hoff[H.hslot[i]] + ch * CHUGE;
+        const int64_t e = H.wl[nxt][w];
+        const int32_t sl = (int32_t)(e >> 32);
+        const int64_t ch = e & 0xffffffffll;
+        const int32_t i = H.hvid[sl];
+        const int64_t rb = H.hoff[sl] + ch * CHUGE;
         const int32_t *src = H.pend + rb;
         const int64_t len = H.pc[rb / CHUGE];
-        if (len == 0 || src[0] >= i) continue;
+        if (src[0] >= i) continue;  // block-uniform
         const int32_t ci = colors[i];
         int32_t jj[HPT];
 #pragma unroll
         for (int u = 0; u < HPT; u++) {
-            const int64_t e = threadIdx.x + u * CB;
-            jj[u] = e < len ? src[e] : i;
+            const int64_t t = threadIdx.x + u * CB;
+            jj[u] = t < len ? src[t] : i;
         }
         bool clash = false;
 #pragma unroll
         for (int u = 0; u < HPT; u++)
             if (jj[u] < i && colors[jj[u]] == ci) clash = true;
-        if (clash) keep[x] = 0;
+        if (clash) keep[H.xof[sl]] = 0;
     }
 }
 
@@ -537,6 +559,13 @@ struct RoundStreams {
     }
 };
 
+// Grid of the huge-row kernels: grid-stride loops over the pairs / chunks;
+// after round 0 only a few chunks have work, so no more than a wave or two.
+constexpr unsigned HUGE_GRID_MAX = 148 * 3;  // 3, 8, 16 measured
+static unsigned huge_grid(unsigned chunks) {
+    return 148 * chunks < HUGE_GRID_MAX ? 148 * chunks : HUGE_GRID_MAX;
+}
+
 static void color_round(const int64_t *off, const int32_t *nbr, ActiveRef R, int64_t na_max,
                         int32_t *colors, int32_t *tent, uint8_t *keep, const ColorScratch &C,
                         cudaStream_t s, RoundStreams *rs = nullptr) {
@@ -552,7 +581,7 @@ static void color_round(const int64_t *off, const int32_t *nbr, ActiveRef R, int
     k_color_assign_mid<<<CBIG_GRID, CB, 0, s2>>>(off, nbr, R, colors, tent, C.mid, C.cnt + 2);
     PLV_LAUNCH_CHECK();
     if (huge) {
-        k_color_assign_huge<<<148 * C.huge_chunks, CB, 0, s>>>(off, nbr, R, colors, C.huge,
+        k_color_assign_huge<<<huge_grid(C.huge_chunks), CB, 0, s>>>(off, nbr, R, colors, C.huge,
                                                                C.cnt + 1, C.H, C.huge_chunks);
         PLV_LAUNCH_CHECK();
         k_color_huge_final<<<148, CB, 0, s>>>(off, nbr, R, colors, C.huge, C.cnt + 1, C.H,
@@ -570,9 +599,7 @@ static void color_round(const int64_t *off, const int32_t *nbr, ActiveRef R, int
     k_color_conflicts_mid<<<CBIG_GRID, CB, 0, s2>>>(off, nbr, R, colors, keep, C.mid, C.cnt + 2);
     PLV_LAUNCH_CHECK();
     if (huge) {
-        k_color_conflicts_huge<<<148 * C.huge_chunks, CB, 0, s>>>(off, nbr, R, colors, C.huge,
-                                                                  C.cnt + 1, C.H, keep,
-                                                                  C.huge_chunks);
+        k_color_conflicts_huge<<<huge_grid(C.huge_chunks), CB, 0, s>>>(R, colors, C.H, keep);
         PLV_LAUNCH_CHECK();
     }
     if (rs) rs->merge(s);
@@ -713,13 +740,14 @@ __global__ void k_count_huge(const int64_t *off, int64_t n, unsigned long long *
 
 // Slots of the huge rows (any order) and their pending-list offsets.
 __global__ void k_huge_slots(const int64_t *off, int64_t n, int32_t *hslot, int64_t *hoff,
-                             unsigned long long *ctr) {
+                             int32_t *hvid, unsigned long long *ctr) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long d = (unsigned long long)(off[i + 1] - off[i]);
         if (d <= (unsigned long long)CHUGE) continue;
         const int32_t sl = (int32_t)atomicAdd(ctr, 1ull);
         hslot[i] = sl;
+        hvid[sl] = (int32_t)i;
         hoff[sl] = (int64_t)atomicAdd(ctr + 1, (d + CHUGE - 1) / CHUGE * CHUGE);
     }
 }
@@ -746,17 +774,18 @@ void color(const int64_t *off, const int32_t *nbr, int64_t n, int32_t *colors, i
     PLV_CUDA(cudaStreamSynchronize(s));
     const int64_t nh = (int64_t)hc[0], nh1 = nh ? nh : 1, ne1 = hc[2] ? (int64_t)hc[2] : 1;
     Buf<int32_t> huge(nh1, s), hslot(nh ? n : 1, s), pend(nh ? ne1 : 1, s),
-        hpc(nh ? ne1 / CHUGE : 1, s);
-    Buf<int64_t> hoff(nh1, s);
-    Buf<unsigned long long> hctr(2, s);
+        hpc(nh ? ne1 / CHUGE : 1, s), hvid(nh1, s), xof(nh1, s);
+    Buf<int64_t> hoff(nh1, s), wl0(nh ? ne1 / CHUGE : 1, s), wl1(nh ? ne1 / CHUGE : 1, s);
+    Buf<unsigned long long> hctr(4, s);
     Buf<uint32_t> hbits(nh1 * (CWIN / 32), s);
     if (nh) {
-        PLV_CUDA(cudaMemsetAsync(hctr.get(), 0, sizeof(unsigned long long) * 2, s));
+        PLV_CUDA(cudaMemsetAsync(hctr.get(), 0, sizeof(unsigned long long) * 4, s));
         PLV_CUDA(cudaMemsetAsync(hbits.get(), 0, sizeof(uint32_t) * nh1 * (CWIN / 32), s));
-        k_huge_slots<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(off, n, hslot, hoff, hctr);
+        k_huge_slots<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(off, n, hslot, hoff, hvid, hctr);
         PLV_LAUNCH_CHECK();
     }
-    HugeState H{hslot.get(), hoff.get(), pend.get(), hpc.get(), hbits.get()};
+    HugeState H{hslot.get(), hoff.get(), pend.get(), hpc.get(), hbits.get(), hvid.get(), xof.get(),
+                {wl0.get(), wl1.get()}, hctr.get() + 2};
     ColorScratch C{big.get(), huge.get(), mid.get(), cnts.get(), H, nh,
                    (unsigned)((hc[1] + CHUGE - 1) / CHUGE)};
     k_color_init<<<grid_for(n, 256), 256, 0, s>>>(colors, act0, n);
