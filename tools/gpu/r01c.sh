@@ -36,3 +36,5 @@ timeout 300 python tools/run_profile.py $c > gpurun_out/rp_$c.txt 2>&1
 done
 timeout 300 python tools/capped_timeline.py c3_grid --phase 4 > gpurun_out/ct_c3p4.txt 2>&1
 timeout 300 python tools/color_timeline.py c4_chung_lu > gpurun_out/colt.txt 2>&1
+for c in c4_chung_lu c2_rmat20; do timeout 600 python tools/color_calls.py $c > gpurun_out/colcalls_$c.txt 2>&1; done
+timeout 300 python tools/color_timeline_k.py c4_chung_lu 3 > gpurun_out/colt_k3.txt 2>&1
