@@ -62,6 +62,7 @@ __device__ __forceinline__ int first_free_thread(const int64_t *off, const int32
 // Tentative colours of low-degree active vertices; the others go to `big`
 // (one block each) or, above CHUGE entries, to `huge` (split over blocks).
 constexpr int64_t CHUGE = 4096;
+constexpr int64_t CPEND = 4096;  // rows above this keep pending lists across rounds (512, 1024 measured slower)
 constexpr int64_t CMID_MAXD = 512;  // warp per vertex up to here, then a block
 
 __global__ void k_color_assign_small(const int64_t *off, const int32_t *nbr, ActiveRef R,
@@ -79,7 +80,7 @@ __global__ void k_color_assign_small(const int64_t *off, const int32_t *nbr, Act
             out[x] = first_free_thread(off, nbr, colors, i);
         else if (d <= CMID_MAXD || !mid)
             big[atomicAdd(nbig, 1ull)] = (int32_t)x;
-        else if (d <= CHUGE || !huge)
+        else if (d <= CPEND || !huge)
             mid[atomicAdd(nmid, 1ull)] = (int32_t)x;
         else
             huge[atomicAdd(nhuge, 1ull)] = (int32_t)x;
@@ -88,7 +89,7 @@ __global__ void k_color_assign_small(const int64_t *off, const int32_t *nbr, Act
 
 constexpr int HPT = CHUGE / CB;  // entries per thread per chunk
 
-// Huge rows (> CHUGE entries) keep state across the rounds of a colouring,
+// Huge rows (> CPEND entries) keep state across the rounds of a colouring,
 // per slot (hslot[i]): the bitmap of the colours of their committed
 // neighbours (first window of CWIN colours) and, per chunk of CHUGE row
 // entries, the sorted list of the chunk's neighbours still uncoloured at the
@@ -100,9 +101,11 @@ constexpr int HPT = CHUGE / CB;  // entries per thread per chunk
 // round r: the only ones a clash can come from.
 struct HugeState {
     const int32_t *hslot;  // [n] slot of a huge vertex (only those entries are read)
-    const int64_t *hoff;   // [slots] first entry of the slot's region (a multiple of CHUGE)
-    int32_t *pend;         // [regions] pending lists, CHUGE entries per chunk
-    int32_t *pc;           // [regions / CHUGE] pending count per chunk
+    const int64_t *hoff;   // [slots] first entry of the slot's region (its degree long)
+    const int64_t *hcb;    // [slots] first chunk index of the slot
+    const int32_t *cown;   // [chunks] the chunk's slot
+    int32_t *pend;         // [entries] pending lists, CHUGE entries per chunk
+    int32_t *pc;           // [chunks] pending count per chunk
     uint32_t *bits;        // [slots * CWIN / 32] colours of committed neighbours
     const int32_t *hvid;   // [slots] the slot's vertex
     int32_t *xof;          // [slots] its position in this round's active list
@@ -126,7 +129,7 @@ __global__ void __launch_bounds__(CB) k_color_assign_huge(const int64_t *off, co
                                                           const int32_t *colors,
                                                           const int32_t *huge,
                                                           const unsigned long long *nhuge,
-                                                          HugeState H, int64_t chunks) {
+                                                          HugeState H, int64_t nchunks) {
     constexpr int NWC = CB / 32;
     __shared__ uint32_t sb[CWIN / 32];
     __shared__ int wofs[HPT * NWC];  // pending per (u, warp), then their offsets
@@ -135,18 +138,20 @@ __global__ void __launch_bounds__(CB) k_color_assign_huge(const int64_t *off, co
     const int64_t r = R.ctl[1];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int cur = (int)(r & 1), nxt = cur ^ 1;
-    // round 0: every (item, chunk) pair; then the chunks left with pending
-    // entries (those of committed vertices are skipped)
-    const int64_t cnt = r == 0 ? (int64_t)*nhuge * chunks : (int64_t)H.wc[cur];
+    // round 0 (every vertex active): every chunk; then the chunks left with
+    // pending entries (those of committed vertices are skipped)
+    (void)active;
+    (void)huge;
+    (void)nhuge;
+    const int64_t cnt = r == 0 ? nchunks : (int64_t)H.wc[cur];
     for (int64_t w0 = blockIdx.x; w0 < cnt; w0 += gridDim.x) {
         int32_t i, sl;
         int64_t ch, r0 = 0;
         if (r == 0) {
-            ch = w0 % chunks;
-            i = active[huge[w0 / chunks]];
+            sl = H.cown[w0];
+            ch = w0 - H.hcb[sl];
+            i = H.hvid[sl];
             r0 = off[i] + ch * CHUGE;
-            if (r0 >= off[i + 1]) continue;  // block-uniform
-            sl = H.hslot[i];
         } else {
             const int64_t e = H.wl[cur][w0];
             sl = (int32_t)(e >> 32);
@@ -157,7 +162,7 @@ __global__ void __launch_bounds__(CB) k_color_assign_huge(const int64_t *off, co
         const int64_t deg = off[i + 1] - off[i];
         const int64_t rb = H.hoff[sl] + ch * CHUGE;
         int32_t *reg = H.pend + rb;
-        int32_t *pcnt = H.pc + rb / CHUGE;
+        int32_t *pcnt = H.pc + H.hcb[sl] + ch;
         const int32_t *src = r == 0 ? nbr + r0 : reg;
         const int64_t len = r == 0 ? (deg - ch * CHUGE < CHUGE ? deg - ch * CHUGE : CHUGE) : *pcnt;
         if (len == 0) continue;
@@ -298,7 +303,7 @@ __global__ void __launch_bounds__(CB) k_color_conflicts_huge(ActiveRef R,
         const int32_t i = H.hvid[sl];
         const int64_t rb = H.hoff[sl] + ch * CHUGE;
         const int32_t *src = H.pend + rb;
-        const int64_t len = H.pc[rb / CHUGE];
+        const int64_t len = H.pc[H.hcb[sl] + ch];
         if (src[0] >= i) continue;  // block-uniform
         const int32_t ci = colors[i];
         int32_t jj[HPT];
@@ -524,7 +529,7 @@ struct ColorScratch {
     unsigned long long *cnt;  // [0] big, [1] huge, [2] mid (zero at the start of a round)
     HugeState H;              // huge rows' state across rounds
     int64_t nhuge_max;
-    unsigned huge_chunks;     // ceil(max_degree / CHUGE)
+    int64_t huge_chunks;      // chunks of the rows above CPEND
 };
 
 // Side streams of a captured round: the big / mid / huge kernels of the
@@ -562,8 +567,8 @@ struct RoundStreams {
 // Grid of the huge-row kernels: grid-stride loops over the pairs / chunks;
 // after round 0 only a few chunks have work, so no more than a wave or two.
 constexpr unsigned HUGE_GRID_MAX = 148 * 3;  // 3, 8, 16 measured
-static unsigned huge_grid(unsigned chunks) {
-    return 148 * chunks < HUGE_GRID_MAX ? 148 * chunks : HUGE_GRID_MAX;
+static unsigned huge_grid(int64_t chunks) {
+    return chunks < (int64_t)HUGE_GRID_MAX ? (unsigned)(chunks > 0 ? chunks : 1) : HUGE_GRID_MAX;
 }
 
 static void color_round(const int64_t *off, const int32_t *nbr, ActiveRef R, int64_t na_max,
@@ -582,9 +587,9 @@ static void color_round(const int64_t *off, const int32_t *nbr, ActiveRef R, int
     PLV_LAUNCH_CHECK();
     if (huge) {
         k_color_assign_huge<<<huge_grid(C.huge_chunks), CB, 0, s>>>(off, nbr, R, colors, C.huge,
-                                                               C.cnt + 1, C.H, C.huge_chunks);
+                                                                    C.cnt + 1, C.H, C.huge_chunks);
         PLV_LAUNCH_CHECK();
-        k_color_huge_final<<<148, CB, 0, s>>>(off, nbr, R, colors, C.huge, C.cnt + 1, C.H,
+        k_color_huge_final<<<148 * 4, CB, 0, s>>>(off, nbr, R, colors, C.huge, C.cnt + 1, C.H,
                                               tent, keep);
         PLV_LAUNCH_CHECK();
     }
@@ -714,14 +719,15 @@ __global__ void k_color_init_ctl(int64_t *ctl, int64_t n, unsigned long long *cn
     cnt[0] = cnt[1] = cnt[2] = 0ull;
 }
 
-// cnt[0] huge rows, cnt[1] max degree, cnt[2] entries of the huge rows' regions.
+// cnt[0] rows above CPEND, cnt[1] max degree, cnt[2] their entries, cnt[3] their chunks.
 __global__ void k_count_huge(const int64_t *off, int64_t n, unsigned long long *cnt) {
-    unsigned long long c = 0, md = 0, te = 0;
+    unsigned long long c = 0, md = 0, te = 0, tk = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         unsigned long long d = (unsigned long long)(off[i + 1] - off[i]);
-        c += d > (unsigned long long)CHUGE;
-        te += d > (unsigned long long)CHUGE ? (d + CHUGE - 1) / CHUGE * CHUGE : 0ull;
+        c += d > (unsigned long long)CPEND;
+        te += d > (unsigned long long)CPEND ? d : 0ull;
+        tk += d > (unsigned long long)CPEND ? (d + CHUGE - 1) / CHUGE : 0ull;
         md = d > md ? d : md;
     }
     typedef cub::BlockReduce<unsigned long long, 256> BR;
@@ -730,25 +736,33 @@ __global__ void k_count_huge(const int64_t *off, int64_t n, unsigned long long *
     __syncthreads();
     unsigned long long tt = BR(t1).Sum(te);
     __syncthreads();
+    unsigned long long tkk = BR(t1).Sum(tk);
+    __syncthreads();
     unsigned long long tm = BR(t1).Reduce(md, cub::Max());
     if (threadIdx.x == 0) {
         if (tc) atomicAdd(cnt, tc);
         if (tt) atomicAdd(cnt + 2, tt);
+        if (tkk) atomicAdd(cnt + 3, tkk);
         atomicMax(cnt + 1, tm);
     }
 }
 
 // Slots of the huge rows (any order) and their pending-list offsets.
 __global__ void k_huge_slots(const int64_t *off, int64_t n, int32_t *hslot, int64_t *hoff,
-                             int32_t *hvid, unsigned long long *ctr) {
+                             int64_t *hcb, int32_t *cown, int32_t *hvid,
+                             unsigned long long *ctr) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long d = (unsigned long long)(off[i + 1] - off[i]);
-        if (d <= (unsigned long long)CHUGE) continue;
+        if (d <= (unsigned long long)CPEND) continue;
         const int32_t sl = (int32_t)atomicAdd(ctr, 1ull);
         hslot[i] = sl;
         hvid[sl] = (int32_t)i;
-        hoff[sl] = (int64_t)atomicAdd(ctr + 1, (d + CHUGE - 1) / CHUGE * CHUGE);
+        hoff[sl] = (int64_t)atomicAdd(ctr + 1, d);
+        const unsigned long long nc = (d + CHUGE - 1) / CHUGE;
+        const int64_t cb = (int64_t)atomicAdd(ctr + 2, nc);
+        hcb[sl] = cb;
+        for (unsigned long long c = 0; c < nc; c++) cown[cb + c] = sl;
     }
 }
 
@@ -769,25 +783,26 @@ void color(const int64_t *off, const int32_t *nbr, int64_t n, int32_t *colors, i
     PLV_CUDA(cudaMemsetAsync(cnts.get(), 0, 8 * sizeof(unsigned long long), s));
     k_count_huge<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(off, n, cnts.get() + 4);
     PLV_LAUNCH_CHECK();
-    unsigned long long hc[3];
+    unsigned long long hc[4];
     PLV_CUDA(cudaMemcpyAsync(hc, cnts.get() + 4, sizeof(hc), cudaMemcpyDeviceToHost, s));
     PLV_CUDA(cudaStreamSynchronize(s));
-    const int64_t nh = (int64_t)hc[0], nh1 = nh ? nh : 1, ne1 = hc[2] ? (int64_t)hc[2] : 1;
-    Buf<int32_t> huge(nh1, s), hslot(nh ? n : 1, s), pend(nh ? ne1 : 1, s),
-        hpc(nh ? ne1 / CHUGE : 1, s), hvid(nh1, s), xof(nh1, s);
-    Buf<int64_t> hoff(nh1, s), wl0(nh ? ne1 / CHUGE : 1, s), wl1(nh ? ne1 / CHUGE : 1, s);
-    Buf<unsigned long long> hctr(4, s);
+    const int64_t nh = (int64_t)hc[0], nh1 = nh ? nh : 1, ne1 = hc[2] ? (int64_t)hc[2] : 1,
+                  nk1 = hc[3] ? (int64_t)hc[3] : 1;
+    Buf<int32_t> huge(nh1, s), hslot(nh ? n : 1, s), pend(ne1, s), hpc(nk1, s), cown(nk1, s),
+        hvid(nh1, s), xof(nh1, s);
+    Buf<int64_t> hoff(nh1, s), hcb(nh1, s), wl0(nk1, s), wl1(nk1, s);
+    Buf<unsigned long long> hctr(6, s);
     Buf<uint32_t> hbits(nh1 * (CWIN / 32), s);
     if (nh) {
-        PLV_CUDA(cudaMemsetAsync(hctr.get(), 0, sizeof(unsigned long long) * 4, s));
+        PLV_CUDA(cudaMemsetAsync(hctr.get(), 0, sizeof(unsigned long long) * 6, s));
         PLV_CUDA(cudaMemsetAsync(hbits.get(), 0, sizeof(uint32_t) * nh1 * (CWIN / 32), s));
-        k_huge_slots<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(off, n, hslot, hoff, hvid, hctr);
+        k_huge_slots<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(off, n, hslot, hoff, hcb, cown, hvid,
+                                                               hctr);
         PLV_LAUNCH_CHECK();
     }
-    HugeState H{hslot.get(), hoff.get(), pend.get(), hpc.get(), hbits.get(), hvid.get(), xof.get(),
-                {wl0.get(), wl1.get()}, hctr.get() + 2};
-    ColorScratch C{big.get(), huge.get(), mid.get(), cnts.get(), H, nh,
-                   (unsigned)((hc[1] + CHUGE - 1) / CHUGE)};
+    HugeState H{hslot.get(), hoff.get(), hcb.get(), cown.get(), pend.get(), hpc.get(), hbits.get(),
+                hvid.get(), xof.get(), {wl0.get(), wl1.get()}, hctr.get() + 4};
+    ColorScratch C{big.get(), huge.get(), mid.get(), cnts.get(), H, nh, (int64_t)hc[3]};
     k_color_init<<<grid_for(n, 256), 256, 0, s>>>(colors, act0, n);
     PLV_LAUNCH_CHECK();
     k_color_init_ctl<<<1, 1, 0, s>>>(ctl, n, cnts);
