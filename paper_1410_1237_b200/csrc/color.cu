@@ -60,8 +60,8 @@ __device__ __forceinline__ int first_free_thread(const int64_t *off, const int32
 }
 
 // Tentative colours of low-degree active vertices; the others go to `big`
-// (one block each) or, above CHUGE entries, to `huge` (split over blocks).
-constexpr int64_t CHUGE = 4096;
+// (one block each) or, above CPEND entries, to `huge` (split over blocks).
+constexpr int64_t CHUGE = 2048;  // entries per huge-row chunk (1024, 2048, 4096 measured)
 constexpr int64_t CPEND = 4096;  // rows above this keep pending lists across rounds (512, 1024 measured slower)
 constexpr int64_t CMID_MAXD = 512;  // warp per vertex up to here, then a block
 
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(CB) k_color_assign_big(const int64_t *off, con
     }
 }
 
-// One block per active vertex of CMID_MAXD < degree <= CHUGE: bitmap of
+// One block per active vertex of CMID_MAXD < degree <= CPEND: bitmap of
 // neighbour colours in shared memory.
 __global__ void __launch_bounds__(CB) k_color_assign_mid(const int64_t *off, const int32_t *nbr,
                                                          ActiveRef R, const int32_t *colors,
