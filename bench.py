@@ -60,9 +60,10 @@ def _args():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--scale", type=int, default=CONFIG["scale"], help="R-MAT scale (c2 config)")
-    p.add_argument("--config", default="c2_rmat20",
+    p.add_argument("--config", default="c4_chung_lu",
                    choices=["c1_sbm", "c2_rmat20", "c3_grid", "c4_chung_lu"],
-                   help="BASELINE config to run (default: config 2, the headline)")
+                   help="BASELINE config to run (default: config 4, the largest that fits "
+                        "one GPU -- the headline)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-louvain", action="store_true", help="skip the full run() timing")
     p.add_argument("--mode", choices=["colored", "uncolored"], default="colored")
@@ -144,14 +145,14 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def _traffic(mode: str, scale: int, config: str = "c2_rmat20"):
+def _traffic(mode: str, scale: int, config: str = "c4_chung_lu"):
     """DRAM bytes per iteration of the decide kernels, from the committed ncu
-    capture (profiles/r01_traffic.json; C2 only), else None."""
-    if scale != CONFIG["scale"] or config != "c2_rmat20":
+    capture (profiles/traffic.json, keyed "config/mode"), else None."""
+    if config == "c2_rmat20" and scale != CONFIG["scale"]:
         return None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
-            return float(json.load(fh)[mode])
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return float(json.load(fh)[f"{config}/{mode}"])
     except Exception:
         return None
 
@@ -162,6 +163,35 @@ def _peak_hbm():
             return float(json.load(fh)["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+DECIDE_KERNELS = ("k_decide_", "k_hub_accum", "k_hub_pass")
+
+
+def _cupti_decide_ms(step):
+    """One replay of `step` under CUPTI: (union of the decide kernels'
+    intervals in ms, span of all kernels in ms, candidates)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        _, _, cand = step()
+        torch.cuda.synchronize()
+    ks = sorted((e.time_range.start, e.time_range.end, e.name) for e in prof.events()
+                if e.device_type.name == "CUDA")
+    span = (max(k[1] for k in ks) - ks[0][0]) / 1e3 if ks else 0.0
+    busy, cs, ce = 0.0, None, None
+    for s0, e0, nm in ks:
+        if not any(d in nm for d in DECIDE_KERNELS):
+            continue
+        if ce is None or s0 > ce:
+            if ce is not None:
+                busy += ce - cs
+            cs, ce = s0, e0
+        else:
+            ce = max(ce, e0)
+    if ce is not None:
+        busy += ce - cs
+    return busy / 1e3, span, cand
 
 
 # ------------------------------------------------------------- CPU arms
@@ -362,18 +392,21 @@ def run_ours(args):
     M = g.num_edges
     nnz = g.nnz
     value = M / t_iter  # one graph, partitioned over the ranks (strong scaling)
-    # decide-kernel timing: same iteration through an engine with event
-    # records around every stage's decide launches
+    # decide-kernel time INSIDE the timed step's graph: CUPTI (torch.profiler)
+    # records every graph-launched kernel of extra replays of the same engine;
+    # the decide family's time is the union of its kernel intervals per
+    # iteration (never more than the step itself)
     per_iter_launches = eng.graph_kernels()  # kernel nodes of the timed step's graph
-    teng = PhaseEngine(g, state, coloring, timing=True)
-    dms, cands = [], []
-    for _ in range(max(3, args.steps // 2)):
+    dms, cands, spans = [], [], []
+    for _ in range(3):
         reset()
-        _, _, cand = teng.iterate()
-        dms.append(teng.decide_ms())
+        torch.cuda.synchronize()
+        dm, span, cand = _cupti_decide_ms(eng.iterate)
+        dms.append(dm)
+        spans.append(span)
         cands.append(cand)
-    teng.close()
     decide_ms = float(np.median(dms))
+    span_ms = float(np.median(spans))
     cand_per_iter = float(np.mean(cands))
     moves_per_iter = float(moves_it)
     launches = per_iter_launches * args.steps
@@ -478,7 +511,10 @@ def run_ours(args):
                          "traffic_unit": "bytes per iteration (ncu, warm caches)",
                          "peak_kind": peak_kind,
                          "kernel": "decide (tiers 0-4)",
-                         "bytes_per_iter": decide_bytes, "ms_per_iter": decide_ms},
+                         "bytes_per_iter": decide_bytes, "ms_per_iter": decide_ms,
+                         "share_of_step": decide_ms / span_ms,
+                         "timing": "union of decide-kernel intervals in the iteration graph "
+                                   "(CUPTI), median of 3 replays; span %.3f ms" % span_ms},
             "iteration": {"bytes": iter_bytes, "gbs": iter_bytes / t_iter / 1e9,
                           "frac": iter_bytes / t_iter / 1e9 / peak,
                           "moves": moves_per_iter, "cand": cand_per_iter, "q": q,
@@ -499,8 +535,26 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _self_launch(args) -> bool:
+    """`--gpus N` without torchrun: re-exec this script under torchrun with N
+    ranks (one per GPU).  With WORLD_SIZE set, N must equal it."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
+        return False
+    if args.gpus <= 1:
+        return False
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={29500 + os.getpid() % 1000}", os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    raise SystemExit(subprocess.run(cmd).returncode)
+
+
 def main():
     args = _args()
+    _self_launch(args)
     if args.impl == "reference":
         run_reference(args)
     else:
