@@ -44,9 +44,18 @@ void *pool_alloc(size_t bytes) {
     return p;
 }
 
+static thread_local unsigned long long g_free_fail = 0;
+
+unsigned long long pool_free_failures() { return g_free_fail; }
+
 void pool_free(void *p) {
     if (!p) return;
-    if (cudaFreeAsync(p, alloc_stream()) != cudaSuccess) cudaGetLastError();
+    cudaError_t e = cudaFreeAsync(p, alloc_stream());
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        g_free_fail++;
+        set_error("cudaFreeAsync failed: %s", cudaGetErrorString(e));
+    }
 }
 
 void check_device() {

@@ -138,8 +138,11 @@ __global__ void __launch_bounds__(CB) k_color_assign_huge(const int64_t *off, co
     const int64_t r = R.ctl[1];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int cur = (int)(r & 1), nxt = cur ^ 1;
-    // round 0 (every vertex active): every chunk; then the chunks left with
-    // pending entries (those of committed vertices are skipped)
+    // round 0: every chunk of every huge row.  color() seeds all n vertices as
+    // active, so every huge row is active in round 0; a row that is already
+    // coloured (a caller starting from a subset) is skipped below instead of
+    // getting pending lists.  Later rounds: the chunks left with pending
+    // entries (those of committed vertices are skipped).
     (void)active;
     (void)huge;
     (void)nhuge;
@@ -152,6 +155,7 @@ __global__ void __launch_bounds__(CB) k_color_assign_huge(const int64_t *off, co
             ch = w0 - H.hcb[sl];
             i = H.hvid[sl];
             r0 = off[i] + ch * CHUGE;
+            if (colors[i] >= 0) continue;  // not active (see above)
         } else {
             const int64_t e = H.wl[cur][w0];
             sl = (int32_t)(e >> 32);

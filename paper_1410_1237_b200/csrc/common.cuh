@@ -74,6 +74,7 @@ inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 // idle (callers synchronise first).
 void *pool_alloc(size_t bytes);
 void pool_free(void *p);
+unsigned long long pool_free_failures();  // failed pool_free calls on this thread
 
 // Stream-ordered scratch buffer (cudaMallocAsync pool); freed on scope exit.
 template <class T>

@@ -933,8 +933,10 @@ extern "C" int plv_phase_destroy(void *handle) {
     PLV_ENTRY
     plv::Phase *P = (plv::Phase *)handle;
     if (P) {
+        const unsigned long long f0 = plv::pool_free_failures();
         P->release();
         delete P;
+        if (plv::pool_free_failures() != f0) throw plv::Fail{PLV_ECUDA};  // message set by pool_free
     }
     PLV_EXIT
 }
