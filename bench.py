@@ -208,43 +208,97 @@ def _reference_module():
     return None
 
 
-def cpu_iteration_rate(off, nbr, wts, selfw, classes, steps: int, warmup: int = 0):
-    """Time phase-1 coloured iterations of the reference (or the oracle port)
-    on host cores.  Returns (seconds per iteration list, kind, cores, M)."""
+def cpu_iteration_rate(off, nbr, wts, selfw, classes, steps: int, warmup: int = 0,
+                       nslices: int = 10):
+    """Time the reference's phase-1 local moving (or the oracle port) on host
+    cores, in bounded samples: step s sweeps the colour classes s mod
+    `nslices`, s mod nslices + nslices, ... (a strided 1/nslices of the
+    iteration's stages; `nslices` consecutive steps cover one whole iteration)
+    on one evolving state, plus 1/nslices of a modularity reduction.  An
+    uncoloured iteration is cut into `nslices` contiguous vertex blocks.
+    Returns (per-step (entries, seconds) list, kind, cores, M, nnz)."""
     ref = _reference_module()
     n = len(off) - 1
+    if len(classes) == 1:
+        classes = np.array_split(np.asarray(classes[0]), nslices)
+    deg = np.diff(off)
+    slices = [classes[j::nslices] for j in range(nslices)]
+    entries = [int(sum(int(deg[c].sum()) for c in sl)) for sl in slices]
     if ref is not None:
         g = ref.Graph(n, off.astype(np.int64), nbr.astype(np.int64), wts.astype(np.float64),
                       selfw.astype(np.float64))
         cores = os.cpu_count() or 1
         kind = "reference"
+        s = ref.singleton_state(g)
 
-        def one():
-            s = ref.singleton_state(g)
-            t0 = time.perf_counter()
-            for st in classes:
+        def sweep(sl):
+            for st in sl:
                 ref.run_iteration(g, s, st, cores)
+
+        def q():
             ref.modularity(g, s)
-            return time.perf_counter() - t0
     else:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as orc
-        og = orc.from_edges(*_csr_to_records(off, nbr, wts, selfw), num_vertices=n)
-        g = og
+        g = orc.from_edges(*_csr_to_records(off, nbr, wts, selfw), num_vertices=n)
         cores = 1
         kind = "port"
+        s = orc.singleton_state(g)
 
-        def one():
-            s = orc.singleton_state(og)
-            t0 = time.perf_counter()
-            for st in classes:
-                orc.run_iteration(og, s, st)
-            orc.modularity(og, s)
-            return time.perf_counter() - t0
-    for _ in range(warmup):
-        one()
-    times = [one() for _ in range(steps)]
-    return times, kind, cores, g.num_edges
+        def sweep(sl):
+            for st in sl:
+                orc.run_iteration(g, s, st)
+
+        def q():
+            orc.modularity(g, s)
+    t0 = time.perf_counter()
+    q()
+    tq = (time.perf_counter() - t0) / nslices
+    out = []
+    for k in range(warmup + steps):
+        j = k % nslices
+        t0 = time.perf_counter()
+        sweep(slices[j])
+        dt = time.perf_counter() - t0 + tq
+        if k >= warmup:
+            out.append((entries[j], dt))
+    return out, kind, cores, g.num_edges, int(len(nbr))
+
+
+def _sampled_value(samples, M, nnz):
+    """edges/s of sampled steps: each step's edges = M x its share of the
+    adjacency entries swept."""
+    ent = sum(e for e, _ in samples)
+    sec = sum(t for _, t in samples)
+    return M * ent / nnz / sec, sec / len(samples), ent / nnz
+
+
+def _parallel_records(config: str, scale: int, procs: int):
+    """The numpy record generator of a config, its record-draw range split
+    over `procs` forked workers (counter-based draws: ranges concatenate to
+    the serial output)."""
+    import multiprocessing as mp
+    from paper_1410_1237_b200 import synthetic as syn
+    if config == "c2_rmat20":
+        fn, params = syn.rmat_records, dict(scale=scale, edge_factor=CONFIG["edge_factor"])
+        R = CONFIG["edge_factor"] << scale
+    elif config == "c4_chung_lu":
+        fn, params = syn.chung_lu_records, dict(syn.CONFIGS[config][2])
+        R = int(round(syn.chung_lu_cdf(**params)[-1] / 2.0))
+    else:
+        host, _, params = syn.CONFIGS[config]
+        return host(seed=CONFIG["seed"], **params)
+    params["seed"] = CONFIG["seed"]
+    step = -(-R // procs)
+    jobs = [(fn, params, a, min(R, a + step)) for a in range(0, R, step)]
+    with mp.get_context("fork").Pool(len(jobs)) as pool:
+        parts = pool.map(_records_range, jobs)
+    return tuple(np.concatenate([p[i] for p in parts]) for i in range(3))
+
+
+def _records_range(job):
+    fn, params, a, b = job
+    return fn(**params, r_begin=a, r_end=b)
 
 
 def _csr_to_records(off, nbr, wts, selfw):
@@ -259,23 +313,50 @@ def _config_desc(args):
 
 
 def host_phase1_inputs(scale: int, config: str = "c2_rmat20"):
-    """numpy generator + CPU oracle (pinned to the reference) -> the VF'd
-    phase-1 graph and its colour classes, without touching the GPU."""
+    """The VF'd phase-1 graph and its colour classes without the GPU: the
+    numpy generator (record ranges on all host cores), the CPU oracle's CSR
+    build and vertex following (pinned to the reference), and the
+    reference's own compiled colouring on all host cores when it is present
+    (else the oracle's)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as orc
     from paper_1410_1237_b200 import synthetic as syn
-    if config == "c2_rmat20":
-        u, v, w = syn.rmat_records(scale, CONFIG["edge_factor"], seed=CONFIG["seed"])
-        n = 1 << scale
-    else:
-        host, _, params = syn.CONFIGS[config]
-        u, v, w = host(seed=CONFIG["seed"], **params)
-        n = syn.config_num_vertices(config)
+    cores = os.cpu_count() or 1
+    u, v, w = _parallel_records(config, scale, cores)
+    n = (1 << scale) if config == "c2_rmat20" else syn.config_num_vertices(config)
     g = orc.from_edges(u, v, w, num_vertices=n)
+    del u, v, w
     vf = orc.vf_compact(g)
-    col = orc.color_graph(vf.graph)
+    del g
     gg = vf.graph
+    ref = _reference_module()
+    if ref is not None:
+        rg = ref.Graph(gg.num_vertices, gg.adjacency_offsets, gg.neighbors, gg.weights,
+                       gg.self_loop_weights)
+        col = ref.color_graph(rg, cores)
+    else:
+        col = orc.color_graph(gg)
     return gg, col.classes(), col.num_colors
+
+
+def reference_louvain(cores: int):
+    """The reference's whole run() (PL/engine.py:259-315, compiled backend,
+    worker_count = all host cores) on config 2, timed from its own
+    Graph.from_edges of the records; None if the reference is absent."""
+    ref = _reference_module()
+    if ref is None:
+        return None
+    u, v, w = _parallel_records("c2_rmat20", CONFIG["scale"], cores)
+    t0 = time.perf_counter()
+    g = ref.Graph.from_edges(u, v, w, num_vertices=1 << CONFIG["scale"])
+    t1 = time.perf_counter()
+    h = ref.run(g, ref.RunConfig(worker_count=cores))
+    t2 = time.perf_counter()
+    return {"config": "c2_rmat20", "seconds": t2 - t1, "graph_build_seconds": t1 - t0,
+            "includes": "reference run() (VF, colouring, all phases, rebuilds) on all host "
+                        "cores; Graph.from_edges timed separately",
+            "cores": cores, "final_modularity": h.final_modularity,
+            "phases": len(h.phases), "communities": h.num_communities}
 
 
 def run_reference(args):
@@ -286,23 +367,27 @@ def run_reference(args):
     gg, classes, ncol = host_phase1_inputs(scale, args.config)
     if args.mode == "uncolored":
         classes = [np.arange(gg.num_vertices, dtype=np.int64)]
-    times, kind, cores, M = cpu_iteration_rate(gg.adjacency_offsets, gg.neighbors, gg.weights,
-                                               gg.self_loop_weights, classes, args.steps,
-                                               args.warmup)
-    t = float(np.mean(times))
-    val = M / t
-    sample = (f"{len(times)} phase-1 {'coloured (' + str(ncol) + ' stages)' if args.mode == 'colored' else 'uncoloured'} "
-              f"local-move iterations of {_config_desc(args)} after VF, singleton start")
+    samples, kind, cores, M, nnz = cpu_iteration_rate(
+        gg.adjacency_offsets, gg.neighbors, gg.weights, gg.self_loop_weights, classes,
+        args.steps, args.warmup)
+    val, t_step, cover = _sampled_value(samples, M, nnz)
+    sample = (f"{len(samples)} steps after {args.warmup} warm-up steps; a step = a strided "
+              f"1/10 of the phase-1 {'coloured (' + str(ncol) + ' stages)' if args.mode == 'colored' else 'uncoloured'} "
+              f"local-move iteration of {_config_desc(args)} after VF (every 10th colour class, "
+              f"one evolving state from the singleton start); the steps swept {cover:.2f} "
+              f"iterations' worth of adjacency entries")
+    louv = None if args.no_louvain else reference_louvain(cores)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (counter-based R-MAT, numpy generator)",
+        "data": "synthetic (counter-based generator of the BASELINE config, numpy)",
         "config": {"workload": f"{_config_desc(args)} phase-1 {args.mode} local-move iteration",
-                   "graph": {"n": gg.num_vertices, "M": M, "nnz": int(len(gg.neighbors))}},
+                   "graph": {"n": gg.num_vertices, "M": M, "nnz": nnz, "colours": ncol}},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "louvain_reference": louv,
     }
     print(json.dumps(line), flush=True)
 
@@ -488,11 +573,13 @@ def run_ours(args):
             cl = col.classes()
         else:
             cl = [np.arange(n, dtype=np.int64)]
-        times, kind, cores, Mc = cpu_iteration_rate(off, nb, wt, sw, cl, steps=3, warmup=1)
-        tc = float(np.mean(times))
-        cpu = {"value": Mc / tc, "unit": UNIT, "cores": cores, "kind": kind,
-               "sample": f"3 phase-1 {args.mode} iterations of the same graph (after 1 warm-up) "
-                         f"({len(cl)} stages), singleton start; {tc * 1e3:.0f} ms each"}
+        smp, kind, cores, Mc, nnzc = cpu_iteration_rate(off, nb, wt, sw, cl, steps=3, warmup=1)
+        cval, tc, cover = _sampled_value(smp, Mc, nnzc)
+        cpu = {"value": cval, "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": f"3 steps after 1 warm-up step on the same graph; a step = a strided "
+                         f"1/10 of the phase-1 {args.mode} iteration ({len(cl)} stages; every "
+                         f"10th class), one evolving state from the singleton start; "
+                         f"{tc * 1e3:.0f} ms per step, {cover:.2f} iterations' worth of entries"}
 
     if rank == 0:
         line = {

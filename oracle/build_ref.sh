@@ -27,3 +27,10 @@ SUFFIX=$("$PY" -c 'import sysconfig; print(sysconfig.get_config_var("EXT_SUFFIX"
 /usr/bin/gcc -O3 -fopenmp -ffp-contract=off -fPIC -shared \
   -I"$INC_PY" "$HERE/_ref/_kernels.c" -o "$OUT/_kernels$SUFFIX" -fopenmp
 echo "built $OUT/_kernels$SUFFIX"
+# the reference's own test suite, verbatim, for oracle/ref_suite.py
+TESTS=${REF_TESTS:-$(dirname "$(dirname "$REF")")/tests}
+if [ -d "$TESTS" ]; then
+  rm -rf "$HERE/_ref/ref_tests"
+  cp -r "$TESTS" "$HERE/_ref/ref_tests"
+  echo "staged $HERE/_ref/ref_tests"
+fi

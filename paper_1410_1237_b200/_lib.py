@@ -14,7 +14,8 @@ import os
 from .errors import EdgelessGraphError, GraphParseError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libplv.so")
+LIB_PATH = os.path.join(_HERE, f"libplv_{os.environ['PLV_VARIANT']}.so"
+                        if os.environ.get("PLV_VARIANT") else "libplv.so")
 
 PLV_OK = 0
 PLV_EINVAL = -1

@@ -18,8 +18,13 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT_DIR = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libplv.so")
+# Experiment variants (A/B sweeps without editing sources):
+#   PLV_VARIANT=name PLV_DEFINES="-DKNOB=1 ..." python -m paper_1410_1237_b200.build
+# builds _build_name/ and libplv_name.so; PLV_VARIANT=name at run time loads it.
+VARIANT = os.environ.get("PLV_VARIANT", "")
+DEFINES = os.environ.get("PLV_DEFINES", "").split()
+OUT_DIR = os.path.join(HERE, "_build" + (f"_{VARIANT}" if VARIANT else ""))
+LIB = os.path.join(HERE, f"libplv_{VARIANT}.so" if VARIANT else "libplv.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -49,7 +54,7 @@ def _stale(target, deps):
 def _compile(src, verbose=False):
     obj = os.path.join(OUT_DIR, os.path.basename(src)[:-3] + ".o")
     if _stale(obj, [src] + _headers()):
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *DEFINES, "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         r = subprocess.run(cmd, capture_output=True, text=True)

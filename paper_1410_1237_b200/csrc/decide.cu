@@ -234,7 +234,10 @@ __device__ __forceinline__ Best block_best(BestSmem<NT> &S, Best b) {
 // ------------------------------------------------------------ tier 0
 
 
-__global__ void __launch_bounds__(256) k_decide_t0(DecideArgs A, TierRef L, int64_t cnt) {
+#ifndef T0_MINB
+#define T0_MINB 1
+#endif
+__global__ void __launch_bounds__(256, T0_MINB) k_decide_t0(DecideArgs A, TierRef L, int64_t cnt) {
     decide_t0_body(A, L, cnt, blockIdx.x, gridDim.x);
 }
 
@@ -271,7 +274,7 @@ __device__ __forceinline__ void decide_t1_body(const DecideArgs &A, const TierRe
         const int64_t x = L.x[q];
         const int32_t i = L.vid[q];
         const int64_t e0 = L.row[q], e1 = L.end[q];
-        const int32_t c_old = A.assign[i];
+        const int32_t c_old = ld_gather(A.assign + (i));
         int deg = (int)(e1 - e0);
         uint32_t ts = 32;
         while (ts < (uint32_t)(deg + deg / 2 + 2)) ts <<= 1;
@@ -290,11 +293,11 @@ __device__ __forceinline__ void decide_t1_body(const DecideArgs &A, const TierRe
 #pragma unroll
         for (int u = 0; u < NCH; u++) {
             const int64_t e = e0 + 32 * u + lane;
-            jv[u] = e < e1 ? A.nbr[e] : i;
-            wv[u] = e < e1 ? A.wts[e] : 0.0;
+            jv[u] = e < e1 ? ld_row(A.nbr + (e)) : i;
+            wv[u] = e < e1 ? ld_row(A.wts + (e)) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < NCH; u++) cv[u] = jv[u] != i ? A.assign[jv[u]] : -1;
+        for (int u = 0; u < NCH; u++) cv[u] = jv[u] != i ? ld_gather(A.assign + jv[u]) : -1;
 #pragma unroll
         for (int u = 0; u < NCH; u++) {
             if (e0 + 32 * u >= e1) break;
@@ -310,7 +313,7 @@ __device__ __forceinline__ void decide_t1_body(const DecideArgs &A, const TierRe
         }
         e_old = __shfl_sync(FULL, e_old, 0);
         double ki = A.k[i];
-        double a_old_excl = dsub(A.a_tot[c_old], ki);
+        double a_old_excl = dsub(ld_gather(A.a_tot + (c_old)), ki);
         Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
         int nc = 0;
         for (uint32_t s = lane; s < ts; s += 32) {
@@ -318,7 +321,7 @@ __device__ __forceinline__ void decide_t1_body(const DecideArgs &A, const TierRe
             if (c < 0) continue;
             nc++;
             if (c == c_old) continue;
-            consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq),
+            consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, ld_gather(A.a_tot + (c)), A.four_m_sq),
                      LBL(A.labels, c), c, vals[s], 0);
         }
         warp_best(b);
@@ -447,7 +450,7 @@ __device__ Best certify_table(const DecideArgs &A, int32_t c_old, double ki, int
     __syncthreads();
     const double f_old = S.f_old;
     const int32_t l_old_n = S.l_old;
-    const double a_old_excl = dsub(A.a_tot[c_old], ki);
+    const double a_old_excl = dsub(ld_gather(A.a_tot + (c_old)), ki);
     const double inv_m = 1.0 / A.m;
     const int64_t l_old = LBL(A.labels, c_old);
     Best b{0.0, l_old, c_old, 0.0, 0};
@@ -467,7 +470,7 @@ __device__ Best certify_table(const DecideArgs &A, int32_t c_old, double ki, int
             L[u] = ok ? cnt[sl[u]] : 0;
         }
 #pragma unroll
-        for (int u = 0; u < CU; u++) at[u] = c[u] >= 0 && c[u] != c_old ? A.a_tot[c[u]] : 0.0;
+        for (int u = 0; u < CU; u++) at[u] = c[u] >= 0 && c[u] != c_old ? ld_gather(A.a_tot + c[u]) : 0.0;
 #pragma unroll
         for (int u = 0; u < CU; u++) {
             if (c[u] < 0 || c[u] == c_old) continue;
@@ -548,9 +551,9 @@ __device__ void exact_folds(const DecideArgs &A, int32_t i, CertSmem<NT> &S) {
         const int64_t eb = base + (int64_t)tid * FU;
         int32_t j[FU], c[FU], idx[FU];
 #pragma unroll
-        for (int u = 0; u < FU; u++) j[u] = eb + u < e1 ? A.nbr[eb + u] : i;
+        for (int u = 0; u < FU; u++) j[u] = eb + u < e1 ? ld_row(A.nbr + (eb + u)) : i;
 #pragma unroll
-        for (int u = 0; u < FU; u++) c[u] = j[u] != i ? A.assign[j[u]] : -1;
+        for (int u = 0; u < FU; u++) c[u] = j[u] != i ? ld_gather(A.assign + j[u]) : -1;
         int cntm = 0;
 #pragma unroll
         for (int u = 0; u < FU; u++) {
@@ -569,7 +572,7 @@ __device__ void exact_folds(const DecideArgs &A, int32_t i, CertSmem<NT> &S) {
         for (int u = 0; u < FU; u++)
             if (idx[u] >= 0) {
                 S.cidx[pos] = idx[u];
-                S.cw[pos] = A.wts[eb + u];
+                S.cw[pos] = ld_row(A.wts + (eb + u));
                 pos++;
             }
         __syncthreads();
@@ -630,11 +633,11 @@ __device__ bool resolve(const DecideArgs &A, int64_t x, int32_t i, int32_t c_old
     __syncthreads();
     exact_folds<NT, FU>(A, i, S);
     if (tid == 0) {
-        double a_old_excl = dsub(A.a_tot[c_old], ki);
+        double a_old_excl = dsub(ld_gather(A.a_tot + (c_old)), ki);
         Best e{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
         for (int t = 1; t < S.nn; t++) {
             int32_t c = S.N[t];
-            consider(e, gain_of(S.acc[t], S.acc[0], A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq),
+            consider(e, gain_of(S.acc[t], S.acc[0], A.m, ki, a_old_excl, ld_gather(A.a_tot + (c)), A.four_m_sq),
                      LBL(A.labels, c), c, S.acc[t], 0);
         }
         finish_vertex(A, x, c_old, S.acc[0], e.g, e.c, e.e);
@@ -665,10 +668,10 @@ __device__ void table_exact(const DecideArgs &A, int64_t x, int32_t i, int32_t c
         int32_t c = -1;
         double w = 0.0;
         if (e < e1) {
-            int32_t j = A.nbr[e];
+            int32_t j = ld_row(A.nbr + (e));
             if (j != i) {
-                c = A.assign[j];
-                w = A.wts[e];
+                c = ld_gather(A.assign + (j));
+                w = ld_row(A.wts + (e));
             }
         }
         cbuf[tid] = c;
@@ -691,12 +694,12 @@ __device__ void table_exact(const DecideArgs &A, int64_t x, int32_t i, int32_t c
         S.f_old = s >= 0 ? vals[s] : 0.0;
     }
     __syncthreads();
-    const double e_old = S.f_old, a_old_excl = dsub(A.a_tot[c_old], ki);
+    const double e_old = S.f_old, a_old_excl = dsub(ld_gather(A.a_tot + (c_old)), ki);
     Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
     for (uint32_t s = tid; s < T.size(); s += NT) {
         int32_t c = keys[s];
         if (c >= 0 && c != c_old)
-            consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq),
+            consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, ld_gather(A.a_tot + (c)), A.four_m_sq),
                      LBL(A.labels, c), c, vals[s], 0);
     }
     b = block_best<NT>(S.bs, b);
@@ -718,7 +721,7 @@ __device__ __forceinline__ void block_decide(const DecideArgs &A, int64_t x, int
                                              int32_t *cntt, CL *clist, int *ncl, CertSmem<NT> &S,
                                              unsigned long long &my_cand, Trace *trp = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31;
-    const int32_t c_old = A.assign[i];
+    const int32_t c_old = ld_gather(A.assign + (i));
     const double ki = A.k[i];
     if (tid == 0) *ncl = 0;
     __syncthreads();
@@ -727,7 +730,7 @@ __device__ __forceinline__ void block_decide(const DecideArgs &A, int64_t x, int
 #pragma unroll
         for (int u = 0; u < U; u++) {
             int64_t e = b0 + u * NT + tid;
-            j[u] = e < e1 ? A.nbr[e] : i;
+            j[u] = e < e1 ? ld_row(A.nbr + (e)) : i;
         }
         int32_t c[U];
         double w[U];
@@ -735,8 +738,8 @@ __device__ __forceinline__ void block_decide(const DecideArgs &A, int64_t x, int
         for (int u = 0; u < U; u++) {
             int64_t e = b0 + u * NT + tid;
             bool ok = j[u] != i;  // out-of-range entries carry j = i
-            c[u] = ok ? A.assign[j[u]] : -1;
-            w[u] = ok ? A.wts[e] : 0.0;
+            c[u] = ok ? ld_gather(A.assign + j[u]) : -1;
+            w[u] = ok ? ld_row(A.wts + (e)) : 0.0;
         }
         if (trp && b0 == e0) {
             volatile int32_t sink = c[0];  // wait for the loads
@@ -874,8 +877,8 @@ __global__ void k_hub_accum(DecideArgs A, const int64_t *eoff, const int64_t *to
             q = hub_of(eoff, nh, t);
             i = H.vid[q];
             const int64_t e = H.row[q] + (t - eoff[q]);
-            j = A.nbr[e];
-            wv = A.wts[e];
+            j = ld_row(A.nbr + (e));
+            wv = ld_row(A.wts + (e));
         }
         if (!waited) {
             // launched programmatically: the loads above overlap the previous
@@ -884,9 +887,9 @@ __global__ void k_hub_accum(DecideArgs A, const int64_t *eoff, const int64_t *to
             waited = true;
         }
         if (t < E) {
-            c_old = A.assign[i];
+            c_old = ld_gather(A.assign + (i));
             if (j != i) {
-                c = A.assign[j];
+                c = ld_gather(A.assign + (j));
                 w = wv;
             }
         }
@@ -956,7 +959,7 @@ __device__ void hub_decide_one(const DecideArgs &A, const int32_t *list, const i
     const int tid = threadIdx.x;
     const int64_t x = list[q];
     const int32_t i = H.vid[q];
-    const int32_t c_old = A.assign[i];
+    const int32_t c_old = ld_gather(A.assign + (i));
     const double ki = A.k[i];
     const int64_t base = toff[q];
     // warp 0: the hub's best from the partials and the overlap test on the
@@ -1064,12 +1067,12 @@ __device__ void hub_decide_one(const DecideArgs &A, const int32_t *list, const i
         __syncthreads();
         exact_folds<NT, HFU>(A, i, S);
         if (tid == 0) {
-            double a_old_excl = dsub(A.a_tot[c_old], ki);
+            double a_old_excl = dsub(ld_gather(A.a_tot + (c_old)), ki);
             Best e{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
             for (int t = 1; t < S.nn; t++) {
                 int32_t c = S.N[t];
                 consider(e,
-                         gain_of(S.acc[t], S.acc[0], A.m, ki, a_old_excl, A.a_tot[c],
+                         gain_of(S.acc[t], S.acc[0], A.m, ki, a_old_excl, ld_gather(A.a_tot + (c)),
                                  A.four_m_sq),
                          LBL(A.labels, c), c, S.acc[t], 0);
             }
@@ -1111,14 +1114,14 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *l
     const int64_t pk = H.blk[blockIdx.x];
     const int64_t q = pk >> 32, y = pk & 0xffffffffll;
     const int32_t i = H.vid[q];
-    const int32_t c_old = A.assign[i];
+    const int32_t c_old = ld_gather(A.assign + (i));
     const int64_t base = toff[q];
     const int64_t cap = toff[q + 1] - base;
     const int64_t dq = q * H.dn, deg = eoff[q + 1] - eoff[q];
     const int32_t so = DENSE ? 0 : H.sold[q];
     const double f_old = DENSE ? H.dval[dq + c_old] : so >= 0 ? hvals[base + so] : 0.0;
     const int32_t l_old = DENSE ? H.dcnt[dq + c_old] : so >= 0 ? hcnt[base + so] : 0;
-    const double ki = A.k[i], a_old_excl = dsub(A.a_tot[c_old], ki);
+    const double ki = A.k[i], a_old_excl = dsub(ld_gather(A.a_tot + (c_old)), ki);
     const double inv_m = 1.0 / A.m;
     TR_MARK
     int32_t c[PU];

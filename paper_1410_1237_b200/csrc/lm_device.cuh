@@ -8,6 +8,10 @@
 
 namespace plv {
 
+#ifndef T0_INPLACE
+#define T0_INPLACE 0
+#endif
+
 __device__ __forceinline__ int64_t LBL(const int32_t *labels, int32_t c) {
     return labels ? (int64_t)labels[c] : (int64_t)c;
 }
@@ -70,17 +74,56 @@ __device__ __forceinline__ void decide_t0_body(const DecideArgs &A, const TierRe
         const int32_t i = L.vid[q];
         const int64_t e0 = L.row[q];
         const int deg = (int)(L.end[q] - e0);
-        const int32_t c_old = A.assign[i];
+        const int32_t c_old = ld_gather(A.assign + (i));
         // all row loads, then all community loads, in flight together
         int32_t jj[T0_MAXD], cc[T0_MAXD];
         double ww[T0_MAXD];
 #pragma unroll
         for (int t = 0; t < T0_MAXD; t++) {
-            jj[t] = t < deg ? A.nbr[e0 + t] : i;
-            ww[t] = t < deg ? A.wts[e0 + t] : 0.0;
+            jj[t] = t < deg ? ld_row(A.nbr + (e0 + t)) : i;
+            ww[t] = t < deg ? ld_row(A.wts + (e0 + t)) : 0.0;
         }
 #pragma unroll
-        for (int t = 0; t < T0_MAXD; t++) cc[t] = jj[t] != i ? A.assign[jj[t]] : -1;
+        for (int t = 0; t < T0_MAXD; t++) cc[t] = jj[t] != i ? ld_gather(A.assign + jj[t]) : -1;
+#if T0_INPLACE
+        // in place: a "head" is the first entry of its community; its weight
+        // becomes the community's sum folded forward in adjacency order
+        // (0.0 + w_first + ... is w_first + ...; PL/_kernels.pyx:64-75)
+        bool head[T0_MAXD];
+        int nc = 0;
+#pragma unroll
+        for (int t = 0; t < T0_MAXD; t++) {
+            bool h = t < deg && cc[t] >= 0;
+#pragma unroll
+            for (int u = 0; u < t; u++) h = h && cc[u] != cc[t];
+            head[t] = h;
+            if (h) {
+                double v = ww[t];
+#pragma unroll
+                for (int u = t + 1; u < T0_MAXD; u++)
+                    if (u < deg && cc[u] == cc[t]) v = dadd(v, ww[u]);
+                ww[t] = v;
+                nc++;
+            }
+        }
+        my_cand += nc;
+        double e_old = 0.0;
+#pragma unroll
+        for (int t = 0; t < T0_MAXD; t++)
+            if (head[t] && cc[t] == c_old) e_old = ww[t];
+        double ki = A.k[i];
+        double a_old_excl = dsub(ld_gather(A.a_tot + (c_old)), ki);
+        Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
+#pragma unroll
+        for (int t = 0; t < T0_MAXD; t++) {
+            if (head[t] && cc[t] != c_old) {
+                int32_t c = cc[t];
+                consider(b, gain_of(ww[t], e_old, A.m, ki, a_old_excl, ld_gather(A.a_tot + c),
+                                    A.four_m_sq),
+                         LBL(A.labels, c), c, ww[t], 0);
+            }
+        }
+#else
         int32_t keys[T0_MAXD];
         double vals[T0_MAXD];
         int nc = 0;
@@ -116,16 +159,17 @@ __device__ __forceinline__ void decide_t0_body(const DecideArgs &A, const TierRe
         for (int s = 0; s < T0_MAXD; s++)
             if (s < nc && keys[s] == c_old) e_old = vals[s];
         double ki = A.k[i];
-        double a_old_excl = dsub(A.a_tot[c_old], ki);
+        double a_old_excl = dsub(ld_gather(A.a_tot + (c_old)), ki);
         Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
 #pragma unroll
         for (int s = 0; s < T0_MAXD; s++) {
             if (s < nc && keys[s] != c_old) {
                 int32_t c = keys[s];
-                consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, A.a_tot[c], A.four_m_sq),
+                consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, ld_gather(A.a_tot + (c)), A.four_m_sq),
                          LBL(A.labels, c), c, vals[s], 0);
             }
         }
+#endif
         finish_vertex(A, x, c_old, e_old, b.g, b.c, b.e);
     }
     if (A.cand) {

@@ -59,15 +59,17 @@ RMAT_ABC = (0.57, 0.19, 0.19)
 
 
 def rmat_records(scale: int, edge_factor: int = 16, abc=RMAT_ABC, w_lo: float = 1.0,
-                 w_hi: float = 10.0, seed: int = 0, chunk: int = 1 << 20):
-    """R-MAT records (self loops dropped, duplicates kept for from_edges)."""
+                 w_hi: float = 10.0, seed: int = 0, chunk: int = 1 << 20, r_begin: int = 0,
+                 r_end: int | None = None):
+    """R-MAT records (self loops dropped, duplicates kept for from_edges).
+    [r_begin, r_end) selects a range of record draws; ranges concatenate."""
     a, b, c = abc
     ab = a + b
     abc_ = ab + c
-    R = edge_factor << scale
+    R = edge_factor << scale if r_end is None else min(r_end, edge_factor << scale)
     klvl, kw = stream_key(seed, 1), stream_key(seed, 2)
-    us, vs, ws = [], [], []
-    for r0 in range(0, R, chunk):
+    us, vs, ws = [np.empty(0, np.int64)], [np.empty(0, np.int64)], [np.empty(0)]
+    for r0 in range(r_begin, R, chunk):
         r = np.arange(r0, min(R, r0 + chunk), dtype=np.uint64)
         s = np.zeros(len(r), dtype=np.int64)
         d = np.zeros(len(r), dtype=np.int64)
@@ -138,13 +140,17 @@ def chung_lu_cdf(n: int = 1 << 24, gamma: float = 2.1, mean_degree: float = 12.0
 
 
 def chung_lu_records(n: int = 1 << 24, gamma: float = 2.1, mean_degree: float = 12.0,
-                     max_degree: float = 1e5, seed: int = 0, chunk: int = 1 << 22):
+                     max_degree: float = 1e5, seed: int = 0, chunk: int = 1 << 22,
+                     r_begin: int = 0, r_end: int | None = None):
+    """Chung-Lu records; [r_begin, r_end) selects a range of record draws."""
     cdf = chung_lu_cdf(n, gamma, mean_degree, max_degree)
     total = cdf[-1]
     R = int(round(total / 2.0))
+    if r_end is not None:
+        R = min(R, r_end)
     key = stream_key(seed, 8)
-    us, vs = [], []
-    for r0 in range(0, R, chunk):
+    us, vs = [np.empty(0, np.int64)], [np.empty(0, np.int64)]
+    for r0 in range(r_begin, R, chunk):
         r = np.arange(r0, min(R, r0 + chunk), dtype=np.uint64)
         u = np.minimum(np.searchsorted(cdf, rnd01(key, r * _U(2)) * total, side="right"), n - 1)
         v = np.minimum(np.searchsorted(cdf, rnd01(key, r * _U(2) + _U(1)) * total,
