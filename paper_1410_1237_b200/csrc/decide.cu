@@ -29,6 +29,7 @@
 #include "localmove.cuh"
 #include "lm_device.cuh"
 #include "csr.cuh"
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 namespace plv {
@@ -1228,6 +1229,215 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *l
 }
 
 
+// ------------------------------------------- tier 4, cluster mode (few hubs)
+//
+// A stage with few hub-tier vertices, none of degree above HC_MAXD: ONE
+// launch decides them all, a thread-block cluster of HC_CL CTAs per vertex.
+// The vertex's any-order table is spread over the cluster's shared memory
+// (distributed shared memory, DSMEM): the owner CTA of community c is the low
+// hash bits, its slot the next ones.  Every CTA accumulates a 1/HC_CL chunk of
+// the row -- warp groups of equal communities pre-summed, then one remote
+// claim (CAS) + any-order add per group into the owner's slice -- so a row is
+// spread over HC_CL SMs, with no global table, no second kernel and no
+// per-hub ticket.  Then each CTA runs the certification passes of
+// certify_table over its own slice (gains, slack; bests gathered in rank 0),
+// and rank 0 takes the decision: at once for integral graphs, else through
+// resolve() (exact left folds of the overlapping communities in adjacency
+// order) or, past MAXS overlaps, table_exact over the hub's clean global
+// table slice -- the same rules, and bits, as k_hub_accum + k_hub_pass.
+constexpr int HC_CL = 8;        // CTAs per cluster (portable size)
+constexpr int HC_NT = 512;      // threads per CTA
+constexpr int HC_TS = 8192;     // table slots per CTA (16 B each)
+constexpr int HC_MAXD = HC_CL * HC_TS / 2;  // load factor <= 1/2
+constexpr int HC_LOGCL = 3;
+static_assert((1 << HC_LOGCL) == HC_CL, "cluster size");
+
+struct HubClArgs {
+    const int32_t *list;  // [nh] stage-local index of each hub-tier vertex
+    const int32_t *vid;   // [nh]
+    const int64_t *row;   // [nh] first entry of its row
+    const int64_t *eoff;  // [nh + 1] entry offsets (degrees)
+    const int64_t *toff;  // [nh + 1] global table slices (overflow fallback)
+    int32_t *hkeys;
+    double *hvals;
+};
+
+static size_t hc_smem() { return (size_t)HC_TS * (sizeof(double) + 2 * sizeof(int32_t)); }
+
+__global__ void __launch_bounds__(HC_NT, 1) k_hub_cluster(DecideArgs A, HubClArgs H) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ CertSmem<HC_NT> S;
+    __shared__ int32_t cidx[HC_NT * HFU];
+    __shared__ double cw[HC_NT * HFU];
+    __shared__ Best cb[HC_CL];
+    double *vals = reinterpret_cast<double *>(dsm);
+    int32_t *keys = reinterpret_cast<int32_t *>(dsm + sizeof(double) * HC_TS);
+    int32_t *cnt = keys + HC_TS;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int r = (int)cl.block_rank();
+    const int64_t q = blockIdx.x / HC_CL;
+    for (int s = tid; s < HC_TS; s += HC_NT) {
+        keys[s] = -1;
+        vals[s] = 0.0;
+        cnt[s] = 0;
+    }
+    if (tid == 0) {
+        S.cidx = cidx;
+        S.cw = cw;
+        S.nS = 0;
+        S.flag = 0;
+    }
+    // static loads first; the state only after the previous stage (PDL)
+    const int32_t i = H.vid[q];
+    const int64_t x = H.list[q];
+    const int64_t e0 = H.row[q], deg = H.eoff[q + 1] - H.eoff[q];
+    const int64_t chunk = (deg + HC_CL - 1) / HC_CL;
+    const int64_t c0 = e0 + (int64_t)r * chunk;
+    const int64_t c1 = c0 + chunk < e0 + deg ? c0 + chunk : e0 + deg;
+    pdl_wait();
+    const int32_t c_old = ld_gather(A.assign + i);
+    const double ki = A.k[i];
+    cl.sync();  // every slice initialised before any remote insert
+    for (int64_t b0 = c0; b0 < c1; b0 += HC_NT) {
+        const int64_t e = b0 + tid;
+        int32_t c = -1;
+        double w = 0.0;
+        if (e < c1) {
+            const int32_t j = ld_row(A.nbr + e);
+            if (j != i) {
+                c = ld_gather(A.assign + j);
+                w = ld_row(A.wts + e);
+            }
+        }
+        // equal communities of the warp: one insert with the group's sum
+        const unsigned grp = __match_any_sync(FULL, c);
+        const double gs = group_sum(grp, w);
+        if (c >= 0 && lane == __ffs(grp) - 1) {
+            const uint32_t h = hslot(c, 0xffffffffu);
+            const unsigned owner = h & (HC_CL - 1);
+            int32_t *rk = cl.map_shared_rank(keys, owner);
+            double *rv = cl.map_shared_rank(vals, owner);
+            int32_t *rc = cl.map_shared_rank(cnt, owner);
+            uint32_t sl = (h >> HC_LOGCL) & (HC_TS - 1);
+            while (true) {
+                const int32_t old = atomicCAS(rk + sl, -1, c);
+                if (old == -1 || old == c) break;
+                sl = (sl + 1) & (HC_TS - 1);
+            }
+            atomicAdd(rv + sl, gs);
+            atomicAdd(rc + sl, __popc(grp));
+        }
+    }
+    cl.sync();
+    if (tid == 0) {  // c_old's any-order sum, from its owner's slice
+        const uint32_t h = hslot(c_old, 0xffffffffu);
+        const unsigned owner = h & (HC_CL - 1);
+        const int32_t *rk = cl.map_shared_rank(keys, owner);
+        uint32_t sl = (h >> HC_LOGCL) & (HC_TS - 1);
+        double f = 0.0;
+        int32_t l = 0;
+        while (true) {
+            const int32_t k = rk[sl];
+            if (k == c_old) {
+                f = cl.map_shared_rank(vals, owner)[sl];
+                l = cl.map_shared_rank(cnt, owner)[sl];
+                break;
+            }
+            if (k == -1) break;
+            sl = (sl + 1) & (HC_TS - 1);
+        }
+        S.f_old = f;
+        S.l_old = l;
+    }
+    cl.sync();  // every remote read done: the slices may be overwritten
+    const double f_old = S.f_old;
+    const int32_t l_old_n = S.l_old;
+    const double a_old_excl = dsub(ld_gather(A.a_tot + c_old), ki);
+    const double inv_m = 1.0 / A.m;
+    // pass 1 (certify_table): gains and slack of this slice, its best
+    Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
+    unsigned long long nc = 0;
+    for (int p0 = tid; p0 < HC_TS; p0 += HC_NT * 4) {
+        int32_t c[4], L[4];
+        double F[4], at[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int sl = p0 + u * HC_NT;
+            c[u] = sl < HC_TS ? keys[sl] : -1;
+            F[u] = c[u] >= 0 ? vals[sl] : 0.0;
+            L[u] = c[u] >= 0 ? cnt[sl] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) at[u] = c[u] >= 0 && c[u] != c_old ? ld_gather(A.a_tot + c[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            if (c[u] < 0) continue;
+            nc++;
+            if (c[u] == c_old) continue;
+            const int sl = p0 + u * HC_NT;
+            const double g = gain_of(F[u], f_old, A.m, ki, a_old_excl, at[u], A.four_m_sq);
+            consider(b, g, LBL(A.labels, c[u]), c[u], F[u], L[u]);
+            vals[sl] = g;
+            cnt[sl] = __float_as_int(__double2float_ru(gain_slack_r(F[u], L[u], f_old, l_old_n, inv_m, g)));
+        }
+    }
+    if (A.cand) {
+        for (int o = 16; o > 0; o >>= 1) nc += __shfl_xor_sync(FULL, nc, o);
+        if (lane == 0 && nc) atomicAdd(A.cand, nc);
+    }
+    b = block_best<HC_NT>(S.bs, b);
+    if (tid == 0) cl.map_shared_rank(cb, 0)[r] = b;
+    cl.sync();
+    if (A.integral) {
+        // exact in any order: the plain argmax is the reference's
+        if (r == 0 && tid == 0) {
+            Best bw = cb[0];
+            for (int t = 1; t < HC_CL; t++) consider(bw, cb[t].g, cb[t].l, cb[t].c, cb[t].e, cb[t].n);
+            finish_vertex(A, x, c_old, f_old, bw.g, bw.c, bw.e);
+        }
+        return;  // rank 0's cb is read by rank 0 only
+    }
+    Best bw;
+    {
+        const Best *rcb = cl.map_shared_rank(cb, 0);
+        bw = rcb[0];
+        for (int t = 1; t < HC_CL; t++) {
+            const Best o = rcb[t];
+            consider(bw, o.g, o.l, o.c, o.e, o.n);
+        }
+    }
+    // pass 2 (certify_table): this slice's candidates overlapping the best,
+    // listed in rank 0
+    const bool stay_best = bw.c == c_old;
+    const double slack_b = stay_best ? 0.0 : gain_slack_r(bw.e, bw.n, f_old, l_old_n, inv_m, bw.g);
+    const double lower = stay_best ? 0.0 : bw.g - slack_b;
+    CertSmem<HC_NT> *S0 = cl.map_shared_rank(&S, 0);
+    for (int sl = tid; sl < HC_TS; sl += HC_NT) {
+        const int32_t c = keys[sl];
+        if (c < 0 || c == c_old || c == bw.c) continue;
+        const double slv = (double)__int_as_float(cnt[sl]);
+        if ((slv > 0.0 || slack_b > 0.0) && vals[sl] + slv >= lower) {
+            const int k = atomicAdd(&S0->nS, 1);
+            if (k < MAXS)
+                S0->N[2 + k] = c;
+            else
+                atomicOr(&S0->flag, 2);
+        }
+    }
+    cl.sync();
+    if (r != 0) return;
+    if (tid == 0 && !stay_best && slack_b > 0.0 && lower <= 0.0) S.flag |= 1;  // "stay" overlaps
+    __syncthreads();
+    if (!resolve<HC_NT, HFU>(A, x, i, c_old, ki, bw, S)) {
+        const int64_t base = H.toff[q];
+        table_exact<HC_NT>(A, x, i, c_old, ki, H.hkeys + base, H.hvals + base,
+                           PowTab{(uint32_t)(H.toff[q + 1] - base - 1)}, S);
+    }
+}
+
+
 // ================================================================ planning
 
 __global__ void k_tier_keys(const int64_t *off, const int32_t *vtx, const int64_t *stage_off,
@@ -1398,8 +1608,10 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
         // few hubs: dense per-hub community arrays (no claims), items are row
         // positions; else hash tables, items are table slices
         sp.hub_dense = sp.tcount[4] > 0 && sp.tcount[4] <= P.dense_k;
+        sp.hub_cluster = sp.hub_dense && PLV_HUB_CLUSTER;
         for (int64_t z = 0; z < sp.tcount[4]; z++) {
             int64_t d = deg[h0 + z];
+            if (d > HC_MAXD) sp.hub_cluster = false;
             int64_t cap = 64;
             while (cap < 2 * d + 2) cap <<= 1;
             int64_t sl = sp.hub_dense ? (d + HSB - 1) / HSB : (cap + HTSL - 1) / HTSL;
@@ -1420,7 +1632,7 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
         sp.hub_nblk = pacc;
         max_parts = pacc > max_parts ? pacc : max_parts;
         P.max_hub_entries = acc > P.max_hub_entries ? acc : P.max_hub_entries;
-        if (sp.hub_dense) P.max_dense_entries = acc > P.max_dense_entries ? acc : P.max_dense_entries;
+        if (sp.hub_dense && !sp.hub_cluster) P.max_dense_entries = acc > P.max_dense_entries ? acc : P.max_dense_entries;
         P.max_hubs = sp.tcount[4] > P.max_hubs ? sp.tcount[4] : P.max_hubs;
         P.max_table = tacc > P.max_table ? tacc : P.max_table;
     }
@@ -1492,6 +1704,8 @@ void ensure_decide_attrs() {
     PLV_CUDA(cudaFuncSetAttribute(k_decide_t2<T2_TS, T2_MAXD, 1024>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)t2_smem(T2_TS)));
+    PLV_CUDA(cudaFuncSetAttribute(k_hub_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)hc_smem()));
     dev_done = dev;
 }
 
@@ -1600,7 +1814,26 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
                      P.cbuf,
                      P.dn};
         unsigned g2 = (unsigned)sp.hub_nblk;
-        if (sp.hub_dense) {
+        if (sp.hub_cluster) {
+            HubClArgs C{list, P.hub_vid + sp.hub_base, P.hub_row + sp.hub_base, eoff, toff,
+                        P.hkeys, P.hvals};
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)(nh * HC_CL));
+            cfg.blockDim = dim3(HC_NT);
+            cfg.dynamicSmemBytes = hc_smem();
+            cfg.stream = st;
+            cudaLaunchAttribute at[2];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = HC_CL;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[1].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 2;
+            PLV_CUDA(cudaLaunchKernelEx(&cfg, k_hub_cluster, A, C));
+            count_launch();
+        } else if (sp.hub_dense) {
             launch_pdl(k_hub_accum<true>, grid_for(E, 256), 256, 0, st, A, eoff, toff, nh, E,
                        P.hkeys, P.hvals, P.hcnt, H);
             launch_pdl(k_hub_pass<true>, g2, HSB, 0, st, A, list, eoff, toff, P.hkeys, P.hvals,

@@ -29,6 +29,9 @@ constexpr int BLK = 512;      // threads per block in tier 3 (128/256/1024 measu
 constexpr int T2_TS = 4096;   // smem slots for tier 2 (>= 1.5 * (2048 + 1))
 constexpr int T2A_TS = 1024;
 constexpr int NTIER = 5;  // t0, t1, t2 (block, small table), t3 (block), t4 (hubs)
+#ifndef PLV_HUB_CLUSTER
+#define PLV_HUB_CLUSTER 1  // few-hub stages decided by one cluster kernel (decide.cu)
+#endif
 
 constexpr int SMALL_APPLY_MAX = 1024;  // stage size handled by the one-CTA apply (2048 measured slower)
 constexpr int SA_THREADS = 256;
@@ -69,6 +72,7 @@ struct StagePlan {
     int64_t hub_nblk = 0;      // hub pass blocks (one per candidate slice)
     int64_t hub_blk_base = 0;  // first of them in hub_blk
     bool hub_dense = false;    // hub tier on dense per-hub community arrays
+    bool hub_cluster = false;  // ... decided by k_hub_cluster (one cluster per hub)
 };
 
 struct Best;  // decide.cu
