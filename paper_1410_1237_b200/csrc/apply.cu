@@ -490,78 +490,10 @@ __global__ void __launch_bounds__(SA_THREADS) k_stage_apply_small(StageArgs A, i
 // of its barriers.
 template <int VPL>
 __global__ void __launch_bounds__(32) k_stage_apply_tiny(StageArgs A) {
-
     pdl_wait();  // the decide outputs
-    constexpr int NE = 64 * VPL;
-    __shared__ unsigned long long sk[NE];
-    __shared__ double sw[NE], sa[NE];
-    const int lane = threadIdx.x;
-    const int64_t ns = A.ns;
-    const unsigned long long S = (unsigned long long)SENTINEL << 32;
-    unsigned nmv = 0;
-#pragma unroll
-    for (int v = 0; v < VPL; v++) {
-        const int x = lane + 32 * v;
-        bool mv = false;
-        int32_t a = 0, b = 0;
-        if (x < ns) {
-            const int32_t i = A.subset[x];
-            b = A.target[x];
-            a = A.assign[i];
-            mv = A.moved[x] && a != b;
-            if (mv) {
-                const double s2 = dmul(2.0, A.selfw[i]);
-                const double ki = A.k[i];
-                sw[2 * x] = -dadd(dmul(2.0, A.e_old[x]), s2);  // leave a
-                sa[2 * x] = -ki;
-                sw[2 * x + 1] = dadd(dmul(2.0, A.e_best[x]), s2);  // join b
-                sa[2 * x + 1] = ki;
-                atomicSub(A.sizes + a, 1);
-                atomicAdd(A.sizes + b, 1);
-                nmv++;
-            }
-        }
-        sk[2 * x] = mv ? ((unsigned long long)(uint32_t)a << 32) | (uint64_t)(2 * x) : S | (2 * x);
-        sk[2 * x + 1] =
-            mv ? ((unsigned long long)(uint32_t)b << 32) | (uint64_t)(2 * x + 1) : S | (2 * x + 1);
-    }
-    __syncwarp();
-    // bitonic sort of NE keys, VPL compare-exchanges per lane per step
-    for (int k = 2; k <= NE; k <<= 1)
-        for (int j = k >> 1; j > 0; j >>= 1) {
-#pragma unroll
-            for (int v = 0; v < VPL; v++) {
-                const int pr = lane + 32 * v;
-                const int i0 = 2 * j * (pr / j) + (pr % j), i1 = i0 + j;
-                const bool up = (i0 & k) == 0;
-                const unsigned long long x = sk[i0], y = sk[i1];
-                if ((x > y) == up) {
-                    sk[i0] = y;
-                    sk[i1] = x;
-                }
-            }
-            __syncwarp();
-        }
-    for (int p = lane; p < NE; p += 32) {
-        const uint32_t c = (uint32_t)(sk[p] >> 32);
-        if (c == SENTINEL) continue;
-        if (p > 0 && (uint32_t)(sk[p - 1] >> 32) == c) continue;
-        double W = A.w_int[c], At = A.a_tot[c];
-        for (int q = p; q < NE && (uint32_t)(sk[q] >> 32) == c; q++) {
-            const int e = (int)(sk[q] & 0xffffffffull);
-            W = dadd(W, sw[e]);
-            At = dadd(At, sa[e]);
-        }
-        A.w_int[c] = W;
-        A.a_tot[c] = At;
-    }
-#pragma unroll
-    for (int v = 0; v < VPL; v++) {
-        const int x = lane + 32 * v;
-        if (x < ns && A.moved[x]) A.assign[A.subset[x]] = A.target[x];
-    }
-    for (int o = 16; o > 0; o >>= 1) nmv += __shfl_xor_sync(0xffffffffu, nmv, o);
-    if (lane == 0 && nmv) atomicAdd(A.moves, (unsigned long long)nmv);
+    __shared__ unsigned long long sk[64 * VPL];
+    __shared__ double sw[64 * VPL], sa[64 * VPL];
+    apply_tiny_warp<VPL>(A, sk, sw, sa);
 }
 
 __global__ void k_pos_scatter(const int32_t *subset, int64_t ns, int32_t *pos, int *dup) {

@@ -110,26 +110,17 @@ struct Buf {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 
-// L2 eviction-priority hints for the local-moving kernels.  The CSR rows are
-// streamed once per sweep (2 GB on C4) and would otherwise push the small,
-// randomly gathered state arrays (assignment, a_tot) out of the 126 MB L2:
-// rows load with L1::no_allocate + L2 evict_first, gathers with evict_last.
-// Read-only (.nc) forms: only for data no kernel of the launch writes.
-// -DPLV_CACHE_HINTS=0 builds plain loads (A/B measurements).
-#ifndef PLV_CACHE_HINTS
-#define PLV_CACHE_HINTS 1
-#endif
+// Loads of the local-moving kernels.  CSR rows are immutable during a phase
+// and streamed once per sweep: read-only path, no L1 allocation, L2
+// evict-first.  The state (assignment, a_tot, sizes) is mutable -- k_tail
+// decides and applies many stages in one launch, across SMs -- so it is read
+// coherently at L2 (ld.global.cg), never through the non-coherent path.
+// (Measured: L2 evict_last / .nc hints on the state gathers changed nothing.)
 __device__ __forceinline__ uint64_t pol_first() {
     uint64_t p;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ uint64_t pol_last() {
-    uint64_t p;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-#if PLV_CACHE_HINTS
 __device__ __forceinline__ int32_t ld_row(const int32_t *p) {
     int32_t v;
     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
@@ -142,22 +133,9 @@ __device__ __forceinline__ double ld_row(const double *p) {
         : "=d"(v) : "l"(p), "l"(pol_first()));
     return v;
 }
-__device__ __forceinline__ int32_t ld_gather(const int32_t *p) {
-    int32_t v;
-    asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol_last()));
-    return v;
-}
-__device__ __forceinline__ double ld_gather(const double *p) {
-    double v;
-    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol_last()));
-    return v;
-}
-#else
-__device__ __forceinline__ int32_t ld_row(const int32_t *p) { return *p; }
-__device__ __forceinline__ double ld_row(const double *p) { return *p; }
-__device__ __forceinline__ int32_t ld_gather(const int32_t *p) { return *p; }
-__device__ __forceinline__ double ld_gather(const double *p) { return *p; }
-#endif
+__device__ __forceinline__ int32_t ld_state(const int32_t *p) { return __ldcg(p); }
+__device__ __forceinline__ double ld_state(const double *p) { return __ldcg(p); }
+__device__ __forceinline__ uint8_t ld_state(const uint8_t *p) { return __ldcg(p); }
 
 void count_launch();
 template <typename... KArgs, typename... Args>

@@ -275,7 +275,7 @@ __device__ __forceinline__ void decide_t1_body(const DecideArgs &A, const TierRe
         const int64_t x = L.x[q];
         const int32_t i = L.vid[q];
         const int64_t e0 = L.row[q], e1 = L.end[q];
-        const int32_t c_old = ld_gather(A.assign + (i));
+        const int32_t c_old = ld_state(A.assign + (i));
         int deg = (int)(e1 - e0);
         uint32_t ts = 32;
         while (ts < (uint32_t)(deg + deg / 2 + 2)) ts <<= 1;
@@ -298,7 +298,7 @@ __device__ __forceinline__ void decide_t1_body(const DecideArgs &A, const TierRe
             wv[u] = e < e1 ? ld_row(A.wts + (e)) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < NCH; u++) cv[u] = jv[u] != i ? ld_gather(A.assign + jv[u]) : -1;
+        for (int u = 0; u < NCH; u++) cv[u] = jv[u] != i ? ld_state(A.assign + jv[u]) : -1;
 #pragma unroll
         for (int u = 0; u < NCH; u++) {
             if (e0 + 32 * u >= e1) break;
@@ -314,7 +314,7 @@ __device__ __forceinline__ void decide_t1_body(const DecideArgs &A, const TierRe
         }
         e_old = __shfl_sync(FULL, e_old, 0);
         double ki = A.k[i];
-        double a_old_excl = dsub(ld_gather(A.a_tot + (c_old)), ki);
+        double a_old_excl = dsub(ld_state(A.a_tot + (c_old)), ki);
         Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
         int nc = 0;
         for (uint32_t s = lane; s < ts; s += 32) {
@@ -322,7 +322,7 @@ __device__ __forceinline__ void decide_t1_body(const DecideArgs &A, const TierRe
             if (c < 0) continue;
             nc++;
             if (c == c_old) continue;
-            consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, ld_gather(A.a_tot + (c)), A.four_m_sq),
+            consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, ld_state(A.a_tot + (c)), A.four_m_sq),
                      LBL(A.labels, c), c, vals[s], 0);
         }
         warp_best(b);
@@ -451,7 +451,7 @@ __device__ Best certify_table(const DecideArgs &A, int32_t c_old, double ki, int
     __syncthreads();
     const double f_old = S.f_old;
     const int32_t l_old_n = S.l_old;
-    const double a_old_excl = dsub(ld_gather(A.a_tot + (c_old)), ki);
+    const double a_old_excl = dsub(ld_state(A.a_tot + (c_old)), ki);
     const double inv_m = 1.0 / A.m;
     const int64_t l_old = LBL(A.labels, c_old);
     Best b{0.0, l_old, c_old, 0.0, 0};
@@ -471,7 +471,7 @@ __device__ Best certify_table(const DecideArgs &A, int32_t c_old, double ki, int
             L[u] = ok ? cnt[sl[u]] : 0;
         }
 #pragma unroll
-        for (int u = 0; u < CU; u++) at[u] = c[u] >= 0 && c[u] != c_old ? ld_gather(A.a_tot + c[u]) : 0.0;
+        for (int u = 0; u < CU; u++) at[u] = c[u] >= 0 && c[u] != c_old ? ld_state(A.a_tot + c[u]) : 0.0;
 #pragma unroll
         for (int u = 0; u < CU; u++) {
             if (c[u] < 0 || c[u] == c_old) continue;
@@ -554,7 +554,7 @@ __device__ void exact_folds(const DecideArgs &A, int32_t i, CertSmem<NT> &S) {
 #pragma unroll
         for (int u = 0; u < FU; u++) j[u] = eb + u < e1 ? ld_row(A.nbr + (eb + u)) : i;
 #pragma unroll
-        for (int u = 0; u < FU; u++) c[u] = j[u] != i ? ld_gather(A.assign + j[u]) : -1;
+        for (int u = 0; u < FU; u++) c[u] = j[u] != i ? ld_state(A.assign + j[u]) : -1;
         int cntm = 0;
 #pragma unroll
         for (int u = 0; u < FU; u++) {
@@ -609,7 +609,7 @@ __device__ bool resolve(const DecideArgs &A, int64_t x, int32_t i, int32_t c_old
         // certain: b is the exact best; the exact gain is > 0 iff b.g > 0
         // (an inexact best has lower > 0 when "stay" does not overlap it)
         bool moved = b.c != c_old && b.g > 0.0;
-        if (moved && A.sizes[c_old] == 1 && A.sizes[b.c] == 1 &&
+        if (moved && ld_state(A.sizes + c_old) == 1 && ld_state(A.sizes + b.c) == 1 &&
             LBL(A.labels, b.c) > LBL(A.labels, c_old))
             moved = false;
         // a mover whose two sums have <= 2 terms already holds the exact e values
@@ -634,11 +634,11 @@ __device__ bool resolve(const DecideArgs &A, int64_t x, int32_t i, int32_t c_old
     __syncthreads();
     exact_folds<NT, FU>(A, i, S);
     if (tid == 0) {
-        double a_old_excl = dsub(ld_gather(A.a_tot + (c_old)), ki);
+        double a_old_excl = dsub(ld_state(A.a_tot + (c_old)), ki);
         Best e{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
         for (int t = 1; t < S.nn; t++) {
             int32_t c = S.N[t];
-            consider(e, gain_of(S.acc[t], S.acc[0], A.m, ki, a_old_excl, ld_gather(A.a_tot + (c)), A.four_m_sq),
+            consider(e, gain_of(S.acc[t], S.acc[0], A.m, ki, a_old_excl, ld_state(A.a_tot + (c)), A.four_m_sq),
                      LBL(A.labels, c), c, S.acc[t], 0);
         }
         finish_vertex(A, x, c_old, S.acc[0], e.g, e.c, e.e);
@@ -671,7 +671,7 @@ __device__ void table_exact(const DecideArgs &A, int64_t x, int32_t i, int32_t c
         if (e < e1) {
             int32_t j = ld_row(A.nbr + (e));
             if (j != i) {
-                c = ld_gather(A.assign + (j));
+                c = ld_state(A.assign + (j));
                 w = ld_row(A.wts + (e));
             }
         }
@@ -695,12 +695,12 @@ __device__ void table_exact(const DecideArgs &A, int64_t x, int32_t i, int32_t c
         S.f_old = s >= 0 ? vals[s] : 0.0;
     }
     __syncthreads();
-    const double e_old = S.f_old, a_old_excl = dsub(ld_gather(A.a_tot + (c_old)), ki);
+    const double e_old = S.f_old, a_old_excl = dsub(ld_state(A.a_tot + (c_old)), ki);
     Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
     for (uint32_t s = tid; s < T.size(); s += NT) {
         int32_t c = keys[s];
         if (c >= 0 && c != c_old)
-            consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, ld_gather(A.a_tot + (c)), A.four_m_sq),
+            consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, ld_state(A.a_tot + (c)), A.four_m_sq),
                      LBL(A.labels, c), c, vals[s], 0);
     }
     b = block_best<NT>(S.bs, b);
@@ -722,7 +722,7 @@ __device__ __forceinline__ void block_decide(const DecideArgs &A, int64_t x, int
                                              int32_t *cntt, CL *clist, int *ncl, CertSmem<NT> &S,
                                              unsigned long long &my_cand, Trace *trp = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31;
-    const int32_t c_old = ld_gather(A.assign + (i));
+    const int32_t c_old = ld_state(A.assign + (i));
     const double ki = A.k[i];
     if (tid == 0) *ncl = 0;
     __syncthreads();
@@ -739,7 +739,7 @@ __device__ __forceinline__ void block_decide(const DecideArgs &A, int64_t x, int
         for (int u = 0; u < U; u++) {
             int64_t e = b0 + u * NT + tid;
             bool ok = j[u] != i;  // out-of-range entries carry j = i
-            c[u] = ok ? ld_gather(A.assign + j[u]) : -1;
+            c[u] = ok ? ld_state(A.assign + j[u]) : -1;
             w[u] = ok ? ld_row(A.wts + (e)) : 0.0;
         }
         if (trp && b0 == e0) {
@@ -888,9 +888,9 @@ __global__ void k_hub_accum(DecideArgs A, const int64_t *eoff, const int64_t *to
             waited = true;
         }
         if (t < E) {
-            c_old = ld_gather(A.assign + (i));
+            c_old = ld_state(A.assign + (i));
             if (j != i) {
-                c = ld_gather(A.assign + (j));
+                c = ld_state(A.assign + (j));
                 w = wv;
             }
         }
@@ -960,7 +960,7 @@ __device__ void hub_decide_one(const DecideArgs &A, const int32_t *list, const i
     const int tid = threadIdx.x;
     const int64_t x = list[q];
     const int32_t i = H.vid[q];
-    const int32_t c_old = ld_gather(A.assign + (i));
+    const int32_t c_old = ld_state(A.assign + (i));
     const double ki = A.k[i];
     const int64_t base = toff[q];
     // warp 0: the hub's best from the partials and the overlap test on the
@@ -1040,7 +1040,7 @@ __device__ void hub_decide_one(const DecideArgs &A, const int32_t *list, const i
         done = true;
     } else if (nS == 0 && !flag) {
         bool moved = b.c != c_old && b.g > 0.0;  // certain: the exact best
-        if (moved && A.sizes[c_old] == 1 && A.sizes[b.c] == 1 &&
+        if (moved && ld_state(A.sizes + c_old) == 1 && ld_state(A.sizes + b.c) == 1 &&
             LBL(A.labels, b.c) > LBL(A.labels, c_old))
             moved = false;
         if (!moved || (b.n <= 2 && l_old <= 2)) {  // exact sums: no refold
@@ -1068,12 +1068,12 @@ __device__ void hub_decide_one(const DecideArgs &A, const int32_t *list, const i
         __syncthreads();
         exact_folds<NT, HFU>(A, i, S);
         if (tid == 0) {
-            double a_old_excl = dsub(ld_gather(A.a_tot + (c_old)), ki);
+            double a_old_excl = dsub(ld_state(A.a_tot + (c_old)), ki);
             Best e{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
             for (int t = 1; t < S.nn; t++) {
                 int32_t c = S.N[t];
                 consider(e,
-                         gain_of(S.acc[t], S.acc[0], A.m, ki, a_old_excl, ld_gather(A.a_tot + (c)),
+                         gain_of(S.acc[t], S.acc[0], A.m, ki, a_old_excl, ld_state(A.a_tot + (c)),
                                  A.four_m_sq),
                          LBL(A.labels, c), c, S.acc[t], 0);
             }
@@ -1115,14 +1115,14 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *l
     const int64_t pk = H.blk[blockIdx.x];
     const int64_t q = pk >> 32, y = pk & 0xffffffffll;
     const int32_t i = H.vid[q];
-    const int32_t c_old = ld_gather(A.assign + (i));
+    const int32_t c_old = ld_state(A.assign + (i));
     const int64_t base = toff[q];
     const int64_t cap = toff[q + 1] - base;
     const int64_t dq = q * H.dn, deg = eoff[q + 1] - eoff[q];
     const int32_t so = DENSE ? 0 : H.sold[q];
     const double f_old = DENSE ? H.dval[dq + c_old] : so >= 0 ? hvals[base + so] : 0.0;
     const int32_t l_old = DENSE ? H.dcnt[dq + c_old] : so >= 0 ? hcnt[base + so] : 0;
-    const double ki = A.k[i], a_old_excl = dsub(ld_gather(A.a_tot + (c_old)), ki);
+    const double ki = A.k[i], a_old_excl = dsub(ld_state(A.a_tot + (c_old)), ki);
     const double inv_m = 1.0 / A.m;
     TR_MARK
     int32_t c[PU];
@@ -1297,7 +1297,7 @@ __global__ void __launch_bounds__(HC_NT, 1) k_hub_cluster(DecideArgs A, HubClArg
     const int64_t c0 = e0 + (int64_t)r * chunk;
     const int64_t c1 = c0 + chunk < e0 + deg ? c0 + chunk : e0 + deg;
     pdl_wait();
-    const int32_t c_old = ld_gather(A.assign + i);
+    const int32_t c_old = ld_state(A.assign + i);
     const double ki = A.k[i];
     cl.sync();  // every slice initialised before any remote insert
     for (int64_t b0 = c0; b0 < c1; b0 += HC_NT) {
@@ -1307,7 +1307,7 @@ __global__ void __launch_bounds__(HC_NT, 1) k_hub_cluster(DecideArgs A, HubClArg
         if (e < c1) {
             const int32_t j = ld_row(A.nbr + e);
             if (j != i) {
-                c = ld_gather(A.assign + j);
+                c = ld_state(A.assign + j);
                 w = ld_row(A.wts + e);
             }
         }
@@ -1354,7 +1354,7 @@ __global__ void __launch_bounds__(HC_NT, 1) k_hub_cluster(DecideArgs A, HubClArg
     cl.sync();  // every remote read done: the slices may be overwritten
     const double f_old = S.f_old;
     const int32_t l_old_n = S.l_old;
-    const double a_old_excl = dsub(ld_gather(A.a_tot + c_old), ki);
+    const double a_old_excl = dsub(ld_state(A.a_tot + c_old), ki);
     const double inv_m = 1.0 / A.m;
     // pass 1 (certify_table): gains and slack of this slice, its best
     Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
@@ -1370,7 +1370,7 @@ __global__ void __launch_bounds__(HC_NT, 1) k_hub_cluster(DecideArgs A, HubClArg
             L[u] = c[u] >= 0 ? cnt[sl] : 0;
         }
 #pragma unroll
-        for (int u = 0; u < 4; u++) at[u] = c[u] >= 0 && c[u] != c_old ? ld_gather(A.a_tot + c[u]) : 0.0;
+        for (int u = 0; u < 4; u++) at[u] = c[u] >= 0 && c[u] != c_old ? ld_state(A.a_tot + c[u]) : 0.0;
 #pragma unroll
         for (int u = 0; u < 4; u++) {
             if (c[u] < 0) continue;
@@ -1438,6 +1438,430 @@ __global__ void __launch_bounds__(HC_NT, 1) k_hub_cluster(DecideArgs A, HubClArg
 }
 
 
+// ------------------------------------------------ tail runs (k_tail)
+//
+// The late colour classes of a heavy-tailed graph hold a few hub-tier
+// vertices each (C4: ~250 classes of 3-16 vertices of degree 15k-70k; C2:
+// ~100 of <= 32).  Per class the multi-kernel path pays accumulate -> pass ->
+// apply launches and a per-hub ticket, ~15-20 us of dependent latency for
+// ~1-2 us of work.  k_tail decides AND applies a whole run of such classes
+// in ONE launch: a single thread-block cluster (16 CTAs when the device
+// allows non-portable clusters, else 8) walks the run's classes in order,
+// separated by hardware cluster barriers (release / acquire at cluster scope:
+// each class reads the state the previous class wrote; state loads are
+// coherent L2 loads, ld_state).  Per class:
+//   1. accumulate: every hub entry of the class, spread over the cluster, into
+//      the dense per-hub arrays (any-order sums, term counts, first position);
+//   2. pass A: 32-position chunks of one hub per warp; the first position of
+//      each community owns it: gain, slack, warp best -> per-hub best (CTA,
+//      then the hub's decider CTA over DSMEM); arrays reset behind it;
+//   3. decide (decider CTA of each hub): integral graphs finish at once; else
+//      pass B lists the candidates overlapping the hub's best (as
+//      certify_table) and resolve() / table_exact decide on exact values --
+//      the rules and bits of k_hub_accum + k_hub_pass;
+//   4. apply: one warp, apply_tiny_warp (the reference's ordered apply).
+constexpr int TL_NT = 512;
+constexpr int TL_MAXH = 32;  // vertices per tail class (one tiny-apply warp)
+constexpr int TL_U = 4;      // entries per thread in flight (accumulate)
+constexpr int TL_DPC = 4;    // decided hubs per CTA (TL_MAXH / 8)
+#ifndef TL_MAXE
+#define TL_MAXE 8192         // hub entries per tail class: more need the whole GPU
+#endif
+
+struct TailStage {
+    int64_t goff;      // class offset in the stage lists and decide outputs
+    int64_t hub_base;  // first hub_eoff / hub_toff / hub_row / hub_vid entry
+    int64_t tstart;    // first tier-list entry of the hub tier
+    int64_t nh;        // its vertices (= the class's active vertices), 0: skip
+};
+
+struct TailArgs {
+    DecideArgs A;  // outputs at class offset 0
+    StageArgs S;   // subset / outputs at class offset 0
+    const TailStage *st;
+    int64_t a0, a1;
+    const int32_t *tier_list, *hub_vid;
+    const int64_t *hub_row, *hub_eoff, *hub_toff;
+    double *dval;
+    int32_t *dcnt, *dmk, *cbuf;
+    int64_t dn;
+    int32_t *hkeys;
+    double *hvals;
+    double *gbuf;
+    float *sbuf;
+};
+
+__device__ __forceinline__ int tl_hub_of(const int64_t *eo, int nh, int64_t t) {
+    int lo = 0, hi = nh;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (eo[mid] <= t)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+template <int CL>
+__global__ void __launch_bounds__(TL_NT, 1) k_tail(TailArgs T) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ int64_t s_eoff[TL_MAXH + 1], s_poff[TL_MAXH + 1], s_row[TL_MAXH], s_x[TL_MAXH];
+    __shared__ int32_t s_vid[TL_MAXH], s_cold[TL_MAXH], s_lold[TL_MAXH];
+    __shared__ double s_ki[TL_MAXH], s_fold[TL_MAXH], s_aoe[TL_MAXH], s_lower[TL_MAXH],
+        s_slb[TL_MAXH];
+    __shared__ Best s_hb[TL_MAXH];   // this CTA's best per hub
+    __shared__ Best s_bw[TL_MAXH];   // the hub's best over the cluster
+    __shared__ int s_lock[TL_MAXH];
+    __shared__ Best s_cb[TL_DPC][CL];  // decider: the CTAs' bests of its hubs
+    __shared__ int32_t s_near[TL_DPC][MAXS];
+    __shared__ int s_nn[TL_DPC], s_nf[TL_DPC];
+    __shared__ CertSmem<TL_NT> S;
+    __shared__ int32_t cidx[TL_NT * HFU];
+    __shared__ double cw[TL_NT * HFU];
+    __shared__ unsigned long long ap_k[64];
+    __shared__ double ap_w[64], ap_a[64];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int r = (int)cl.block_rank();
+    const int64_t gt = (int64_t)r * TL_NT + tid, G = (int64_t)CL * TL_NT;
+    const int64_t gw = gt >> 5, GW = G >> 5;
+    const bool integral = T.A.integral != 0;
+    const double inv_m = 1.0 / T.A.m;
+    if (tid == 0) {
+        S.cidx = cidx;
+        S.cw = cw;
+    }
+    pdl_wait();  // the state of the previous stage
+    for (int64_t a = T.a0; a < T.a1; a++) {
+        const TailStage d = T.st[a];
+        const int nh = (int)d.nh;
+        if (nh == 0) continue;
+        DecideArgs A = T.A;
+        A.out_target += d.goff;
+        A.out_moved += d.goff;
+        A.out_e_old += d.goff;
+        A.out_e_best += d.goff;
+        if (tid < nh) {
+            const int q = tid;
+            const int32_t i = T.hub_vid[d.hub_base + q];
+            s_vid[q] = i;
+            s_row[q] = T.hub_row[d.hub_base + q];
+            s_x[q] = T.tier_list[d.tstart + q];
+            s_eoff[q] = T.hub_eoff[d.hub_base + q];
+            const int32_t c_old = ld_state(A.assign + i);
+            s_cold[q] = c_old;
+            s_ki[q] = A.k[i];
+            s_hb[q] = Best{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
+            s_lock[q] = 0;
+        }
+        if (tid < TL_DPC) {
+            s_nn[tid] = 0;
+            s_nf[tid] = 0;
+        }
+        if (tid == 0) {
+            s_eoff[nh] = T.hub_eoff[d.hub_base + nh];
+            s_poff[0] = 0;
+        }
+        __syncthreads();
+        if (tid == 0)  // 32-aligned chunk positions: a chunk belongs to one hub
+            for (int q = 0; q < nh; q++)
+                s_poff[q + 1] = s_poff[q] + ((s_eoff[q + 1] - s_eoff[q] + 31) & ~(int64_t)31);
+        const int64_t E = s_eoff[nh];
+        // ---- 1. accumulate
+        for (int64_t t0 = gt; t0 < E; t0 += G * TL_U) {
+            int qv[TL_U];
+            int32_t jv[TL_U], cv[TL_U];
+            double wv[TL_U];
+#pragma unroll
+            for (int u = 0; u < TL_U; u++) {
+                const int64_t t = t0 + u * G;
+                qv[u] = t < E ? tl_hub_of(s_eoff, nh, t) : 0;
+                const int64_t e = s_row[qv[u]] + (t - s_eoff[qv[u]]);
+                jv[u] = t < E ? ld_row(A.nbr + e) : -1;
+                wv[u] = t < E ? ld_row(A.wts + e) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < TL_U; u++)
+                cv[u] = jv[u] >= 0 && jv[u] != s_vid[qv[u]] ? ld_state(A.assign + jv[u]) : -1;
+#pragma unroll
+            for (int u = 0; u < TL_U; u++) {
+                const int64_t t = t0 + u * G;
+                if (t >= E) continue;
+                T.cbuf[t] = cv[u];
+                if (cv[u] < 0) continue;
+                const int64_t dq = (int64_t)qv[u] * T.dn + cv[u];
+                atomicAdd(T.dval + dq, wv[u]);
+                atomicAdd(T.dcnt + dq, 1);
+                atomicMin(T.dmk + dq, (int32_t)(t - s_eoff[qv[u]]));
+            }
+        }
+        cl.sync();
+        if (tid < nh) {
+            const int q = tid;
+            const int64_t dq = (int64_t)q * T.dn + s_cold[q];
+            s_fold[q] = ld_state(T.dval + dq);
+            s_lold[q] = ld_state(T.dcnt + dq);
+            s_aoe[q] = dsub(ld_state(A.a_tot + s_cold[q]), s_ki[q]);
+        }
+        __syncthreads();
+        // ---- 2. pass A: one hub per 32-position chunk
+        const int64_t PP = s_poff[nh];
+        unsigned long long nc = 0;
+        for (int64_t k = gw; k * 32 < PP; k += GW) {
+            const int64_t p = k * 32;
+            const int q = tl_hub_of(s_poff, nh, p);
+            const int64_t pos = p - s_poff[q] + lane;  // row position
+            const int64_t t = s_eoff[q] + pos;
+            const bool ok = t < s_eoff[q + 1];
+            const int32_t c_old = s_cold[q];
+            const int32_t c = ok ? ld_state(T.cbuf + t) : -1;
+            const int64_t dq = (int64_t)q * T.dn + (c >= 0 ? c : 0);
+            const bool own = c >= 0 && ld_state(T.dmk + dq) == (int32_t)pos;
+            nc += own;
+            const bool cand = own && c != c_old;
+            const double F = cand ? ld_state(T.dval + dq) : 0.0;
+            const int32_t L = cand ? ld_state(T.dcnt + dq) : 0;
+            const double at = cand ? ld_state(A.a_tot + c) : 0.0;
+            Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
+            if (cand) {
+                const double g = gain_of(F, s_fold[q], A.m, s_ki[q], s_aoe[q], at, A.four_m_sq);
+                consider(b, g, LBL(A.labels, c), c, F, L);
+                if (!integral) {
+                    T.gbuf[t] = g;
+                    T.sbuf[t] = __double2float_ru(gain_slack_r(F, L, s_fold[q], s_lold[q], inv_m, g));
+                }
+                T.dval[dq] = 0.0;  // back to idle (c_old's slot: by the decider)
+                T.dcnt[dq] = 0;
+                T.dmk[dq] = INT_MAX;
+            } else if (!integral && ok) {
+                T.gbuf[t] = -INFINITY;
+            }
+            warp_best(b);
+            if (lane == 0) {
+                while (atomicCAS(&s_lock[q], 0, 1) != 0) {
+                }
+                __threadfence_block();
+                Best h = s_hb[q];
+                consider(h, b.g, b.l, b.c, b.e, b.n);
+                s_hb[q] = h;
+                __threadfence_block();
+                atomicExch(&s_lock[q], 0);
+            }
+        }
+        if (A.cand) {
+            for (int o = 16; o > 0; o >>= 1) nc += __shfl_xor_sync(FULL, nc, o);
+            if (lane == 0 && nc) atomicAdd(A.cand, nc);
+        }
+        __syncthreads();
+        if (tid < nh) cl.map_shared_rank(&s_cb[0][0], tid % CL)[(tid / CL) * CL + r] = s_hb[tid];
+        cl.sync();
+        // ---- 3. decide: CTA r decides hubs r, r + CL, ...
+        if (tid < TL_DPC) {
+            const int q = r + tid * CL;
+            if (q < nh) {
+                Best bw = s_cb[tid][0];
+                for (int t = 1; t < CL; t++)
+                    consider(bw, s_cb[tid][t].g, s_cb[tid][t].l, s_cb[tid][t].c, s_cb[tid][t].e,
+                             s_cb[tid][t].n);
+                if (integral) {
+                    finish_vertex(A, s_x[q], s_cold[q], s_fold[q], bw.g, bw.c, bw.e);
+                } else {
+                    for (int rr = 0; rr < CL; rr++) cl.map_shared_rank(s_bw, rr)[q] = bw;
+                }
+                if (integral) {  // c_old's slot back to idle
+                    const int64_t dq = (int64_t)q * T.dn + s_cold[q];
+                    T.dval[dq] = 0.0;
+                    T.dcnt[dq] = 0;
+                    T.dmk[dq] = INT_MAX;
+                }
+            }
+        }
+        if (!integral) {
+            cl.sync();  // every hub's best in every CTA
+            if (tid < nh) {
+                const int q = tid;
+                const Best bw = s_bw[q];
+                const bool stay = bw.c == s_cold[q];
+                const double slb =
+                    stay ? 0.0 : gain_slack_r(bw.e, bw.n, s_fold[q], s_lold[q], inv_m, bw.g);
+                s_slb[q] = slb;
+                s_lower[q] = stay ? 0.0 : bw.g - slb;
+            }
+            __syncthreads();
+            // pass B: candidates overlapping the best, listed at the decider
+            for (int64_t k = gw; k * 32 < PP; k += GW) {
+                const int64_t p = k * 32;
+                const int q = tl_hub_of(s_poff, nh, p);
+                const int64_t t = s_eoff[q] + (p - s_poff[q]) + lane;
+                if (t >= s_eoff[q + 1]) continue;
+                const double g = ld_state(T.gbuf + t);
+                if (g == -INFINITY) continue;
+                const int32_t c = ld_state(T.cbuf + t);
+                if (c == s_bw[q].c) continue;
+                const double slv = (double)__ldcg(T.sbuf + t);
+                if ((slv > 0.0 || s_slb[q] > 0.0) && g + slv >= s_lower[q]) {
+                    const int dr = q % CL, dk = q / CL;
+                    const int kk = atomicAdd(cl.map_shared_rank(&s_nn[dk], dr), 1);
+                    if (kk < MAXS)
+                        cl.map_shared_rank(&s_near[dk][0], dr)[kk] = c;
+                    else
+                        atomicOr(cl.map_shared_rank(&s_nf[dk], dr), 2);
+                }
+            }
+            cl.sync();
+            for (int dk = 0; dk < TL_DPC; dk++) {  // block-uniform
+                const int q = r + dk * CL;
+                if (q >= nh) break;
+                const Best bw = s_bw[q];
+                if (tid == 0) {
+                    S.f_old = s_fold[q];
+                    S.l_old = s_lold[q];
+                    const int nn = s_nn[dk];
+                    S.nS = nn;
+                    int fl = s_nf[dk] | (nn > MAXS ? 2 : 0);
+                    if (bw.c != s_cold[q] && s_slb[q] > 0.0 && s_lower[q] <= 0.0) fl |= 1;
+                    S.flag = fl;
+                    for (int t = 0; t < nn && t < MAXS; t++) S.N[2 + t] = s_near[dk][t];
+                }
+                __syncthreads();
+                if (!resolve<TL_NT, HFU>(A, s_x[q], s_vid[q], s_cold[q], s_ki[q], bw, S)) {
+                    const int64_t base = T.hub_toff[d.hub_base + q];
+                    table_exact<TL_NT>(A, s_x[q], s_vid[q], s_cold[q], s_ki[q], T.hkeys + base,
+                                       T.hvals + base,
+                                       PowTab{(uint32_t)(T.hub_toff[d.hub_base + q + 1] - base - 1)},
+                                       S);
+                }
+                if (tid == 0) {
+                    const int64_t dq = (int64_t)q * T.dn + s_cold[q];
+                    T.dval[dq] = 0.0;
+                    T.dcnt[dq] = 0;
+                    T.dmk[dq] = INT_MAX;
+                }
+                __syncthreads();
+            }
+        }
+        cl.sync();  // the class's decisions
+        // ---- 4. apply (rank 0, warp 0)
+        if (r == 0 && tid < 32) {
+            StageArgs SA = T.S;
+            SA.subset += d.goff;
+            SA.ns = nh;
+            SA.target += d.goff;
+            SA.moved += d.goff;
+            SA.e_old += d.goff;
+            SA.e_best += d.goff;
+            apply_tiny_warp<1>(SA, ap_k, ap_w, ap_a);
+        }
+        cl.sync();  // the class's moves, before the next class reads the state
+    }
+}
+
+static bool tail_cluster_ok(int cl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cl);
+    cfg.blockDim = dim3(TL_NT);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclu = 0;
+    cudaError_t e = cl == 16 ? cudaOccupancyMaxActiveClusters(&nclu, k_tail<16>, &cfg)
+                             : cudaOccupancyMaxActiveClusters(&nclu, k_tail<8>, &cfg);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return nclu > 0;
+}
+
+void tail_plan(Plan &P, bool enable, bool integral, cudaStream_t s) {
+    P.tail_first.clear();
+    P.tail_last.clear();
+    const int64_t nst = (int64_t)P.st.size();
+    if (!enable || !PLV_TAIL || nst == 0) return;
+    std::vector<TailStage> ts(nst);
+    std::vector<bool> ok(nst, false);
+    int64_t max_e = 0;
+    for (int64_t a = 0; a < nst; a++) {
+        const StagePlan &sp = P.st[a];
+        ts[a] = TailStage{sp.off, sp.hub_base, sp.tstart[4], sp.tcount[4]};
+        if (sp.ns == 0) {
+            ok[a] = true;  // nothing to do; may sit inside a run
+            ts[a].nh = 0;
+            continue;
+        }
+        ok[a] = !sp.tcount[0] && !sp.tcount[1] && !sp.tcount[2] && !sp.tcount[3] &&
+                sp.tcount[4] == sp.ns && sp.ns <= TL_MAXH && sp.hub_dense && !sp.hub_cluster &&
+                sp.hub_entries <= TL_MAXE;
+        if (ok[a]) max_e = sp.hub_entries > max_e ? sp.hub_entries : max_e;
+    }
+    for (int64_t a = 0; a < nst;) {
+        if (!ok[a] || P.st[a].ns == 0) {
+            a++;
+            continue;
+        }
+        int64_t b = a;
+        while (b < nst && ok[b]) b++;
+        P.tail_first.push_back(a);
+        P.tail_last.push_back(b);
+        a = b;
+    }
+    if (P.tail_first.empty()) return;
+    if (!P.tail_cl) {
+        static int attr_dev = -1;
+        int dev = 0;
+        PLV_CUDA(cudaGetDevice(&dev));
+        if (attr_dev != dev) {
+            cudaFuncSetAttribute(k_tail<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            cudaGetLastError();
+            attr_dev = dev;
+        }
+        P.tail_cl = tail_cluster_ok(16) ? 16 : tail_cluster_ok(8) ? 8 : 0;
+    }
+    if (!P.tail_cl) {
+        P.tail_first.clear();
+        P.tail_last.clear();
+        return;
+    }
+    P.tail_st = dalloc<TailStage>(nst);
+    PLV_CUDA(cudaMemcpyAsync(P.tail_st, ts.data(), sizeof(TailStage) * nst,
+                             cudaMemcpyHostToDevice, s));
+    if (!integral) {
+        P.tail_g = dalloc<double>(max_e);
+        P.tail_s = dalloc<float>(max_e);
+    }
+    PLV_CUDA(cudaStreamSynchronize(s));
+}
+
+void launch_tail(const Plan &P, int64_t k, DecideArgs A, StageArgs S, cudaStream_t st) {
+    TailArgs T{A, S, (const TailStage *)P.tail_st, P.tail_first[k], P.tail_last[k],
+               P.tier_list, P.hub_vid, P.hub_row, P.hub_eoff, P.hub_toff, P.dval, P.dcnt,
+               P.dmk, P.cbuf, P.dn, P.hkeys, P.hvals, P.tail_g, P.tail_s};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P.tail_cl);
+    cfg.blockDim = dim3(TL_NT);
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = P.tail_cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    if (P.tail_cl == 16)
+        PLV_CUDA(cudaLaunchKernelEx(&cfg, k_tail<16>, T));
+    else
+        PLV_CUDA(cudaLaunchKernelEx(&cfg, k_tail<8>, T));
+    count_launch();
+}
+
+
 // ================================================================ planning
 
 __global__ void k_tier_keys(const int64_t *off, const int32_t *vtx, const int64_t *stage_off,
@@ -1500,7 +1924,7 @@ void Plan::release() {
     cudaDeviceSynchronize();  // buffers go back to the pool idle
     void *ps[] = {tier_list, tier_vid, tier_row, tier_end, hub_eoff, hub_toff, hub_poff, hub_blk, hub_row, hub_vid, hkeys,
                   hvals,     hcnt,     hsold,    hncnt,    hnear,   hpart,
-                  dval,      dcnt,     dmk,      cbuf};
+                  dval,      dcnt,     dmk,      cbuf,     tail_st, tail_g,  tail_s};
     for (void *p : ps)
         pool_free(p);
     tier_list = nullptr;
@@ -1514,6 +1938,11 @@ void Plan::release() {
     hpart = nullptr;
     dval = nullptr;
     dcnt = dmk = cbuf = nullptr;
+    tail_st = nullptr;
+    tail_g = nullptr;
+    tail_s = nullptr;
+    tail_first.clear();
+    tail_last.clear();
 }
 
 void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *stage_off_h,

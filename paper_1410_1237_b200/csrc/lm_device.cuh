@@ -34,7 +34,7 @@ __device__ __forceinline__ double gain_of(double e_c, double e_old, double m, do
 __device__ __forceinline__ void finish_vertex(const DecideArgs &A, int64_t x, int32_t c_old,
                                               double e_old, double bg, int32_t bc, double be) {
     bool moved = bg > 0.0 && bc != c_old;
-    if (moved && A.sizes[c_old] == 1 && A.sizes[bc] == 1 &&
+    if (moved && ld_state(A.sizes + c_old) == 1 && ld_state(A.sizes + bc) == 1 &&
         LBL(A.labels, bc) > LBL(A.labels, c_old))
         moved = false;  // singleton-pair guard
     A.out_target[x] = moved ? bc : c_old;
@@ -74,7 +74,7 @@ __device__ __forceinline__ void decide_t0_body(const DecideArgs &A, const TierRe
         const int32_t i = L.vid[q];
         const int64_t e0 = L.row[q];
         const int deg = (int)(L.end[q] - e0);
-        const int32_t c_old = ld_gather(A.assign + (i));
+        const int32_t c_old = ld_state(A.assign + (i));
         // all row loads, then all community loads, in flight together
         int32_t jj[T0_MAXD], cc[T0_MAXD];
         double ww[T0_MAXD];
@@ -84,7 +84,7 @@ __device__ __forceinline__ void decide_t0_body(const DecideArgs &A, const TierRe
             ww[t] = t < deg ? ld_row(A.wts + (e0 + t)) : 0.0;
         }
 #pragma unroll
-        for (int t = 0; t < T0_MAXD; t++) cc[t] = jj[t] != i ? ld_gather(A.assign + jj[t]) : -1;
+        for (int t = 0; t < T0_MAXD; t++) cc[t] = jj[t] != i ? ld_state(A.assign + jj[t]) : -1;
 #if T0_INPLACE
         // in place: a "head" is the first entry of its community; its weight
         // becomes the community's sum folded forward in adjacency order
@@ -112,13 +112,13 @@ __device__ __forceinline__ void decide_t0_body(const DecideArgs &A, const TierRe
         for (int t = 0; t < T0_MAXD; t++)
             if (head[t] && cc[t] == c_old) e_old = ww[t];
         double ki = A.k[i];
-        double a_old_excl = dsub(ld_gather(A.a_tot + (c_old)), ki);
+        double a_old_excl = dsub(ld_state(A.a_tot + (c_old)), ki);
         Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
 #pragma unroll
         for (int t = 0; t < T0_MAXD; t++) {
             if (head[t] && cc[t] != c_old) {
                 int32_t c = cc[t];
-                consider(b, gain_of(ww[t], e_old, A.m, ki, a_old_excl, ld_gather(A.a_tot + c),
+                consider(b, gain_of(ww[t], e_old, A.m, ki, a_old_excl, ld_state(A.a_tot + c),
                                     A.four_m_sq),
                          LBL(A.labels, c), c, ww[t], 0);
             }
@@ -159,13 +159,13 @@ __device__ __forceinline__ void decide_t0_body(const DecideArgs &A, const TierRe
         for (int s = 0; s < T0_MAXD; s++)
             if (s < nc && keys[s] == c_old) e_old = vals[s];
         double ki = A.k[i];
-        double a_old_excl = dsub(ld_gather(A.a_tot + (c_old)), ki);
+        double a_old_excl = dsub(ld_state(A.a_tot + (c_old)), ki);
         Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
 #pragma unroll
         for (int s = 0; s < T0_MAXD; s++) {
             if (s < nc && keys[s] != c_old) {
                 int32_t c = keys[s];
-                consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, ld_gather(A.a_tot + (c)), A.four_m_sq),
+                consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, ld_state(A.a_tot + (c)), A.four_m_sq),
                          LBL(A.labels, c), c, vals[s], 0);
             }
         }
@@ -223,6 +223,87 @@ __device__ __forceinline__ void event_delta(const StageArgs &A, int32_t v, doubl
         dw = -A.ta[x];
         da = -ki;
     }
+}
+
+// One warp applies a tiny independent stage (<= 32 VPL vertices, 64 VPL
+// events): lane l owns vertices l, l + 32, ... and their leave / join events;
+// the (community, event) keys are ordered by a bitonic network in shared
+// memory (sk, sw, sa: 64 VPL entries each), then the first lane of every
+// community run folds its deltas in event order -- the reference's
+// sequential apply (PL/_kernels.pyx:116-144) restated exactly.  State loads
+// are coherent (k_tail runs it between stages of one launch).
+template <int VPL>
+__device__ __forceinline__ void apply_tiny_warp(const StageArgs &A, unsigned long long *sk,
+                                                double *sw, double *sa) {
+    constexpr int NE = 64 * VPL;
+    const int lane = threadIdx.x & 31;
+    const int64_t ns = A.ns;
+    const unsigned long long S = (unsigned long long)SENTINEL << 32;
+    unsigned nmv = 0;
+#pragma unroll
+    for (int v = 0; v < VPL; v++) {
+        const int x = lane + 32 * v;
+        bool mv = false;
+        int32_t a = 0, b = 0;
+        if (x < ns) {
+            const int32_t i = ld_state(A.subset + x);
+            b = ld_state(A.target + x);
+            a = ld_state(A.assign + i);
+            mv = ld_state(A.moved + x) && a != b;
+            if (mv) {
+                const double s2 = dmul(2.0, A.selfw[i]);
+                const double ki = A.k[i];
+                sw[2 * x] = -dadd(dmul(2.0, ld_state(A.e_old + x)), s2);  // leave a
+                sa[2 * x] = -ki;
+                sw[2 * x + 1] = dadd(dmul(2.0, ld_state(A.e_best + x)), s2);  // join b
+                sa[2 * x + 1] = ki;
+                atomicSub(A.sizes + a, 1);
+                atomicAdd(A.sizes + b, 1);
+                nmv++;
+            }
+        }
+        sk[2 * x] = mv ? ((unsigned long long)(uint32_t)a << 32) | (uint64_t)(2 * x) : S | (2 * x);
+        sk[2 * x + 1] =
+            mv ? ((unsigned long long)(uint32_t)b << 32) | (uint64_t)(2 * x + 1) : S | (2 * x + 1);
+    }
+    __syncwarp();
+    // bitonic sort of NE keys, VPL compare-exchanges per lane per step
+    for (int k = 2; k <= NE; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+            for (int v = 0; v < VPL; v++) {
+                const int pr = lane + 32 * v;
+                const int i0 = 2 * j * (pr / j) + (pr % j), i1 = i0 + j;
+                const bool up = (i0 & k) == 0;
+                const unsigned long long x = sk[i0], y = sk[i1];
+                if ((x > y) == up) {
+                    sk[i0] = y;
+                    sk[i1] = x;
+                }
+            }
+            __syncwarp();
+        }
+    for (int p = lane; p < NE; p += 32) {
+        const uint32_t c = (uint32_t)(sk[p] >> 32);
+        if (c == SENTINEL) continue;
+        if (p > 0 && (uint32_t)(sk[p - 1] >> 32) == c) continue;
+        double W = ld_state(A.w_int + c), At = ld_state(A.a_tot + c);
+        for (int q = p; q < NE && (uint32_t)(sk[q] >> 32) == c; q++) {
+            const int e = (int)(sk[q] & 0xffffffffull);
+            W = dadd(W, sw[e]);
+            At = dadd(At, sa[e]);
+        }
+        A.w_int[c] = W;
+        A.a_tot[c] = At;
+    }
+#pragma unroll
+    for (int v = 0; v < VPL; v++) {
+        const int x = lane + 32 * v;
+        if (x < ns && ld_state(A.moved + x)) A.assign[ld_state(A.subset + x)] = ld_state(A.target + x);
+    }
+    for (int o = 16; o > 0; o >>= 1) nmv += __shfl_xor_sync(0xffffffffu, nmv, o);
+    if (lane == 0 && nmv) atomicAdd(A.moves, (unsigned long long)nmv);
+    __syncwarp();
 }
 
 }  // namespace plv
