@@ -112,10 +112,11 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 // Loads of the local-moving kernels.  CSR rows are immutable during a phase
 // and streamed once per sweep: read-only path, no L1 allocation, L2
-// evict-first.  The state (assignment, a_tot, sizes) is mutable -- k_tail
-// decides and applies many stages in one launch, across SMs -- so it is read
-// coherently at L2 (ld.global.cg), never through the non-coherent path.
-// (Measured: L2 evict_last / .nc hints on the state gathers changed nothing.)
+// evict-first.  The state (assignment, a_tot, sizes) is mutable, so it is read
+// coherently at L2 (ld.global.cg), never through the non-coherent path (a
+// kernel that decides and applies several stages between cluster / grid
+// barriers must not see stale lines).  Measured: L2 evict_last / .nc hints on
+// the state gathers changed nothing.
 __device__ __forceinline__ uint64_t pol_first() {
     uint64_t p;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

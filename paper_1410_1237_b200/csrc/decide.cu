@@ -29,7 +29,6 @@
 #include "localmove.cuh"
 #include "lm_device.cuh"
 #include "csr.cuh"
-#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 namespace plv {
@@ -1229,639 +1228,6 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *l
 }
 
 
-// ------------------------------------------- tier 4, cluster mode (few hubs)
-//
-// A stage with few hub-tier vertices, none of degree above HC_MAXD: ONE
-// launch decides them all, a thread-block cluster of HC_CL CTAs per vertex.
-// The vertex's any-order table is spread over the cluster's shared memory
-// (distributed shared memory, DSMEM): the owner CTA of community c is the low
-// hash bits, its slot the next ones.  Every CTA accumulates a 1/HC_CL chunk of
-// the row -- warp groups of equal communities pre-summed, then one remote
-// claim (CAS) + any-order add per group into the owner's slice -- so a row is
-// spread over HC_CL SMs, with no global table, no second kernel and no
-// per-hub ticket.  Then each CTA runs the certification passes of
-// certify_table over its own slice (gains, slack; bests gathered in rank 0),
-// and rank 0 takes the decision: at once for integral graphs, else through
-// resolve() (exact left folds of the overlapping communities in adjacency
-// order) or, past MAXS overlaps, table_exact over the hub's clean global
-// table slice -- the same rules, and bits, as k_hub_accum + k_hub_pass.
-constexpr int HC_CL = 8;        // CTAs per cluster (portable size)
-constexpr int HC_NT = 512;      // threads per CTA
-constexpr int HC_TS = 8192;     // table slots per CTA (16 B each)
-constexpr int HC_MAXD = HC_CL * HC_TS / 2;  // load factor <= 1/2
-constexpr int HC_LOGCL = 3;
-static_assert((1 << HC_LOGCL) == HC_CL, "cluster size");
-
-struct HubClArgs {
-    const int32_t *list;  // [nh] stage-local index of each hub-tier vertex
-    const int32_t *vid;   // [nh]
-    const int64_t *row;   // [nh] first entry of its row
-    const int64_t *eoff;  // [nh + 1] entry offsets (degrees)
-    const int64_t *toff;  // [nh + 1] global table slices (overflow fallback)
-    int32_t *hkeys;
-    double *hvals;
-};
-
-static size_t hc_smem() { return (size_t)HC_TS * (sizeof(double) + 2 * sizeof(int32_t)); }
-
-__global__ void __launch_bounds__(HC_NT, 1) k_hub_cluster(DecideArgs A, HubClArgs H) {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cl = cg::this_cluster();
-    extern __shared__ __align__(16) unsigned char dsm[];
-    __shared__ CertSmem<HC_NT> S;
-    __shared__ int32_t cidx[HC_NT * HFU];
-    __shared__ double cw[HC_NT * HFU];
-    __shared__ Best cb[HC_CL];
-    double *vals = reinterpret_cast<double *>(dsm);
-    int32_t *keys = reinterpret_cast<int32_t *>(dsm + sizeof(double) * HC_TS);
-    int32_t *cnt = keys + HC_TS;
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int r = (int)cl.block_rank();
-    const int64_t q = blockIdx.x / HC_CL;
-    for (int s = tid; s < HC_TS; s += HC_NT) {
-        keys[s] = -1;
-        vals[s] = 0.0;
-        cnt[s] = 0;
-    }
-    if (tid == 0) {
-        S.cidx = cidx;
-        S.cw = cw;
-        S.nS = 0;
-        S.flag = 0;
-    }
-    // static loads first; the state only after the previous stage (PDL)
-    const int32_t i = H.vid[q];
-    const int64_t x = H.list[q];
-    const int64_t e0 = H.row[q], deg = H.eoff[q + 1] - H.eoff[q];
-    const int64_t chunk = (deg + HC_CL - 1) / HC_CL;
-    const int64_t c0 = e0 + (int64_t)r * chunk;
-    const int64_t c1 = c0 + chunk < e0 + deg ? c0 + chunk : e0 + deg;
-    pdl_wait();
-    const int32_t c_old = ld_state(A.assign + i);
-    const double ki = A.k[i];
-    cl.sync();  // every slice initialised before any remote insert
-    for (int64_t b0 = c0; b0 < c1; b0 += HC_NT) {
-        const int64_t e = b0 + tid;
-        int32_t c = -1;
-        double w = 0.0;
-        if (e < c1) {
-            const int32_t j = ld_row(A.nbr + e);
-            if (j != i) {
-                c = ld_state(A.assign + j);
-                w = ld_row(A.wts + e);
-            }
-        }
-        // equal communities of the warp: one insert with the group's sum
-        const unsigned grp = __match_any_sync(FULL, c);
-        const double gs = group_sum(grp, w);
-        if (c >= 0 && lane == __ffs(grp) - 1) {
-            const uint32_t h = hslot(c, 0xffffffffu);
-            const unsigned owner = h & (HC_CL - 1);
-            int32_t *rk = cl.map_shared_rank(keys, owner);
-            double *rv = cl.map_shared_rank(vals, owner);
-            int32_t *rc = cl.map_shared_rank(cnt, owner);
-            uint32_t sl = (h >> HC_LOGCL) & (HC_TS - 1);
-            while (true) {
-                const int32_t old = atomicCAS(rk + sl, -1, c);
-                if (old == -1 || old == c) break;
-                sl = (sl + 1) & (HC_TS - 1);
-            }
-            atomicAdd(rv + sl, gs);
-            atomicAdd(rc + sl, __popc(grp));
-        }
-    }
-    cl.sync();
-    if (tid == 0) {  // c_old's any-order sum, from its owner's slice
-        const uint32_t h = hslot(c_old, 0xffffffffu);
-        const unsigned owner = h & (HC_CL - 1);
-        const int32_t *rk = cl.map_shared_rank(keys, owner);
-        uint32_t sl = (h >> HC_LOGCL) & (HC_TS - 1);
-        double f = 0.0;
-        int32_t l = 0;
-        while (true) {
-            const int32_t k = rk[sl];
-            if (k == c_old) {
-                f = cl.map_shared_rank(vals, owner)[sl];
-                l = cl.map_shared_rank(cnt, owner)[sl];
-                break;
-            }
-            if (k == -1) break;
-            sl = (sl + 1) & (HC_TS - 1);
-        }
-        S.f_old = f;
-        S.l_old = l;
-    }
-    cl.sync();  // every remote read done: the slices may be overwritten
-    const double f_old = S.f_old;
-    const int32_t l_old_n = S.l_old;
-    const double a_old_excl = dsub(ld_state(A.a_tot + c_old), ki);
-    const double inv_m = 1.0 / A.m;
-    // pass 1 (certify_table): gains and slack of this slice, its best
-    Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
-    unsigned long long nc = 0;
-    for (int p0 = tid; p0 < HC_TS; p0 += HC_NT * 4) {
-        int32_t c[4], L[4];
-        double F[4], at[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const int sl = p0 + u * HC_NT;
-            c[u] = sl < HC_TS ? keys[sl] : -1;
-            F[u] = c[u] >= 0 ? vals[sl] : 0.0;
-            L[u] = c[u] >= 0 ? cnt[sl] : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; u++) at[u] = c[u] >= 0 && c[u] != c_old ? ld_state(A.a_tot + c[u]) : 0.0;
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            if (c[u] < 0) continue;
-            nc++;
-            if (c[u] == c_old) continue;
-            const int sl = p0 + u * HC_NT;
-            const double g = gain_of(F[u], f_old, A.m, ki, a_old_excl, at[u], A.four_m_sq);
-            consider(b, g, LBL(A.labels, c[u]), c[u], F[u], L[u]);
-            vals[sl] = g;
-            cnt[sl] = __float_as_int(__double2float_ru(gain_slack_r(F[u], L[u], f_old, l_old_n, inv_m, g)));
-        }
-    }
-    if (A.cand) {
-        for (int o = 16; o > 0; o >>= 1) nc += __shfl_xor_sync(FULL, nc, o);
-        if (lane == 0 && nc) atomicAdd(A.cand, nc);
-    }
-    b = block_best<HC_NT>(S.bs, b);
-    if (tid == 0) cl.map_shared_rank(cb, 0)[r] = b;
-    cl.sync();
-    if (A.integral) {
-        // exact in any order: the plain argmax is the reference's
-        if (r == 0 && tid == 0) {
-            Best bw = cb[0];
-            for (int t = 1; t < HC_CL; t++) consider(bw, cb[t].g, cb[t].l, cb[t].c, cb[t].e, cb[t].n);
-            finish_vertex(A, x, c_old, f_old, bw.g, bw.c, bw.e);
-        }
-        return;  // rank 0's cb is read by rank 0 only
-    }
-    Best bw;
-    {
-        const Best *rcb = cl.map_shared_rank(cb, 0);
-        bw = rcb[0];
-        for (int t = 1; t < HC_CL; t++) {
-            const Best o = rcb[t];
-            consider(bw, o.g, o.l, o.c, o.e, o.n);
-        }
-    }
-    // pass 2 (certify_table): this slice's candidates overlapping the best,
-    // listed in rank 0
-    const bool stay_best = bw.c == c_old;
-    const double slack_b = stay_best ? 0.0 : gain_slack_r(bw.e, bw.n, f_old, l_old_n, inv_m, bw.g);
-    const double lower = stay_best ? 0.0 : bw.g - slack_b;
-    CertSmem<HC_NT> *S0 = cl.map_shared_rank(&S, 0);
-    for (int sl = tid; sl < HC_TS; sl += HC_NT) {
-        const int32_t c = keys[sl];
-        if (c < 0 || c == c_old || c == bw.c) continue;
-        const double slv = (double)__int_as_float(cnt[sl]);
-        if ((slv > 0.0 || slack_b > 0.0) && vals[sl] + slv >= lower) {
-            const int k = atomicAdd(&S0->nS, 1);
-            if (k < MAXS)
-                S0->N[2 + k] = c;
-            else
-                atomicOr(&S0->flag, 2);
-        }
-    }
-    cl.sync();
-    if (r != 0) return;
-    if (tid == 0 && !stay_best && slack_b > 0.0 && lower <= 0.0) S.flag |= 1;  // "stay" overlaps
-    __syncthreads();
-    if (!resolve<HC_NT, HFU>(A, x, i, c_old, ki, bw, S)) {
-        const int64_t base = H.toff[q];
-        table_exact<HC_NT>(A, x, i, c_old, ki, H.hkeys + base, H.hvals + base,
-                           PowTab{(uint32_t)(H.toff[q + 1] - base - 1)}, S);
-    }
-}
-
-
-// ------------------------------------------------ tail runs (k_tail)
-//
-// The late colour classes of a heavy-tailed graph hold a few hub-tier
-// vertices each (C4: ~250 classes of 3-16 vertices of degree 15k-70k; C2:
-// ~100 of <= 32).  Per class the multi-kernel path pays accumulate -> pass ->
-// apply launches and a per-hub ticket, ~15-20 us of dependent latency for
-// ~1-2 us of work.  k_tail decides AND applies a whole run of such classes
-// in ONE launch: a single thread-block cluster (16 CTAs when the device
-// allows non-portable clusters, else 8) walks the run's classes in order,
-// separated by hardware cluster barriers (release / acquire at cluster scope:
-// each class reads the state the previous class wrote; state loads are
-// coherent L2 loads, ld_state).  Per class:
-//   1. accumulate: every hub entry of the class, spread over the cluster, into
-//      the dense per-hub arrays (any-order sums, term counts, first position);
-//   2. pass A: 32-position chunks of one hub per warp; the first position of
-//      each community owns it: gain, slack, warp best -> per-hub best (CTA,
-//      then the hub's decider CTA over DSMEM); arrays reset behind it;
-//   3. decide (decider CTA of each hub): integral graphs finish at once; else
-//      pass B lists the candidates overlapping the hub's best (as
-//      certify_table) and resolve() / table_exact decide on exact values --
-//      the rules and bits of k_hub_accum + k_hub_pass;
-//   4. apply: one warp, apply_tiny_warp (the reference's ordered apply).
-constexpr int TL_NT = 512;
-constexpr int TL_MAXH = 32;  // vertices per tail class (one tiny-apply warp)
-constexpr int TL_U = 4;      // entries per thread in flight (accumulate)
-constexpr int TL_DPC = 4;    // decided hubs per CTA (TL_MAXH / 8)
-#ifndef TL_MAXE
-#define TL_MAXE 8192         // hub entries per tail class: more need the whole GPU
-#endif
-
-struct TailStage {
-    int64_t goff;      // class offset in the stage lists and decide outputs
-    int64_t hub_base;  // first hub_eoff / hub_toff / hub_row / hub_vid entry
-    int64_t tstart;    // first tier-list entry of the hub tier
-    int64_t nh;        // its vertices (= the class's active vertices), 0: skip
-};
-
-struct TailArgs {
-    DecideArgs A;  // outputs at class offset 0
-    StageArgs S;   // subset / outputs at class offset 0
-    const TailStage *st;
-    int64_t a0, a1;
-    const int32_t *tier_list, *hub_vid;
-    const int64_t *hub_row, *hub_eoff, *hub_toff;
-    double *dval;
-    int32_t *dcnt, *dmk, *cbuf;
-    int64_t dn;
-    int32_t *hkeys;
-    double *hvals;
-    double *gbuf;
-    float *sbuf;
-};
-
-__device__ __forceinline__ int tl_hub_of(const int64_t *eo, int nh, int64_t t) {
-    int lo = 0, hi = nh;
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (eo[mid] <= t)
-            lo = mid;
-        else
-            hi = mid;
-    }
-    return lo;
-}
-
-template <int CL>
-__global__ void __launch_bounds__(TL_NT, 1) k_tail(TailArgs T) {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cl = cg::this_cluster();
-    __shared__ int64_t s_eoff[TL_MAXH + 1], s_poff[TL_MAXH + 1], s_row[TL_MAXH], s_x[TL_MAXH];
-    __shared__ int32_t s_vid[TL_MAXH], s_cold[TL_MAXH], s_lold[TL_MAXH];
-    __shared__ double s_ki[TL_MAXH], s_fold[TL_MAXH], s_aoe[TL_MAXH], s_lower[TL_MAXH],
-        s_slb[TL_MAXH];
-    __shared__ Best s_hb[TL_MAXH];   // this CTA's best per hub
-    __shared__ Best s_bw[TL_MAXH];   // the hub's best over the cluster
-    __shared__ int s_lock[TL_MAXH];
-    __shared__ Best s_cb[TL_DPC][CL];  // decider: the CTAs' bests of its hubs
-    __shared__ int32_t s_near[TL_DPC][MAXS];
-    __shared__ int s_nn[TL_DPC], s_nf[TL_DPC];
-    __shared__ CertSmem<TL_NT> S;
-    __shared__ int32_t cidx[TL_NT * HFU];
-    __shared__ double cw[TL_NT * HFU];
-    __shared__ unsigned long long ap_k[64];
-    __shared__ double ap_w[64], ap_a[64];
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int r = (int)cl.block_rank();
-    const int64_t gt = (int64_t)r * TL_NT + tid, G = (int64_t)CL * TL_NT;
-    const int64_t gw = gt >> 5, GW = G >> 5;
-    const bool integral = T.A.integral != 0;
-    const double inv_m = 1.0 / T.A.m;
-    if (tid == 0) {
-        S.cidx = cidx;
-        S.cw = cw;
-    }
-    pdl_wait();  // the state of the previous stage
-    for (int64_t a = T.a0; a < T.a1; a++) {
-        const TailStage d = T.st[a];
-        const int nh = (int)d.nh;
-        if (nh == 0) continue;
-        DecideArgs A = T.A;
-        A.out_target += d.goff;
-        A.out_moved += d.goff;
-        A.out_e_old += d.goff;
-        A.out_e_best += d.goff;
-        if (tid < nh) {
-            const int q = tid;
-            const int32_t i = T.hub_vid[d.hub_base + q];
-            s_vid[q] = i;
-            s_row[q] = T.hub_row[d.hub_base + q];
-            s_x[q] = T.tier_list[d.tstart + q];
-            s_eoff[q] = T.hub_eoff[d.hub_base + q];
-            const int32_t c_old = ld_state(A.assign + i);
-            s_cold[q] = c_old;
-            s_ki[q] = A.k[i];
-            s_hb[q] = Best{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
-            s_lock[q] = 0;
-        }
-        if (tid < TL_DPC) {
-            s_nn[tid] = 0;
-            s_nf[tid] = 0;
-        }
-        if (tid == 0) {
-            s_eoff[nh] = T.hub_eoff[d.hub_base + nh];
-            s_poff[0] = 0;
-        }
-        __syncthreads();
-        if (tid == 0)  // 32-aligned chunk positions: a chunk belongs to one hub
-            for (int q = 0; q < nh; q++)
-                s_poff[q + 1] = s_poff[q] + ((s_eoff[q + 1] - s_eoff[q] + 31) & ~(int64_t)31);
-        const int64_t E = s_eoff[nh];
-        // ---- 1. accumulate
-        for (int64_t t0 = gt; t0 < E; t0 += G * TL_U) {
-            int qv[TL_U];
-            int32_t jv[TL_U], cv[TL_U];
-            double wv[TL_U];
-#pragma unroll
-            for (int u = 0; u < TL_U; u++) {
-                const int64_t t = t0 + u * G;
-                qv[u] = t < E ? tl_hub_of(s_eoff, nh, t) : 0;
-                const int64_t e = s_row[qv[u]] + (t - s_eoff[qv[u]]);
-                jv[u] = t < E ? ld_row(A.nbr + e) : -1;
-                wv[u] = t < E ? ld_row(A.wts + e) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < TL_U; u++)
-                cv[u] = jv[u] >= 0 && jv[u] != s_vid[qv[u]] ? ld_state(A.assign + jv[u]) : -1;
-#pragma unroll
-            for (int u = 0; u < TL_U; u++) {
-                const int64_t t = t0 + u * G;
-                if (t >= E) continue;
-                T.cbuf[t] = cv[u];
-                if (cv[u] < 0) continue;
-                const int64_t dq = (int64_t)qv[u] * T.dn + cv[u];
-                atomicAdd(T.dval + dq, wv[u]);
-                atomicAdd(T.dcnt + dq, 1);
-                atomicMin(T.dmk + dq, (int32_t)(t - s_eoff[qv[u]]));
-            }
-        }
-        cl.sync();
-        if (tid < nh) {
-            const int q = tid;
-            const int64_t dq = (int64_t)q * T.dn + s_cold[q];
-            s_fold[q] = ld_state(T.dval + dq);
-            s_lold[q] = ld_state(T.dcnt + dq);
-            s_aoe[q] = dsub(ld_state(A.a_tot + s_cold[q]), s_ki[q]);
-        }
-        __syncthreads();
-        // ---- 2. pass A: one hub per 32-position chunk
-        const int64_t PP = s_poff[nh];
-        unsigned long long nc = 0;
-        for (int64_t k = gw; k * 32 < PP; k += GW) {
-            const int64_t p = k * 32;
-            const int q = tl_hub_of(s_poff, nh, p);
-            const int64_t pos = p - s_poff[q] + lane;  // row position
-            const int64_t t = s_eoff[q] + pos;
-            const bool ok = t < s_eoff[q + 1];
-            const int32_t c_old = s_cold[q];
-            const int32_t c = ok ? ld_state(T.cbuf + t) : -1;
-            const int64_t dq = (int64_t)q * T.dn + (c >= 0 ? c : 0);
-            const bool own = c >= 0 && ld_state(T.dmk + dq) == (int32_t)pos;
-            nc += own;
-            const bool cand = own && c != c_old;
-            const double F = cand ? ld_state(T.dval + dq) : 0.0;
-            const int32_t L = cand ? ld_state(T.dcnt + dq) : 0;
-            const double at = cand ? ld_state(A.a_tot + c) : 0.0;
-            Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
-            if (cand) {
-                const double g = gain_of(F, s_fold[q], A.m, s_ki[q], s_aoe[q], at, A.four_m_sq);
-                consider(b, g, LBL(A.labels, c), c, F, L);
-                if (!integral) {
-                    T.gbuf[t] = g;
-                    T.sbuf[t] = __double2float_ru(gain_slack_r(F, L, s_fold[q], s_lold[q], inv_m, g));
-                }
-                T.dval[dq] = 0.0;  // back to idle (c_old's slot: by the decider)
-                T.dcnt[dq] = 0;
-                T.dmk[dq] = INT_MAX;
-            } else if (!integral && ok) {
-                T.gbuf[t] = -INFINITY;
-            }
-            warp_best(b);
-            if (lane == 0) {
-                while (atomicCAS(&s_lock[q], 0, 1) != 0) {
-                }
-                __threadfence_block();
-                Best h = s_hb[q];
-                consider(h, b.g, b.l, b.c, b.e, b.n);
-                s_hb[q] = h;
-                __threadfence_block();
-                atomicExch(&s_lock[q], 0);
-            }
-        }
-        if (A.cand) {
-            for (int o = 16; o > 0; o >>= 1) nc += __shfl_xor_sync(FULL, nc, o);
-            if (lane == 0 && nc) atomicAdd(A.cand, nc);
-        }
-        __syncthreads();
-        if (tid < nh) cl.map_shared_rank(&s_cb[0][0], tid % CL)[(tid / CL) * CL + r] = s_hb[tid];
-        cl.sync();
-        // ---- 3. decide: CTA r decides hubs r, r + CL, ...
-        if (tid < TL_DPC) {
-            const int q = r + tid * CL;
-            if (q < nh) {
-                Best bw = s_cb[tid][0];
-                for (int t = 1; t < CL; t++)
-                    consider(bw, s_cb[tid][t].g, s_cb[tid][t].l, s_cb[tid][t].c, s_cb[tid][t].e,
-                             s_cb[tid][t].n);
-                if (integral) {
-                    finish_vertex(A, s_x[q], s_cold[q], s_fold[q], bw.g, bw.c, bw.e);
-                } else {
-                    for (int rr = 0; rr < CL; rr++) cl.map_shared_rank(s_bw, rr)[q] = bw;
-                }
-                if (integral) {  // c_old's slot back to idle
-                    const int64_t dq = (int64_t)q * T.dn + s_cold[q];
-                    T.dval[dq] = 0.0;
-                    T.dcnt[dq] = 0;
-                    T.dmk[dq] = INT_MAX;
-                }
-            }
-        }
-        if (!integral) {
-            cl.sync();  // every hub's best in every CTA
-            if (tid < nh) {
-                const int q = tid;
-                const Best bw = s_bw[q];
-                const bool stay = bw.c == s_cold[q];
-                const double slb =
-                    stay ? 0.0 : gain_slack_r(bw.e, bw.n, s_fold[q], s_lold[q], inv_m, bw.g);
-                s_slb[q] = slb;
-                s_lower[q] = stay ? 0.0 : bw.g - slb;
-            }
-            __syncthreads();
-            // pass B: candidates overlapping the best, listed at the decider
-            for (int64_t k = gw; k * 32 < PP; k += GW) {
-                const int64_t p = k * 32;
-                const int q = tl_hub_of(s_poff, nh, p);
-                const int64_t t = s_eoff[q] + (p - s_poff[q]) + lane;
-                if (t >= s_eoff[q + 1]) continue;
-                const double g = ld_state(T.gbuf + t);
-                if (g == -INFINITY) continue;
-                const int32_t c = ld_state(T.cbuf + t);
-                if (c == s_bw[q].c) continue;
-                const double slv = (double)__ldcg(T.sbuf + t);
-                if ((slv > 0.0 || s_slb[q] > 0.0) && g + slv >= s_lower[q]) {
-                    const int dr = q % CL, dk = q / CL;
-                    const int kk = atomicAdd(cl.map_shared_rank(&s_nn[dk], dr), 1);
-                    if (kk < MAXS)
-                        cl.map_shared_rank(&s_near[dk][0], dr)[kk] = c;
-                    else
-                        atomicOr(cl.map_shared_rank(&s_nf[dk], dr), 2);
-                }
-            }
-            cl.sync();
-            for (int dk = 0; dk < TL_DPC; dk++) {  // block-uniform
-                const int q = r + dk * CL;
-                if (q >= nh) break;
-                const Best bw = s_bw[q];
-                if (tid == 0) {
-                    S.f_old = s_fold[q];
-                    S.l_old = s_lold[q];
-                    const int nn = s_nn[dk];
-                    S.nS = nn;
-                    int fl = s_nf[dk] | (nn > MAXS ? 2 : 0);
-                    if (bw.c != s_cold[q] && s_slb[q] > 0.0 && s_lower[q] <= 0.0) fl |= 1;
-                    S.flag = fl;
-                    for (int t = 0; t < nn && t < MAXS; t++) S.N[2 + t] = s_near[dk][t];
-                }
-                __syncthreads();
-                if (!resolve<TL_NT, HFU>(A, s_x[q], s_vid[q], s_cold[q], s_ki[q], bw, S)) {
-                    const int64_t base = T.hub_toff[d.hub_base + q];
-                    table_exact<TL_NT>(A, s_x[q], s_vid[q], s_cold[q], s_ki[q], T.hkeys + base,
-                                       T.hvals + base,
-                                       PowTab{(uint32_t)(T.hub_toff[d.hub_base + q + 1] - base - 1)},
-                                       S);
-                }
-                if (tid == 0) {
-                    const int64_t dq = (int64_t)q * T.dn + s_cold[q];
-                    T.dval[dq] = 0.0;
-                    T.dcnt[dq] = 0;
-                    T.dmk[dq] = INT_MAX;
-                }
-                __syncthreads();
-            }
-        }
-        cl.sync();  // the class's decisions
-        // ---- 4. apply (rank 0, warp 0)
-        if (r == 0 && tid < 32) {
-            StageArgs SA = T.S;
-            SA.subset += d.goff;
-            SA.ns = nh;
-            SA.target += d.goff;
-            SA.moved += d.goff;
-            SA.e_old += d.goff;
-            SA.e_best += d.goff;
-            apply_tiny_warp<1>(SA, ap_k, ap_w, ap_a);
-        }
-        cl.sync();  // the class's moves, before the next class reads the state
-    }
-}
-
-static bool tail_cluster_ok(int cl) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cl);
-    cfg.blockDim = dim3(TL_NT);
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cl;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int nclu = 0;
-    cudaError_t e = cl == 16 ? cudaOccupancyMaxActiveClusters(&nclu, k_tail<16>, &cfg)
-                             : cudaOccupancyMaxActiveClusters(&nclu, k_tail<8>, &cfg);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return nclu > 0;
-}
-
-void tail_plan(Plan &P, bool enable, bool integral, cudaStream_t s) {
-    P.tail_first.clear();
-    P.tail_last.clear();
-    const int64_t nst = (int64_t)P.st.size();
-    if (!enable || !PLV_TAIL || nst == 0) return;
-    std::vector<TailStage> ts(nst);
-    std::vector<bool> ok(nst, false);
-    int64_t max_e = 0;
-    for (int64_t a = 0; a < nst; a++) {
-        const StagePlan &sp = P.st[a];
-        ts[a] = TailStage{sp.off, sp.hub_base, sp.tstart[4], sp.tcount[4]};
-        if (sp.ns == 0) {
-            ok[a] = true;  // nothing to do; may sit inside a run
-            ts[a].nh = 0;
-            continue;
-        }
-        ok[a] = !sp.tcount[0] && !sp.tcount[1] && !sp.tcount[2] && !sp.tcount[3] &&
-                sp.tcount[4] == sp.ns && sp.ns <= TL_MAXH && sp.hub_dense && !sp.hub_cluster &&
-                sp.hub_entries <= TL_MAXE;
-        if (ok[a]) max_e = sp.hub_entries > max_e ? sp.hub_entries : max_e;
-    }
-    for (int64_t a = 0; a < nst;) {
-        if (!ok[a] || P.st[a].ns == 0) {
-            a++;
-            continue;
-        }
-        int64_t b = a;
-        while (b < nst && ok[b]) b++;
-        P.tail_first.push_back(a);
-        P.tail_last.push_back(b);
-        a = b;
-    }
-    if (P.tail_first.empty()) return;
-    if (!P.tail_cl) {
-        static int attr_dev = -1;
-        int dev = 0;
-        PLV_CUDA(cudaGetDevice(&dev));
-        if (attr_dev != dev) {
-            cudaFuncSetAttribute(k_tail<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            cudaGetLastError();
-            attr_dev = dev;
-        }
-        P.tail_cl = tail_cluster_ok(16) ? 16 : tail_cluster_ok(8) ? 8 : 0;
-    }
-    if (!P.tail_cl) {
-        P.tail_first.clear();
-        P.tail_last.clear();
-        return;
-    }
-    P.tail_st = dalloc<TailStage>(nst);
-    PLV_CUDA(cudaMemcpyAsync(P.tail_st, ts.data(), sizeof(TailStage) * nst,
-                             cudaMemcpyHostToDevice, s));
-    if (!integral) {
-        P.tail_g = dalloc<double>(max_e);
-        P.tail_s = dalloc<float>(max_e);
-    }
-    PLV_CUDA(cudaStreamSynchronize(s));
-}
-
-void launch_tail(const Plan &P, int64_t k, DecideArgs A, StageArgs S, cudaStream_t st) {
-    TailArgs T{A, S, (const TailStage *)P.tail_st, P.tail_first[k], P.tail_last[k],
-               P.tier_list, P.hub_vid, P.hub_row, P.hub_eoff, P.hub_toff, P.dval, P.dcnt,
-               P.dmk, P.cbuf, P.dn, P.hkeys, P.hvals, P.tail_g, P.tail_s};
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(P.tail_cl);
-    cfg.blockDim = dim3(TL_NT);
-    cfg.stream = st;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = P.tail_cl;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 2;
-    if (P.tail_cl == 16)
-        PLV_CUDA(cudaLaunchKernelEx(&cfg, k_tail<16>, T));
-    else
-        PLV_CUDA(cudaLaunchKernelEx(&cfg, k_tail<8>, T));
-    count_launch();
-}
-
-
 // ================================================================ planning
 
 __global__ void k_tier_keys(const int64_t *off, const int32_t *vtx, const int64_t *stage_off,
@@ -1924,7 +1290,7 @@ void Plan::release() {
     cudaDeviceSynchronize();  // buffers go back to the pool idle
     void *ps[] = {tier_list, tier_vid, tier_row, tier_end, hub_eoff, hub_toff, hub_poff, hub_blk, hub_row, hub_vid, hkeys,
                   hvals,     hcnt,     hsold,    hncnt,    hnear,   hpart,
-                  dval,      dcnt,     dmk,      cbuf,     tail_st, tail_g,  tail_s};
+                  dval,      dcnt,     dmk,      cbuf};
     for (void *p : ps)
         pool_free(p);
     tier_list = nullptr;
@@ -1938,11 +1304,6 @@ void Plan::release() {
     hpart = nullptr;
     dval = nullptr;
     dcnt = dmk = cbuf = nullptr;
-    tail_st = nullptr;
-    tail_g = nullptr;
-    tail_s = nullptr;
-    tail_first.clear();
-    tail_last.clear();
 }
 
 void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *stage_off_h,
@@ -2037,10 +1398,8 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
         // few hubs: dense per-hub community arrays (no claims), items are row
         // positions; else hash tables, items are table slices
         sp.hub_dense = sp.tcount[4] > 0 && sp.tcount[4] <= P.dense_k;
-        sp.hub_cluster = sp.hub_dense && PLV_HUB_CLUSTER;
         for (int64_t z = 0; z < sp.tcount[4]; z++) {
             int64_t d = deg[h0 + z];
-            if (d > HC_MAXD) sp.hub_cluster = false;
             int64_t cap = 64;
             while (cap < 2 * d + 2) cap <<= 1;
             int64_t sl = sp.hub_dense ? (d + HSB - 1) / HSB : (cap + HTSL - 1) / HTSL;
@@ -2061,7 +1420,7 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
         sp.hub_nblk = pacc;
         max_parts = pacc > max_parts ? pacc : max_parts;
         P.max_hub_entries = acc > P.max_hub_entries ? acc : P.max_hub_entries;
-        if (sp.hub_dense && !sp.hub_cluster) P.max_dense_entries = acc > P.max_dense_entries ? acc : P.max_dense_entries;
+        if (sp.hub_dense) P.max_dense_entries = acc > P.max_dense_entries ? acc : P.max_dense_entries;
         P.max_hubs = sp.tcount[4] > P.max_hubs ? sp.tcount[4] : P.max_hubs;
         P.max_table = tacc > P.max_table ? tacc : P.max_table;
     }
@@ -2133,8 +1492,6 @@ void ensure_decide_attrs() {
     PLV_CUDA(cudaFuncSetAttribute(k_decide_t2<T2_TS, T2_MAXD, 1024>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)t2_smem(T2_TS)));
-    PLV_CUDA(cudaFuncSetAttribute(k_hub_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)hc_smem()));
     dev_done = dev;
 }
 
@@ -2243,26 +1600,7 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
                      P.cbuf,
                      P.dn};
         unsigned g2 = (unsigned)sp.hub_nblk;
-        if (sp.hub_cluster) {
-            HubClArgs C{list, P.hub_vid + sp.hub_base, P.hub_row + sp.hub_base, eoff, toff,
-                        P.hkeys, P.hvals};
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3((unsigned)(nh * HC_CL));
-            cfg.blockDim = dim3(HC_NT);
-            cfg.dynamicSmemBytes = hc_smem();
-            cfg.stream = st;
-            cudaLaunchAttribute at[2];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = HC_CL;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            at[1].val.programmaticStreamSerializationAllowed = 1;
-            cfg.attrs = at;
-            cfg.numAttrs = 2;
-            PLV_CUDA(cudaLaunchKernelEx(&cfg, k_hub_cluster, A, C));
-            count_launch();
-        } else if (sp.hub_dense) {
+        if (sp.hub_dense) {
             launch_pdl(k_hub_accum<true>, grid_for(E, 256), 256, 0, st, A, eoff, toff, nh, E,
                        P.hkeys, P.hvals, P.hcnt, H);
             launch_pdl(k_hub_pass<true>, g2, HSB, 0, st, A, list, eoff, toff, P.hkeys, P.hvals,
