@@ -216,12 +216,31 @@ int plv_phase_create_part(const int64_t *off, const int32_t *nbr, const double *
 #define PLV_STEP_DECIDE 0 /* decide this rank's slice of `stage`              */
 #define PLV_STEP_APPLY 1  /* exact apply of the whole of `stage`               */
 #define PLV_STEP_FINISH 2 /* modularity; q_h / moves_h of the stepped iteration */
+#define PLV_STEP_LIVE 3   /* uncoloured stage: live e_a / e_b of this rank's movers (the
+                             reference's apply folds, PL/_kernels.pyx:116-136) into
+                             the slice's e_old / e_best, to be exchanged before APPLY */
 int plv_phase_step(void *handle, int64_t stage, int op, double *q_h, int64_t *moves_h,
                    void *stream);
 /* The engine's stage offsets (nstages+1; stage lists keep only vertices with
  * a non-self neighbour -- the others never move) and the slice bounds of
  * every stage (nstages * (world+1), relative to the stage). */
 int plv_phase_slices(void *handle, int64_t *stage_off_h, int64_t *slices_h);
+
+/* plv_phase_create_part on a graph holding only the rows of this rank's
+ * vertices (off / nbr / wts with empty rows elsewhere; k / selfw replicated):
+ * deg (n, replicated) gives every vertex's degree for the stage lists'
+ * activity rule.  In this mode an uncoloured stage folds its movers' live
+ * e_a / e_b on their owner (PLV_STEP_LIVE) and exchanges them; with a
+ * communicator the exchange is one in-place ncclAllGather of 24-byte records
+ * per stage (and per live step), captured in the iteration graph. */
+int plv_phase_create_part2(const int64_t *off, const int32_t *nbr, const double *wts,
+                           const double *k, const double *selfw, int64_t n, double m, int flags,
+                           const int32_t *labels, const int64_t *stage_off_h,
+                           const int32_t *stage_vtx, int64_t nstages, int32_t *assign,
+                           double *a_tot, double *w_int, int32_t *sizes, int64_t rank,
+                           int64_t world, const int64_t *bounds_h, void *comm,
+                           const int32_t *deg, int32_t *out_target, uint8_t *out_moved,
+                           double *out_e_old, double *out_e_best, void **handle_h, void *stream);
 
 /* NCCL communicator for plv_phase_create_part (NCCL is bound at run time). */
 #define PLV_NCCL_ID_BYTES 128
@@ -308,6 +327,63 @@ int plv_gen_grid(uint64_t seed, int64_t side, double keep, int64_t pendants, dou
 /* Chung-Lu: endpoints drawn by searchsorted(cdf, U * cdf[n-1], 'right'). */
 int plv_gen_chung_lu(uint64_t seed, const double *cdf, int64_t n, int64_t records, int32_t *u,
                      int32_t *v, double *w, int64_t cap, int64_t *count_h, void *stream);
+
+/* ---------------------------------------------------- 1D vertex partition
+ * (new design -- the reference has no distributed mode).  Rank
+ * r owns vertices [bounds[r], bounds[r+1]) and holds only their rows; the
+ * host driver (paper_1410_1237_b200/partition.py) moves data between ranks.
+ */
+
+/* R-MAT records of draws [r_begin, r_end) (plv_gen_rmat restricted: the
+ * ranges of all ranks concatenate to plv_gen_rmat's output). */
+int plv_gen_rmat_range(uint64_t seed, int scale, int64_t edge_factor, double a, double b,
+                       double c, double w_lo, double w_hi, int64_t r_begin, int64_t r_end,
+                       int32_t *u, int32_t *v, double *w, int64_t cap, int64_t *count_h,
+                       void *stream);
+/* Route records to the owners of both endpoints (Graph.from_edges,
+ * PL/graph.py:88-147, split by rows): every record once per distinct owner,
+ * grouped by destination rank, input order kept within a group.  bounds:
+ * device, world+1.  send_counts_h[world].  R < 2^31 per call. */
+int plv_route_records(const int32_t *u, const int32_t *v, const double *w, int64_t R,
+                      const int64_t *bounds, int world, int32_t *ou, int32_t *ov, double *ow,
+                      int64_t cap, int64_t *send_counts_h, void *stream);
+/* Keep rows [lo, hi) of a CSR (off n+1): out_off (n+1, empty rows outside),
+ * out_nbr / out_wts (the rows' entries), deg[n] (zero outside).  info_h =
+ * {entries, self loops, unique pairs (nbr >= row), max degree, non-integral}. */
+int plv_part_own_rows(const int64_t *off, const int32_t *nbr, const double *wts, int64_t n,
+                      int64_t lo, int64_t hi, int64_t *out_off, int32_t *out_nbr,
+                      double *out_wts, int32_t *deg, int64_t *info_h, void *stream);
+/* vf_compact (PL/heuristics.py:46-89) on owned rows: only_p1[v] = the single
+ * neighbour + 1 of owned candidates, 0 elsewhere (to be summed over ranks). */
+int plv_part_vf_only(const int64_t *off, const int32_t *nbr, const int32_t *deg,
+                     const double *selfw, int64_t n, int64_t lo, int64_t hi, int32_t *only_p1,
+                     void *stream);
+/* ... from the replicated only_p1: merged flags, new_id (n+1, exclusive scan
+ * of the survivors) and vertex_map; info_h = {n_new, merged_count}. */
+int plv_part_vf_map(const int32_t *only_p1, int64_t n, uint8_t *merged, int32_t *new_id,
+                    int32_t *vertex_map, int64_t *info_h, void *stream);
+/* ... the owned rows' compacted records: kept (a <= b, row-major) and folded
+ * (t, t, w) per owned merged vertex in ascending id; counts_h = {kept, folded}. */
+int plv_part_vf_records(const int64_t *off, const int32_t *nbr, const double *wts, int64_t n,
+                        int64_t lo, int64_t hi, const uint8_t *merged, const int32_t *new_id,
+                        const int32_t *only_p1, int32_t *ku, int32_t *kv, double *kw,
+                        int32_t *fu, int32_t *fv, double *fw, int64_t *counts_h, void *stream);
+/* out[idx[t]] = val ? val[t] : fill (colour rounds, PL/heuristics.py:109-113). */
+int plv_scatter_i32(const int32_t *idx, const int32_t *val, int32_t fill, int64_t cnt,
+                    int32_t *out, void *stream);
+/* active[t] for every keep[t] == 0, in order (PL/heuristics.py:114). */
+int plv_select_rejected(const int32_t *active, const uint8_t *keep, int64_t na, int32_t *out,
+                        int64_t *count_h, void *stream);
+/* rebuild's renumbering (PL/engine.py:237-239): renumber[n] dense in ascending
+ * community id, -1 for empty ids. */
+int plv_renumber(const int32_t *assign, int64_t n, int32_t *renumber, int64_t *n_new_h,
+                 void *stream);
+/* rebuild's records (PL/engine.py:240-243) of the owned rows, row-major:
+ * (renumber[assign[a]], renumber[assign[b]], w) for every entry b >= a. */
+int plv_part_rebuild_records(const int64_t *off, const int32_t *nbr, const double *wts,
+                             int64_t n, int64_t lo, int64_t hi, const int32_t *assign,
+                             const int32_t *renumber, int32_t *ou, int32_t *ov, double *ow,
+                             int64_t *count_h, void *stream);
 
 /* ------------------------------------------------------------ diagnostics */
 

@@ -32,6 +32,7 @@ F_IDENTITY = 4
 STEP_DECIDE = 0
 STEP_APPLY = 1
 STEP_FINISH = 2
+STEP_LIVE = 3
 NCCL_ID_BYTES = 128
 INGEST_HOST = 1
 
@@ -68,6 +69,8 @@ _SIGS = {
                          _INT, _P, _P],
     "plv_phase_create_part": [_P, _P, _P, _P, _P, _I64, _D, _INT, _P, _P, _P, _I64, _P, _P, _P,
                               _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P],
+    "plv_phase_create_part2": [_P, _P, _P, _P, _P, _I64, _D, _INT, _P, _P, _P, _I64, _P, _P,
+                               _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "plv_phase_step": [_P, _I64, _INT, _P, _P, _P],
     "plv_phase_slices": [_P, _P, _P],
     "plv_nccl_unique_id": [_P],
@@ -87,6 +90,18 @@ _SIGS = {
     "plv_gen_sbm": [_U64, _I64, _I64, _D, _D, _P, _P, _P, _I64, _P, _P],
     "plv_gen_grid": [_U64, _I64, _D, _I64, _D, _P, _P, _P, _I64, _P, _P],
     "plv_gen_chung_lu": [_U64, _P, _I64, _I64, _P, _P, _P, _I64, _P, _P],
+    "plv_gen_rmat_range": [_U64, _INT, _I64, _D, _D, _D, _D, _D, _I64, _I64, _P, _P, _P, _I64,
+                           _P, _P],
+    "plv_route_records": [_P, _P, _P, _I64, _P, _INT, _P, _P, _P, _I64, _P, _P],
+    "plv_part_own_rows": [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P],
+    "plv_part_vf_only": [_P, _P, _P, _P, _I64, _I64, _I64, _P, _P],
+    "plv_part_vf_map": [_P, _I64, _P, _P, _P, _P, _P],
+    "plv_part_vf_records": [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                            _P, _P],
+    "plv_scatter_i32": [_P, _P, ctypes.c_int32, _I64, _P, _P],
+    "plv_select_rejected": [_P, _P, _I64, _P, _P, _P],
+    "plv_renumber": [_P, _I64, _P, _P, _P],
+    "plv_part_rebuild_records": [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P],
 }
 _RESTYPE = {"plv_last_error": ctypes.c_char_p, "plv_launch_count": ctypes.c_ulonglong}
 

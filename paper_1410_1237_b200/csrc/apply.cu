@@ -181,12 +181,13 @@ __global__ void __launch_bounds__(256) k_stage_prep(StageArgs A) {
         int64_t x = base + lane;
         bool mover = false, big = false;
         int32_t i = 0, a = 0, b = 0;
-        if (x < A.ns) {
+        const bool live_only = A.live_a != nullptr;
+        if (x < A.ns && (!live_only || (x >= A.xlo && x < A.xhi))) {
             i = A.subset[x];
             b = A.target[x];
             a = A.assign[i];
             mover = A.moved[x] && a != b;
-            if (!integral) {
+            if (!integral && !live_only) {
                 A.ekey[2 * x] = mover ? (uint32_t)a : SENTINEL;
                 A.ekey[2 * x + 1] = mover ? (uint32_t)b : SENTINEL;
                 A.eval[2 * x] = (int32_t)(2 * x);
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(256) k_stage_prep(StageArgs A) {
         }
         double e_a = 0.0, e_b = 0.0;
         if (mover) {
-            my_moves++;
+            if (!live_only) my_moves++;
             if (indep) {
                 e_a = A.e_old[x];
                 e_b = A.e_best[x];
@@ -549,6 +550,20 @@ void ApplyBuffers::release() {
     eval = eval2 = nullptr;
     dW = dA = nullptr;
     tmp = nullptr;
+}
+
+void launch_live(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {
+    if (S.ns == 0 || S.xhi <= S.xlo) return;
+    S.big = B.big;
+    S.nbig = B.nbig;
+    S.huge = B.big + B.big_cap;
+    S.nhuge = B.nbig + 1;
+    S.lcnt = nullptr;
+    S.dirty = nullptr;
+    S.chash = nullptr;
+    launch_pdl(k_stage_prep, grid_for((S.ns + 31) / 32 * 32, 256, 148 * 16), 256, 0, st, S);
+    launch_pdl(k_stage_live, APPLY_HB + APPLY_BB, 256, 0, st, S);
+    PLV_CUDA(cudaMemsetAsync(B.nbig, 0, 2 * sizeof(unsigned long long), st));
 }
 
 void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {

@@ -193,6 +193,11 @@ __device__ __forceinline__ int32_t live_comm(const StageArgs &A, int32_t j, int6
 // sizes are integers either way.
 __device__ __forceinline__ void mover_deltas(const StageArgs &A, int64_t x, int32_t i, int32_t a,
                                              int32_t b, double e_a, double e_b, bool integral) {
+    if (A.live_a) {  // live-only pass: the folds are the product
+        A.live_a[x] = e_a;
+        A.live_b[x] = e_b;
+        return;
+    }
     double sw = A.selfw[i], ki = A.k[i];
     double ta = dadd(dmul(2.0, e_a), dmul(2.0, sw));
     double tb = dadd(dmul(2.0, e_b), dmul(2.0, sw));

@@ -153,6 +153,11 @@ struct StageArgs {
     unsigned long long *chash = nullptr;  // cycle skipping: XOR hash of the assignment
     int64_t tree_n = 0;
     int tree_d0 = 0;
+    // live-only pass of a partitioned uncoloured stage (phase.cu): the live
+    // e_a / e_b of the movers at positions [xlo, xhi) go to live_a / live_b
+    // and nothing else is written (the replicated apply follows)
+    double *live_a = nullptr, *live_b = nullptr;
+    int64_t xlo = 0, xhi = 0;
 };
 
 // Event / sort scratch for stages of up to max_ns vertices.
@@ -175,6 +180,9 @@ struct ApplyBuffers {
 
 // Launch one stage's apply (no host synchronisation; capturable).
 void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st);
+// Live e_a / e_b of the movers at positions [S.xlo, S.xhi) into S.live_a / S.live_b
+// (a partitioned uncoloured stage; the rows of those movers must be present).
+void launch_live(StageArgs S, const ApplyBuffers &B, cudaStream_t st);
 
 template <class T>
 T *dalloc(size_t count) {

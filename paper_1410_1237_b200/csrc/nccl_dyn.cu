@@ -21,6 +21,8 @@ struct NcclApi {
                               cudaStream_t) = nullptr;
     ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t,
                               ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
     ncclResult_t (*groupStart)() = nullptr;
     ncclResult_t (*groupEnd)() = nullptr;
     const char *(*getErrorString)(ncclResult_t) = nullptr;
@@ -45,6 +47,7 @@ void load() {
     PLV_SYM(commDestroy, "ncclCommDestroy");
     PLV_SYM(broadcast, "ncclBroadcast");
     PLV_SYM(allReduce, "ncclAllReduce");
+    PLV_SYM(allGather, "ncclAllGather");
     PLV_SYM(groupStart, "ncclGroupStart");
     PLV_SYM(groupEnd, "ncclGroupEnd");
     PLV_SYM(getErrorString, "ncclGetErrorString");
@@ -73,6 +76,15 @@ void nccl_group_end() { nccl_check(api().groupEnd(), "ncclGroupEnd"); }
 void nccl_bcast_inplace(void *buf, size_t count, ncclDataType_t type, int root, void *comm,
                         cudaStream_t s) {
     nccl_check(api().broadcast(buf, buf, count, type, root, (ncclComm_t)comm, s), "ncclBroadcast");
+}
+
+void nccl_allgather_inplace(void *buf, size_t bytes_per_rank, int rank, void *comm,
+                            cudaStream_t s) {
+    const NcclApi &a = api();
+    if (!a.allGather) PLV_FAIL(PLV_ECUDA, "ncclAllGather is not available");
+    nccl_check(a.allGather((const char *)buf + (size_t)rank * bytes_per_rank, buf, bytes_per_rank,
+                           ncclUint8, (ncclComm_t)comm, s),
+               "ncclAllGather");
 }
 
 }  // namespace plv

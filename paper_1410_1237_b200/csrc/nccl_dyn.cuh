@@ -13,4 +13,8 @@ void nccl_group_end();
 void nccl_bcast_inplace(void *buf, size_t count, ncclDataType_t type, int root, void *comm,
                         cudaStream_t s);
 
+// In-place all-gather: rank r's bytes_per_rank bytes sit at buf + r * bytes_per_rank.
+void nccl_allgather_inplace(void *buf, size_t bytes_per_rank, int rank, void *comm,
+                            cudaStream_t s);
+
 }  // namespace plv

@@ -12,14 +12,19 @@
 // range [bounds[r], bounds[r+1]).  Stages list their vertices in ascending
 // id, so a rank's share of a stage is one contiguous slice and rank order is
 // subset order.  Per stage, every rank decides its slice only (the decide
-// plan covers the rank's slices), the slices' (target, moved, e_old, e_best)
-// are exchanged by one NCCL group of in-place broadcasts (root r sends slice
-// r), and every rank replays the whole stage's exact apply -- the replicated
-// assignment / a_tot / w_internal / sizes stay bit-identical on every rank and
-// to the single-GPU run.  The broadcasts are captured into the iteration's
-// graph with the kernels.  Without a communicator (world > 1, comm NULL) the
-// stages are stepped from the host (plv_phase_step) and the caller moves the
-// slices (the single-GPU test of the partitioned plan).
+// plan covers the rank's slices, and a rank may hold only its own rows), the
+// slices' (target, moved, e_old, e_best) are packed into 24-byte records and
+// exchanged by ONE in-place NCCL all-gather (slices padded to the stage's
+// largest), and every rank replays the whole stage's exact apply -- the
+// replicated assignment / a_tot / w_internal / sizes stay bit-identical on
+// every rank and to the single-GPU run.  An uncoloured stage needs the movers'
+// LIVE e_a / e_b, which only a row's owner can fold: after the first exchange
+// each rank folds its own movers' (launch_live), a second all-gather carries
+// them, and the apply runs on them as on a colour class.  The collectives are
+// captured into the iteration's graph with the kernels.  Without a
+// communicator (world > 1, comm NULL) the stages are stepped from the host
+// (plv_phase_step: decide, live, apply) and the caller moves the slices
+// (gloo in the tests).
 #include "localmove.cuh"
 #include "nccl_dyn.cuh"
 #include "pairwise.cuh"
@@ -67,6 +72,10 @@ struct Phase {
     std::vector<int64_t> slo;   // per stage: W + 1 slice bounds, relative to the stage
     int64_t rank = 0, world = 1;
     void *comm = nullptr;       // ncclComm_t (partitioned, captured exchange)
+    const int32_t *deg = nullptr;  // replicated degrees (partitioned rows: activity)
+    unsigned char *xbuf = nullptr;  // exchange records: world x (largest slice) x 24 B
+    std::vector<int64_t> xmax;      // per stage: largest slice
+    int64_t xcap = 0;               // largest slice of any stage
     bool own_out = true;        // decide outputs allocated here (else the caller's)
     Plan plan;
     ApplyBuffers ab;
@@ -136,7 +145,7 @@ struct Phase {
         fork = nullptr;
         plan.release();
         ab.release();
-        void *ps[] = {counters, q, mod_scratch, lvtx, fvtx, pos};
+        void *ps[] = {counters, q, mod_scratch, lvtx, fvtx, pos, xbuf};
         for (void *p : ps)
             pool_free(p);
         if (own_out) {
@@ -145,6 +154,7 @@ struct Phase {
                 pool_free(p);
         }
         lvtx = fvtx = pos = nullptr;
+        xbuf = nullptr;
         target = nullptr;
         moved = nullptr;
         e_old = e_best = nullptr;
@@ -173,23 +183,66 @@ static void record_decide(Phase &P, size_t a, cudaStream_t st) {
         PLV_CUDA(cudaEventRecordWithFlags(P.ev[2 * a + 1], st, cudaEventRecordExternal));
 }
 
-// Every rank's slice of stage a to every rank: one group of in-place
-// broadcasts per decide output (root r owns slice r).
+// Exchange record of one decided (or live-folded) stage position.
+struct XRec {
+    int32_t target;
+    int32_t moved;
+    double e_old, e_best;
+};
+
+__global__ void k_xpack(const int32_t *target, const uint8_t *moved, const double *e_old,
+                        const double *e_best, int64_t cnt, XRec *out) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < cnt;
+         t += (int64_t)gridDim.x * blockDim.x)
+        out[t] = XRec{target[t], (int32_t)moved[t], e_old[t], e_best[t]};
+}
+
+// every other rank's slice back to stage positions (sl: W + 1 slice bounds)
+__global__ void k_xunpack(const XRec *in, const int64_t *sl, int W, int rank, int64_t cmax,
+                          int32_t *target, uint8_t *moved, double *e_old, double *e_best) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < (int64_t)W * cmax;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(g / cmax);
+        const int64_t t = g - (int64_t)r * cmax;
+        if (r == rank || t >= sl[r + 1] - sl[r]) continue;
+        const XRec x = in[g];
+        const int64_t p = sl[r] + t;
+        target[p] = x.target;
+        moved[p] = (uint8_t)x.moved;
+        e_old[p] = x.e_old;
+        e_best[p] = x.e_best;
+    }
+}
+
+// Every rank's slice of stage a to every rank: pack this rank's slice, one
+// in-place all-gather of the padded slices, unpack the others.
 static void record_exchange(Phase &P, size_t a, cudaStream_t st) {
     if (!P.comm) return;  // (a 1-rank communicator still runs: the capture path)
     const int64_t *sl = P.slo.data() + a * (P.world + 1);
-    const int64_t g = P.goff[a];
-    nccl_group_start();
-    for (int64_t r = 0; r < P.world; r++) {
-        const int64_t o = g + sl[r], c = sl[r + 1] - sl[r];
-        if (!c) continue;
-        nccl_bcast_inplace(P.target + o, c, ncclInt32, (int)r, P.comm, st);
-        nccl_bcast_inplace(P.moved + o, c, ncclUint8, (int)r, P.comm, st);
-        nccl_bcast_inplace(P.e_old + o, c, ncclFloat64, (int)r, P.comm, st);
-        nccl_bcast_inplace(P.e_best + o, c, ncclFloat64, (int)r, P.comm, st);
+    const int64_t g = P.goff[a], cmax = P.xmax[a];
+    if (!cmax) return;
+    XRec *xb = (XRec *)P.xbuf;
+    const int64_t mine = sl[P.rank + 1] - sl[P.rank];
+    const int64_t o = g + sl[P.rank];
+    if (mine) {
+        k_xpack<<<grid_for(mine, 256), 256, 0, st>>>(P.target + o, P.moved + o, P.e_old + o,
+                                                     P.e_best + o, mine, xb + P.rank * cmax);
+        PLV_LAUNCH_CHECK();
     }
-    nccl_group_end();
+    nccl_allgather_inplace(xb, sizeof(XRec) * (size_t)cmax, (int)P.rank, P.comm, st);
+    if (P.world > 1) {
+        // slice bounds of this stage, relative to the stage, on device: kept
+        // in the tail of the exchange buffer (written once at creation)
+        const int64_t *dsl = (const int64_t *)(P.xbuf + sizeof(XRec) * P.world * P.xcap) + a * (P.world + 1);
+        k_xunpack<<<grid_for(P.world * cmax, 256), 256, 0, st>>>(
+            xb, dsl, (int)P.world, (int)P.rank, cmax, P.target + g, P.moved + g, P.e_old + g,
+            P.e_best + g);
+        PLV_LAUNCH_CHECK();
+    }
 }
+
+// Partitioned uncoloured stage: the live e_a / e_b of this rank's movers.
+static void record_live(Phase &P, size_t a, cudaStream_t st);
 
 // Stage a's exact apply over the whole stage (replicated on every rank).
 static StageArgs stage_args(const Phase &P, size_t a, uint8_t *dirty, unsigned long long *chash) {
@@ -205,9 +258,28 @@ static StageArgs stage_args(const Phase &P, size_t a, uint8_t *dirty, unsigned l
     return S;
 }
 
+// A partitioned uncoloured stage runs decide -> exchange -> live -> exchange
+// -> apply: its apply then uses the exchanged live e_a / e_b like a colour
+// class does its decide values.
+static bool live_mode(const Phase &P) {
+    return (P.world > 1 || P.comm) && !(P.flags & PLV_F_INDEPENDENT);
+}
+
 static void record_apply(Phase &P, size_t a, cudaStream_t st, uint8_t *dirty = nullptr,
                          unsigned long long *chash = nullptr) {
-    launch_apply(stage_args(P, a, dirty, chash), P.ab, st);
+    StageArgs S = stage_args(P, a, dirty, chash);
+    if (live_mode(P)) S.flags = (S.flags | PLV_F_INDEPENDENT) & ~PLV_F_IDENTITY;
+    launch_apply(S, P.ab, st);
+}
+
+static void record_live(Phase &P, size_t a, cudaStream_t st) {
+    StageArgs S = stage_args(P, a, nullptr, nullptr);
+    const int64_t *sl = P.slo.data() + a * (P.world + 1);
+    S.xlo = sl[P.rank];
+    S.xhi = sl[P.rank + 1];
+    S.live_a = P.e_old + P.goff[a];
+    S.live_b = P.e_best + P.goff[a];
+    launch_live(S, P.ab, st);
 }
 
 static void record_finish(Phase &P, cudaStream_t st) {
@@ -223,6 +295,10 @@ static void record_iteration(Phase &P, cudaStream_t st) {
         if (P.goff[a + 1] == P.goff[a]) continue;
         record_decide(P, a, st);
         record_exchange(P, a, st);
+        if (live_mode(P)) {
+            record_live(P, a, st);
+            record_exchange(P, a, st);
+        }
         record_apply(P, a, st);
     }
     record_finish(P, st);
@@ -252,12 +328,12 @@ __global__ void k_stage_slices(const int32_t *vtx, const int64_t *goff, int64_t 
 // A vertex whose row holds nothing but (at most) its self loop has no
 // candidate community: decide keeps it (PL/_kernels.pyx:77-95 with an empty
 // e_to) and apply has nothing to do, so stage lists keep only the others.
-__global__ void k_active_flags(const int64_t *off, const double *selfw, const int32_t *vtx,
-                               int64_t total, int32_t *flag) {
+__global__ void k_active_flags(const int64_t *off, const int32_t *deg, const double *selfw,
+                               const int32_t *vtx, int64_t total, int32_t *flag) {
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
          g += (int64_t)gridDim.x * blockDim.x) {
         const int32_t i = vtx[g];
-        const int64_t d = off[i + 1] - off[i] - (selfw[i] != 0.0 ? 1 : 0);
+        const int64_t d = (deg ? (int64_t)deg[i] : off[i + 1] - off[i]) - (selfw[i] != 0.0 ? 1 : 0);
         flag[g] = d > 0 ? 1 : 0;
     }
 }
@@ -291,7 +367,7 @@ static void filter_active(Phase &P, const int32_t *vtx, int64_t nst, cudaStream_
     const int64_t total = P.goff[nst];
     if (!total) return;
     Buf<int32_t> flag(total, s), scan(total, s);
-    k_active_flags<<<grid_for(total, 256), 256, 0, s>>>(P.off, P.selfw, vtx, total, flag);
+    k_active_flags<<<grid_for(total, 256), 256, 0, s>>>(P.off, P.deg, P.selfw, vtx, total, flag);
     PLV_LAUNCH_CHECK();
     size_t tb = 0;
     PLV_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag.get(), scan.get(), total, s));
@@ -359,9 +435,9 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
                            const int32_t *labels, const int64_t *stage_off_h, const int32_t *vtx,
                            int64_t nst, int32_t *assign, double *a_tot, double *w_int,
                            int32_t *sizes, int timing, int64_t rank, int64_t world,
-                           const int64_t *bounds_h, void *comm, int32_t *out_target,
-                           uint8_t *out_moved, double *out_e_old, double *out_e_best,
-                           cudaStream_t s) {
+                           const int64_t *bounds_h, void *comm, const int32_t *deg,
+                           int32_t *out_target, uint8_t *out_moved, double *out_e_old,
+                           double *out_e_best, cudaStream_t s) {
     Phase *P = new Phase();
     try {
         P->off = off;
@@ -381,6 +457,7 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
         P->rank = rank;
         P->world = world;
         P->comm = comm;
+        P->deg = deg;
         P->goff.assign(stage_off_h, stage_off_h + nst + 1);
         ensure_decide_attrs();
         filter_active(*P, vtx, nst, s);
@@ -427,6 +504,20 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
             }
         }
         plan_build(P->plan, off, P->lvtx, loff.data(), nst, n, s);
+        if (comm) {  // exchange records + the slice table on device
+            P->xmax.assign(nst, 0);
+            for (int64_t a = 0; a < nst; a++)
+                for (int64_t r = 0; r < world; r++) {
+                    const int64_t c = P->slo[a * (world + 1) + r + 1] - P->slo[a * (world + 1) + r];
+                    P->xmax[a] = c > P->xmax[a] ? c : P->xmax[a];
+                }
+            for (int64_t a = 0; a < nst; a++) P->xcap = P->xmax[a] > P->xcap ? P->xmax[a] : P->xcap;
+            const size_t rec = sizeof(XRec) * (size_t)world * (size_t)P->xcap;
+            P->xbuf = (unsigned char *)pool_alloc(rec + sizeof(int64_t) * P->slo.size());
+            if (!P->slo.empty())
+                PLV_CUDA(cudaMemcpyAsync(P->xbuf + rec, P->slo.data(), sizeof(int64_t) * P->slo.size(),
+                                         cudaMemcpyHostToDevice, s));
+        }
         int64_t max_large = 0;
         for (int64_t a = 0; a < nst; a++) {
             const int64_t ns = stage_off_h[a + 1] - stage_off_h[a];
@@ -789,18 +880,20 @@ extern "C" int plv_phase_create(const int64_t *off, const int32_t *nbr, const do
     int64_t b[2] = {0, n};
     *handle_h = plv::phase_create(off, nbr, wts, k, selfw, n, m, flags, labels, stage_off_h,
                                   stage_vtx, nstages, assign, a_tot, w_int, sizes, timing, 0, 1, b,
-                                  nullptr, nullptr, nullptr, nullptr, nullptr, plv::S(stream));
+                                  nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                  plv::S(stream));
     PLV_EXIT
 }
 
-extern "C" int plv_phase_create_part(const int64_t *off, const int32_t *nbr, const double *wts,
-                                     const double *k, const double *selfw, int64_t n, double m,
-                                     int flags, const int32_t *labels, const int64_t *stage_off_h,
-                                     const int32_t *stage_vtx, int64_t nstages, int32_t *assign,
-                                     double *a_tot, double *w_int, int32_t *sizes, int64_t rank,
-                                     int64_t world, const int64_t *bounds_h, void *comm,
-                                     int32_t *out_target, uint8_t *out_moved, double *out_e_old,
-                                     double *out_e_best, void **handle_h, void *stream) {
+static int phase_create_part(const int64_t *off, const int32_t *nbr, const double *wts,
+                             const double *k, const double *selfw, int64_t n, double m, int flags,
+                             const int32_t *labels, const int64_t *stage_off_h,
+                             const int32_t *stage_vtx, int64_t nstages, int32_t *assign,
+                             double *a_tot, double *w_int, int32_t *sizes, int64_t rank,
+                             int64_t world, const int64_t *bounds_h, void *comm,
+                             const int32_t *deg, int32_t *out_target, uint8_t *out_moved,
+                             double *out_e_old, double *out_e_best, void **handle_h,
+                             void *stream) {
     PLV_ENTRY
     if (!(m > 0.0)) PLV_FAIL(PLV_EINVAL, "modularity undefined for edgeless graph");
     if (world < 1 || rank < 0 || rank >= world) PLV_FAIL(PLV_EINVAL, "bad rank/world");
@@ -814,9 +907,38 @@ extern "C" int plv_phase_create_part(const int64_t *off, const int32_t *nbr, con
         PLV_FAIL(PLV_EINVAL, "decide outputs: all four or none");
     *handle_h = plv::phase_create(off, nbr, wts, k, selfw, n, m, flags, labels, stage_off_h,
                                   stage_vtx, nstages, assign, a_tot, w_int, sizes, 0, rank, world,
-                                  bounds_h, comm, out_target, out_moved, out_e_old, out_e_best,
+                                  bounds_h, comm, deg, out_target, out_moved, out_e_old, out_e_best,
                                   plv::S(stream));
     PLV_EXIT
+}
+
+extern "C" int plv_phase_create_part(const int64_t *off, const int32_t *nbr, const double *wts,
+                                     const double *k, const double *selfw, int64_t n, double m,
+                                     int flags, const int32_t *labels, const int64_t *stage_off_h,
+                                     const int32_t *stage_vtx, int64_t nstages, int32_t *assign,
+                                     double *a_tot, double *w_int, int32_t *sizes, int64_t rank,
+                                     int64_t world, const int64_t *bounds_h, void *comm,
+                                     int32_t *out_target, uint8_t *out_moved, double *out_e_old,
+                                     double *out_e_best, void **handle_h, void *stream) {
+    return phase_create_part(off, nbr, wts, k, selfw, n, m, flags, labels, stage_off_h,
+                             stage_vtx, nstages, assign, a_tot, w_int, sizes, rank, world,
+                             bounds_h, comm, nullptr, out_target, out_moved, out_e_old,
+                             out_e_best, handle_h, stream);
+}
+
+extern "C" int plv_phase_create_part2(const int64_t *off, const int32_t *nbr, const double *wts,
+                                      const double *k, const double *selfw, int64_t n, double m,
+                                      int flags, const int32_t *labels, const int64_t *stage_off_h,
+                                      const int32_t *stage_vtx, int64_t nstages, int32_t *assign,
+                                      double *a_tot, double *w_int, int32_t *sizes, int64_t rank,
+                                      int64_t world, const int64_t *bounds_h, void *comm,
+                                      const int32_t *deg, int32_t *out_target,
+                                      uint8_t *out_moved, double *out_e_old, double *out_e_best,
+                                      void **handle_h, void *stream) {
+    return phase_create_part(off, nbr, wts, k, selfw, n, m, flags, labels, stage_off_h,
+                             stage_vtx, nstages, assign, a_tot, w_int, sizes, rank, world,
+                             bounds_h, comm, deg, out_target, out_moved, out_e_old, out_e_best,
+                             handle_h, stream);
 }
 
 extern "C" int plv_phase_step(void *handle, int64_t stage, int op, double *q_h, int64_t *moves_h,
@@ -840,6 +962,9 @@ extern "C" int plv_phase_step(void *handle, int64_t stage, int op, double *q_h, 
                 plv::record_decide(*P, (size_t)stage, s);
             else if (op == PLV_STEP_APPLY)
                 plv::record_apply(*P, (size_t)stage, s);
+            else if (op == PLV_STEP_LIVE) {
+                if (plv::live_mode(*P)) plv::record_live(*P, (size_t)stage, s);
+            }
             else
                 PLV_FAIL(PLV_EINVAL, "unknown step op");
         }
