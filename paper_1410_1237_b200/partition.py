@@ -187,27 +187,45 @@ class PartGraph:
         return int(self.d_nbr.numel())
 
 
-def _route(du, dv, dw, bounds, ex: Exchange):
-    """Every record to the owner of each endpoint; received in global order."""
+ROUTE_CHUNK = 1 << 30  # records per routing call (plv_route_records takes < 2^31)
+
+
+def _route(du, dv, dw, bounds, ex: Exchange, chunk: int = ROUTE_CHUNK):
+    """Every record to the owner of each endpoint.  Returns the received
+    records in global order: per sender (rank order), that sender's records
+    in input order -- reassembled across routing chunks."""
     import torch
     R = int(du.numel())
     dev = du.device
     db = torch.from_numpy(np.ascontiguousarray(bounds, dtype=np.int64)).to(dev)
-    ou = torch.empty(max(2 * R, 1), dtype=torch.int32, device=dev)
-    ov = torch.empty_like(ou)
-    ow = torch.empty(max(2 * R, 1), dtype=torch.float64, device=dev)
-    cnt = _lib.i64_host(ex.world)
-    _lib.check(_lib.lib().route_records(_lib.ptr(du), _lib.ptr(dv), _lib.ptr(dw), R,
-                                        _lib.ptr(db), ex.world, _lib.ptr(ou), _lib.ptr(ov),
-                                        _lib.ptr(ow), 2 * R, _lib.hp(cnt), _lib.stream()),
-               "route_records")
-    sc = [int(cnt[r]) for r in range(ex.world)]
-    tot = sum(sc)
-    (ru, rv, rw), _ = ex.all_to_all_v([ou[:tot], ov[:tot], ow[:tot]], sc)
-    return ru, rv, rw
+    nchunks = max(1, ex.max_int(-(-R // chunk)))
+    per_src = [[] for _ in range(ex.world)]
+    for c in range(nchunks):
+        a, b = min(R, c * chunk), min(R, (c + 1) * chunk)
+        m = b - a
+        ou = torch.empty(max(2 * m, 1), dtype=torch.int32, device=dev)
+        ov = torch.empty_like(ou)
+        ow = torch.empty(max(2 * m, 1), dtype=torch.float64, device=dev)
+        cnt = _lib.i64_host(ex.world)
+        _lib.check(_lib.lib().route_records(_lib.ptr(du) + 4 * a if m else None,
+                                            _lib.ptr(dv) + 4 * a if m else None,
+                                            _lib.ptr(dw) + 8 * a if m else None, m,
+                                            _lib.ptr(db), ex.world, _lib.ptr(ou), _lib.ptr(ov),
+                                            _lib.ptr(ow), 2 * m, _lib.hp(cnt), _lib.stream()),
+                   "route_records")
+        sc = [int(cnt[r]) for r in range(ex.world)]
+        tot = sum(sc)
+        (ru, rv, rw), recv = ex.all_to_all_v([ou[:tot], ov[:tot], ow[:tot]], sc)
+        o = 0
+        for src, k in enumerate(recv):
+            per_src[src].append((ru[o:o + k], rv[o:o + k], rw[o:o + k]))
+            o += k
+    cat = lambda i: torch.cat([x[i] for src in per_src for x in src])  # noqa: E731
+    return cat(0), cat(1), cat(2)
 
 
-def from_records_part(segments, n: int, bounds, ex: Exchange, count_merges=True) -> PartGraph:
+def from_records_part(segments, n: int, bounds, ex: Exchange, count_merges=True,
+                      chunk: int = ROUTE_CHUNK) -> PartGraph:
     """Graph.from_edges (PL/graph.py:88-147) over the records of all ranks,
     this rank keeping its rows.  `segments`: list of (u, v, w) device tensors;
     the global record order is segment 0 of every rank (rank order), then
@@ -215,7 +233,7 @@ def from_records_part(segments, n: int, bounds, ex: Exchange, count_merges=True)
     import torch
     from .graph import Graph
     bounds = np.ascontiguousarray(bounds, dtype=np.int64)
-    parts = [_route(u, v, w, bounds, ex) for (u, v, w) in segments]
+    parts = [_route(u, v, w, bounds, ex, chunk) for (u, v, w) in segments]
     ru = torch.cat([p[0] for p in parts])
     rv = torch.cat([p[1] for p in parts])
     rw = torch.cat([p[2] for p in parts])
@@ -283,10 +301,10 @@ def rmat_part(scale: int, ex: Exchange, edge_factor: int = 16, seed: int = 0,
     return u[:k], v[:k], w[:k], 1 << scale
 
 
-def rmat_graph_part(scale: int, ex: Exchange, **kw) -> PartGraph:
+def rmat_graph_part(scale: int, ex: Exchange, chunk: int = ROUTE_CHUNK, **kw) -> PartGraph:
     u, v, w, n = rmat_part(scale, ex, **kw)
     bounds = balanced_bounds(u, v, n, ex)
-    return from_records_part([(u, v, w)], n, bounds, ex)
+    return from_records_part([(u, v, w)], n, bounds, ex, chunk=chunk)
 
 
 # ---------------------------------------------------------- vertex following

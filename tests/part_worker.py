@@ -4,7 +4,7 @@ pipeline (paper_1410_1237_b200.partition) on cuda:0, exchanging over gloo."""
 import os
 
 
-def worker(rank, world, port, scale, cfg_kw, out):
+def worker(rank, world, port, scale, cfg_kw, out, chunk=1 << 30, nccl=False):
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -15,7 +15,7 @@ def worker(rank, world, port, scale, cfg_kw, out):
         import paper_1410_1237_b200 as pl
         from paper_1410_1237_b200 import partition as P
         ex = P.Exchange()
-        g = P.rmat_graph_part(scale, ex, edge_factor=8, seed=5)
+        g = P.rmat_graph_part(scale, ex, chunk=chunk, edge_factor=8, seed=5)
         rows = dict(off=g.d_off.cpu().numpy(), nbr=g.d_nbr.cpu().numpy(),
                     w=g.d_w.cpu().numpy(), k=g.d_k.cpu().numpy(),
                     selfw=g.d_selfw.cpu().numpy(), deg=g.d_deg.cpu().numpy(),
@@ -24,7 +24,13 @@ def worker(rank, world, port, scale, cfg_kw, out):
                     bounds=np.asarray(g.bounds), lo=g.lo, hi=g.hi)
         vf = P.vf_compact_part(g, ex)
         col = P.color_part(vf.graph, ex)
-        h = P.run_part(g, ex, pl.RunConfig(**cfg_kw))
+        comm = None
+        if nccl:  # the captured-graph path: one rank, a 1-rank NCCL communicator
+            from paper_1410_1237_b200 import dist as pdist
+            comm = pdist.nccl_communicator(rank, world)
+        h = P.run_part(g, ex, pl.RunConfig(**cfg_kw), comm=comm)
+        if comm is not None:
+            pdist.destroy_communicator(comm)
         out.put((rank, dict(rows=rows, vmap=vf.vertex_map.cpu().numpy(),
                             colors=col.colors.copy(),
                             assign=h.final_assignment.cpu().numpy(), q=h.final_modularity,

@@ -31,13 +31,14 @@ def _free_port():
     return port
 
 
-def _run(world, scale, cfg_kw):
+def _run(world, scale, cfg_kw, chunk=1 << 30, nccl=False):
     import torch.multiprocessing as mp
     import part_worker
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=part_worker.worker, args=(r, world, port, scale, cfg_kw, q))
+    procs = [ctx.Process(target=part_worker.worker,
+                         args=(r, world, port, scale, cfg_kw, q, chunk, nccl))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -58,12 +59,17 @@ def _whole(scale):
     return pl.Graph.from_device_records(u, v, w, n)
 
 
-@pytest.mark.parametrize("world,cfg", [(2, "colored"), (3, "colored"), (2, "uncolored")])
-def test_partitioned_pipeline(world, cfg):
+@pytest.mark.parametrize("world,cfg,chunk,nccl", [
+    (2, "colored", 1 << 30, False), (3, "colored", 7919, False), (2, "uncolored", 1 << 30, False),
+    (1, "colored", 1 << 30, True), (1, "uncolored", 1 << 30, True)])
+def test_partitioned_pipeline(world, cfg, chunk, nccl):
+    """W gloo ranks (host-stepped stages), or one rank with a 1-rank NCCL
+    communicator (the iteration graph with its captured all-gathers and, for
+    uncoloured phases, the live folds); chunk: records per routing call."""
     scale = 13
     cfg_kw = (dict(color_cutoff=0, max_iterations_per_phase=200) if cfg == "colored"
               else dict(use_coloring=False, max_iterations_per_phase=200))
-    res = _run(world, scale, cfg_kw)
+    res = _run(world, scale, cfg_kw, chunk, nccl)
     g = _whole(scale)
     off, nbr, w = g.adjacency_offsets, g.neighbors, g.weights
     for r in range(world):
