@@ -37,6 +37,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -59,7 +60,8 @@ def _args():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--scale", type=int, default=CONFIG["scale"], help="R-MAT scale (c2 config)")
+    p.add_argument("--scale", type=int, default=None,
+                   help="R-MAT scale (c2 config; N > 1: default 25 + log2 N)")
     p.add_argument("--config", default="c4_chung_lu",
                    choices=["c1_sbm", "c2_rmat20", "c3_grid", "c4_chung_lu"],
                    help="BASELINE config to run (default: config 4, the largest that fits "
@@ -68,8 +70,14 @@ def _args():
     p.add_argument("--no-louvain", action="store_true", help="skip the full run() timing")
     p.add_argument("--mode", choices=["colored", "uncolored"], default="colored")
     p.add_argument("--partitioned", action="store_true",
-                   help="use the partitioned (NCCL) engine even on one rank (plumbing check)")
-    return p.parse_args()
+                   help="under torchrun with one rank: the partitioned pipeline (1-rank NCCL)")
+    p.add_argument("--partitioned-replicated", action="store_true",
+                   help="N > 1: the older replicated-CSR partitioned engine on the config graph")
+    a = p.parse_args()
+    a.scale_set = a.scale is not None
+    if a.scale is None:
+        a.scale = CONFIG["scale"]
+    return a
 
 
 def _dist():
@@ -394,16 +402,157 @@ def run_reference(args):
 
 # ------------------------------------------------------------------ ours
 
+def run_partitioned(args):
+    """N > 1 ranks: the 1D vertex-partitioned pipeline (paper_1410_1237_b200.
+    partition) on R-MAT scale 25 + log2 N (weak scaling: N = 8 is config 5,
+    R-MAT s28; --scale overrides).  Each rank generates 1/N of the record
+    draws, owns 1/N of the rows (entry-balanced ranges) and holds the
+    replicated state; construction, VF and colouring run partitioned; one
+    step = one phase-1 coloured local-move iteration (every colour class:
+    decide own slice, one NCCL all-gather of the slices, replicated exact
+    apply), timed with CUDA events, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    import paper_1410_1237_b200 as pl
+    from paper_1410_1237_b200 import partition as P
+    from paper_1410_1237_b200 import dist as pdist
+    ws, rank, local = _dist()
+    dev = torch.device("cuda", local)
+    ex = P.Exchange()
+    scale = args.scale if args.scale_set else 25 + int(round(math.log2(ws)))
+    comm = pdist.nccl_communicator(rank, ws)
+
+    def tmax(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g0 = P.rmat_graph_part(scale, ex, edge_factor=CONFIG["edge_factor"], seed=CONFIG["seed"])
+    torch.cuda.synchronize()
+    t_build = tmax(time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    vf = P.vf_compact_part(g0, ex)
+    g = vf.graph
+    del g0
+    col = P.color_part(g, ex)
+    torch.cuda.synchronize()
+    t_vfcol = tmax(time.perf_counter() - t0)
+    s0 = P.singleton_state_part(g)
+    d0 = s0.device()
+    st = {k: (t.clone() if t is not None else None) for k, t in d0.items()}
+    state = pl.CommunityState.from_device(st["assignment"], st["a_tot"], st["w_internal"],
+                                          st["sizes"])
+    eng = P.PartEngine(g, state, col, ex, comm=comm)
+
+    def reset():
+        for k in ("assignment", "a_tot", "w_internal", "sizes"):
+            st[k].copy_(d0[k])
+
+    def step():
+        reset()
+        return eng.iterate()
+
+    for _ in range(args.warmup):
+        step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    with ClockSampler(local) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            q, moves, cand = step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = tmax(ev0.elapsed_time(ev1)) / args.steps
+    M = g.num_edges
+    value = M / (ms / 1e3)
+    reset()
+    torch.cuda.synchronize()
+    dm, span, cand = _cupti_decide_ms(eng.iterate)
+    dm = tmax(dm)
+    n = g.num_vertices
+    nnz_own = g.nnz_local
+    own = g.hi - g.lo
+    decide_bytes = 41 * own + 16 * nnz_own + 8 * cand
+    peak, peak_kind = _peak_hbm()
+    achieved = decide_bytes / (dm / 1e3) / 1e9 if dm > 0 else 0.0
+    # e2e: the step's input state from pinned host memory, the assignment back
+    h = {k: torch.empty(d0[k].shape, dtype=d0[k].dtype, pin_memory=True)
+         for k in ("assignment", "a_tot", "w_internal", "sizes")}
+    for k in h:
+        h[k].copy_(d0[k].cpu())
+    o_assign = torch.empty(n, dtype=torch.int32, pin_memory=True)
+
+    def e2e_step():
+        for k in h:
+            st[k].copy_(h[k], non_blocking=True)
+        eng.iterate()
+        o_assign.copy_(st["assignment"], non_blocking=True)
+        stream.synchronize()
+
+    e2e_step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = tmax(e0.elapsed_time(e1)) / args.steps
+    launches = eng.graph_kernels() * args.steps
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (counter-based R-MAT, generated on device, 1/N of the draws "
+                    "per rank)",
+            "config": {"workload": f"rmat_s{scale} phase-1 colored local-move iteration "
+                                   f"(1D vertex partition over {ws} ranks)",
+                       "graph": {"n": n, "M": M, "colours": col.num_colors,
+                                 "nnz_rank0": nnz_own, "bounds": [int(b) for b in g.bounds]},
+                       "parallelism": f"vertex-partition{ws} (NCCL all-gather of the decided "
+                                      f"slices per colour class, replicated exact apply)",
+                       "construction_seconds": t_build, "vf_coloring_seconds": t_vfcol,
+                       "l2": "inputs larger than L2"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "decide (tiers 0-4), rank 0's slices",
+                         "bytes_per_iter": decide_bytes, "ms_per_iter": dm,
+                         "timing": "union of decide-kernel intervals (CUPTI), max over ranks"},
+            "iteration": {"q": q, "moves": moves},
+            "cpu_baseline": None,
+            "e2e": {"value": M / (e2e_ms / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": 4 * n},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    pdist.destroy_communicator(comm)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
-    if ws > 1:
+    if ws > 1 or (args.partitioned and "WORLD_SIZE" in os.environ):
         from paper_1410_1237_b200.dist import stdout_to_stderr
         with stdout_to_stderr():  # NCCL's banner must not share stdout with the JSON line
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
             dist.barrier()
+        if not args.partitioned_replicated:
+            run_partitioned(args)
+            dist.destroy_process_group()
+            return
     import paper_1410_1237_b200 as pl
     from paper_1410_1237_b200 import _lib, synthetic as syn
     from paper_1410_1237_b200.engine import PhaseEngine
