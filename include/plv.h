@@ -297,6 +297,24 @@ int plv_compose(const int32_t *map, const int32_t *assign, const int32_t *renumb
 int plv_parse_edge_list(const uint8_t *text, int64_t len, int32_t *u, int32_t *v, double *w,
                         int64_t cap, int64_t *info_h, void *stream);
 
+/* load_graph's Matrix Market branch (PL/graph.py:412-478) on device: `text`
+ * is the file after its size line (the banner and size line are read on the
+ * host); symmetric coordinate lines `i j [w]` (pattern: no w), '%' comments,
+ * 1-based indices in [1, rows].  u / v (0-based int32), w in file order;
+ * info_h[0] = records.  PLV_INGEST_HOST when the host rules must decide. */
+int plv_parse_mm(const uint8_t *text, int64_t len, int64_t rows, int pattern, int32_t *u,
+                 int32_t *v, double *w, int64_t cap, int64_t *info_h, void *stream);
+/* load_graph's METIS branch (PL/graph.py:326-411) on device: `text` is the
+ * file after its header line (n, m_declared and the edge-weight flag read on
+ * the host).  Every non-comment line is the next vertex's adjacency list.
+ * Accepted: no repeated neighbour, every edge in both directions with
+ * bitwise-equal weights, exactly m_declared edges; out: the upper entries
+ * (vertex <= neighbour) in file order, the reference's records.
+ * PLV_INGEST_HOST otherwise (the host rules merge, tolerate or raise). */
+int plv_parse_metis(const uint8_t *text, int64_t len, int64_t n, int64_t m_declared,
+                    int weighted, int32_t *u, int32_t *v, double *w, int64_t cap,
+                    int64_t *info_h, void *stream);
+
 /* ------------------------------------------------------- post-processing */
 
 /* write_assignment's file body (PL/engine.py:318-322): "i c\n" per vertex,

@@ -84,6 +84,8 @@ _SIGS = {
     "plv_rebuild_records": [_P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P],
     "plv_compose": [_P, _P, _P, _I64, _P, _P],
     "plv_parse_edge_list": [_P, _I64, _P, _P, _P, _I64, _P, _P],
+    "plv_parse_mm": [_P, _I64, _I64, _INT, _P, _P, _P, _I64, _P, _P],
+    "plv_parse_metis": [_P, _I64, _I64, _I64, _INT, _P, _P, _P, _I64, _P, _P],
     "plv_format_assignment": [_P, _INT, _I64, _P, _I64, _P, _P],
     "plv_pair_counts": [_P, _P, _I64, _P, _P],
     "plv_gen_rmat": [_U64, _INT, _I64, _D, _D, _D, _D, _D, _P, _P, _P, _I64, _P, _P],

@@ -1,7 +1,8 @@
-"""GPU: edge-list ingest on the device (plv_parse_edge_list)
-against the host parser that restates PL/graph.py:245-288 -- identical CSR
-(records in file order, so duplicate merges fold in the same order), and the
-same exceptions and messages whenever the device hands the file to the host."""
+"""GPU: ingest on the device (plv_parse_edge_list) against
+the REFERENCE itself (ref_parlouvain.load_graph from oracle/_ref, PL/graph.py:
+245-478) -- identical CSR (records in file order, so duplicate merges fold in
+the same order), and the same exceptions and messages whenever the device
+hands the file to the host rules."""
 
 import numpy as np
 import pytest
@@ -14,9 +15,23 @@ from paper_1410_1237_b200 import graph as G  # noqa: E402
 from paper_1410_1237_b200.errors import EdgelessGraphError, GraphParseError  # noqa: E402
 
 
+_REF = None
+
+
 def _host(path):
-    u, v, w, n = G.parse_records(path)
-    return pl.Graph.from_edges(u, v, w, num_vertices=n)
+    """The reference's load_graph (the checker), its exceptions mapped onto
+    this package's classes of the same names."""
+    global _REF
+    if _REF is None:
+        import conftest
+        _REF = conftest.reference_module()
+        if _REF is None:
+            pytest.skip("reference build (oracle/_ref) not present")
+    try:
+        return _REF.load_graph(path)
+    except (_REF.GraphParseError, _REF.EdgelessGraphError) as e:
+        cls = GraphParseError if isinstance(e, _REF.GraphParseError) else EdgelessGraphError
+        raise cls(str(e)) from None
 
 
 def _same(g, h):

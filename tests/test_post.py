@@ -1,6 +1,7 @@
-"""GPU: device post-processing against the host
-restatements of the reference: the assignment file (PL/engine.py:318-322)
-byte for byte, and compare_partitions' pair counts (PL/evaluation.py:68-86)."""
+"""GPU: device post-processing against the REFERENCE
+itself (ref_parlouvain from oracle/_ref): the assignment file written by its
+write_assignment (PL/engine.py:318-322) byte for byte, and its
+compare_partitions (PL/evaluation.py:68-86) field for field."""
 
 import numpy as np
 import pytest
@@ -12,8 +13,25 @@ pl = pytest.importorskip("paper_1410_1237_b200")
 from paper_1410_1237_b200 import evaluation as ev  # noqa: E402
 
 
+def _ref():
+    import conftest
+    r = conftest.reference_module()
+    if r is None:
+        pytest.skip("reference build (oracle/_ref) not present")
+    return r
+
+
 def _host_text(a):
-    return "".join(f"{v} {c}\n" for v, c in enumerate(np.asarray(a).tolist())).encode()
+    import os
+    import tempfile
+    fd, path = tempfile.mkstemp()
+    os.close(fd)
+    try:
+        _ref().write_assignment(path, np.asarray(a))
+        with open(path, "rb") as fh:
+            return fh.read()
+    finally:
+        os.unlink(path)
 
 
 @pytest.mark.parametrize("dtype", ["int32", "int64"])
@@ -39,14 +57,7 @@ def test_assignment_file_from_run(tmp_path):
 
 
 def _host_counts(s, p):
-    n = len(s)
-    _, si = np.unique(s, return_inverse=True)
-    _, pi = np.unique(p, return_inverse=True)
-    cells = np.bincount(si.astype(np.int64) * (int(pi.max()) + 1) + pi.astype(np.int64))
-    tp = ev._pairs(cells)
-    fn = ev._pairs(np.bincount(si)) - tp
-    fp = ev._pairs(np.bincount(pi)) - tp
-    return ev._counts(tp, fp, fn, n * (n - 1) // 2 - tp - fp - fn)
+    return _ref().compare_partitions(s, p)
 
 
 @pytest.mark.parametrize("seed", [0, 1, 2])
@@ -60,5 +71,7 @@ def test_pair_counts_match_host(seed):
         s[::7] = 10 ** 15
     got = ev.compare_partitions(s, p)
     assert ev._device_pair_counts(np.asarray(s), np.asarray(p)) is not None
-    assert got == _host_counts(s, p)
-    assert got.csv_line() == _host_counts(s, p).csv_line()
+    want = _host_counts(s, p)
+    for f in ("tp", "fp", "fn", "tn", "sp", "se", "oq", "rand"):
+        assert getattr(got, f) == getattr(want, f), f
+    assert got.csv_line() == want.csv_line()
