@@ -612,8 +612,10 @@ static int parse_metis(const uint8_t *text, int64_t len, int64_t n, int64_t m_de
     // the upper entries in file order
     if ((int64_t)c[0] > cap) PLV_FAIL(PLV_EINVAL, "record buffer too small");
     Buf<int> nu(1, s);
-    size_t t7 = 0;
+    size_t t7 = 0, t8 = 0;
     PLV_CUDA(cub::DeviceSelect::Flagged(nullptr, t7, ea.get(), up.get(), u32, nu.get(), E, s));
+    PLV_CUDA(cub::DeviceSelect::Flagged(nullptr, t8, ew.get(), up.get(), wout, nu.get(), E, s));
+    t7 = t7 > t8 ? t7 : t8;
     Buf<char> tmp7(t7, s);
     PLV_CUDA(cub::DeviceSelect::Flagged(tmp7.get(), t7, ea.get(), up.get(), u32, nu.get(), E, s));
     PLV_CUDA(cub::DeviceSelect::Flagged(tmp7.get(), t7, eb.get(), up.get(), v32, nu.get(), E, s));
