@@ -730,7 +730,11 @@ static void build_run_graph(Phase &P, int64_t cap, cudaStream_t s) {
         P.dirty = dalloc<uint8_t>((size_t)1 << P.mod_d0);
         PLV_CUDA(cudaMemsetAsync(P.dirty, 0, (size_t)1 << P.mod_d0, s));
     }
-    if (nonempty == 1 && !(P.flags & PLV_F_INDEPENDENT) && (P.flags & PLV_F_INTEGRAL)) {
+#ifndef PLV_CYCLE_FLOAT
+#define PLV_CYCLE_FLOAT 0
+#endif
+    if (nonempty == 1 && !(P.flags & PLV_F_INDEPENDENT) &&
+        ((P.flags & PLV_F_INTEGRAL) || PLV_CYCLE_FLOAT)) {
         P.chash = dalloc<unsigned long long>(1);
         P.snap_i = dalloc<int32_t>(2 * P.n);
         P.snap_d = dalloc<double>(2 * P.n);
