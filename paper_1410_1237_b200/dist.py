@@ -175,6 +175,7 @@ class PartitionedPhaseEngine:
             self.stage_off = np.array([0, n], dtype=np.int64)
             self.vtx = torch.arange(n, dtype=torch.int32, device=dev)
             flags = _lib.F_IDENTITY
+        self.independent = coloring is not None
         if g.integral:
             flags |= _lib.F_INTEGRAL
         self.nstages = len(self.stage_off) - 1
@@ -261,11 +262,7 @@ def stepped_iteration(engines):
     sl = [e.slices() for e in engines]
     off = engines[0].engine_stage_off()
     W = len(engines)
-    for a in range(engines[0].nstages):
-        if off[a + 1] == off[a]:
-            continue
-        for e in engines:
-            e.step(a, _lib.STEP_DECIDE)
+    def exchange(a):
         for r in range(W):
             lo, hi = int(off[a] + sl[r][a][r]), int(off[a] + sl[r][a][r + 1])
             if hi == lo:
@@ -274,6 +271,18 @@ def stepped_iteration(engines):
                 if q != r:
                     for key in ("target", "moved", "e_old", "e_best"):
                         engines[q].outputs[key][lo:hi].copy_(engines[r].outputs[key][lo:hi])
+
+    live = W > 1 and not engines[0].independent
+    for a in range(engines[0].nstages):
+        if off[a + 1] == off[a]:
+            continue
+        for e in engines:
+            e.step(a, _lib.STEP_DECIDE)
+        exchange(a)
+        if live:  # uncoloured: each row owner folds its movers' live e_a / e_b
+            for e in engines:
+                e.step(a, _lib.STEP_LIVE)
+            exchange(a)
         for e in engines:
             e.step(a, _lib.STEP_APPLY)
     return [e.finish() for e in engines]
