@@ -874,7 +874,12 @@ void color(const int64_t *off, const int32_t *nbr, int64_t n, int32_t *colors, i
 __global__ void k_class_count(const int32_t *colors, int64_t n, int32_t *cnt) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(cnt + colors[i], 1);
+    {
+        // one atomic per (warp, colour): colour 0 holds most vertices
+        const int32_t c = colors[i];
+        const unsigned grp = __match_any_sync(__activemask(), c);
+        if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(cnt + c, __popc(grp));
+    }
 }
 
 void color_classes(const int32_t *colors, int64_t n, int64_t nc, int64_t *class_off,

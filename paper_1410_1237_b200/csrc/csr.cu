@@ -146,18 +146,31 @@ __global__ void k_decode_runs(const uint64_t *key, const int64_t *starts, int64_
     }
 }
 
+// a[] is sorted: a row's forward records are one run, counted once by the
+// run's last record (a hub's run would otherwise serialise its atomics on one
+// counter); reversed records are counted per record.
 __global__ void k_count_rows(const int32_t *a, const int32_t *b, int64_t M, int32_t *deg,
                              int32_t *nrev, uint8_t *nonself, int32_t *fstart) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < M;
          t += (int64_t)gridDim.x * blockDim.x) {
         int32_t x = a[t], y = b[t];
-        atomicAdd(deg + x, 1);
+        if (t == M - 1 || a[t + 1] != x) {
+            int64_t lo = 0, hi = t;  // first record of the run
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (a[mid] < x)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            atomicAdd(deg + x, (int32_t)(t - lo + 1));
+            fstart[x] = (int32_t)lo;
+        }
         if (x != y) {
             atomicAdd(deg + y, 1);
             atomicAdd(nrev + y, 1);
         }
         nonself[t] = (x != y);
-        if (t == 0 || a[t - 1] != x) fstart[x] = (int32_t)t;
     }
 }
 
@@ -198,26 +211,55 @@ __global__ void k_place_reverse(const int32_t *bkey, const int32_t *tidx, int64_
 constexpr int64_t DEG_LONG = 256;  // longer rows are folded by a whole block
 
 __global__ void k_degrees(const int64_t *off, const double *wts, const double *selfw, int64_t n,
-                          double *k) {
+                          double *k, int32_t *longs, unsigned long long *nlong) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         int64_t e0 = off[i], e1 = off[i + 1];
-        if (e1 - e0 > DEG_LONG) continue;
+        if (e1 - e0 > DEG_LONG) {  // listed for k_degrees_long
+            longs[atomicAdd(nlong, 1ull)] = (int32_t)i;
+            continue;
+        }
         double acc = 0.0;
         for (int64_t e = e0; e < e1; e++) acc = __dadd_rn(acc, wts[e]);
         k[i] = __dadd_rn(acc, selfw[i]);
     }
 }
 
+// A long row's fold.  When every weight of the graph is an integer (stats[2]
+// == 0, k_integral_check ran first) all partial sums of the row are integers
+// below the row total, so a parallel tree is exact -- and equal to the
+// sequential fold -- whenever its total is below 2^53 (a total at or above it
+// cannot come out below, rounding being monotone); otherwise, and for
+// non-integral graphs, the ordered block fold.
 __global__ void __launch_bounds__(256) k_degrees_long(const int64_t *off, const double *wts,
-                                                     const double *selfw, int64_t n, double *k) {
+                                                     const double *selfw, const int32_t *longs,
+                                                     const unsigned long long *nlong, double *k,
+                                                     const unsigned long long *stats) {
     __shared__ double sb[2 * FOLD_CH];
-    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    typedef cub::BlockReduce<double, 256> BR;
+    __shared__ typename BR::TempStorage red;
+    __shared__ double s_tot;
+    const bool integral = stats[2] == 0;
+    const int64_t nl = (int64_t)*nlong;
+    for (int64_t q = blockIdx.x; q < nl; q += gridDim.x) {
+        const int64_t i = longs[q];
         const int64_t e0 = off[i], len = off[i + 1] - e0;
-        if (len <= DEG_LONG) continue;
-        double acc = block_fold([=] __device__(int64_t t) { return wts[e0 + t]; }, len, 0.0, sb);
-        if (threadIdx.x == 0) k[i] = __dadd_rn(acc, selfw[i]);
-        __syncthreads();
+        bool done = false;
+        if (integral) {
+            double part = 0.0;
+            for (int64_t t = threadIdx.x; t < len; t += 256) part = __dadd_rn(part, wts[e0 + t]);
+            const double tot = BR(red).Sum(part);
+            if (threadIdx.x == 0) s_tot = tot;
+            __syncthreads();
+            done = s_tot < 9007199254740992.0;
+            if (done && threadIdx.x == 0) k[i] = __dadd_rn(s_tot, selfw[i]);
+            __syncthreads();
+        }
+        if (!done) {
+            double acc = block_fold([=] __device__(int64_t t) { return wts[e0 + t]; }, len, 0.0, sb);
+            if (threadIdx.x == 0) k[i] = __dadd_rn(acc, selfw[i]);
+            __syncthreads();
+        }
     }
 }
 
@@ -288,20 +330,23 @@ void csr_from_merged(const int32_t *a, const int32_t *b, const double *w, int64_
             PLV_LAUNCH_CHECK();
         }
     }
-    if (n > 0) {
-        k_degrees<<<grid_for(n, 128), 128, 0, s>>>(off, wts, selfw, n, k);
-        PLV_LAUNCH_CHECK();
-        k_degrees_long<<<148 * 4, 256, 0, s>>>(off, wts, selfw, n, k);
-        PLV_LAUNCH_CHECK();
-    }
     Buf<unsigned long long> stats(3, s);
     PLV_CUDA(cudaMemsetAsync(stats.get(), 0, sizeof(unsigned long long) * 3, s));
-    if (n > 0) {
-        k_graph_stats<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(off, selfw, n, stats);
-        PLV_LAUNCH_CHECK();
-    }
     if (M > 0) {
         k_integral_check<<<grid_for(M, 256), 256, 0, s>>>(w, M, stats);
+        PLV_LAUNCH_CHECK();
+    }
+    if (n > 0) {
+        // rows longer than DEG_LONG: listed by k_degrees, a block each
+        const int64_t lcap = 2 * M / DEG_LONG + 2;  // nnz <= 2M
+        Buf<int32_t> longs(lcap, s);
+        Buf<unsigned long long> nlong(1, s);
+        PLV_CUDA(cudaMemsetAsync(nlong.get(), 0, sizeof(unsigned long long), s));
+        k_degrees<<<grid_for(n, 128), 128, 0, s>>>(off, wts, selfw, n, k, longs, nlong);
+        PLV_LAUNCH_CHECK();
+        k_degrees_long<<<148 * 4, 256, 0, s>>>(off, wts, selfw, longs, nlong, k, stats.get());
+        PLV_LAUNCH_CHECK();
+        k_graph_stats<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(off, selfw, n, stats);
         PLV_LAUNCH_CHECK();
     }
     Buf<double> msum(2, s);

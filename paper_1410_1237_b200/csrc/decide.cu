@@ -1251,7 +1251,10 @@ __global__ void k_tier_keys(const int64_t *off, const int32_t *vtx, const int64_
                                      : 4;
         uint32_t kk = (uint32_t)(a * NTIER + t);
         key[g] = kk;
-        atomicAdd(hist + kk, 1ull);
+        // one atomic per (warp, bucket): a stage's tier-0 bucket takes millions
+        const unsigned act = __activemask();
+        const unsigned grp = __match_any_sync(act, kk);
+        if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(hist + kk, (unsigned long long)__popc(grp));
     }
 }
 

@@ -243,8 +243,11 @@ void modularity_async_inc(const double *w_int, const double *a_tot, int64_t n, d
 
 constexpr int64_t SEG_SERIAL_MAX = 4096;
 
+constexpr int64_t SEG_BLOCK_NODES = 4096;  // mid segments: <= 4096 depth-d0 nodes, one block
+
 __global__ void k_reduceat_short(const double *__restrict__ w, const int64_t *__restrict__ starts,
-                                 int64_t M, int64_t R, double *out, int64_t *long_list,
+                                 int64_t M, int64_t R, double *out, int64_t *mid_list,
+                                 unsigned long long *mid_cnt, int64_t *long_list,
                                  unsigned long long *long_cnt) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < M;
          t += (int64_t)gridDim.x * blockDim.x) {
@@ -255,10 +258,76 @@ __global__ void k_reduceat_short(const double *__restrict__ w, const int64_t *__
             out[t] = w[st];
         } else if (len - 1 <= SEG_SERIAL_MAX) {
             out[t] = __dadd_rn(w[st], pw_serial(w + st + 1, len - 1, Ident{}));
+        } else if (len - 1 <= SEG_BLOCK_NODES * 128) {
+            mid_list[atomicAdd(mid_cnt, 1ull)] = t;
         } else {
-            unsigned long long p = atomicAdd(long_cnt, 1ull);
-            long_list[p] = t;
+            long_list[atomicAdd(long_cnt, 1ull)] = t;
         }
+    }
+}
+
+// Depth at which every node of the pairwise tree of n has <= 256 elements,
+// with no leaf above it (pw_depth on device: the largest node of a depth is
+// the repeated right half, the smallest the repeated left half); -1 if a leaf
+// sits above it (the host path decides then).
+__device__ __forceinline__ int pw_depth_dev(int64_t n) {
+    int64_t mx = n, mn = n;
+    int d = 0;
+    while (mx > 256) {
+        if (mn <= 128) return -1;
+        mx = mx - pw_split(mx);
+        mn = pw_split(mn);
+        d++;
+    }
+    return d;
+}
+
+// One block per mid segment: w[st] + pairwise(w[st+1:en]) -- a warp per
+// depth-d0 node (pw_node_warp), then the perfect top tree pair by pair.
+__global__ void __launch_bounds__(512) k_reduceat_mid(const double *__restrict__ w,
+                                                      const int64_t *__restrict__ starts,
+                                                      int64_t M, int64_t R, double *out,
+                                                      const int64_t *mid_list,
+                                                      const unsigned long long *mid_cnt,
+                                                      int64_t *long_list,
+                                                      unsigned long long *long_cnt) {
+    __shared__ double vals[SEG_BLOCK_NODES];
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t cnt = (int64_t)*mid_cnt;
+    for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
+        const int64_t t = mid_list[q];
+        const int64_t st = starts[t], en = (t + 1 < M) ? starts[t + 1] : R;
+        const double *a = w + st + 1;
+        const int64_t L = en - st - 1;
+        const int d0 = pw_depth_dev(L);
+        if (d0 < 0 || ((int64_t)1 << d0) > SEG_BLOCK_NODES) {
+            if (threadIdx.x == 0) long_list[atomicAdd(long_cnt, 1ull)] = t;
+            continue;
+        }
+        const int64_t nn = (int64_t)1 << d0;
+        for (int64_t j = warp; j < nn; j += nw) {
+            const double v = pw_node_warp(a, L, d0, (uint64_t)j, Ident{});
+            if ((threadIdx.x & 31) == 0) vals[j] = v;
+        }
+        __syncthreads();
+        for (int64_t h = nn >> 1; h >= 1; h >>= 1) {  // (2i, 2i+1) -> i, level by level
+            double v[SEG_BLOCK_NODES / 512];
+#pragma unroll
+            for (int u = 0; u < SEG_BLOCK_NODES / 512; u++) {
+                const int64_t i = threadIdx.x + (int64_t)u * 512;
+                v[u] = i < h ? __dadd_rn(vals[2 * i], vals[2 * i + 1]) : 0.0;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < SEG_BLOCK_NODES / 512; u++) {
+                const int64_t i = threadIdx.x + (int64_t)u * 512;
+                if (i < h) vals[i] = v[u];
+            }
+            __syncthreads();
+        }
+        // ndarray.sum's leading 0.0 is the identity for these (positive) weights
+        if (threadIdx.x == 0) out[t] = __dadd_rn(w[st], vals[0]);
+        __syncthreads();
     }
 }
 
@@ -266,29 +335,45 @@ __global__ void k_seg_finish(const double *w, int64_t st, const double *tail, do
     out_t[0] = __dadd_rn(w[st], tail[0]);
 }
 
+__global__ void k_seg_bounds(const int64_t *starts, int64_t M, int64_t R, const int64_t *list,
+                             const unsigned long long *cnt, int64_t *se) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < (int64_t)*cnt;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = list[q];
+        se[2 * q] = starts[t];
+        se[2 * q + 1] = (t + 1 < M) ? starts[t + 1] : R;
+    }
+}
+
 void reduceat_async(const double *w, const int64_t *starts, int64_t M, int64_t R, double *out,
                     cudaStream_t s) {
     if (M <= 0) return;
-    Buf<int64_t> long_list(M, s);
-    Buf<unsigned long long> long_cnt(1, s);
-    PLV_CUDA(cudaMemsetAsync(long_cnt.get(), 0, sizeof(unsigned long long), s));
-    k_reduceat_short<<<grid_for(M, 256), 256, 0, s>>>(w, starts, M, R, out, long_list.get(),
-                                                     long_cnt.get());
+    Buf<int64_t> mid_list(M, s), long_list(M, s);
+    Buf<unsigned long long> cnts(2, s);
+    PLV_CUDA(cudaMemsetAsync(cnts.get(), 0, 2 * sizeof(unsigned long long), s));
+    k_reduceat_short<<<grid_for(M, 256), 256, 0, s>>>(w, starts, M, R, out, mid_list.get(),
+                                                     cnts.get(), long_list.get(), cnts.get() + 1);
     PLV_LAUNCH_CHECK();
-    unsigned long long nl = d2h(long_cnt.get(), s);
+    k_reduceat_mid<<<148 * 2, 512, 0, s>>>(w, starts, M, R, out, mid_list.get(), cnts.get(),
+                                          long_list.get(), cnts.get() + 1);
+    PLV_LAUNCH_CHECK();
+    unsigned long long nl = d2h(cnts.get() + 1, s);
     if (!nl) return;
-    std::vector<int64_t> lst(nl), st_h(nl), en_h(nl);
+    // the rare segments of more than 2^19 terms: the whole-array pairwise
+    // launcher each; their bounds come back in one copy
+    Buf<int64_t> se(2 * nl, s);
+    k_seg_bounds<<<grid_for(nl, 256), 256, 0, s>>>(starts, M, R, long_list.get(), cnts.get() + 1,
+                                                  se.get());
+    PLV_LAUNCH_CHECK();
+    std::vector<int64_t> lst(nl), seh(2 * nl);
     PLV_CUDA(cudaMemcpyAsync(lst.data(), long_list.get(), sizeof(int64_t) * nl,
+                             cudaMemcpyDeviceToHost, s));
+    PLV_CUDA(cudaMemcpyAsync(seh.data(), se.get(), sizeof(int64_t) * 2 * nl,
                              cudaMemcpyDeviceToHost, s));
     PLV_CUDA(cudaStreamSynchronize(s));
     Buf<double> tail(nl, s);
     for (unsigned long long q = 0; q < nl; q++) {
-        int64_t t = lst[q];
-        int64_t se[2];
-        PLV_CUDA(cudaMemcpyAsync(se, starts + t, sizeof(int64_t) * ((t + 1 < M) ? 2 : 1),
-                                 cudaMemcpyDeviceToHost, s));
-        PLV_CUDA(cudaStreamSynchronize(s));
-        int64_t st = se[0], en = (t + 1 < M) ? se[1] : R;
+        const int64_t t = lst[q], st = seh[2 * q], en = seh[2 * q + 1];
         pw_sum_async(w + st + 1, en - st - 1, tail.get() + q, s);
         // pw_sum adds a leading 0.0; 0.0 + x == x for every x the weights
         // produce (x > 0), so the tail value is the pairwise sum itself.
