@@ -17,6 +17,8 @@ Two families:
 
 from __future__ import annotations
 
+import functools
+
 import numpy as np
 
 from . import _lib
@@ -128,6 +130,7 @@ def grid_records(side: int = 2048, keep: float = 0.9, pendants: int = 1_000_000,
     return np.concatenate([a, pu]), np.concatenate([b, pv]), np.concatenate([w, pw])
 
 
+@functools.lru_cache(maxsize=4)
 def chung_lu_cdf(n: int = 1 << 24, gamma: float = 2.1, mean_degree: float = 12.0,
                  max_degree: float = 1e5):
     """Expected-degree sequence w_i ~ i^(-1/(gamma-1)), scaled to the mean and
@@ -136,7 +139,9 @@ def chung_lu_cdf(n: int = 1 << 24, gamma: float = 2.1, mean_degree: float = 12.0
     w = i ** (-1.0 / (gamma - 1.0))
     w *= mean_degree / w.mean()
     np.minimum(w, max_degree, out=w)
-    return np.cumsum(w)
+    c = np.cumsum(w)
+    c.setflags(write=False)  # cached: shared by every caller
+    return c
 
 
 def chung_lu_records(n: int = 1 << 24, gamma: float = 2.1, mean_degree: float = 12.0,
@@ -212,7 +217,7 @@ def chung_lu_device(n: int = 1 << 24, gamma: float = 2.1, mean_degree: float = 1
     import torch
     cdf = chung_lu_cdf(n, gamma, mean_degree, max_degree)
     R = int(round(cdf[-1] / 2.0))
-    d_cdf = torch.from_numpy(cdf).to(_lib.device())
+    d_cdf = torch.from_numpy(np.array(cdf)).to(_lib.device())  # (the cached cdf is read-only)
     u, v, w = _records_out(R)
     cnt = _lib.i64_host(1)
     _lib.check(_lib.lib().gen_chung_lu(seed, _lib.ptr(d_cdf), n, R, _lib.ptr(u), _lib.ptr(v),
