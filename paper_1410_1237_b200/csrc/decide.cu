@@ -1228,434 +1228,6 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *l
 }
 
 
-// ------------------------------------------------ tail runs (k_tailg)
-//
-// The late colour classes of a heavy-tailed graph hold a few hub-tier
-// vertices each (C4: ~250 classes of 3-16 vertices of degree 15 k-70 k; C2:
-// ~100 of <= 32).  Per class the multi-kernel path pays accumulate -> pass
-// -> apply launches and a per-hub ticket: ~15-25 us of dependent latency.
-// k_tailg decides AND applies a whole run of such classes in ONE cooperative
-// launch over the whole GPU (one CTA per SM), the classes in order, its
-// steps separated by software grid barriers (release / acquire at gpu scope;
-// state is read with coherent L2 loads, ld_state).  Per class:
-//   1. accumulate: every hub entry of the class, spread over the grid, into
-//      the dense per-hub arrays (any-order sums, term counts, first position);
-//   2. pass A: 32-position chunks of one hub per warp; the first position of
-//      each community owns it: gain, slack, warp best -> per-hub best of the
-//      CTA (a lock in shared memory) -> one partial per (hub, CTA);
-//   3. decide (the hub's decider CTA): integral graphs finish at once; else
-//      pass B lists the candidates overlapping the hub's best (the rule of
-//      certify_table) and resolve() / table_exact decide on exact values --
-//      the rules and the bits of k_hub_accum + k_hub_pass;
-//   4. apply: one warp, apply_tiny_warp (the reference's ordered apply).
-constexpr int TL_NT = 512;
-constexpr int TL_MAXH = 32;  // vertices per tail class (one tiny-apply warp)
-constexpr int TL_U = 4;      // entries per thread in flight (accumulate)
-
-struct TailStage {
-    int64_t goff;      // class offset in the stage lists and decide outputs
-    int64_t hub_base;  // first hub_eoff / hub_toff / hub_row / hub_vid entry
-    int64_t tstart;    // first tier-list entry of the hub tier
-    int64_t nh;        // its vertices (= the class's active vertices), 0: skip
-};
-
-struct GridBar {
-    unsigned int count, gen;
-};
-
-struct TailArgs {
-    DecideArgs A;  // outputs at class offset 0
-    StageArgs S;   // subset / outputs at class offset 0
-    const TailStage *st;
-    int64_t a0, a1;
-    const int32_t *tier_list, *hub_vid;
-    const int64_t *hub_row, *hub_eoff, *hub_toff;
-    double *dval;
-    int32_t *dcnt, *dmk, *cbuf;
-    int64_t dn;
-    int32_t *hkeys;
-    double *hvals;
-    double *gbuf;  // per hub entry: pass A gain (non-integral)
-    float *sbuf;   // ... and slack
-    Best *part;    // [TL_MAXH * nblocks] per (hub, CTA) bests
-    Best *bw;      // [TL_MAXH] hub bests
-    int32_t *near;  // [TL_MAXH * MAXS] overlapping candidates
-    int *nn;        // [TL_MAXH] their count; [TL_MAXH + q]: overflow flag
-    GridBar *bar;
-};
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-// Grid-wide barrier of a cooperative launch (every CTA resident): release
-// this CTA's writes, count in, the last arrival opens the next generation.
-__device__ __forceinline__ void grid_sync(GridBar *b) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned g = ld_acquire_u32(&b->gen);
-        __threadfence();
-        if (atomicAdd(&b->count, 1u) == gridDim.x - 1) {
-            atomicExch(&b->count, 0u);
-            __threadfence();
-            atomicAdd(&b->gen, 1u);
-        } else {
-            while (ld_acquire_u32(&b->gen) == g) {
-            }
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-__device__ __forceinline__ int tl_hub_of(const int64_t *eo, int nh, int64_t t) {
-    int lo = 0, hi = nh;
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (eo[mid] <= t)
-            lo = mid;
-        else
-            hi = mid;
-    }
-    return lo;
-}
-
-__device__ __forceinline__ Best ldcg_best2(const Best *p) {
-    Best b;
-    b.g = __ldcg(&p->g);
-    b.l = __ldcg(&p->l);
-    b.c = __ldcg(&p->c);
-    b.e = __ldcg(&p->e);
-    b.n = __ldcg(&p->n);
-    return b;
-}
-
-__global__ void __launch_bounds__(TL_NT, 1) k_tailg(TailArgs T) {
-    __shared__ int64_t s_eoff[TL_MAXH + 1], s_poff[TL_MAXH + 1], s_row[TL_MAXH], s_x[TL_MAXH];
-    __shared__ int32_t s_vid[TL_MAXH], s_cold[TL_MAXH], s_lold[TL_MAXH];
-    __shared__ double s_ki[TL_MAXH], s_fold[TL_MAXH], s_aoe[TL_MAXH], s_lower[TL_MAXH],
-        s_slb[TL_MAXH];
-    __shared__ Best s_hb[TL_MAXH];
-    __shared__ Best s_bw[TL_MAXH];
-    __shared__ int s_lock[TL_MAXH];
-    __shared__ CertSmem<TL_NT> S;
-    __shared__ int32_t cidx[TL_NT * HFU];
-    __shared__ double cw[TL_NT * HFU];
-    __shared__ unsigned long long ap_k[64];
-    __shared__ double ap_w[64], ap_a[64];
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int r = (int)blockIdx.x, NB = (int)gridDim.x;
-    const int64_t gt = (int64_t)r * TL_NT + tid, G = (int64_t)NB * TL_NT;
-    const int64_t gw = gt >> 5, GW = G >> 5;
-    const bool integral = T.A.integral != 0;
-    const double inv_m = 1.0 / T.A.m;
-    if (tid == 0) {
-        S.cidx = cidx;
-        S.cw = cw;
-    }
-    pdl_wait();  // the state of the previous stage
-    for (int64_t a = T.a0; a < T.a1; a++) {
-        const TailStage d = T.st[a];
-        const int nh = (int)d.nh;
-        if (nh == 0) continue;  // grid-uniform
-        DecideArgs A = T.A;
-        A.out_target += d.goff;
-        A.out_moved += d.goff;
-        A.out_e_old += d.goff;
-        A.out_e_best += d.goff;
-        if (tid < nh) {
-            const int q = tid;
-            const int32_t i = T.hub_vid[d.hub_base + q];
-            s_vid[q] = i;
-            s_row[q] = T.hub_row[d.hub_base + q];
-            s_x[q] = T.tier_list[d.tstart + q];
-            s_eoff[q] = T.hub_eoff[d.hub_base + q];
-            const int32_t c_old = ld_state(A.assign + i);
-            s_cold[q] = c_old;
-            s_ki[q] = A.k[i];
-            s_hb[q] = Best{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
-            s_lock[q] = 0;
-        }
-        if (tid == 0) {
-            s_eoff[nh] = T.hub_eoff[d.hub_base + nh];
-            s_poff[0] = 0;
-        }
-        __syncthreads();
-        if (tid == 0)  // 32-aligned chunk positions: a chunk belongs to one hub
-            for (int q = 0; q < nh; q++)
-                s_poff[q + 1] = s_poff[q] + ((s_eoff[q + 1] - s_eoff[q] + 31) & ~(int64_t)31);
-        const int64_t E = s_eoff[nh];
-        // ---- 1. accumulate
-        for (int64_t t0 = gt; t0 < E; t0 += G * TL_U) {
-            int qv[TL_U];
-            int32_t jv[TL_U], cv[TL_U];
-            double wv[TL_U];
-#pragma unroll
-            for (int u = 0; u < TL_U; u++) {
-                const int64_t t = t0 + u * G;
-                qv[u] = t < E ? tl_hub_of(s_eoff, nh, t) : 0;
-                const int64_t e = s_row[qv[u]] + (t - s_eoff[qv[u]]);
-                jv[u] = t < E ? ld_row(A.nbr + e) : -1;
-                wv[u] = t < E ? ld_row(A.wts + e) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < TL_U; u++)
-                cv[u] = jv[u] >= 0 && jv[u] != s_vid[qv[u]] ? ld_state(A.assign + jv[u]) : -1;
-#pragma unroll
-            for (int u = 0; u < TL_U; u++) {
-                const int64_t t = t0 + u * G;
-                if (t >= E) continue;
-                T.cbuf[t] = cv[u];
-                if (cv[u] < 0) continue;
-                const int64_t dq = (int64_t)qv[u] * T.dn + cv[u];
-                atomicAdd(T.dval + dq, wv[u]);
-                atomicAdd(T.dcnt + dq, 1);
-                atomicMin(T.dmk + dq, (int32_t)(t - s_eoff[qv[u]]));
-            }
-        }
-        grid_sync(T.bar);
-        if (tid < nh) {
-            const int q = tid;
-            const int64_t dq = (int64_t)q * T.dn + s_cold[q];
-            s_fold[q] = ld_state(T.dval + dq);
-            s_lold[q] = ld_state(T.dcnt + dq);
-            s_aoe[q] = dsub(ld_state(A.a_tot + s_cold[q]), s_ki[q]);
-        }
-        __syncthreads();
-        // ---- 2. pass A: one hub per 32-position chunk
-        const int64_t PP = s_poff[nh];
-        unsigned long long nc = 0;
-        for (int64_t k = gw; k * 32 < PP; k += GW) {
-            const int64_t p = k * 32;
-            const int q = tl_hub_of(s_poff, nh, p);
-            const int64_t pos = p - s_poff[q] + lane;  // row position
-            const int64_t t = s_eoff[q] + pos;
-            const bool ok = t < s_eoff[q + 1];
-            const int32_t c_old = s_cold[q];
-            const int32_t c = ok ? ld_state(T.cbuf + t) : -1;
-            const int64_t dq = (int64_t)q * T.dn + (c >= 0 ? c : 0);
-            const bool own = c >= 0 && ld_state(T.dmk + dq) == (int32_t)pos;
-            nc += own;
-            const bool cand = own && c != c_old;
-            const double F = cand ? ld_state(T.dval + dq) : 0.0;
-            const int32_t L = cand ? ld_state(T.dcnt + dq) : 0;
-            const double at = cand ? ld_state(A.a_tot + c) : 0.0;
-            Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
-            if (cand) {
-                const double g = gain_of(F, s_fold[q], A.m, s_ki[q], s_aoe[q], at, A.four_m_sq);
-                consider(b, g, LBL(A.labels, c), c, F, L);
-                if (!integral) {
-                    T.gbuf[t] = g;
-                    T.sbuf[t] = __double2float_ru(gain_slack_r(F, L, s_fold[q], s_lold[q], inv_m, g));
-                }
-                T.dval[dq] = 0.0;  // back to idle (c_old's slot: by the decider)
-                T.dcnt[dq] = 0;
-                T.dmk[dq] = INT_MAX;
-            } else if (!integral && ok) {
-                T.gbuf[t] = -INFINITY;
-            }
-            warp_best(b);
-            if (lane == 0) {
-                while (atomicCAS(&s_lock[q], 0, 1) != 0) {
-                }
-                __threadfence_block();
-                Best h = s_hb[q];
-                consider(h, b.g, b.l, b.c, b.e, b.n);
-                s_hb[q] = h;
-                __threadfence_block();
-                atomicExch(&s_lock[q], 0);
-            }
-        }
-        if (A.cand) {
-            for (int o = 16; o > 0; o >>= 1) nc += __shfl_xor_sync(FULL, nc, o);
-            if (lane == 0 && nc) atomicAdd(A.cand, nc);
-        }
-        __syncthreads();
-        if (tid < nh) T.part[(int64_t)tid * NB + r] = s_hb[tid];
-        grid_sync(T.bar);
-        // ---- 3. decide: CTA r decides hubs r, r + NB, ...
-        for (int q = r; q < nh; q += NB) {  // block-uniform
-            if (tid < 32) {  // the hub's best over the CTAs' partials
-                Best bw{0.0, LBL(A.labels, s_cold[q]), s_cold[q], 0.0, 0};
-                for (int t = tid; t < NB; t += 32) {
-                    const Best o = ldcg_best2(T.part + (int64_t)q * NB + t);
-                    consider(bw, o.g, o.l, o.c, o.e, o.n);
-                }
-                warp_best(bw);
-                if (tid == 0) {
-                    if (integral)
-                        finish_vertex(A, s_x[q], s_cold[q], s_fold[q], bw.g, bw.c, bw.e);
-                    else
-                        T.bw[q] = bw;
-                }
-            }
-        }
-        if (!integral) {
-            grid_sync(T.bar);  // every hub's best, for everyone
-            if (tid < nh) {
-                const int q = tid;
-                const Best bw = ldcg_best2(T.bw + q);
-                s_bw[q] = bw;
-                const bool stay = bw.c == s_cold[q];
-                const double slb =
-                    stay ? 0.0 : gain_slack_r(bw.e, bw.n, s_fold[q], s_lold[q], inv_m, bw.g);
-                s_slb[q] = slb;
-                s_lower[q] = stay ? 0.0 : bw.g - slb;
-            }
-            __syncthreads();
-            // pass B: candidates overlapping the best, listed per hub
-            for (int64_t k = gw; k * 32 < PP; k += GW) {
-                const int64_t p = k * 32;
-                const int q = tl_hub_of(s_poff, nh, p);
-                const int64_t t = s_eoff[q] + (p - s_poff[q]) + lane;
-                if (t >= s_eoff[q + 1]) continue;
-                const double g = __ldcg(T.gbuf + t);
-                if (g == -INFINITY) continue;
-                const int32_t c = ld_state(T.cbuf + t);
-                if (c == s_bw[q].c) continue;
-                const double slv = (double)__ldcg(T.sbuf + t);
-                if ((slv > 0.0 || s_slb[q] > 0.0) && g + slv >= s_lower[q]) {
-                    const int kk = atomicAdd(T.nn + q, 1);
-                    if (kk < MAXS)
-                        T.near[q * MAXS + kk] = c;
-                    else
-                        atomicOr(T.nn + TL_MAXH + q, 2);
-                }
-            }
-            grid_sync(T.bar);
-            for (int q = r; q < nh; q += NB) {  // block-uniform
-                const Best bw = s_bw[q];
-                if (tid == 0) {
-                    S.f_old = s_fold[q];
-                    S.l_old = s_lold[q];
-                    const int nnq = __ldcg(T.nn + q);
-                    S.nS = nnq;
-                    int fl = __ldcg(T.nn + TL_MAXH + q) | (nnq > MAXS ? 2 : 0);
-                    if (bw.c != s_cold[q] && s_slb[q] > 0.0 && s_lower[q] <= 0.0) fl |= 1;
-                    S.flag = fl;
-                    for (int t = 0; t < nnq && t < MAXS; t++) S.N[2 + t] = __ldcg(T.near + q * MAXS + t);
-                    T.nn[q] = 0;  // idle again
-                    T.nn[TL_MAXH + q] = 0;
-                }
-                __syncthreads();
-                if (!resolve<TL_NT, HFU>(A, s_x[q], s_vid[q], s_cold[q], s_ki[q], bw, S)) {
-                    const int64_t base = T.hub_toff[d.hub_base + q];
-                    table_exact<TL_NT>(A, s_x[q], s_vid[q], s_cold[q], s_ki[q], T.hkeys + base,
-                                       T.hvals + base,
-                                       PowTab{(uint32_t)(T.hub_toff[d.hub_base + q + 1] - base - 1)},
-                                       S);
-                }
-                __syncthreads();
-            }
-        }
-        // c_old's slot back to idle (read by every CTA above: after the barrier)
-        grid_sync(T.bar);  // the class's decisions
-        if (r == 0 && tid < nh) {
-            const int64_t dq = (int64_t)tid * T.dn + s_cold[tid];
-            T.dval[dq] = 0.0;
-            T.dcnt[dq] = 0;
-            T.dmk[dq] = INT_MAX;
-        }
-        // ---- 4. apply (CTA 0, warp 0)
-        if (r == 0 && tid < 32) {
-            StageArgs SA = T.S;
-            SA.subset += d.goff;
-            SA.ns = nh;
-            SA.target += d.goff;
-            SA.moved += d.goff;
-            SA.e_old += d.goff;
-            SA.e_best += d.goff;
-            apply_tiny_warp<1>(SA, ap_k, ap_w, ap_a);
-        }
-        grid_sync(T.bar);  // the class's moves, before the next class reads the state
-    }
-}
-
-void tail_plan(Plan &P, bool enable, bool integral, cudaStream_t s) {
-    P.tail_first.clear();
-    P.tail_last.clear();
-    const int64_t nst = (int64_t)P.st.size();
-    if (!enable || !PLV_TAIL || nst == 0) return;
-    std::vector<TailStage> ts(nst);
-    std::vector<bool> ok(nst, false);
-    int64_t max_e = 0;
-    for (int64_t a = 0; a < nst; a++) {
-        const StagePlan &sp = P.st[a];
-        ts[a] = TailStage{sp.off, sp.hub_base, sp.tstart[4], sp.tcount[4]};
-        if (sp.ns == 0) {
-            ok[a] = true;  // nothing to do; may sit inside a run
-            ts[a].nh = 0;
-            continue;
-        }
-        ok[a] = !sp.tcount[0] && !sp.tcount[1] && !sp.tcount[2] && !sp.tcount[3] &&
-                sp.tcount[4] == sp.ns && sp.ns <= TL_MAXH && sp.hub_dense;
-        if (ok[a]) max_e = sp.hub_entries > max_e ? sp.hub_entries : max_e;
-    }
-    for (int64_t a = 0; a < nst;) {
-        if (!ok[a] || P.st[a].ns == 0) {
-            a++;
-            continue;
-        }
-        int64_t b = a;
-        while (b < nst && ok[b]) b++;
-        if (b - a >= PLV_TAIL_MIN) {
-            P.tail_first.push_back(a);
-            P.tail_last.push_back(b);
-        }
-        a = b;
-    }
-    if (P.tail_first.empty()) return;
-    int dev = 0, sms = 0, per = 0;
-    PLV_CUDA(cudaGetDevice(&dev));
-    PLV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    PLV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tailg, TL_NT, 0));
-    if (per < 1) {
-        P.tail_first.clear();
-        P.tail_last.clear();
-        return;
-    }
-#ifndef PLV_TAIL_NB
-#define PLV_TAIL_NB 0  // CTAs of the cooperative launch (0: one per SM)
-#endif
-    P.tail_nb = PLV_TAIL_NB > 0 && PLV_TAIL_NB < sms ? PLV_TAIL_NB : sms;  // co-resident
-    P.tail_st = dalloc<TailStage>(nst);
-    PLV_CUDA(cudaMemcpyAsync(P.tail_st, ts.data(), sizeof(TailStage) * nst,
-                             cudaMemcpyHostToDevice, s));
-    if (!integral) {
-        P.tail_g = dalloc<double>(max_e);
-        P.tail_s = dalloc<float>(max_e);
-    }
-    P.tail_part = dalloc<Best>((size_t)TL_MAXH * P.tail_nb);
-    P.tail_bw = dalloc<Best>(TL_MAXH);
-    P.tail_near = dalloc<int32_t>(TL_MAXH * MAXS);
-    P.tail_nn = dalloc<int>(2 * TL_MAXH);
-    P.tail_bar = dalloc<GridBar>(1);
-    PLV_CUDA(cudaMemsetAsync(P.tail_nn, 0, sizeof(int) * 2 * TL_MAXH, s));
-    PLV_CUDA(cudaMemsetAsync(P.tail_bar, 0, sizeof(GridBar), s));
-    PLV_CUDA(cudaStreamSynchronize(s));
-}
-
-void launch_tail(const Plan &P, int64_t k, DecideArgs A, StageArgs S, cudaStream_t st) {
-    TailArgs T{A, S, (const TailStage *)P.tail_st, P.tail_first[k], P.tail_last[k],
-               P.tier_list, P.hub_vid, P.hub_row, P.hub_eoff, P.hub_toff, P.dval, P.dcnt,
-               P.dmk, P.cbuf, P.dn, P.hkeys, P.hvals, P.tail_g, P.tail_s, P.tail_part,
-               P.tail_bw, P.tail_near, P.tail_nn, (GridBar *)P.tail_bar};
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(P.tail_nb);
-    cfg.blockDim = dim3(TL_NT);
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    PLV_CUDA(cudaLaunchKernelEx(&cfg, k_tailg, T));
-    count_launch();
-}
-
-
 // ================================================================ planning
 
 __global__ void k_tier_keys(const int64_t *off, const int32_t *vtx, const int64_t *stage_off,
@@ -1721,8 +1293,7 @@ void Plan::release() {
     cudaDeviceSynchronize();  // buffers go back to the pool idle
     void *ps[] = {tier_list, tier_vid, tier_row, tier_end, hub_eoff, hub_toff, hub_poff, hub_blk, hub_row, hub_vid, hkeys,
                   hvals,     hcnt,     hsold,    hncnt,    hnear,   hpart,
-                  dval,      dcnt,     dmk,      cbuf,     tail_st,  tail_g,  tail_s,
-                  tail_part, tail_bw,  tail_near, tail_nn, tail_bar};
+                  dval,      dcnt,     dmk,      cbuf};
     for (void *p : ps)
         pool_free(p);
     tier_list = nullptr;
@@ -1736,14 +1307,6 @@ void Plan::release() {
     hpart = nullptr;
     dval = nullptr;
     dcnt = dmk = cbuf = nullptr;
-    tail_st = tail_bar = nullptr;
-    tail_g = nullptr;
-    tail_s = nullptr;
-    tail_part = tail_bw = nullptr;
-    tail_near = nullptr;
-    tail_nn = nullptr;
-    tail_first.clear();
-    tail_last.clear();
 }
 
 void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *stage_off_h,

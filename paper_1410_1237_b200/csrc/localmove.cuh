@@ -29,12 +29,6 @@ constexpr int BLK = 512;      // threads per block in tier 3 (128/256/1024 measu
 constexpr int T2_TS = 4096;   // smem slots for tier 2 (>= 1.5 * (2048 + 1))
 constexpr int T2A_TS = 1024;
 constexpr int NTIER = 5;  // t0, t1, t2 (block, small table), t3 (block), t4 (hubs)
-#ifndef PLV_TAIL
-#define PLV_TAIL 1  // runs of hub-only colour classes in one cooperative launch (k_tailg)
-#endif
-#ifndef PLV_TAIL_MIN
-#define PLV_TAIL_MIN 2  // shortest run worth a k_tailg launch
-#endif
 
 constexpr int SMALL_APPLY_MAX = 1024;  // stage size handled by the one-CTA apply (2048 measured slower)
 constexpr int SA_THREADS = 256;
@@ -109,26 +103,8 @@ struct Plan {
     int32_t *cbuf = nullptr;    // communities of a dense stage's hub entries
     int64_t dn = 0, max_dense_entries = 0, dense_k = 0;
     int64_t max_slices = 1;
-    // k_tailg: runs [tail_first[k], tail_last[k]) of small hub-only stages
-    std::vector<int64_t> tail_first, tail_last;
-    void *tail_st = nullptr;   // TailStage per stage (device)
-    double *tail_g = nullptr;  // per hub entry: gain / slack of pass A (non-integral)
-    float *tail_s = nullptr;
-    Best *tail_part = nullptr, *tail_bw = nullptr;
-    int32_t *tail_near = nullptr;
-    int *tail_nn = nullptr;
-    void *tail_bar = nullptr;
-    int tail_nb = 0;           // CTAs of the cooperative launch
-    int64_t tail_run_at(int64_t a) const {
-        for (size_t k = 0; k < tail_first.size(); k++)
-            if (tail_first[k] == a) return (int64_t)k;
-        return -1;
-    }
     void release();
 };
-
-// Plan the k_tailg runs (after plan_build; stage offsets are the plan's).
-void tail_plan(Plan &P, bool enable, bool integral, cudaStream_t s);
 
 
 void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *stage_off_h,
@@ -207,9 +183,6 @@ void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st);
 // Live e_a / e_b of the movers at positions [S.xlo, S.xhi) into S.live_a / S.live_b
 // (a partitioned uncoloured stage; the rows of those movers must be present).
 void launch_live(StageArgs S, const ApplyBuffers &B, cudaStream_t st);
-// Decide + apply of tail run k (decide / stage args with base pointers:
-// subset / outputs at stage offset 0).
-void launch_tail(const Plan &P, int64_t k, DecideArgs A, StageArgs S, cudaStream_t st);
 
 template <class T>
 T *dalloc(size_t count) {

@@ -289,30 +289,10 @@ static void record_finish(Phase &P, cudaStream_t st) {
                              cudaMemcpyDeviceToHost, st));
 }
 
-// Tail run k (k_tailg): decide + apply of its classes in one launch.
-static void record_tail(Phase &P, int64_t k, cudaStream_t st) {
-    DecideArgs A = make_decide_args(P.off, P.nbr, P.wts, P.k, P.labels, nullptr, P.assign,
-                                    P.a_tot, P.sizes, P.m, (P.flags & PLV_F_INTEGRAL) ? 1 : 0,
-                                    P.target, P.moved, P.e_old, P.e_best, P.counters + 1);
-    StageArgs S = stage_args(P, 0, nullptr, nullptr);
-    S.subset = P.vtx;
-    S.target = P.target;
-    S.moved = P.moved;
-    S.e_old = P.e_old;
-    S.e_best = P.e_best;
-    launch_tail(P.plan, k, A, S, st);
-}
-
 static void record_iteration(Phase &P, cudaStream_t st) {
     PLV_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 2, st));
     for (size_t a = 0; a + 1 < P.goff.size(); a++) {
         if (P.goff[a + 1] == P.goff[a]) continue;
-        const int64_t k = P.plan.tail_run_at((int64_t)a);
-        if (k >= 0) {
-            record_tail(P, k, st);
-            a = (size_t)P.plan.tail_last[k] - 1;
-            continue;
-        }
         record_decide(P, a, st);
         record_exchange(P, a, st);
         if (live_mode(P)) {
@@ -524,9 +504,6 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
             }
         }
         plan_build(P->plan, off, P->lvtx, loff.data(), nst, n, s);
-        // runs of small hub-only colour classes: one cooperative launch each (k_tailg)
-        tail_plan(P->plan, world == 1 && !comm && !P->timing && (flags & PLV_F_INDEPENDENT),
-                  (flags & PLV_F_INTEGRAL) != 0, s);
         if (comm) {  // exchange records + the slice table on device
             P->xmax.assign(nst, 0);
             for (int64_t a = 0; a < nst; a++)
@@ -794,12 +771,6 @@ static void build_run_graph(Phase &P, int64_t cap, cudaStream_t s) {
         PLV_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 2, cs));
         for (size_t a = 0; a + 1 < P.goff.size(); a++) {
             if (P.goff[a + 1] == P.goff[a]) continue;
-            const int64_t k = P.plan.tail_run_at((int64_t)a);
-            if (k >= 0 && !P.dirty && !P.chash) {
-                record_tail(P, k, cs);
-                a = (size_t)P.plan.tail_last[k] - 1;
-                continue;
-            }
             record_decide(P, a, cs);
             record_apply(P, a, cs, P.dirty, P.chash);
         }
