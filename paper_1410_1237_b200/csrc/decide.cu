@@ -836,9 +836,9 @@ struct HubScratch {
     const int64_t *poff; // [nh + 1] first partial of each hub
     int64_t nh;
     // dense mode (few hubs): per-hub arrays indexed by community, no claims
-    double *dval;        // [dense_k * dn] any-order sums (0 idle)
-    int32_t *dcnt;       // [dense_k * dn] term counts (0 idle)
-    int32_t *dmk;        // [dense_k * dn] first row position per community (INT_MAX idle)
+    DenseRec *drec;      // [dense_k * dn] sum / term count / first row position (idle:
+                         // 0 / 0 / INT_MAX), one 16-byte record: an entry's three
+                         // updates and the pass's three reads touch ONE 32-byte sector
     int32_t *cbuf;       // [entries] community of every hub entry (-1: self loop)
     int64_t dn;
 };
@@ -898,9 +898,9 @@ __global__ void k_hub_accum(DecideArgs A, const int64_t *eoff, const int64_t *to
         if (DENSE) {  // every lane adds its own entry: plain reductions, no grouping
             if (c >= 0) {
                 const int64_t d = q * H.dn + c;
-                atomicAdd(H.dval + d, w);
-                atomicAdd(H.dcnt + d, 1);
-                atomicMin(H.dmk + d, (int32_t)(t - eoff[q]));
+                atomicAdd(&H.drec[d].val, w);
+                atomicAdd(&H.drec[d].cnt, 1);
+                atomicMin(&H.drec[d].mk, (int32_t)(t - eoff[q]));
             }
             continue;
         }
@@ -974,8 +974,8 @@ __device__ void hub_decide_one(const DecideArgs &A, const int32_t *list, const i
         warp_best(bw);
         const int64_t dq = q * H.dn;
         const int32_t so = DENSE ? 0 : H.sold[q];
-        const double f_old = DENSE ? H.dval[dq + c_old] : so >= 0 ? hvals[base + so] : 0.0;
-        const int32_t l_old = DENSE ? H.dcnt[dq + c_old] : so >= 0 ? hcnt[base + so] : 0;
+        const double f_old = DENSE ? H.drec[dq + c_old].val : so >= 0 ? hvals[base + so] : 0.0;
+        const int32_t l_old = DENSE ? H.drec[dq + c_old].cnt : so >= 0 ? hcnt[base + so] : 0;
         const int na = __ldcg(H.ncnt + q * HCPAD), nb = __ldcg(H.ncnt + q * HCPAD + 1);
         const bool stay_best = bw.c == c_old;
         const double slack_b =
@@ -1012,9 +1012,7 @@ __device__ void hub_decide_one(const DecideArgs &A, const int32_t *list, const i
             S.l_old = l_old;
             // back to idle: c_old's slot / entries, the counters
             if (DENSE) {
-                H.dval[dq + c_old] = 0.0;
-                H.dcnt[dq + c_old] = 0;
-                H.dmk[dq + c_old] = INT_MAX;
+                H.drec[dq + c_old] = DenseRec{0.0, 0, INT_MAX};
             } else {
                 if (so >= 0) {
                     hkeys[base + so] = -1;
@@ -1119,8 +1117,8 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *l
     const int64_t cap = toff[q + 1] - base;
     const int64_t dq = q * H.dn, deg = eoff[q + 1] - eoff[q];
     const int32_t so = DENSE ? 0 : H.sold[q];
-    const double f_old = DENSE ? H.dval[dq + c_old] : so >= 0 ? hvals[base + so] : 0.0;
-    const int32_t l_old = DENSE ? H.dcnt[dq + c_old] : so >= 0 ? hcnt[base + so] : 0;
+    const double f_old = DENSE ? H.drec[dq + c_old].val : so >= 0 ? hvals[base + so] : 0.0;
+    const int32_t l_old = DENSE ? H.drec[dq + c_old].cnt : so >= 0 ? hcnt[base + so] : 0;
     const double ki = A.k[i], a_old_excl = dsub(ld_state(A.a_tot + (c_old)), ki);
     const double inv_m = 1.0 / A.m;
     TR_MARK
@@ -1142,9 +1140,10 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *l
 #pragma unroll
         for (int u = 0; u < PU; u++) {
             const bool ok = cc[u] >= 0;
-            mk[u] = ok ? H.dmk[dq + cc[u]] : -1;
-            F[u] = ok ? H.dval[dq + cc[u]] : 0.0;
-            L[u] = ok ? H.dcnt[dq + cc[u]] : 0;
+            const DenseRec rr = ok ? H.drec[dq + cc[u]] : DenseRec{0.0, 0, -1};
+            mk[u] = rr.mk;
+            F[u] = rr.val;
+            L[u] = rr.cnt;
             at[u] = ok ? __ldg(A.a_tot + cc[u]) : 0.0;
         }
 #pragma unroll
@@ -1179,9 +1178,7 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *l
         const int64_t s = s0 + u * HSB;
         if (c[u] < 0) continue;
         if (DENSE) {
-            H.dval[dq + c[u]] = 0.0;
-            H.dcnt[dq + c[u]] = 0;
-            H.dmk[dq + c[u]] = INT_MAX;
+            H.drec[dq + c[u]] = DenseRec{0.0, 0, INT_MAX};
         } else {
             hkeys[base + s] = -1;
             hvals[base + s] = 0.0;
@@ -1283,6 +1280,12 @@ __global__ void k_hub_degrees(const int64_t *off, const int32_t *vtx, const int6
     }
 }
 
+__global__ void k_fill_drec(DenseRec *p, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = DenseRec{0.0, 0, INT_MAX};
+}
+
 __global__ void k_fill_i32_d(int32_t *p, int64_t n, int32_t v) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -1293,7 +1296,7 @@ void Plan::release() {
     cudaDeviceSynchronize();  // buffers go back to the pool idle
     void *ps[] = {tier_list, tier_vid, tier_row, tier_end, hub_eoff, hub_toff, hub_poff, hub_blk, hub_row, hub_vid, hkeys,
                   hvals,     hcnt,     hsold,    hncnt,    hnear,   hpart,
-                  dval,      dcnt,     dmk,      cbuf};
+                  drec,      cbuf};
     for (void *p : ps)
         pool_free(p);
     tier_list = nullptr;
@@ -1305,8 +1308,8 @@ void Plan::release() {
     hvals = nullptr;
     hnear = nullptr;
     hpart = nullptr;
-    dval = nullptr;
-    dcnt = dmk = cbuf = nullptr;
+    drec = nullptr;
+    cbuf = nullptr;
 }
 
 void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *stage_off_h,
@@ -1463,13 +1466,9 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
     if (P.max_dense_entries) {
         P.dn = n;
         const int64_t D = P.dense_k * n;
-        P.dval = dalloc<double>(D);
-        P.dcnt = dalloc<int32_t>(D);
-        P.dmk = dalloc<int32_t>(D);
+        P.drec = dalloc<DenseRec>(D);
         P.cbuf = dalloc<int32_t>(P.max_dense_entries);
-        PLV_CUDA(cudaMemsetAsync(P.dval, 0, sizeof(double) * D, s));
-        PLV_CUDA(cudaMemsetAsync(P.dcnt, 0, sizeof(int32_t) * D, s));
-        k_fill_i32_d<<<grid_for(D, 256), 256, 0, s>>>(P.dmk, D, INT_MAX);
+        k_fill_drec<<<grid_for(D, 256), 256, 0, s>>>(P.drec, D);
         PLV_LAUNCH_CHECK();
     }
     P.hpart = dalloc<Best>(max_parts);
@@ -1597,9 +1596,7 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
                      P.hub_blk + sp.hub_blk_base,
                      P.hub_poff + sp.hub_base,
                      nh,
-                     P.dval,
-                     P.dcnt,
-                     P.dmk,
+                     P.drec,
                      P.cbuf,
                      P.dn};
         unsigned g2 = (unsigned)sp.hub_nblk;

@@ -73,6 +73,14 @@ struct StagePlan {
 
 struct Best;  // decide.cu
 
+// A dense hub-array entry (hub, community): any-order sum, term count, first
+// row position.  16-byte aligned, so one record never spans two sectors.
+struct __align__(16) DenseRec {
+    double val;
+    int32_t cnt;
+    int32_t mk;
+};
+
 constexpr int MAXS = 32;  // overlapping candidates resolved exactly per vertex
 
 // Static per-phase decide plan: each stage's vertices split into the five
@@ -98,8 +106,7 @@ struct Plan {
     int32_t *hncnt = nullptr;   // per hub: near-candidate counters (0 idle)
     void *hnear = nullptr;      // per hub: 2 * MAXS near candidates
     Best *hpart = nullptr;      // pass partial bests
-    double *dval = nullptr;     // dense hub arrays [dense_k * n] (idle: 0 / 0 / INT_MAX)
-    int32_t *dcnt = nullptr, *dmk = nullptr;
+    DenseRec *drec = nullptr;   // dense hub records [dense_k * n] (idle: 0 / 0 / INT_MAX)
     int32_t *cbuf = nullptr;    // communities of a dense stage's hub entries
     int64_t dn = 0, max_dense_entries = 0, dense_k = 0;
     int64_t max_slices = 1;
