@@ -173,7 +173,7 @@ def _peak_hbm():
         return 6650.0, "fallback"
 
 
-DECIDE_KERNELS = ("k_decide_", "k_hub_accum", "k_hub_pass")
+DECIDE_KERNELS = ("k_decide_", "k_hub_accum", "k_hub_pass", "k_single_")
 
 
 def _cupti_decide_ms(step):
@@ -644,7 +644,12 @@ def run_ours(args):
     cand_per_iter = float(np.mean(cands))
     moves_per_iter = float(moves_it)
     launches = per_iter_launches * args.steps
-    decide_bytes = 41 * n + 16 * nnz + 8 * cand_per_iter
+    # the first stage starts from the singleton state: its rows' neighbours
+    # are their own communities, so it reads no assign[j] (4 B per entry)
+    off_h = g.adjacency_offsets
+    first = col.classes()[0] if col is not None else np.arange(n)
+    e_first = int((off_h[np.asarray(first) + 1] - off_h[np.asarray(first)]).sum())
+    decide_bytes = 41 * n + 16 * nnz + 8 * cand_per_iter - 4 * e_first
     iter_bytes = decide_bytes + 84 * moves_per_iter + 16 * n
     peak, peak_kind = _peak_hbm()
     achieved = decide_bytes / (decide_ms / 1e3) / 1e9

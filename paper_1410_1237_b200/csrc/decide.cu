@@ -237,7 +237,13 @@ __device__ __forceinline__ Best block_best(BestSmem<NT> &S, Best b) {
 #ifndef T0_MINB
 #define T0_MINB 1
 #endif
+// The general kernels of a first stage step aside when the state is singleton.
+__device__ __forceinline__ bool single_state(const DecideArgs &A) {
+    return A.notsingle && ld_state(A.notsingle) == 0;
+}
+
 __global__ void __launch_bounds__(256, T0_MINB) k_decide_t0(DecideArgs A, TierRef L, int64_t cnt) {
+    if (single_state(A)) return;
     decide_t0_body(A, L, cnt, blockIdx.x, gridDim.x);
 }
 
@@ -337,6 +343,7 @@ __device__ __forceinline__ void decide_t1_body(const DecideArgs &A, const TierRe
 
 __global__ void __launch_bounds__(T1_WARPS * 32) k_decide_t1(DecideArgs A, TierRef L,
                                                               int64_t cnt) {
+    if (single_state(A)) return;
     decide_t1_body<T1_WARPS>(A, L, cnt, blockIdx.x, gridDim.x);
 }
 
@@ -347,6 +354,7 @@ __global__ void __launch_bounds__(T1_WARPS * 32) k_decide_t1(DecideArgs A, TierR
 __global__ void __launch_bounds__(256) k_decide_t01(DecideArgs A, TierRef L0, int64_t cnt0,
                                                     TierRef L1, int64_t cnt1, int nb0) {
     pdl_wait();
+    if (single_state(A)) return;
     if ((int)blockIdx.x < nb0)
         decide_t0_body(A, L0, cnt0, blockIdx.x, nb0);
     else
@@ -773,6 +781,7 @@ constexpr int T2_WIDE_MAX = 600;  // tiers 2-3 with at most this many vertices: 
 // memory; tier 2's small tables let 3x more vertices be in flight per SM.
 template <int TS, int MAXD, int NT>
 __global__ void __launch_bounds__(NT) k_decide_t2(DecideArgs A, TierRef L, int64_t cnt) {
+    if (single_state(A)) return;
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ CertSmem<NT> S;
     __shared__ int32_t cidx[NT * T2_FU];
@@ -862,6 +871,10 @@ __device__ __forceinline__ int64_t hub_of(const int64_t *eoff, int64_t nh, int64
 template <bool DENSE>
 __global__ void k_hub_accum(DecideArgs A, const int64_t *eoff, const int64_t *toff, int64_t nh,
                             int64_t E, int32_t *hkeys, double *hvals, int32_t *hcnt, HubScratch H) {
+    if (A.notsingle) {  // a first stage: the singleton kernels may take it
+        pdl_wait();
+        if (ld_state(A.notsingle) == 0) return;
+    }
 
     TR_BEGIN
     const int lane = threadIdx.x & 31;
@@ -1097,6 +1110,7 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *l
                                                  HubScratch H) {
 
     pdl_wait();  // the accumulation's sums
+    if (single_state(A)) return;
     TR_BEGIN
     __shared__ CertSmem<HSB> S;
     __shared__ int32_t cidx[HSB * HFU];
@@ -1224,6 +1238,192 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *l
     TR_END(2)
 }
 
+
+// ------------------------------------------------- singleton state
+//
+// The first stage of a phase's first iteration sees the singleton state
+// (PL/modularity.py:47-56: assign[v] == v, every community one vertex).  Then
+// decide_moves (PL/_kernels.pyx:21-101) needs no aggregation: rows hold
+// distinct neighbours, so every neighbour j != i is its own community with
+// e_{i->j} = 0.0 + w_ij = w_ij (one term, exact), e_{i->c_old} = 0.0, and the
+// decision is the argmax of gain(w_ij) under (gain desc, label asc) against
+// "stay" -- the same operands and operations as the general tiers, without
+// tables, certification or the hub chain.  These kernels take the stage when
+// *notsingle == 0 (launch_single_check); the general ones step aside.
+
+__device__ __forceinline__ void single_entry(const DecideArgs &A, int32_t i, double ki,
+                                             double aoe, int32_t j, double w, Best &b) {
+    const double g = gain_of(w, 0.0, A.m, ki, aoe, ld_state(A.a_tot + j), A.four_m_sq);
+    consider(b, g, LBL(A.labels, j), j, w, 1);
+}
+
+// thread per vertex (tier 0)
+__global__ void __launch_bounds__(256) k_single_t0(DecideArgs A, TierRef L, int64_t cnt) {
+    if (!single_state(A)) return;
+    unsigned long long my = 0;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < cnt;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = L.x[q];
+        const int32_t i = L.vid[q];
+        const int64_t e0 = L.row[q];
+        const int deg = (int)(L.end[q] - e0);
+        int32_t jj[T0_MAXD];
+        double ww[T0_MAXD], at[T0_MAXD];
+#pragma unroll
+        for (int t = 0; t < T0_MAXD; t++) {
+            jj[t] = t < deg ? ld_row(A.nbr + e0 + t) : i;
+            ww[t] = t < deg ? ld_row(A.wts + e0 + t) : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < T0_MAXD; t++) at[t] = jj[t] != i ? ld_state(A.a_tot + jj[t]) : 0.0;
+        const double ki = A.k[i];
+        const double aoe = dsub(ld_state(A.a_tot + i), ki);
+        Best b{0.0, LBL(A.labels, i), i, 0.0, 0};
+#pragma unroll
+        for (int t = 0; t < T0_MAXD; t++) {
+            if (jj[t] == i) continue;
+            my++;
+            consider(b, gain_of(ww[t], 0.0, A.m, ki, aoe, at[t], A.four_m_sq),
+                     LBL(A.labels, jj[t]), jj[t], ww[t], 1);
+        }
+        finish_vertex(A, x, i, 0.0, b.g, b.c, b.e);
+    }
+    if (A.cand) {
+        for (int o = 16; o > 0; o >>= 1) my += __shfl_xor_sync(FULL, my, o);
+        if ((threadIdx.x & 31) == 0 && my) atomicAdd(A.cand, my);
+    }
+}
+
+// warp per vertex (tier 1)
+__global__ void __launch_bounds__(256) k_single_warp(DecideArgs A, TierRef L, int64_t cnt) {
+    if (!single_state(A)) return;
+    const int lane = threadIdx.x & 31;
+    unsigned long long my = 0;
+    for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < cnt;
+         q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t x = L.x[q];
+        const int32_t i = L.vid[q];
+        const int64_t e0 = L.row[q], e1 = L.end[q];
+        const double ki = A.k[i];
+        const double aoe = dsub(ld_state(A.a_tot + i), ki);
+        Best b{0.0, LBL(A.labels, i), i, 0.0, 0};
+        for (int64_t c0 = e0; c0 < e1; c0 += 128) {
+            int32_t jj[4];
+            double ww[4], at[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int64_t e = c0 + 32 * u + lane;
+                jj[u] = e < e1 ? ld_row(A.nbr + e) : i;
+                ww[u] = e < e1 ? ld_row(A.wts + e) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) at[u] = jj[u] != i ? ld_state(A.a_tot + jj[u]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                if (jj[u] == i) continue;
+                my++;
+                consider(b, gain_of(ww[u], 0.0, A.m, ki, aoe, at[u], A.four_m_sq),
+                         LBL(A.labels, jj[u]), jj[u], ww[u], 1);
+            }
+        }
+        warp_best(b);
+        if (lane == 0) finish_vertex(A, x, i, 0.0, b.g, b.c, b.e);
+    }
+    if (A.cand) {
+        for (int o = 16; o > 0; o >>= 1) my += __shfl_xor_sync(FULL, my, o);
+        if (lane == 0 && my) atomicAdd(A.cand, my);
+    }
+}
+
+// block per vertex (tiers 2-4, hubs included)
+constexpr int SB_NT = 512;
+__global__ void __launch_bounds__(SB_NT) k_single_block(DecideArgs A, TierRef L, int64_t cnt) {
+    if (!single_state(A)) return;
+    __shared__ BestSmem<SB_NT> S;
+    unsigned long long my = 0;
+    for (int64_t q = blockIdx.x; q < cnt; q += gridDim.x) {
+        const int64_t x = L.x[q];
+        const int32_t i = L.vid[q];
+        const int64_t e0 = L.row[q], e1 = L.end[q];
+        const double ki = A.k[i];
+        const double aoe = dsub(ld_state(A.a_tot + i), ki);
+        Best b{0.0, LBL(A.labels, i), i, 0.0, 0};
+        for (int64_t c0 = e0; c0 < e1; c0 += 4 * SB_NT) {
+            int32_t jj[4];
+            double ww[4], at[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int64_t e = c0 + (int64_t)SB_NT * u + threadIdx.x;
+                jj[u] = e < e1 ? ld_row(A.nbr + e) : i;
+                ww[u] = e < e1 ? ld_row(A.wts + e) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) at[u] = jj[u] != i ? ld_state(A.a_tot + jj[u]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                if (jj[u] == i) continue;
+                my++;
+                consider(b, gain_of(ww[u], 0.0, A.m, ki, aoe, at[u], A.four_m_sq),
+                         LBL(A.labels, jj[u]), jj[u], ww[u], 1);
+            }
+        }
+        b = block_best<SB_NT>(S, b);
+        if (threadIdx.x == 0) finish_vertex(A, x, i, 0.0, b.g, b.c, b.e);
+    }
+    if (A.cand) {
+        for (int o = 16; o > 0; o >>= 1) my += __shfl_xor_sync(FULL, my, o);
+        if ((threadIdx.x & 31) == 0 && my) atomicAdd(A.cand, my);
+    }
+}
+
+__global__ void k_single_check(const int32_t *assign, int64_t n, int *bad) {
+    bool b = false;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x)
+        b |= assign[v] != (int32_t)v;
+    if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
+cudaGraphNode_t add_single_check_nodes(cudaGraph_t g, cudaGraphNode_t dep, const int32_t *assign,
+                                       int64_t n, int *bad) {
+    cudaMemsetParams mp = {};
+    mp.dst = bad;
+    mp.value = 0;
+    mp.elementSize = sizeof(int);
+    mp.width = 1;
+    mp.height = 1;
+    cudaGraphNode_t ms, ks;
+    PLV_CUDA(cudaGraphAddMemsetNode(&ms, g, &dep, 1, &mp));
+    cudaKernelNodeParams kp = {};
+    void *args[] = {(void *)&assign, (void *)&n, (void *)&bad};
+    kp.func = (void *)k_single_check;
+    kp.gridDim = dim3(grid_for(n > 0 ? n : 1, 256, 148 * 16));
+    kp.blockDim = dim3(256);
+    kp.kernelParams = args;
+    PLV_CUDA(cudaGraphAddKernelNode(&ks, g, &ms, 1, &kp));
+    count_launch();
+    return ks;
+}
+
+void launch_single_check(const int32_t *assign, int64_t n, int *bad, cudaStream_t st) {
+    PLV_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    if (n > 0) {
+        k_single_check<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(assign, n, bad);
+        PLV_LAUNCH_CHECK();
+    }
+}
+
+static void launch_single_tier(const DecideArgs &A, TierRef L, int64_t cnt, int t,
+                               cudaStream_t st) {
+    if (!cnt) return;
+    if (t == 0)
+        k_single_t0<<<grid_for(cnt, 256), 256, 0, st>>>(A, L, cnt);
+    else if (t == 1)
+        k_single_warp<<<grid_for(cnt, 8), 256, 0, st>>>(A, L, cnt);
+    else
+        k_single_block<<<grid_for(cnt, 1, 148 * 8), SB_NT, 0, st>>>(A, L, cnt);
+    PLV_LAUNCH_CHECK();
+}
 
 // ================================================================ planning
 
@@ -1542,6 +1742,8 @@ static bool launch_small_t01(const Plan &P, int64_t a, const DecideArgs &A, cuda
     const int nb1 = sp.tcount[1] ? (int)grid_for(sp.tcount[1], 8) : 0;  // 8 warps per block
     launch_pdl(k_decide_t01, nb0 + nb1, 256, 0, st, A, tier_ref(P, sp, 0), sp.tcount[0],
                tier_ref(P, sp, 1), sp.tcount[1], nb0);
+    if (A.notsingle)
+        for (int t = 0; t < 2; t++) launch_single_tier(A, tier_ref(P, sp, t), sp.tcount[t], t, st);
     return true;
 }
 
@@ -1579,6 +1781,9 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
             A, tier_ref(P, sp, 3), sp.tcount[3]);
         PLV_LAUNCH_CHECK();
     }
+    if (A.notsingle)  // a first stage: the singleton kernels, after each tier's own
+        for (int t = 0; t < NTIER; t++)
+            launch_single_tier(A, tier_ref(P, sp, t), sp.tcount[t], t, ts[t]);
     cudaStream_t st = ts[4];
     if (sp.tcount[4]) {
         const int32_t *list = P.tier_list + sp.tstart[4];

@@ -52,6 +52,10 @@ struct DecideArgs {
     double *out_e_old;
     double *out_e_best;
     unsigned long long *cand;  // nullable: += distinct candidate communities
+    // First stage of an iteration: *notsingle == 0 when the state is the
+    // singleton state (assign[v] == v for all v) -- then the k_single_* kernels
+    // decide and the general tier kernels return at once; nullptr otherwise.
+    const int *notsingle = nullptr;
 };
 
 DecideArgs make_decide_args(const int64_t *off, const int32_t *nbr, const double *wts,
@@ -117,6 +121,12 @@ struct Plan {
 void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *stage_off_h,
                 int64_t nst, int64_t n, cudaStream_t s);
 void ensure_decide_attrs();
+// *bad = 1 unless assign[v] == v for every v (the singleton state of
+// PL/modularity.py:47-56); *bad must be 0 on entry.
+void launch_single_check(const int32_t *assign, int64_t n, int *bad, cudaStream_t st);
+// The same as graph nodes after `dep` (memset, scan); returns the last node.
+cudaGraphNode_t add_single_check_nodes(cudaGraph_t g, cudaGraphNode_t dep, const int32_t *assign,
+                                       int64_t n, int *bad);
 // Launch stage `a`'s decide kernels (no host synchronisation; capturable).
 void launch_decide(const Plan &P, int64_t a, DecideArgs A, cudaStream_t st);
 // Tier t on stream ts[t].

@@ -73,6 +73,7 @@ struct Phase {
     int64_t rank = 0, world = 1;
     void *comm = nullptr;       // ncclComm_t (partitioned, captured exchange)
     const int32_t *deg = nullptr;  // replicated degrees (partitioned rows: activity)
+    int *single_bad = nullptr;     // 0: the iteration starts from the singleton state
     unsigned char *xbuf = nullptr;  // exchange records: world x (largest slice) x 24 B
     std::vector<int64_t> xmax;      // per stage: largest slice
     int64_t xcap = 0;               // largest slice of any stage
@@ -145,7 +146,7 @@ struct Phase {
         fork = nullptr;
         plan.release();
         ab.release();
-        void *ps[] = {counters, q, mod_scratch, lvtx, fvtx, pos, xbuf};
+        void *ps[] = {counters, q, mod_scratch, lvtx, fvtx, pos, xbuf, single_bad};
         for (void *p : ps)
             pool_free(p);
         if (own_out) {
@@ -155,6 +156,7 @@ struct Phase {
         }
         lvtx = fvtx = pos = nullptr;
         xbuf = nullptr;
+        single_bad = nullptr;
         target = nullptr;
         moved = nullptr;
         e_old = e_best = nullptr;
@@ -166,7 +168,9 @@ struct Phase {
 };
 
 // Stage a's decide over this rank's slice (outputs at their global positions).
-static void record_decide(Phase &P, size_t a, cudaStream_t st) {
+// first: the iteration's first stage, which may see the singleton state
+// (*P.single_bad == 0: decided by the k_single_* kernels, decide.cu).
+static void record_decide(Phase &P, size_t a, cudaStream_t st, bool first = false) {
     const StagePlan &sp = P.plan.st[a];
     if (!sp.ns) return;
     const int64_t o = P.goff[a] + P.slo[a * (P.world + 1) + P.rank];
@@ -174,6 +178,7 @@ static void record_decide(Phase &P, size_t a, cudaStream_t st) {
                                     P.a_tot, P.sizes, P.m, (P.flags & PLV_F_INTEGRAL) ? 1 : 0,
                                     P.target + o, P.moved + o, P.e_old + o, P.e_best + o,
                                     P.counters + 1);
+    if (first) A.notsingle = P.single_bad;
     if (P.timing) PLV_CUDA(cudaEventRecordWithFlags(P.ev[2 * a], st, cudaEventRecordExternal));
     if (P.timing)
         launch_decide(P.plan, (int64_t)a, A, st);  // serial, so the events bracket all tiers
@@ -291,9 +296,12 @@ static void record_finish(Phase &P, cudaStream_t st) {
 
 static void record_iteration(Phase &P, cudaStream_t st) {
     PLV_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 2, st));
+    if (P.single_bad) launch_single_check(P.assign, P.n, P.single_bad, st);
+    bool first = true;
     for (size_t a = 0; a + 1 < P.goff.size(); a++) {
         if (P.goff[a + 1] == P.goff[a]) continue;
-        record_decide(P, a, st);
+        record_decide(P, a, st, first);
+        first = false;
         record_exchange(P, a, st);
         if (live_mode(P)) {
             record_live(P, a, st);
@@ -458,6 +466,10 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
         P->world = world;
         P->comm = comm;
         P->deg = deg;
+#ifndef PLV_SINGLE
+#define PLV_SINGLE 1  // the singleton-state decide of a phase's first stage (decide.cu)
+#endif
+        if (PLV_SINGLE) P->single_bad = dalloc<int>(1);
         P->goff.assign(stage_off_h, stage_off_h + nst + 1);
         ensure_decide_attrs();
         filter_active(*P, vtx, nst, s);
@@ -599,8 +611,11 @@ __global__ void k_run_start(RunCtl *c) { c->t0 = gtimer(); }
 // (PL/engine.py:203-212, _iteration_converged :134-137), loop condition.
 __global__ void k_run_ctl(RunCtl *c, const double *q, const unsigned long long *counters,
                           double *tr_q, unsigned long long *tr_mv, unsigned long long *tr_t,
-                          const unsigned long long *chash, cudaGraphConditionalHandle h) {
+                          const unsigned long long *chash, int *single_bad,
+                          cudaGraphConditionalHandle h) {
     pdl_wait();  // Q and the move counter
+    // a further iteration follows only after moves: no longer the singleton state
+    if (single_bad) *single_bad = 1;
     const double q_cur = *q;
     const unsigned long long moves = counters[0];
     const int64_t it = c->it;
@@ -759,7 +774,10 @@ static void build_run_graph(Phase &P, int64_t cap, cudaStream_t s) {
     cp.conditional.type = cudaGraphCondTypeWhile;
     cp.conditional.size = 1;
     cudaGraphNode_t loop;
-    PLV_CUDA(cudaGraphAddNode(&loop, P.rgraph, &start, 1, &cp));
+    cudaGraphNode_t before = start;
+    if (P.single_bad)  // iteration 0 may start from the singleton state
+        before = add_single_check_nodes(P.rgraph, start, P.assign, P.n, P.single_bad);
+    PLV_CUDA(cudaGraphAddNode(&loop, P.rgraph, &before, 1, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     int prio_lo = 0, prio_hi = 0;
     PLV_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
@@ -769,9 +787,11 @@ static void build_run_graph(Phase &P, int64_t cap, cudaStream_t s) {
                                            cudaStreamCaptureModeThreadLocal));
     try {
         PLV_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 2, cs));
+        bool first = true;
         for (size_t a = 0; a + 1 < P.goff.size(); a++) {
             if (P.goff[a + 1] == P.goff[a]) continue;
-            record_decide(P, a, cs);
+            record_decide(P, a, cs, first);
+            first = false;
             record_apply(P, a, cs, P.dirty, P.chash);
         }
         if (P.dirty)
@@ -781,7 +801,7 @@ static void build_run_graph(Phase &P, int64_t cap, cudaStream_t s) {
             modularity_async(P.w_int, P.a_tot, P.n, P.m, P.q, P.mod_scratch, cs);
         launch_pdl(k_run_ctl, 1, 1, 0, cs, P.ctl, (const double *)P.q,
                    (const unsigned long long *)P.counters, P.tr_q, P.tr_mv, P.tr_t,
-                   (const unsigned long long *)P.chash, h);
+                   (const unsigned long long *)P.chash, P.single_bad, h);
         if (P.chash) {
             k_cycle<<<grid_for(P.n, 256, 148 * 8), 256, 0, cs>>>(P.ctl, P.assign, P.sizes, P.a_tot,
                                                                 P.w_int, P.n, P.snap_i, P.snap_d);
