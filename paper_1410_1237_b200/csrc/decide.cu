@@ -1257,40 +1257,95 @@ __device__ __forceinline__ void single_entry(const DecideArgs &A, int32_t i, dou
     consider(b, g, LBL(A.labels, j), j, w, 1);
 }
 
-// thread per vertex (tier 0)
-__global__ void __launch_bounds__(256) k_single_t0(DecideArgs A, TierRef L, int64_t cnt) {
+// Tier 0, flattened: a warp takes 32 consecutive tier-0 vertices and walks
+// their entries 32 at a time (one entry per lane: row loads adjacent, every
+// a_tot gather of the chunk in flight, few registers); a segmented warp
+// argmax folds each chunk into the per-vertex bests in shared memory -- the
+// argmax is a total order, so its association does not matter.
+constexpr int SF_WARPS = 8;
+__global__ void __launch_bounds__(SF_WARPS * 32) k_single_t0(DecideArgs A, TierRef L, int64_t cnt) {
     if (!single_state(A)) return;
+    __shared__ int s_off[SF_WARPS][33];
+    __shared__ Best s_b[SF_WARPS][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     unsigned long long my = 0;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < cnt;
-         q += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t x = L.x[q];
-        const int32_t i = L.vid[q];
-        const int64_t e0 = L.row[q];
-        const int deg = (int)(L.end[q] - e0);
-        int32_t jj[T0_MAXD];
-        double ww[T0_MAXD], at[T0_MAXD];
-#pragma unroll
-        for (int t = 0; t < T0_MAXD; t++) {
-            jj[t] = t < deg ? ld_row(A.nbr + e0 + t) : i;
-            ww[t] = t < deg ? ld_row(A.wts + e0 + t) : 0.0;
+    for (int64_t q0 = ((int64_t)blockIdx.x * SF_WARPS + wid) * 32; q0 < cnt;
+         q0 += (int64_t)gridDim.x * SF_WARPS * 32) {
+        const int64_t q = q0 + lane;
+        const bool has = q < cnt;
+        const int32_t i = has ? L.vid[q] : 0;
+        const int64_t e0 = has ? L.row[q] : 0;
+        const int deg = has ? (int)(L.end[q] - e0) : 0;
+        // entry offsets of the 32 vertices (warp exclusive scan)
+        int inc = deg;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += y;
         }
-#pragma unroll
-        for (int t = 0; t < T0_MAXD; t++) at[t] = jj[t] != i ? ld_state(A.a_tot + jj[t]) : 0.0;
-        const double ki = A.k[i];
-        const double aoe = dsub(ld_state(A.a_tot + i), ki);
-        Best b{0.0, LBL(A.labels, i), i, 0.0, 0};
-#pragma unroll
-        for (int t = 0; t < T0_MAXD; t++) {
-            if (jj[t] == i) continue;
-            my++;
-            consider(b, gain_of(ww[t], 0.0, A.m, ki, aoe, at[t], A.four_m_sq),
-                     LBL(A.labels, jj[t]), jj[t], ww[t], 1);
+        s_off[wid][lane + 1] = inc;
+        if (lane == 0) s_off[wid][0] = 0;
+        s_b[wid][lane] = Best{0.0, LBL(A.labels, i), i, 0.0, 0};  // "stay"
+        __syncwarp();
+        const int T = __shfl_sync(FULL, inc, 31);
+        for (int c0 = 0; c0 < T; c0 += 32) {
+            const int p = c0 + lane;
+            int v = 0;  // owner: the last vertex with s_off[v] <= p
+            if (p < T) {
+                int lo = 0, hi = 32;
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_off[wid][mid] <= p)
+                        lo = mid;
+                    else
+                        hi = mid;
+                }
+                v = lo;
+            }
+            const int32_t vi = __shfl_sync(FULL, i, v);
+            const int64_t ve = __shfl_sync(FULL, e0, v);
+            Best b{-INFINITY, INT64_MAX, -1, 0.0, 0};  // neutral
+            if (p < T) {
+                const int64_t e = ve + (p - s_off[wid][v]);
+                const int32_t j = ld_row(A.nbr + e);
+                if (j != vi) {
+                    const double w = ld_row(A.wts + e);
+                    const double ki = A.k[vi];
+                    const double aoe = dsub(ld_state(A.a_tot + vi), ki);
+                    my++;
+                    b = Best{gain_of(w, 0.0, A.m, ki, aoe, ld_state(A.a_tot + j), A.four_m_sq),
+                             LBL(A.labels, j), j, w, 1};
+                }
+            }
+            // segmented argmax over the chunk (segments: owners)
+            const int vv = p < T ? v : 32;
+            for (int o = 1; o < 32; o <<= 1) {
+                Best y;
+                y.g = __shfl_down_sync(FULL, b.g, o);
+                y.l = __shfl_down_sync(FULL, b.l, o);
+                y.c = __shfl_down_sync(FULL, b.c, o);
+                y.e = __shfl_down_sync(FULL, b.e, o);
+                y.n = __shfl_down_sync(FULL, b.n, o);
+                const int yv = __shfl_down_sync(FULL, vv, o);
+                if (lane + o < 32 && yv == vv) consider(b, y.g, y.l, y.c, y.e, y.n);
+            }
+            // the first lane of each segment in the chunk now holds its best
+            const int pv = __shfl_up_sync(FULL, vv, 1);
+            if (vv < 32 && (lane == 0 || pv != vv)) {
+                Best h = s_b[wid][vv];
+                consider(h, b.g, b.l, b.c, b.e, b.n);
+                s_b[wid][vv] = h;
+            }
+            __syncwarp();
         }
-        finish_vertex(A, x, i, 0.0, b.g, b.c, b.e);
+        if (has) {
+            const Best b = s_b[wid][lane];
+            finish_vertex(A, L.x[q], i, 0.0, b.g, b.c, b.e);
+        }
+        __syncwarp();
     }
     if (A.cand) {
         for (int o = 16; o > 0; o >>= 1) my += __shfl_xor_sync(FULL, my, o);
-        if ((threadIdx.x & 31) == 0 && my) atomicAdd(A.cand, my);
+        if (lane == 0 && my) atomicAdd(A.cand, my);
     }
 }
 
@@ -1417,7 +1472,7 @@ static void launch_single_tier(const DecideArgs &A, TierRef L, int64_t cnt, int 
                                cudaStream_t st) {
     if (!cnt) return;
     if (t == 0)
-        k_single_t0<<<grid_for(cnt, 256), 256, 0, st>>>(A, L, cnt);
+        k_single_t0<<<grid_for(cnt, SF_WARPS * 32), SF_WARPS * 32, 0, st>>>(A, L, cnt);
     else if (t == 1)
         k_single_warp<<<grid_for(cnt, 8), 256, 0, st>>>(A, L, cnt);
     else
