@@ -37,7 +37,6 @@ through host copies (the multi-process tests on one GPU).
 from __future__ import annotations
 
 import logging
-import math
 import time
 from dataclasses import dataclass, field
 
