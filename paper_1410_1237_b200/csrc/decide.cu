@@ -1472,7 +1472,10 @@ void launch_single_check(const int32_t *assign, int64_t n, int *bad, cudaStream_
 static void launch_single_tier(const DecideArgs &A, TierRef L, int64_t cnt, int t,
                                cudaStream_t st) {
     if (!cnt) return;
-    if (t == 0)
+#ifndef PLV_SINGLE_FLAT_MAXT
+#define PLV_SINGLE_FLAT_MAXT 1  // tiers decided by the flattened kernel (0..this)
+#endif
+    if (t <= PLV_SINGLE_FLAT_MAXT)
         k_single_t0<<<grid_for(cnt, SF_WARPS * 32), SF_WARPS * 32, 0, st>>>(A, L, cnt);
     else if (t == 1)
         k_single_warp<<<grid_for(cnt, 8), 256, 0, st>>>(A, L, cnt);
