@@ -850,7 +850,6 @@ struct HubScratch {
                          // updates and the pass's three reads touch ONE 32-byte sector
     int32_t *cbuf;       // [entries] community of every hub entry (-1: self loop)
     int64_t dn;
-    const uint16_t *eidx;  // [entries] the hub of every entry (nullptr: search eoff)
 };
 
 // Largest hub q with eoff[q] <= t.
@@ -888,7 +887,7 @@ __global__ void k_hub_accum(DecideArgs A, const int64_t *eoff, const int64_t *to
         double w = 0.0, wv = 0.0;
         int64_t q = 0;
         if (t < E) {  // the static part of the entry (graph, plan)
-            q = H.eidx ? (int64_t)H.eidx[t] : hub_of(eoff, nh, t);
+            q = hub_of(eoff, nh, t);
             i = H.vid[q];
             const int64_t e = H.row[q] + (t - eoff[q]);
             j = ld_row(A.nbr + (e));
@@ -1539,12 +1538,6 @@ __global__ void k_hub_degrees(const int64_t *off, const int32_t *vtx, const int6
     }
 }
 
-__global__ void k_hub_eidx(const int64_t *eoff, int64_t nh, int64_t E, uint16_t *out) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < E;
-         t += (int64_t)gridDim.x * blockDim.x)
-        out[t] = (uint16_t)hub_of(eoff, nh, t);
-}
-
 __global__ void k_fill_drec(DenseRec *p, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -1561,7 +1554,7 @@ void Plan::release() {
     cudaDeviceSynchronize();  // buffers go back to the pool idle
     void *ps[] = {tier_list, tier_vid, tier_row, tier_end, hub_eoff, hub_toff, hub_poff, hub_blk, hub_row, hub_vid, hkeys,
                   hvals,     hcnt,     hsold,    hncnt,    hnear,   hpart,
-                  drec,      cbuf,     hub_eidx};
+                  drec,      cbuf};
     for (void *p : ps)
         pool_free(p);
     tier_list = nullptr;
@@ -1575,7 +1568,6 @@ void Plan::release() {
     hpart = nullptr;
     drec = nullptr;
     cbuf = nullptr;
-    hub_eidx = nullptr;
 }
 
 void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *stage_off_h,
@@ -1714,24 +1706,6 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
                              cudaMemcpyHostToDevice, s));
     PLV_CUDA(cudaMemcpyAsync(P.hub_blk, blk.data(), sizeof(int64_t) * blk.size(),
                              cudaMemcpyHostToDevice, s));
-    // the hub of every stage entry, so k_hub_accum needs no search over eoff
-    int64_t tot_e = 0;
-    bool small = true;
-    for (int64_t a = 0; a < nst; a++) {
-        P.st[a].hub_ebase = tot_e;
-        tot_e += P.st[a].hub_entries;
-        small &= P.st[a].tcount[4] <= 65535;
-    }
-    if (small && tot_e > 0) {
-        P.hub_eidx = dalloc<uint16_t>(tot_e);
-        for (int64_t a = 0; a < nst; a++) {
-            const StagePlan &sp = P.st[a];
-            if (!sp.hub_entries) continue;
-            k_hub_eidx<<<grid_for(sp.hub_entries, 256), 256, 0, s>>>(
-                P.hub_eoff + sp.hub_base, sp.tcount[4], sp.hub_entries, P.hub_eidx + sp.hub_ebase);
-            PLV_LAUNCH_CHECK();
-        }
-    }
     int64_t T = P.max_table;
     P.hkeys = dalloc<int32_t>(T);
     P.hvals = dalloc<double>(T);
@@ -1887,8 +1861,7 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
                      nh,
                      P.drec,
                      P.cbuf,
-                     P.dn,
-                     P.hub_eidx ? P.hub_eidx + sp.hub_ebase : nullptr};
+                     P.dn};
         unsigned g2 = (unsigned)sp.hub_nblk;
         if (sp.hub_dense) {
             launch_pdl(k_hub_accum<true>, grid_for(E, 256), 256, 0, st, A, eoff, toff, nh, E,

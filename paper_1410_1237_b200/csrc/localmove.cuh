@@ -72,7 +72,6 @@ struct StagePlan {
     int64_t hub_entries = 0;
     int64_t hub_nblk = 0;      // hub pass blocks (one per candidate slice)
     int64_t hub_blk_base = 0;  // first of them in hub_blk
-    int64_t hub_ebase = 0;     // first of the stage's entries in hub_eidx
     bool hub_dense = false;    // hub tier on dense per-hub community arrays
 };
 
@@ -113,7 +112,6 @@ struct Plan {
     Best *hpart = nullptr;      // pass partial bests
     DenseRec *drec = nullptr;   // dense hub records [dense_k * n] (idle: 0 / 0 / INT_MAX)
     int32_t *cbuf = nullptr;    // communities of a dense stage's hub entries
-    uint16_t *hub_eidx = nullptr;  // the hub of every hub entry, stage after stage
     int64_t dn = 0, max_dense_entries = 0, dense_k = 0;
     int64_t max_slices = 1;
     void release();
