@@ -29,7 +29,6 @@
 #include "localmove.cuh"
 #include "lm_device.cuh"
 #include "csr.cuh"
-#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 namespace plv {
@@ -1484,209 +1483,6 @@ static void launch_single_tier(const DecideArgs &A, TierRef L, int64_t cnt, int 
     PLV_LAUNCH_CHECK();
 }
 
-// -------------------------- tier 4, integral graphs: one cluster per hub
-//
-// A colour class of few hubs in an INTEGRAL graph (every weight an integer,
-// 2m < 2^31: C1, C4 and their coarse levels): each hub's any-order sums are
-// exact in 32-bit integers, so its table can live in a thread-block
-// cluster's distributed shared memory with NATIVE 32-bit atomics (a float64
-// add on DSMEM is a CAS loop, SASS ATOMS.CAST.SPIN.64 -- the round-2 f64
-// attempt lost to contention).  One launch decides the class: HCI_CL CTAs per
-// hub accumulate their chunk of the row (warp groups of equal communities
-// pre-summed) into the owner CTA's slice (low hash bits), then each CTA scans
-// its slice -- gain from the exact sums, its best -- and rank 0 reduces the
-// bests and finishes the vertex.  Integral sums need no certification: the
-// argmax on exact sums is the reference's decision (decide_moves,
-// PL/_kernels.pyx:21-101).  Replaces k_hub_accum + k_hub_pass for such
-// classes.
-constexpr int HCI_CL = 16;                // CTAs per hub (non-portable cluster)
-constexpr int HCI_NT = 512;
-constexpr int HCI_TS = 12288;             // slots per CTA: key, sum, count (12 B)
-constexpr int64_t HCI_MAXD = (int64_t)HCI_CL * HCI_TS / 2;
-
-struct HubCiArgs {
-    const int32_t *list;  // [nh] stage-local index
-    const int32_t *vid;
-    const int64_t *row;
-    const int64_t *eoff;
-};
-
-static size_t hci_smem() { return (size_t)HCI_TS * 3 * sizeof(int32_t); }
-
-__global__ void __launch_bounds__(HCI_NT, 1) k_hub_cluster_int(DecideArgs A, HubCiArgs H) {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cl = cg::this_cluster();
-    extern __shared__ __align__(16) unsigned char dsm[];
-    __shared__ BestSmem<HCI_NT> BS;
-    __shared__ Best cb[HCI_CL];
-    __shared__ int32_t s_fold;
-    int32_t *keys = reinterpret_cast<int32_t *>(dsm);
-    int32_t *sums = keys + HCI_TS;
-    int32_t *cnts = sums + HCI_TS;
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int r = (int)cl.block_rank();
-    const int64_t q = blockIdx.x / HCI_CL;
-    for (int t = tid; t < HCI_TS; t += HCI_NT) {
-        keys[t] = -1;
-        sums[t] = 0;
-        cnts[t] = 0;
-    }
-    const int32_t i = H.vid[q];
-    const int64_t x = H.list[q];
-    const int64_t e0 = H.row[q], deg = H.eoff[q + 1] - H.eoff[q];
-    const int64_t chunk = (deg + HCI_CL - 1) / HCI_CL;
-    const int64_t c0 = e0 + (int64_t)r * chunk;
-    const int64_t c1 = c0 + chunk < e0 + deg ? c0 + chunk : e0 + deg;
-    pdl_wait();  // the previous stage's state
-    if (single_state(A)) return;  // (never: a tail class; kept for symmetry)
-    const int32_t c_old = ld_state(A.assign + i);
-    const double ki = A.k[i];
-    cl.sync();  // every slice initialised before any remote insert
-    for (int64_t b0 = c0; b0 < c1; b0 += 2 * HCI_NT) {
-        int32_t cc[2], ww[2];
-#pragma unroll
-        for (int u = 0; u < 2; u++) {
-            const int64_t e = b0 + (int64_t)u * HCI_NT + tid;
-            int32_t j = i;
-            double w = 0.0;
-            if (e < c1) {
-                j = ld_row(A.nbr + e);
-                w = ld_row(A.wts + e);
-            }
-            cc[u] = j;
-            ww[u] = (int32_t)w;  // integral weight, < 2^31
-        }
-#pragma unroll
-        for (int u = 0; u < 2; u++) cc[u] = cc[u] != i ? ld_state(A.assign + cc[u]) : -1;
-#pragma unroll
-        for (int u = 0; u < 2; u++) {
-            const int32_t c = cc[u];
-            const unsigned grp = __match_any_sync(FULL, c);
-            // the group's exact sum (integers); every shuffle is full-warp and
-            // in a warp-uniform loop (groups differ in size)
-            int32_t gs = 0;
-            {
-                const int nmax = (int)__reduce_max_sync(FULL, (unsigned)__popc(grp));
-                unsigned g = grp;
-                for (int t = 0; t < nmax; t++) {
-                    const int src = g ? __ffs(g) - 1 : lane;
-                    const int32_t v = __shfl_sync(FULL, ww[u], src);
-                    if (g) {
-                        gs += v;
-                        g &= g - 1;
-                    }
-                }
-            }
-            if (c >= 0 && lane == __ffs(grp) - 1) {
-                const uint32_t h = hslot(c, 0xffffffffu);
-                const unsigned owner = h % HCI_CL;
-                int32_t *rk = cl.map_shared_rank(keys, owner);
-                uint32_t sl = (h / HCI_CL) % HCI_TS;
-                while (true) {
-                    const int32_t old = atomicCAS(rk + sl, -1, c);
-                    if (old == -1 || old == c) break;
-                    sl = sl + 1 == HCI_TS ? 0 : sl + 1;
-                }
-                atomicAdd(cl.map_shared_rank(sums, owner) + sl, gs);
-                atomicAdd(cl.map_shared_rank(cnts, owner) + sl, __popc(grp));
-            }
-        }
-    }
-    cl.sync();
-    if (tid == 0) {  // c_old's exact sum, from its owner's slice
-        const uint32_t h = hslot(c_old, 0xffffffffu);
-        const unsigned owner = h % HCI_CL;
-        const int32_t *rk = cl.map_shared_rank(keys, owner);
-        uint32_t sl = (h / HCI_CL) % HCI_TS;
-        int32_t f = 0;
-        while (true) {
-            const int32_t k = rk[sl];
-            if (k == c_old) {
-                f = cl.map_shared_rank(sums, owner)[sl];
-                break;
-            }
-            if (k == -1) break;
-            sl = sl + 1 == HCI_TS ? 0 : sl + 1;
-        }
-        s_fold = f;
-    }
-    __syncthreads();
-    const double f_old = (double)s_fold;  // exact
-    const double aoe = dsub(ld_state(A.a_tot + c_old), ki);
-    Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
-    unsigned long long nc = 0;
-    for (int t0 = tid; t0 < HCI_TS; t0 += 4 * HCI_NT) {
-        int32_t c[4];
-        double F[4], at[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const int t = t0 + u * HCI_NT;
-            c[u] = t < HCI_TS ? keys[t] : -1;
-            F[u] = c[u] >= 0 ? (double)sums[t] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; u++) at[u] = c[u] >= 0 && c[u] != c_old ? ld_state(A.a_tot + c[u]) : 0.0;
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            if (c[u] < 0) continue;
-            nc++;
-            if (c[u] == c_old) continue;
-            consider(b, gain_of(F[u], f_old, A.m, ki, aoe, at[u], A.four_m_sq), LBL(A.labels, c[u]),
-                     c[u], F[u], 0);
-        }
-    }
-    if (A.cand) {
-        for (int o = 16; o > 0; o >>= 1) nc += __shfl_xor_sync(FULL, nc, o);
-        if (lane == 0 && nc) atomicAdd(A.cand, nc);
-    }
-    b = block_best<HCI_NT>(BS, b);
-    if (tid == 0) cl.map_shared_rank(cb, 0)[r] = b;
-    cl.sync();  // rank 0 reads the bests; the others may leave
-    if (r == 0 && tid == 0) {
-        Best bw = cb[0];
-        for (int t = 1; t < HCI_CL; t++) consider(bw, cb[t].g, cb[t].l, cb[t].c, cb[t].e, cb[t].n);
-        finish_vertex(A, x, c_old, f_old, bw.g, bw.c, bw.e);
-    }
-}
-
-#ifndef PLV_HUB_CINT
-#define PLV_HUB_CINT 1
-#endif
-
-static int hci_ok_dev = INT_MIN;  // dev: usable on dev; -2 - dev: not usable on dev
-
-static bool hci_available() {
-    int dev = 0;
-    PLV_CUDA(cudaGetDevice(&dev));
-    if (hci_ok_dev == dev) return true;
-    if (hci_ok_dev == -1 - dev - 1) return false;
-    bool ok = cudaFuncSetAttribute(k_hub_cluster_int, cudaFuncAttributeNonPortableClusterSizeAllowed,
-                                   1) == cudaSuccess &&
-              cudaFuncSetAttribute(k_hub_cluster_int, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)hci_smem()) == cudaSuccess;
-    if (ok) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(HCI_CL);
-        cfg.blockDim = dim3(HCI_NT);
-        cfg.dynamicSmemBytes = hci_smem();
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = HCI_CL;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        int nclu = 0;
-        ok = cudaOccupancyMaxActiveClusters(&nclu, k_hub_cluster_int, &cfg) == cudaSuccess &&
-             nclu > 0;
-    }
-    cudaGetLastError();
-    hci_ok_dev = ok ? dev : -1 - dev - 1;
-    return ok;
-}
-
-bool hub_cint_usable() { return PLV_HUB_CINT && hci_available(); }
-
 // ================================================================ planning
 
 __global__ void k_tier_keys(const int64_t *off, const int32_t *vtx, const int64_t *stage_off,
@@ -1866,10 +1662,8 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
         // few hubs: dense per-hub community arrays (no claims), items are row
         // positions; else hash tables, items are table slices
         sp.hub_dense = sp.tcount[4] > 0 && sp.tcount[4] <= P.dense_k;
-        sp.hub_cint = sp.hub_dense && P.cint_ok;
         for (int64_t z = 0; z < sp.tcount[4]; z++) {
             int64_t d = deg[h0 + z];
-            if (d > HCI_MAXD) sp.hub_cint = false;
             int64_t cap = 64;
             while (cap < 2 * d + 2) cap <<= 1;
             int64_t sl = sp.hub_dense ? (d + HSB - 1) / HSB : (cap + HTSL - 1) / HTSL;
@@ -2069,25 +1863,7 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
                      P.cbuf,
                      P.dn};
         unsigned g2 = (unsigned)sp.hub_nblk;
-        if (sp.hub_cint && A.integral) {
-            HubCiArgs C{list, P.hub_vid + sp.hub_base, P.hub_row + sp.hub_base, eoff};
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3((unsigned)(nh * HCI_CL));
-            cfg.blockDim = dim3(HCI_NT);
-            cfg.dynamicSmemBytes = hci_smem();
-            cfg.stream = st;
-            cudaLaunchAttribute at[2];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = HCI_CL;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            at[1].val.programmaticStreamSerializationAllowed = 1;
-            cfg.attrs = at;
-            cfg.numAttrs = 2;
-            PLV_CUDA(cudaLaunchKernelEx(&cfg, k_hub_cluster_int, A, C));
-            count_launch();
-        } else if (sp.hub_dense) {
+        if (sp.hub_dense) {
             launch_pdl(k_hub_accum<true>, grid_for(E, 256), 256, 0, st, A, eoff, toff, nh, E,
                        P.hkeys, P.hvals, P.hcnt, H);
             launch_pdl(k_hub_pass<true>, g2, HSB, 0, st, A, list, eoff, toff, P.hkeys, P.hvals,

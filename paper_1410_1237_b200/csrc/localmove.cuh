@@ -73,7 +73,6 @@ struct StagePlan {
     int64_t hub_nblk = 0;      // hub pass blocks (one per candidate slice)
     int64_t hub_blk_base = 0;  // first of them in hub_blk
     bool hub_dense = false;    // hub tier on dense per-hub community arrays
-    bool hub_cint = false;     // ... or, integral graphs, one DSMEM cluster per hub
 };
 
 struct Best;  // decide.cu
@@ -115,7 +114,6 @@ struct Plan {
     int32_t *cbuf = nullptr;    // communities of a dense stage's hub entries
     int64_t dn = 0, max_dense_entries = 0, dense_k = 0;
     int64_t max_slices = 1;
-    bool cint_ok = false;      // set before plan_build: integral, 2m < 2^31, clusters usable
     void release();
 };
 
@@ -123,9 +121,6 @@ struct Plan {
 void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *stage_off_h,
                 int64_t nst, int64_t n, cudaStream_t s);
 void ensure_decide_attrs();
-// Whether the cluster hub kernel of integral graphs may be planned (device
-// support for 16-CTA clusters); PLV_HUB_CINT=0 builds disable it.
-bool hub_cint_usable();
 // *bad = 1 unless assign[v] == v for every v (the singleton state of
 // PL/modularity.py:47-56); *bad must be 0 on entry.
 void launch_single_check(const int32_t *assign, int64_t n, int *bad, cudaStream_t st);

@@ -515,8 +515,6 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
                                              sizeof(int32_t) * c, cudaMemcpyDeviceToDevice, s));
             }
         }
-        // integral graphs (2m < 2^31): few-hub classes on DSMEM clusters
-        P->plan.cint_ok = (flags & PLV_F_INTEGRAL) && 2.0 * m < 2147483647.0 && hub_cint_usable();
         plan_build(P->plan, off, P->lvtx, loff.data(), nst, n, s);
         if (comm) {  // exchange records + the slice table on device
             P->xmax.assign(nst, 0);
