@@ -61,7 +61,8 @@ def _whole(scale):
 
 @pytest.mark.parametrize("world,cfg,chunk,nccl", [
     (2, "colored", 1 << 30, False), (3, "colored", 7919, False), (2, "uncolored", 1 << 30, False),
-    (1, "colored", 1 << 30, True), (1, "uncolored", 1 << 30, True)])
+    (1, "colored", 1 << 30, True), (1, "uncolored", 1 << 30, True),
+    (4, "colored", 1 << 30, False)])
 def test_partitioned_pipeline(world, cfg, chunk, nccl):
     """W gloo ranks (host-stepped stages), or one rank with a 1-rank NCCL
     communicator (the iteration graph with its captured all-gathers and, for
