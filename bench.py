@@ -173,7 +173,7 @@ def _peak_hbm():
         return 6650.0, "fallback"
 
 
-DECIDE_KERNELS = ("k_decide_", "k_hub_accum", "k_hub_pass", "k_single_")
+DECIDE_KERNELS = ("k_decide_", "k_hub_accum", "k_hub_pass", "k_single_", "k_ah_accum", "k_ah_pass")
 
 
 def _cupti_decide_ms(step):

@@ -251,6 +251,12 @@ int plv_nccl_comm_destroy(void *comm);
 /* Kernel nodes in the engine's single-iteration CUDA graph (captured now if
  * needed): the kernels one plv_phase_iterate launches. */
 int plv_phase_graph_kernels(void *handle, int64_t *n_h);
+/* Ahead tables of the engine's plan (integral coloured single-rank phases:
+ * small high-degree colour classes are decided from per-vertex tables
+ * accumulated at the start of their window of stages, csrc/ahead.cuh):
+ * out_h[0] stages, [1] vertices, [2] windows, [3] static fix entries,
+ * [4] table slots.  All zero when the plan has none. */
+int plv_phase_ahead_stats(void *handle, int64_t *out_h);
 /* Sum over stages of the decide time of the last iteration (timing handles). */
 int plv_phase_decide_ms(void *handle, double *ms_h);
 int plv_phase_destroy(void *handle);

@@ -80,6 +80,7 @@ _SIGS = {
     "plv_phase_run": [_P, _D, _I64, _P, _P, _P, _P, _P],
     "plv_phase_decide_ms": [_P, _P],
     "plv_phase_graph_kernels": [_P, _P],
+    "plv_phase_ahead_stats": [_P, _P],
     "plv_phase_destroy": [_P],
     "plv_rebuild_records": [_P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P],
     "plv_compose": [_P, _P, _P, _I64, _P, _P],

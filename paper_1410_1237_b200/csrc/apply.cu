@@ -20,6 +20,10 @@
 #include "pairwise.cuh"
 #include <cub/cub.cuh>
 
+#ifndef AH_TRIGGER
+#define AH_TRIGGER 0
+#endif
+
 namespace plv {
 
 __global__ void k_fill_i32_a(int32_t *p, int64_t n, int32_t v) {
@@ -169,13 +173,22 @@ __global__ void __launch_bounds__(256) k_stage_live(StageArgs A) {
 // scatter for independent stages).  Low-degree movers fold their live
 // e_a / e_b here; high-degree ones go to the k_stage_big worklist.
 __global__ void __launch_bounds__(256) k_stage_prep(StageArgs A) {
+#if AH_TRIGGER
+    if (A.fx.tab) pdl_trigger();  // an ahead stage: the next pass may preload its plan
+#endif
     pdl_wait();  // launched programmatically after its predecessor
+    // an ahead stage: the blocks from fx.pb on push its movers' weights into
+    // the ahead tables of later stages (ahead.cuh)
+    if (A.fx.n && blockIdx.x >= A.fx.pb) {
+        ahead_fixup(A.fx, blockIdx.x);
+        return;
+    }
     if (A.lcnt && blockIdx.x == 0 && threadIdx.x == 0) *A.lcnt = 0ull;  // long runs of this stage
     const bool indep = A.flags & PLV_F_INDEPENDENT;
     const bool integral = A.flags & PLV_F_INTEGRAL;
     int lane = threadIdx.x & 31;
     int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int64_t nw = ((int64_t)(A.fx.n ? A.fx.pb : gridDim.x) * blockDim.x) >> 5;
     unsigned long long my_moves = 0;
     for (int64_t base = gw * 32; base < A.ns; base += nw * 32) {
         int64_t x = base + lane;
@@ -596,7 +609,12 @@ void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {
     S.lcnt = B.lcnt;
     // worklist counters are zero on entry: allocation clears them, and the
     // apply that used them last cleared them after its last reader
-    launch_pdl(k_stage_prep, grid_for((S.ns + 31) / 32 * 32, 256, 148 * 16), 256, 0, st, S);
+    unsigned nbp = grid_for((S.ns + 31) / 32 * 32, 256, 148 * 16);
+    if (S.fx.n) {  // + one thread per fix entry of an ahead stage
+        S.fx.pb = nbp;
+        nbp += (unsigned)((S.fx.n + 255) / 256);
+    }
+    launch_pdl(k_stage_prep, nbp, 256, 0, st, S);
     if (!indep) {
         launch_pdl(k_stage_live, APPLY_HB + APPLY_BB, 256, 0, st, S);
     }

@@ -30,6 +30,7 @@
 #include "lm_device.cuh"
 #include "csr.cuh"
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 namespace plv {
 
@@ -86,17 +87,8 @@ __device__ __forceinline__ double gain_slack(double Fc, int32_t Lc, double Fo, i
            8.0 * U_RND * (fabs(Fc - Fo) / m + fabs(g)) + 1e-300;
 }
 
-// Table slot of community c: murmur3's 32-bit finaliser (community ids of a
-// hub's neighbours share low bits, so a plain multiplicative hash clusters).
-__device__ __forceinline__ uint32_t hslot(int32_t c, uint32_t mask) {
-    uint32_t h = (uint32_t)c;
-    h ^= h >> 16;
-    h *= 0x85EBCA6Bu;
-    h ^= h >> 13;
-    h *= 0xC2B2AE35u;
-    h ^= h >> 16;
-    return h & mask;
-}
+// Table slot of community c (comm_hash, lm_device.cuh).
+__device__ __forceinline__ uint32_t hslot(int32_t c, uint32_t mask) { return comm_hash(c) & mask; }
 
 // Open-addressing geometry: power-of-two tables (mask) and arbitrary-size
 // tables (multiply-shift range reduction of the same hash), linear probing.
@@ -1483,6 +1475,10 @@ static void launch_single_tier(const DecideArgs &A, TierRef L, int64_t cnt, int 
     PLV_LAUNCH_CHECK();
 }
 
+}  // namespace plv
+#include "ahead.cuh"
+namespace plv {
+
 // ================================================================ planning
 
 __global__ void k_tier_keys(const int64_t *off, const int32_t *vtx, const int64_t *stage_off,
@@ -1568,10 +1564,16 @@ void Plan::release() {
     hpart = nullptr;
     drec = nullptr;
     cbuf = nullptr;
+    if (ah) {
+        ah->release();
+        delete ah;
+        ah = nullptr;
+    }
 }
 
 void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *stage_off_h,
-                int64_t nst, int64_t n, cudaStream_t s) {
+                int64_t nst, int64_t n, cudaStream_t s, const int32_t *nbr, const double *wts,
+                bool ahead_ok) {
     int64_t total = stage_off_h[nst];
     P.st.assign(nst, StagePlan{});
     for (int64_t a = 0; a < nst; a++) {
@@ -1613,6 +1615,15 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
             sp.tstart[t] = pos;
             sp.tcount[t] = (int64_t)h[NTIER * a + t];
             pos += sp.tcount[t];
+        }
+    }
+    // small high-degree stages of an integral coloured phase: ahead tables
+    if (ahead_ok && nbr && wts) ahead_plan(P, off, nbr, wts, vtx, stage_off_h, d_soff, nst, n, s);
+    for (int64_t a = 0; a < nst; a++) {
+        StagePlan &sp = P.st[a];
+        if (sp.ahead) {
+            for (int t = 0; t < NTIER; t++) sp.tcount[t] = 0;
+            continue;
         }
         // a small colour class with hubs: its block-tier vertices join the
         // hub tier (their lists directly precede it) -- one vertex per block
@@ -1807,6 +1818,10 @@ static bool launch_small_t01(const Plan &P, int64_t a, const DecideArgs &A, cuda
 
 void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStream_t *ts) {
     const StagePlan &sp = P.st[a];
+    if (sp.ahead) {
+        ahead_launch_decide(P, a, A, ts[NTIER - 1]);
+        return;
+    }
     if (sp.tcount[0]) {
         k_decide_t0<<<grid_for(sp.tcount[0], 256), 256, 0, ts[0]>>>(A, tier_ref(P, sp, 0),
                                                                     sp.tcount[0]);
@@ -1875,6 +1890,16 @@ void launch_decide_tiers(const Plan &P, int64_t a, DecideArgs A, const cudaStrea
                        P.hcnt, H);
         }
     }
+}
+
+void ahead_stats(const Plan &P, int64_t *out) {
+    for (int t = 0; t < 5; t++) out[t] = 0;
+    if (!P.ah) return;
+    for (const StagePlan &sp : P.st) out[0] += sp.ahead;
+    out[1] = P.ah->nvert;
+    out[2] = (int64_t)P.ah->wins.size();
+    out[3] = P.ah->nfix;
+    out[4] = P.ah->nslots;
 }
 
 DecideArgs make_decide_args(const int64_t *off, const int32_t *nbr, const double *wts,

@@ -16,6 +16,59 @@ __device__ __forceinline__ int64_t LBL(const int32_t *labels, int32_t c) {
     return labels ? (int64_t)labels[c] : (int64_t)c;
 }
 
+// Community hash of the decide tables: murmur3's 32-bit finaliser (community
+// ids of a hub's neighbours share low bits, so a plain multiplicative hash
+// clusters).
+__device__ __forceinline__ uint32_t comm_hash(int32_t c) {
+    uint32_t h = (uint32_t)c;
+    h ^= h >> 16;
+    h *= 0x85EBCA6Bu;
+    h ^= h >> 13;
+    h *= 0xC2B2AE35u;
+    h ^= h >> 16;
+    return h;
+}
+
+// Ahead tables (ahead.cuh): find-or-insert community c by CAS alone; reports
+// whether this call inserted the key.  The table always keeps an empty slot.
+__device__ __forceinline__ uint32_t ahead_claim(AheadRec *t, int32_t c, uint32_t mask, bool *fresh) {
+    uint32_t s = comm_hash(c) & mask;
+    while (true) {
+        const int32_t old = atomicCAS(&t[s].key, -1, c);
+        if (old == -1 || old == c) {
+            *fresh = old == -1;
+            return s;
+        }
+        s = (s + 1) & mask;
+    }
+}
+
+// One fix entry per thread: the ahead vertex `src` of this stage moved from
+// community a to b, so its weight in the table of the later ahead vertex
+// `dst` moves with it (exact: integral weights).  b's slot may be new; if b is
+// dst's own community, dst's c_old slot is recorded.
+__device__ __forceinline__ void ahead_fixup(const AheadFix &F, unsigned blk) {
+    const int64_t e = (int64_t)(blk - F.pb) * blockDim.x + threadIdx.x;
+    if (e >= F.n) return;
+    const int32_t src = F.src[e];
+    const int2 mv = __ldcg(F.amove + src);
+    if (mv.x < 0) return;
+    const int32_t dst = F.dst[e];
+    const double w = F.w[e];
+    AheadRec *t = F.tab + F.tbase[dst];
+    const uint32_t mask = F.tmask[dst];
+    uint32_t s = comm_hash(mv.x) & mask;
+    for (uint32_t it = 0; it <= mask; it++) {  // a's slot exists: src was counted there
+        if (__ldcg(&t[s].key) == mv.x) break;
+        s = (s + 1) & mask;
+    }
+    atomicAdd(&t[s].val, -w);
+    bool fresh;
+    const uint32_t s2 = ahead_claim(t, mv.y, mask, &fresh);
+    atomicAdd(&t[s2].val, w);
+    if (fresh && mv.y == F.cold[dst]) F.sold[dst] = (int32_t)s2;
+}
+
 // (gain, label) lexicographic order of PL/_kernels.pyx:88.
 __device__ __forceinline__ bool better(double g1, int64_t l1, double g2, int64_t l2) {
     return g1 > g2 || (g1 == g2 && l1 < l2);

@@ -73,9 +73,33 @@ struct StagePlan {
     int64_t hub_nblk = 0;      // hub pass blocks (one per candidate slice)
     int64_t hub_blk_base = 0;  // first of them in hub_blk
     bool hub_dense = false;    // hub tier on dense per-hub community arrays
+    bool ahead = false;        // decided from tables accumulated ahead (ahead.cuh)
 };
 
 struct Best;  // decide.cu
+struct Ahead;  // ahead.cuh: tables of small colour classes accumulated ahead
+
+// A slot of an ahead table: community and its exact integer-valued sum.
+struct __align__(16) AheadRec {
+    int32_t key;  // -1: empty
+    int32_t pad;
+    double val;
+};
+
+// What a stage's apply needs to push its movers' changes into the ahead tables
+// of later stages of the same window (ahead.cuh).
+struct AheadFix {
+    int64_t n = 0;    // fix entries of this stage (0: none)
+    unsigned pb = 0;  // first fix block of the apply launch
+    const int32_t *src = nullptr, *dst = nullptr;  // ahead vertex that may move -> later one
+    const double *w = nullptr;
+    const int2 *amove = nullptr;  // per ahead vertex: (c_old, c_new) of its move, or (-1, -1)
+    AheadRec *tab = nullptr;
+    const int64_t *tbase = nullptr;
+    const uint32_t *tmask = nullptr;
+    const int32_t *cold = nullptr;
+    int32_t *sold = nullptr;
+};
 
 // A dense hub-array entry (hub, community): any-order sum, term count, first
 // row position.  16-byte aligned, so one record never spans two sectors.
@@ -114,12 +138,16 @@ struct Plan {
     int32_t *cbuf = nullptr;    // communities of a dense stage's hub entries
     int64_t dn = 0, max_dense_entries = 0, dense_k = 0;
     int64_t max_slices = 1;
+    Ahead *ah = nullptr;  // ahead tables (integral coloured phases; ahead.cuh)
     void release();
 };
 
 
+// nbr / wts / ahead_ok: stages of at most AH_MAX_NS high-degree vertices of an
+// integral, single-rank, coloured phase are planned for the ahead tables.
 void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *stage_off_h,
-                int64_t nst, int64_t n, cudaStream_t s);
+                int64_t nst, int64_t n, cudaStream_t s, const int32_t *nbr = nullptr,
+                const double *wts = nullptr, bool ahead_ok = false);
 void ensure_decide_attrs();
 // *bad = 1 unless assign[v] == v for every v (the singleton state of
 // PL/modularity.py:47-56); *bad must be 0 on entry.
@@ -175,6 +203,7 @@ struct StageArgs {
     // and nothing else is written (the replicated apply follows)
     double *live_a = nullptr, *live_b = nullptr;
     int64_t xlo = 0, xhi = 0;
+    AheadFix fx;  // an ahead stage's pushes into later ahead tables
 };
 
 // Event / sort scratch for stages of up to max_ns vertices.
@@ -195,6 +224,10 @@ struct ApplyBuffers {
     void release();
 };
 
+// out[0..4]: ahead stages, vertices, windows, fix entries, table slots.
+void ahead_stats(const Plan &P, int64_t *out);
+// Stage a's ahead fix entries into S.fx (nothing for other stages).
+void ahead_stage_args(const Plan &P, int64_t a, StageArgs &S);
 // Launch one stage's apply (no host synchronisation; capturable).
 void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st);
 // Live e_a / e_b of the movers at positions [S.xlo, S.xhi) into S.live_a / S.live_b

@@ -274,6 +274,7 @@ static void record_apply(Phase &P, size_t a, cudaStream_t st, uint8_t *dirty = n
                          unsigned long long *chash = nullptr) {
     StageArgs S = stage_args(P, a, dirty, chash);
     if (live_mode(P)) S.flags = (S.flags | PLV_F_INDEPENDENT) & ~PLV_F_IDENTITY;
+    ahead_stage_args(P.plan, (int64_t)a, S);
     launch_apply(S, P.ab, st);
 }
 
@@ -515,7 +516,11 @@ static Phase *phase_create(const int64_t *off, const int32_t *nbr, const double 
                                              sizeof(int32_t) * c, cudaMemcpyDeviceToDevice, s));
             }
         }
-        plan_build(P->plan, off, P->lvtx, loff.data(), nst, n, s);
+        // small colour classes of an integral single-rank phase are decided from
+        // tables accumulated ahead (ahead.cuh)
+        const bool ahead_ok = (flags & PLV_F_INTEGRAL) && (flags & PLV_F_INDEPENDENT) &&
+                              world == 1 && !comm;
+        plan_build(P->plan, off, P->lvtx, loff.data(), nst, n, s, nbr, wts, ahead_ok);
         if (comm) {  // exchange records + the slice table on device
             P->xmax.assign(nst, 0);
             for (int64_t a = 0; a < nst; a++)
@@ -1060,6 +1065,13 @@ extern "C" int plv_phase_graph_kernels(void *handle, int64_t *n_h) {
         plv::capture_iteration(*P);
     }
     *n_h = P->graph_kernels;
+    PLV_EXIT
+}
+
+extern "C" int plv_phase_ahead_stats(void *handle, int64_t *out_h) {
+    PLV_ENTRY
+    plv::Phase *P = (plv::Phase *)handle;
+    plv::ahead_stats(P->plan, out_h);
     PLV_EXIT
 }
 
