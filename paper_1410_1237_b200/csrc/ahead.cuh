@@ -32,7 +32,10 @@
 namespace plv {
 
 constexpr int AH_NT = 256;             // threads per pass block
-constexpr int AH_U = 8;                // table slots per pass thread
+#ifndef AH_UU
+#define AH_UU 4                        // (8 measured slower: 86 registers, 2 blocks per SM)
+#endif
+constexpr int AH_U = AH_UU;            // table slots per pass thread
 constexpr int AH_SL = AH_NT * AH_U;    // table slots per pass block
 constexpr int AH_CH = 1024;            // row entries per accumulate block (256 threads x 4)
 #ifndef AH_MAX_NS
@@ -43,10 +46,10 @@ constexpr int AH_CH = 1024;            // row entries per accumulate block (256 
 #endif
 constexpr int64_t AH_MAX_SLOTS = (int64_t)1 << 28;  // 4 GB of slots per window
 #ifndef AH_TRIGGER
-#define AH_TRIGGER 0  // early programmatic launch of the next kernel of an ahead stage
+#define AH_TRIGGER 1  // early programmatic launch of the next kernel of an ahead stage
 #endif
 #ifndef AH_MINB
-#define AH_MINB 2     // pass blocks per SM the register budget allows
+#define AH_MINB 4     // pass blocks per SM (64 registers)
 #endif
 
 struct AheadDev {
@@ -161,6 +164,11 @@ __global__ void __launch_bounds__(AH_NT, AH_MINB) k_ah_pass(DecideArgs A, AheadD
 #endif
     __shared__ BestSmem<AH_NT> S;
     __shared__ int s_last;
+    // plv_debug_trace(2): begin, wait over, gains done, block best, ticket, end
+    const bool tr_on = g_tr_on == 2 && threadIdx.x == 0;
+    Trace tr;
+    tr.n = 0;
+    if (tr_on) tr.mark();
     const int tid = threadIdx.x;
     const int64_t pk = blk[blockIdx.x];
     const int64_t g = pk >> 32, y = pk & 0xffffffffll;
@@ -170,6 +178,7 @@ __global__ void __launch_bounds__(AH_NT, AH_MINB) k_ah_pass(DecideArgs A, AheadD
     const double ki = A.k[i];
     const int nsl = (int)(D.poff[g + 1] - D.poff[g]);
     pdl_wait();  // the window's accumulation / the previous stage's apply and pushes
+    TR_MARK
     const int32_t c_old = __ldcg(D.cold + g);
     const int32_t so = __ldcg(D.sold + g);
     AheadRec r[AH_U];
@@ -203,8 +212,10 @@ __global__ void __launch_bounds__(AH_NT, AH_MINB) k_ah_pass(DecideArgs A, AheadD
         for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(FULL, w, o);
         if ((tid & 31) == 0 && w) atomicAdd(A.cand, w);
     }
+    if (tr_on && b.g != -1.0) tr.mark();  // (the gains are computed)
     if (nsl > 1) {
         b = block_best<AH_NT>(S, b);
+        TR_MARK
         if (tid == 0) {
             D.part[D.poff[g] + y] = b;
             __threadfence();
@@ -212,7 +223,11 @@ __global__ void __launch_bounds__(AH_NT, AH_MINB) k_ah_pass(DecideArgs A, AheadD
             if (s_last) __threadfence();
         }
         __syncthreads();
-        if (!s_last) return;
+        TR_MARK
+        if (!s_last) {
+            TR_END(8)
+            return;
+        }
         if (tid >= 32) return;
         Best bw{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
         for (int64_t t = D.poff[g] + tid; t < D.poff[g + 1]; t += 32) {
@@ -239,6 +254,7 @@ __global__ void __launch_bounds__(AH_NT, AH_MINB) k_ah_pass(DecideArgs A, AheadD
         D.sold[g] = -1;
         D.tick[g] = 0;
     }
+    TR_END(9)
 }
 
 // ------------------------------------------------------------------ planning

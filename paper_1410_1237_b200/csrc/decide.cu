@@ -59,7 +59,7 @@ struct Trace {
     }
 };
 #define TR_BEGIN                                    \
-    const bool tr_on = g_tr_on && threadIdx.x == 0; \
+    const bool tr_on = g_tr_on == 1 && threadIdx.x == 0; \
     Trace tr;                                       \
     tr.n = 0;                                       \
     if (tr_on) tr.mark();

@@ -17,7 +17,8 @@ from paper_1410_1237_b200 import synthetic as syn  # noqa: E402
 from paper_1410_1237_b200.engine import PhaseEngine  # noqa: E402
 
 mode = sys.argv[1] if len(sys.argv) > 1 else "colored"
-g = pl.vf_compact(syn.config_graph("c2_rmat20")).graph
+cfg = sys.argv[2] if len(sys.argv) > 2 else "c2_rmat20"
+g = pl.vf_compact(syn.config_graph(cfg)).graph
 col = pl.color_graph(g) if mode == "colored" else None
 s0 = pl.singleton_state(g)
 d0 = s0.device()
@@ -38,16 +39,17 @@ reset()
 eng.iterate()
 reset()
 torch.cuda.synchronize()
-cl.plv_debug_trace(1)
+cl.plv_debug_trace(int(os.environ.get("KTRACE_ON", "1")))  # 2: the ahead pass only
 eng.iterate()
 torch.cuda.synchronize()
-buf = np.zeros(8 << 18, dtype=np.uint64)
+buf = np.zeros(8 << 18, dtype=np.uint64)  # (records beyond 2^18 are dropped)
 n = ctypes.c_int64(0)
 cl.plv_debug_trace_read(buf.ctypes.data, 1 << 18, ctypes.byref(n))
 cl.plv_debug_trace(0)
 r = buf[: 8 * n.value].reshape(-1, 8).astype(np.int64)
 kid = r[:, 0] >> 32
-names = {1: "hub_accum", 2: "hub_pass", 5: "t2b_wide", 6: "t2a_wide", 7: "t2_narrow"}
+names = {1: "hub_accum", 2: "hub_pass", 5: "t2b_wide", 6: "t2a_wide", 7: "t2_narrow",
+         8: "ah_pass", 9: "ah_pass_dec"}  # ah_pass: begin, wait, gains, best, ticket, end
 print(f"records {len(r)}")
 for k, nm in names.items():
     m = kid == k
