@@ -45,6 +45,9 @@ constexpr int AH_CH = 1024;            // row entries per accumulate block (256 
 #define AH_MAX_ENTRIES (3 << 20)       // row entries of an ahead stage
 #endif
 constexpr int64_t AH_MAX_SLOTS = (int64_t)1 << 28;  // 4 GB of slots per window
+#ifndef AH_CAP8
+#define AH_CAP8 14  // table slots: (deg + pushes + 2) * AH_CAP8 / 8
+#endif
 #ifndef AH_TRIGGER
 #define AH_TRIGGER 1  // early programmatic launch of the next kernel of an ahead stage
 #endif
@@ -55,7 +58,7 @@ constexpr int64_t AH_MAX_SLOTS = (int64_t)1 << 28;  // 4 GB of slots per window
 struct AheadDev {
     AheadRec *tab;
     const int64_t *tbase;   // per ahead vertex: first slot (window-relative)
-    const uint32_t *tmask;  // slots - 1 (power of two >= 2 deg + 2)
+    const uint32_t *tcap;   // slots (deg + pushes into it + 2, and an eighth more)
     const int32_t *vid;
     const int64_t *row;
     const int32_t *deg;
@@ -85,7 +88,7 @@ struct Ahead {
     std::vector<int64_t> fx_base, fx_cnt;  // per stage: fix entries
     int64_t nvert = 0, nfix = 0, nslots = 0;
     void release() {
-        void *ps[] = {d.tab, (void *)d.tbase, (void *)d.tmask, (void *)d.vid, (void *)d.row,
+        void *ps[] = {d.tab, (void *)d.tbase, (void *)d.tcap, (void *)d.vid, (void *)d.row,
                       (void *)d.deg, d.cold, d.sold, d.tick, d.amove, (void *)d.poff, d.part,
                       acc_blk, pass_blk, fx_src, fx_dst, fx_w};
         for (void *p : ps) pool_free(p);
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(256) k_ah_accum(DecideArgs A, AheadDev D, cons
         ww[u] = t < deg ? ld_row(A.wts + (row + t)) : 0.0;
     }
     AheadRec *tab = D.tab + D.tbase[g];
-    const uint32_t mask = D.tmask[g];
+    const uint32_t cap = D.tcap[g];
     pdl_wait();  // the previous stage's apply: the assignment
     const int32_t c_old = ld_state(A.assign + i);
     if (ch == 0 && tid == 0) D.cold[g] = c_old;
@@ -132,7 +135,7 @@ __global__ void __launch_bounds__(256) k_ah_accum(DecideArgs A, AheadDev D, cons
         uint32_t s = 0;
         if (c >= 0 && lane == leader) {
             bool fresh;
-            s = ahead_claim(tab, c, mask, &fresh);
+            s = ahead_claim(tab, c, cap, &fresh);
             if (fresh && c == c_old) D.sold[g] = (int32_t)s;
         }
         s = __shfl_sync(FULL, s, leader);
@@ -174,7 +177,7 @@ __global__ void __launch_bounds__(AH_NT, AH_MINB) k_ah_pass(DecideArgs A, AheadD
     const int64_t g = pk >> 32, y = pk & 0xffffffffll;
     const int32_t i = D.vid[g];
     AheadRec *tab = D.tab + D.tbase[g];
-    const int64_t cap = (int64_t)D.tmask[g] + 1;
+    const int64_t cap = (int64_t)D.tcap[g];
     const double ki = A.k[i];
     const int nsl = (int)(D.poff[g + 1] - D.poff[g]);
     pdl_wait();  // the window's accumulation / the previous stage's apply and pushes
@@ -312,6 +315,7 @@ __global__ void __launch_bounds__(256) k_ah_fix(const int32_t *nbr, const double
                                                 const int64_t *row, const int32_t *deg,
                                                 const int32_t *hubidx, const int32_t *gstage,
                                                 const int32_t *gwin, unsigned long long *cnt,
+                                                unsigned long long *cin,
                                                 const unsigned long long *fx_off, int32_t *fx_src,
                                                 int32_t *fx_dst, double *fx_w) {
     const int64_t pk = blk[blockIdx.x];
@@ -326,6 +330,7 @@ __global__ void __launch_bounds__(256) k_ah_fix(const int32_t *nbr, const double
         const int32_t gj = hubidx[j];
         if (gj < 0 || gwin[gj] != wn || gstage[gj] >= st) continue;
         const unsigned long long k = atomicAdd(cnt + gj, 1ull);
+        if (!FILL) atomicAdd(cin + g, 1ull);
         if (FILL) {
             const unsigned long long p = fx_off[gj] + k;
             fx_src[p] = gj;
@@ -346,11 +351,12 @@ static bool ahead_env_lowdeg() {  // tests: low-degree stages qualify too
 
 // Choose the ahead stages (clearing their tiers), group them into windows and
 // build the tables, block lists and fix lists.  h: the (stage, tier) histogram.
-static int64_t ahead_env_slots() {  // experiments: table slots per window
-    const char *e = getenv("PLV_AHEAD_SLOTS");
+static int64_t ahead_env(const char *name, int64_t dflt) {  // experiments
+    const char *e = getenv(name);
     const int64_t v = e ? atoll(e) : 0;
-    return v > 0 ? v : AH_MAX_SLOTS;
+    return v > 0 ? v : dflt;
 }
+static int64_t ahead_env_slots() { return ahead_env("PLV_AHEAD_SLOTS", AH_MAX_SLOTS); }
 
 static void ahead_plan(Plan &P, const int64_t *off, const int32_t *nbr, const double *wts,
                        const int32_t *vtx, const int64_t *soff_h, const int64_t *d_soff,
@@ -419,22 +425,18 @@ static void ahead_plan(Plan &P, const int64_t *off, const int32_t *nbr, const do
     std::vector<int32_t> hdeg(G);
     PLV_CUDA(cudaMemcpyAsync(hdeg.data(), deg, sizeof(int32_t) * G, cudaMemcpyDeviceToHost, s));
     PLV_CUDA(cudaStreamSynchronize(s));
-    // windows, table slices, block lists
-    std::vector<int64_t> tbase(G), poff(G + 1, 0), acc, pass;
-    std::vector<uint32_t> tmask(G);
-    int64_t cur = -1, wslots = 0, max_slots = 0;
+    // windows (runs of consecutive ahead stages, cut where a window's tables
+    // could exceed the slot budget) and the accumulation blocks
+    std::vector<int64_t> acc;
+    int64_t cur = -1, wslots = 0;
     for (int64_t a = 0; a < nst; a++) {
         if (!P.st[a].ns) continue;  // an empty stage does not end a window
         if (!is_ah[a]) {
             cur = -1;
             continue;
         }
-        int64_t sslots = 0;
-        for (int64_t g = H->g0[a]; g < H->g0[a + 1]; g++) {
-            int64_t cap = 64;
-            while (cap < 2 * (int64_t)hdeg[g] + 2) cap <<= 1;
-            sslots += cap;
-        }
+        int64_t sslots = 0;  // (an upper bound: a table has at most 2.25 deg + 36 slots)
+        for (int64_t g = H->g0[a]; g < H->g0[a + 1]; g++) sslots += 3 * (int64_t)hdeg[g] + 64;
         if (cur < 0 || wslots + sslots > max_win_slots) {
             AheadWin w;
             w.s0 = a;
@@ -443,43 +445,90 @@ static void ahead_plan(Plan &P, const int64_t *off, const int32_t *nbr, const do
             cur = (int64_t)H->wins.size() - 1;
             wslots = 0;
         }
+        wslots += sslots;
         H->win_of[a] = (int)cur;
-        H->pb_base[a] = (int64_t)pass.size();
         for (int64_t g = H->g0[a]; g < H->g0[a + 1]; g++) {
-            int64_t cap = 64;
-            while (cap < 2 * (int64_t)hdeg[g] + 2) cap <<= 1;
-            tbase[g] = wslots;
-            tmask[g] = (uint32_t)(cap - 1);
-            wslots += cap;
             gwin[g] = (int32_t)cur;
-            const int64_t nsl = (cap + AH_SL - 1) / AH_SL;
-            for (int64_t y = 0; y < nsl; y++) pass.push_back((g << 32) | y);
-            poff[g + 1] = poff[g] + nsl;
             const int64_t nch = ((int64_t)hdeg[g] + AH_CH - 1) / AH_CH;
             for (int64_t c = 0; c < nch; c++) acc.push_back((g << 32) | c);
         }
-        H->pb_cnt[a] = (int64_t)pass.size() - H->pb_base[a];
         H->wins[cur].nacc = (int64_t)acc.size() - H->wins[cur].acc_base;
-        H->wins[cur].slots = wslots;
-        max_slots = wslots > max_slots ? wslots : max_slots;
     }
-    for (int64_t g = 0; g < G; g++)
-        if (poff[g + 1] < poff[g]) poff[g + 1] = poff[g];  // (never: every g is in a window)
-    H->nslots = max_slots;
-    int64_t *d_tbase = dalloc<int64_t>(G), *d_poff = dalloc<int64_t>(G + 1);
-    uint32_t *d_tmask = dalloc<uint32_t>(G);
-    D.tbase = d_tbase;
-    D.tmask = d_tmask;
-    D.poff = d_poff;
-    PLV_CUDA(cudaMemcpyAsync(d_tbase, tbase.data(), sizeof(int64_t) * G, cudaMemcpyHostToDevice, s));
-    PLV_CUDA(cudaMemcpyAsync(d_tmask, tmask.data(), sizeof(uint32_t) * G, cudaMemcpyHostToDevice, s));
-    PLV_CUDA(cudaMemcpyAsync(d_poff, poff.data(), sizeof(int64_t) * (G + 1), cudaMemcpyHostToDevice,
-                             s));
     H->acc_blk = dalloc<int64_t>(acc.size());
-    H->pass_blk = dalloc<int64_t>(pass.size());
     if (!acc.empty())
         PLV_CUDA(cudaMemcpyAsync(H->acc_blk, acc.data(), sizeof(int64_t) * acc.size(),
                                  cudaMemcpyHostToDevice, s));
+    // fix lists: counts per source (the list offsets) and per destination (the
+    // table sizes)
+    Buf<int32_t> d_gstage(G, s), d_gwin(G, s);
+    Buf<unsigned long long> cnt(G + 1, s), cin(G, s), fx_off(G + 1, s);
+    PLV_CUDA(cudaMemcpyAsync(d_gstage.get(), gstage.data(), sizeof(int32_t) * G,
+                             cudaMemcpyHostToDevice, s));
+    PLV_CUDA(cudaMemcpyAsync(d_gwin.get(), gwin.data(), sizeof(int32_t) * G, cudaMemcpyHostToDevice,
+                             s));
+    PLV_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long) * (G + 1), s));
+    PLV_CUDA(cudaMemsetAsync(cin.get(), 0, sizeof(unsigned long long) * G, s));
+    const unsigned na = (unsigned)acc.size();
+    if (na) {
+        k_ah_fix<false><<<na, 256, 0, s>>>(nbr, wts, H->acc_blk, vid, row, deg, hubidx, d_gstage,
+                                           d_gwin, cnt, cin, nullptr, nullptr, nullptr, nullptr);
+        PLV_LAUNCH_CHECK();
+    }
+    size_t tb = 0;
+    PLV_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.get(), fx_off.get(), G + 1, s));
+    Buf<char> tmp(tb, s);
+    PLV_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, cnt.get(), fx_off.get(), G + 1, s));
+    std::vector<unsigned long long> foff(G + 1), hin(G);
+    PLV_CUDA(cudaMemcpyAsync(foff.data(), fx_off.get(), sizeof(unsigned long long) * (G + 1),
+                             cudaMemcpyDeviceToHost, s));
+    PLV_CUDA(cudaMemcpyAsync(hin.data(), cin.get(), sizeof(unsigned long long) * G,
+                             cudaMemcpyDeviceToHost, s));
+    PLV_CUDA(cudaStreamSynchronize(s));
+    // table slices and pass blocks.  A table holds at most one community per
+    // row entry plus one per push into it, so deg + pushes + 2 slots can never
+    // fill up (the claim loops end); an eighth more keeps the probe runs short.
+    // (Power-of-two tables of >= 2 deg + 2 slots measured ~2x the pass and
+    // accumulation traffic.)
+    std::vector<int64_t> tbase(G), poff(G + 1, 0), pass;
+    std::vector<uint32_t> tcap(G);
+    const int64_t cap8 = ahead_env("PLV_AHEAD_CAP8", AH_CAP8) < 9 ? 9 : ahead_env("PLV_AHEAD_CAP8", AH_CAP8);
+    int64_t max_slots = 0;
+    cur = -1;
+    wslots = 0;
+    for (int64_t a = 0; a < nst; a++) {
+        if (!is_ah[a]) continue;
+        if (H->win_of[a] != cur) {
+            cur = H->win_of[a];
+            wslots = 0;
+        }
+        H->pb_base[a] = (int64_t)pass.size();
+        for (int64_t g = H->g0[a]; g < H->g0[a + 1]; g++) {
+            const int64_t need = (int64_t)hdeg[g] + (int64_t)hin[g] + 2;
+            int64_t cap = need * cap8 / 8;
+            cap = (cap + 3) / 4 * 4;
+            if (cap < 32) cap = 32;
+            tbase[g] = wslots;
+            tcap[g] = (uint32_t)cap;
+            wslots += cap;
+            const int64_t nsl = (cap + AH_SL - 1) / AH_SL;
+            for (int64_t y = 0; y < nsl; y++) pass.push_back((g << 32) | y);
+            poff[g + 1] = poff[g] + nsl;
+        }
+        H->pb_cnt[a] = (int64_t)pass.size() - H->pb_base[a];
+        H->wins[cur].slots = wslots;
+        max_slots = wslots > max_slots ? wslots : max_slots;
+    }
+    H->nslots = max_slots;
+    int64_t *d_tbase = dalloc<int64_t>(G), *d_poff = dalloc<int64_t>(G + 1);
+    uint32_t *d_tcap = dalloc<uint32_t>(G);
+    D.tbase = d_tbase;
+    D.tcap = d_tcap;
+    D.poff = d_poff;
+    PLV_CUDA(cudaMemcpyAsync(d_tbase, tbase.data(), sizeof(int64_t) * G, cudaMemcpyHostToDevice, s));
+    PLV_CUDA(cudaMemcpyAsync(d_tcap, tcap.data(), sizeof(uint32_t) * G, cudaMemcpyHostToDevice, s));
+    PLV_CUDA(cudaMemcpyAsync(d_poff, poff.data(), sizeof(int64_t) * (G + 1), cudaMemcpyHostToDevice,
+                             s));
+    H->pass_blk = dalloc<int64_t>(pass.size());
     PLV_CUDA(cudaMemcpyAsync(H->pass_blk, pass.data(), sizeof(int64_t) * pass.size(),
                              cudaMemcpyHostToDevice, s));
     D.tab = dalloc<AheadRec>(max_slots);
@@ -495,28 +544,6 @@ static void ahead_plan(Plan &P, const int64_t *off, const int32_t *nbr, const do
     PLV_CUDA(cudaMemsetAsync(D.tick, 0, sizeof(int32_t) * G, s));
     k_ah_fill_move<<<grid_for(G, 256), 256, 0, s>>>(D.amove, G);
     PLV_LAUNCH_CHECK();
-    // fix lists
-    Buf<int32_t> d_gstage(G, s), d_gwin(G, s);
-    Buf<unsigned long long> cnt(G + 1, s), fx_off(G + 1, s);
-    PLV_CUDA(cudaMemcpyAsync(d_gstage.get(), gstage.data(), sizeof(int32_t) * G,
-                             cudaMemcpyHostToDevice, s));
-    PLV_CUDA(cudaMemcpyAsync(d_gwin.get(), gwin.data(), sizeof(int32_t) * G, cudaMemcpyHostToDevice,
-                             s));
-    PLV_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long) * (G + 1), s));
-    const unsigned na = (unsigned)acc.size();
-    if (na) {
-        k_ah_fix<false><<<na, 256, 0, s>>>(nbr, wts, H->acc_blk, vid, row, deg, hubidx, d_gstage,
-                                           d_gwin, cnt, nullptr, nullptr, nullptr, nullptr);
-        PLV_LAUNCH_CHECK();
-    }
-    size_t tb = 0;
-    PLV_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.get(), fx_off.get(), G + 1, s));
-    Buf<char> tmp(tb, s);
-    PLV_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, cnt.get(), fx_off.get(), G + 1, s));
-    std::vector<unsigned long long> foff(G + 1);
-    PLV_CUDA(cudaMemcpyAsync(foff.data(), fx_off.get(), sizeof(unsigned long long) * (G + 1),
-                             cudaMemcpyDeviceToHost, s));
-    PLV_CUDA(cudaStreamSynchronize(s));
     H->nfix = (int64_t)foff[G];
     H->fx_src = dalloc<int32_t>(H->nfix);
     H->fx_dst = dalloc<int32_t>(H->nfix);
@@ -524,7 +551,8 @@ static void ahead_plan(Plan &P, const int64_t *off, const int32_t *nbr, const do
     if (H->nfix) {
         PLV_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long) * (G + 1), s));
         k_ah_fix<true><<<na, 256, 0, s>>>(nbr, wts, H->acc_blk, vid, row, deg, hubidx, d_gstage,
-                                          d_gwin, cnt, fx_off, H->fx_src, H->fx_dst, H->fx_w);
+                                          d_gwin, cnt, nullptr, fx_off, H->fx_src, H->fx_dst,
+                                          H->fx_w);
         PLV_LAUNCH_CHECK();
     }
     for (int64_t a = 0; a < nst; a++) {
@@ -559,7 +587,7 @@ void ahead_stage_args(const Plan &P, int64_t a, StageArgs &S) {
     S.fx.amove = H.d.amove;
     S.fx.tab = H.d.tab;
     S.fx.tbase = H.d.tbase;
-    S.fx.tmask = H.d.tmask;
+    S.fx.tcap = H.d.tcap;
     S.fx.cold = H.d.cold;
     S.fx.sold = H.d.sold;
 }

@@ -29,17 +29,22 @@ __device__ __forceinline__ uint32_t comm_hash(int32_t c) {
     return h;
 }
 
-// Ahead tables (ahead.cuh): find-or-insert community c by CAS alone; reports
-// whether this call inserted the key.  The table always keeps an empty slot.
-__device__ __forceinline__ uint32_t ahead_claim(AheadRec *t, int32_t c, uint32_t mask, bool *fresh) {
-    uint32_t s = comm_hash(c) & mask;
+// Ahead tables (ahead.cuh): `cap` slots (any size: multiply-shift range
+// reduction of the hash, linear probing).  Find-or-insert community c by CAS
+// alone; reports whether this call inserted the key.  The table always keeps
+// an empty slot.
+__device__ __forceinline__ uint32_t ahead_first(int32_t c, uint32_t cap) {
+    return (uint32_t)(((uint64_t)comm_hash(c) * cap) >> 32);
+}
+__device__ __forceinline__ uint32_t ahead_claim(AheadRec *t, int32_t c, uint32_t cap, bool *fresh) {
+    uint32_t s = ahead_first(c, cap);
     while (true) {
         const int32_t old = atomicCAS(&t[s].key, -1, c);
         if (old == -1 || old == c) {
             *fresh = old == -1;
             return s;
         }
-        s = (s + 1) & mask;
+        s = s + 1 == cap ? 0 : s + 1;
     }
 }
 
@@ -56,15 +61,15 @@ __device__ __forceinline__ void ahead_fixup(const AheadFix &F, unsigned blk) {
     const int32_t dst = F.dst[e];
     const double w = F.w[e];
     AheadRec *t = F.tab + F.tbase[dst];
-    const uint32_t mask = F.tmask[dst];
-    uint32_t s = comm_hash(mv.x) & mask;
-    for (uint32_t it = 0; it <= mask; it++) {  // a's slot exists: src was counted there
+    const uint32_t cap = F.tcap[dst];
+    uint32_t s = ahead_first(mv.x, cap);
+    for (uint32_t it = 0; it < cap; it++) {  // a's slot exists: src was counted there
         if (__ldcg(&t[s].key) == mv.x) break;
-        s = (s + 1) & mask;
+        s = s + 1 == cap ? 0 : s + 1;
     }
     atomicAdd(&t[s].val, -w);
     bool fresh;
-    const uint32_t s2 = ahead_claim(t, mv.y, mask, &fresh);
+    const uint32_t s2 = ahead_claim(t, mv.y, cap, &fresh);
     atomicAdd(&t[s2].val, w);
     if (fresh && mv.y == F.cold[dst]) F.sold[dst] = (int32_t)s2;
 }

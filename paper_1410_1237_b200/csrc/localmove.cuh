@@ -96,7 +96,7 @@ struct AheadFix {
     const int2 *amove = nullptr;  // per ahead vertex: (c_old, c_new) of its move, or (-1, -1)
     AheadRec *tab = nullptr;
     const int64_t *tbase = nullptr;
-    const uint32_t *tmask = nullptr;
+    const uint32_t *tcap = nullptr;
     const int32_t *cold = nullptr;
     int32_t *sold = nullptr;
 };

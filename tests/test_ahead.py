@@ -100,6 +100,17 @@ def test_ahead_default_rule_iterations(orc, monkeypatch, name):
         assert stats["stages"] >= 8 and stats["fix_entries"] > 0, stats
 
 
+@pytest.mark.parametrize("name,slots", [("chung_lu", "60000"), ("hubs", "20000"), ("sbm", "50000")])
+def test_ahead_several_windows(orc, monkeypatch, name, slots):
+    """A small slot budget cuts the run of ahead stages into several windows
+    that reuse one table region (each window's accumulation at its start)."""
+    monkeypatch.setenv("PLV_AHEAD_LOWDEG", "1")
+    monkeypatch.setenv("PLV_AHEAD_SLOTS", slots)
+    u, v, w, n = _graphs(name)
+    stats = _iterations(orc, u, v, w, n, 3)
+    assert stats["windows"] >= 2, stats
+
+
 def test_ahead_off_is_the_tier_path(orc, monkeypatch):
     monkeypatch.setenv("PLV_AHEAD", "0")
     u, v, w, n = _graphs("hubs")
