@@ -227,7 +227,7 @@ __device__ __forceinline__ Best block_best(BestSmem<NT> &S, Best b) {
 
 
 #ifndef T0_MINB
-#define T0_MINB 1
+#define T0_MINB 2
 #endif
 // The general kernels of a first stage step aside when the state is singleton.
 __device__ __forceinline__ bool single_state(const DecideArgs &A) {
@@ -1919,6 +1919,8 @@ DecideArgs make_decide_args(const int64_t *off, const int32_t *nbr, const double
     A.sizes = sizes;
     A.m = m;
     A.four_m_sq = (2.0 * m) * (2.0 * m);
+    A.inv_m = 1.0 / m;
+    A.inv_f = 1.0 / A.four_m_sq;
     A.integral = integral;
     A.out_target = out_target;
     A.out_moved = out_moved;

@@ -11,6 +11,9 @@ namespace plv {
 #ifndef T0_INPLACE
 #define T0_INPLACE 0
 #endif
+#ifndef T0_FILTER
+#define T0_FILTER 1  // approximate gains select the candidates evaluated exactly
+#endif
 
 __device__ __forceinline__ int64_t LBL(const int32_t *labels, int32_t c) {
     return labels ? (int64_t)labels[c] : (int64_t)c;
@@ -219,6 +222,42 @@ __device__ __forceinline__ void decide_t0_body(const DecideArgs &A, const TierRe
         double ki = A.k[i];
         double a_old_excl = dsub(ld_state(A.a_tot + (c_old)), ki);
         Best b{0.0, LBL(A.labels, c_old), c_old, 0.0, 0};
+#if T0_FILTER
+        // The exact gain costs two float64 divisions per candidate (a quarter
+        // of this kernel's stall samples).  Approximate gains first
+        // (reciprocal multiplies: the sums and products are the exact ones,
+        // each quotient is within 3 ulp and the final sum within 2, so the
+        // exact gain lies within gm of ga); only a candidate that can still be
+        // the exact best, or tie with it, is evaluated exactly:
+        //   exact best k with g_k > 0:  ga_k + gm_k >= g_k >= g_j >= ga_j - gm_j
+        // for every j, and g_k > 0 bounds from below too.  A best with
+        // g_k <= 0 never moves the vertex (finish_vertex), with or without it.
+        double at[T0_MAXD];
+#pragma unroll
+        for (int s = 0; s < T0_MAXD; s++)
+            at[s] = s < nc && keys[s] != c_old ? ld_state(A.a_tot + keys[s]) : 0.0;
+        const double tk = dmul(2.0, ki), tka = dmul(tk, a_old_excl);
+        double lo = 0.0;
+#pragma unroll
+        for (int s = 0; s < T0_MAXD; s++) {
+            if (s < nc && keys[s] != c_old) {
+                const double t2 = dsub(vals[s], e_old) * A.inv_m;
+                const double t3 = dsub(tka, dmul(tk, at[s])) * A.inv_f;
+                lo = fmax(lo, (t2 + t3) - (1.8e-15 * (fabs(t2) + fabs(t3)) + 1e-300));
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < T0_MAXD; s++) {
+            if (s < nc && keys[s] != c_old) {
+                const double t2 = dsub(vals[s], e_old) * A.inv_m;
+                const double t3 = dsub(tka, dmul(tk, at[s])) * A.inv_f;
+                if ((t2 + t3) + (1.8e-15 * (fabs(t2) + fabs(t3)) + 1e-300) < lo) continue;
+                int32_t c = keys[s];
+                consider(b, gain_of(vals[s], e_old, A.m, ki, a_old_excl, at[s], A.four_m_sq),
+                         LBL(A.labels, c), c, vals[s], 0);
+            }
+        }
+#else
 #pragma unroll
         for (int s = 0; s < T0_MAXD; s++) {
             if (s < nc && keys[s] != c_old) {
@@ -227,6 +266,7 @@ __device__ __forceinline__ void decide_t0_body(const DecideArgs &A, const TierRe
                          LBL(A.labels, c), c, vals[s], 0);
             }
         }
+#endif
 #endif
         finish_vertex(A, x, c_old, e_old, b.g, b.c, b.e);
     }

@@ -46,6 +46,7 @@ struct DecideArgs {
     const double *a_tot;
     const int32_t *sizes;
     double m, four_m_sq;
+    double inv_m, inv_f;  // 1 / m, 1 / four_m_sq: approximate gains only (never in a result)
     int integral;
     int32_t *out_target;  // per stage index
     uint8_t *out_moved;
