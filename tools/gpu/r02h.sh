@@ -38,3 +38,5 @@ timeout 600 python tools/timeline.py --config c2_rmat20 > gpurun_out/tl_c2c.txt 
 KTRACE_ON=2 timeout 600 python tools/ktrace.py colored c4_chung_lu > gpurun_out/ktrace_c4_ah.txt 2>&1
 for c in c2_rmat20 c3_grid c4_chung_lu; do timeout 300 python tools/run_profile.py $c > gpurun_out/rp_$c.txt 2>&1; done
 timeout 300 python tools/run_kernels.py c4_chung_lu 30 > gpurun_out/rk_c4.txt 2>&1
+timeout 300 python tools/ahead_stats.py c4_chung_lu > gpurun_out/ahead_stats_c4.txt 2>&1
+[ -x tools/l2_gather ] && tools/l2_gather > gpurun_out/l2_gather.txt 2>&1

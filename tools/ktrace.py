@@ -56,12 +56,14 @@ for k, nm in names.items():
     if not m.any():
         continue
     t = r[m, 1:7]
-    ns = r[m, 7]
-    nmk = min(int(ns.max()), 6)
-    segs = [np.mean(t[:, i + 1] - t[:, i]) / 1e3 for i in range(min(nmk, 6) - 1)]
-    print(f"{nm:11s} blocks {m.sum():6d}  mean per-block segments (us): " +
-          " / ".join(f"{x:.2f}" for x in segs) +
-          f"   total {np.mean(t[:, nmk - 1] - t[:, 0]) / 1e3:.2f}")
+    ns = r[m, 7].clip(1, 6)
+    nmk = int(ns.max())
+    full = ns == nmk  # blocks that recorded every mark (others took a shorter path)
+    segs = [np.mean(t[full, i + 1] - t[full, i]) / 1e3 for i in range(nmk - 1)]
+    last = t[np.arange(len(t)), ns - 1]
+    print(f"{nm:11s} blocks {m.sum():6d} ({full.sum()} with all {nmk} marks)  mean per-block "
+          f"segments (us): " + " / ".join(f"{x:.2f}" for x in segs) +
+          f"   total {np.mean(last - t[:, 0]) / 1e3:.2f}")
 # per launch (records of one kernel id clustered by time): start spread and span
 for k, nm in names.items():
     m = kid == k
