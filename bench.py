@@ -782,7 +782,7 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": _traffic(args.mode, scale, args.config),
                          "traffic_unit": "bytes per iteration (ncu, warm caches)",
                          "peak_kind": peak_kind,
-                         "kernel": "decide (tiers 0-4)",
+                         "kernel": "decide (tiers 0-4 and the ahead tables)",
                          "bytes_per_iter": decide_bytes, "ms_per_iter": decide_ms,
                          "share_of_step": decide_ms / span_ms,
                          "timing": "union of decide-kernel intervals in the iteration graph "
