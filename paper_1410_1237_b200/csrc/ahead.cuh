@@ -58,7 +58,7 @@ constexpr int64_t AH_MAX_SLOTS = (int64_t)1 << 28;  // 4 GB of slots per window
 struct AheadDev {
     AheadRec *tab;
     const int64_t *tbase;   // per ahead vertex: first slot (window-relative)
-    const uint32_t *tcap;   // slots (deg + pushes into it + 2, and an eighth more)
+    const uint32_t *tcap;   // slots: (deg + pushes into it + 2) x AH_CAP8 / 8
     const int32_t *vid;
     const int64_t *row;
     const int32_t *deg;
