@@ -1241,7 +1241,21 @@ __global__ void __launch_bounds__(HSB) k_hub_pass(DecideArgs A, const int32_t *l
 // decision is the argmax of gain(w_ij) under (gain desc, label asc) against
 // "stay" -- the same operands and operations as the general tiers, without
 // tables, certification or the hub chain.  These kernels take the stage when
-// *notsingle == 0 (launch_single_check); the general ones step aside.
+// *notsingle == 0 (launch_single_check: assign[v] == v and sizes[v] == 1 for
+// every v); the general ones step aside.
+
+// finish_vertex in the singleton state: both communities of the
+// singleton-pair guard (PL/_kernels.pyx:92-98) have size 1 (k_single_check), so
+// the guard is the label comparison alone -- no sizes gathers.
+__device__ __forceinline__ void finish_single(const DecideArgs &A, int64_t x, int32_t c_old,
+                                              double bg, int32_t bc, double be) {
+    bool moved = bg > 0.0 && bc != c_old;
+    if (moved && LBL(A.labels, bc) > LBL(A.labels, c_old)) moved = false;
+    A.out_target[x] = moved ? bc : c_old;
+    A.out_moved[x] = moved ? 1 : 0;
+    A.out_e_old[x] = 0.0;
+    A.out_e_best[x] = moved ? be : 0.0;
+}
 
 __device__ __forceinline__ void single_entry(const DecideArgs &A, int32_t i, double ki,
                                              double aoe, int32_t j, double w, Best &b) {
@@ -1331,7 +1345,7 @@ __global__ void __launch_bounds__(SF_WARPS * 32) k_single_t0(DecideArgs A, TierR
         }
         if (has) {
             const Best b = s_b[wid][lane];
-            finish_vertex(A, L.x[q], i, 0.0, b.g, b.c, b.e);
+            finish_single(A, L.x[q], i, b.g, b.c, b.e);
         }
         __syncwarp();
     }
@@ -1374,7 +1388,7 @@ __global__ void __launch_bounds__(256) k_single_warp(DecideArgs A, TierRef L, in
             }
         }
         warp_best(b);
-        if (lane == 0) finish_vertex(A, x, i, 0.0, b.g, b.c, b.e);
+        if (lane == 0) finish_single(A, x, i, b.g, b.c, b.e);
     }
     if (A.cand) {
         for (int o = 16; o > 0; o >>= 1) my += __shfl_xor_sync(FULL, my, o);
@@ -1415,7 +1429,7 @@ __global__ void __launch_bounds__(SB_NT) k_single_block(DecideArgs A, TierRef L,
             }
         }
         b = block_best<SB_NT>(S, b);
-        if (threadIdx.x == 0) finish_vertex(A, x, i, 0.0, b.g, b.c, b.e);
+        if (threadIdx.x == 0) finish_single(A, x, i, b.g, b.c, b.e);
     }
     if (A.cand) {
         for (int o = 16; o > 0; o >>= 1) my += __shfl_xor_sync(FULL, my, o);
@@ -1423,16 +1437,18 @@ __global__ void __launch_bounds__(SB_NT) k_single_block(DecideArgs A, TierRef L,
     }
 }
 
-__global__ void k_single_check(const int32_t *assign, int64_t n, int *bad) {
+// (sizes too: the singleton kernels then know both sizes of the singleton-pair
+// guard without gathering them)
+__global__ void k_single_check(const int32_t *assign, const int32_t *sizes, int64_t n, int *bad) {
     bool b = false;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
          v += (int64_t)gridDim.x * blockDim.x)
-        b |= assign[v] != (int32_t)v;
+        b |= assign[v] != (int32_t)v || sizes[v] != 1;
     if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1);
 }
 
 cudaGraphNode_t add_single_check_nodes(cudaGraph_t g, cudaGraphNode_t dep, const int32_t *assign,
-                                       int64_t n, int *bad) {
+                                       const int32_t *sizes, int64_t n, int *bad) {
     cudaMemsetParams mp = {};
     mp.dst = bad;
     mp.value = 0;
@@ -1442,7 +1458,7 @@ cudaGraphNode_t add_single_check_nodes(cudaGraph_t g, cudaGraphNode_t dep, const
     cudaGraphNode_t ms, ks;
     PLV_CUDA(cudaGraphAddMemsetNode(&ms, g, &dep, 1, &mp));
     cudaKernelNodeParams kp = {};
-    void *args[] = {(void *)&assign, (void *)&n, (void *)&bad};
+    void *args[] = {(void *)&assign, (void *)&sizes, (void *)&n, (void *)&bad};
     kp.func = (void *)k_single_check;
     kp.gridDim = dim3(grid_for(n > 0 ? n : 1, 256, 148 * 16));
     kp.blockDim = dim3(256);
@@ -1452,10 +1468,11 @@ cudaGraphNode_t add_single_check_nodes(cudaGraph_t g, cudaGraphNode_t dep, const
     return ks;
 }
 
-void launch_single_check(const int32_t *assign, int64_t n, int *bad, cudaStream_t st) {
+void launch_single_check(const int32_t *assign, const int32_t *sizes, int64_t n, int *bad,
+                         cudaStream_t st) {
     PLV_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
     if (n > 0) {
-        k_single_check<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(assign, n, bad);
+        k_single_check<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(assign, sizes, n, bad);
         PLV_LAUNCH_CHECK();
     }
 }

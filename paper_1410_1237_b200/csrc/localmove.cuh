@@ -150,12 +150,13 @@ void plan_build(Plan &P, const int64_t *off, const int32_t *vtx, const int64_t *
                 int64_t nst, int64_t n, cudaStream_t s, const int32_t *nbr = nullptr,
                 const double *wts = nullptr, bool ahead_ok = false);
 void ensure_decide_attrs();
-// *bad = 1 unless assign[v] == v for every v (the singleton state of
+// *bad = 1 unless assign[v] == v and sizes[v] == 1 for every v (the singleton state of
 // PL/modularity.py:47-56); *bad must be 0 on entry.
-void launch_single_check(const int32_t *assign, int64_t n, int *bad, cudaStream_t st);
+void launch_single_check(const int32_t *assign, const int32_t *sizes, int64_t n, int *bad,
+                         cudaStream_t st);
 // The same as graph nodes after `dep` (memset, scan); returns the last node.
 cudaGraphNode_t add_single_check_nodes(cudaGraph_t g, cudaGraphNode_t dep, const int32_t *assign,
-                                       int64_t n, int *bad);
+                                       const int32_t *sizes, int64_t n, int *bad);
 // Launch stage `a`'s decide kernels (no host synchronisation; capturable).
 void launch_decide(const Plan &P, int64_t a, DecideArgs A, cudaStream_t st);
 // Tier t on stream ts[t].

@@ -297,7 +297,7 @@ static void record_finish(Phase &P, cudaStream_t st) {
 
 static void record_iteration(Phase &P, cudaStream_t st) {
     PLV_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 2, st));
-    if (P.single_bad) launch_single_check(P.assign, P.n, P.single_bad, st);
+    if (P.single_bad) launch_single_check(P.assign, P.sizes, P.n, P.single_bad, st);
     bool first = true;
     for (size_t a = 0; a + 1 < P.goff.size(); a++) {
         if (P.goff[a + 1] == P.goff[a]) continue;
@@ -781,7 +781,7 @@ static void build_run_graph(Phase &P, int64_t cap, cudaStream_t s) {
     cudaGraphNode_t loop;
     cudaGraphNode_t before = start;
     if (P.single_bad)  // iteration 0 may start from the singleton state
-        before = add_single_check_nodes(P.rgraph, start, P.assign, P.n, P.single_bad);
+        before = add_single_check_nodes(P.rgraph, start, P.assign, P.sizes, P.n, P.single_bad);
     PLV_CUDA(cudaGraphAddNode(&loop, P.rgraph, &before, 1, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     int prio_lo = 0, prio_hi = 0;

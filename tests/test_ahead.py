@@ -130,3 +130,29 @@ def test_ahead_runs_match_oracle(orc, monkeypatch, name, lowdeg):
     assert [p.stats.iterations for p in h.phases] == [p.iterations for p in oh.phases]
     assert np.array_equal(h.final_assignment, oh.final_assignment)
     assert h.final_modularity == oh.final_modularity
+
+
+def test_singleton_shortcut_needs_singleton_sizes(orc):
+    """The singleton-state kernels skip the size gathers of the singleton-pair
+    guard (PL/_kernels.pyx:92-98), so the device check must reject a state whose
+    assignment is the identity but whose sizes are not all 1: the general
+    kernels then decide it, as the reference does."""
+    from paper_1410_1237_b200 import synthetic as syn
+    u, v, w = syn.gnm_records(400, 2400, seed=9, weight_range=(0.0, 2.0))
+    g = pl.Graph.from_edges(u, v, w, num_vertices=400)
+    og = orc.from_edges(u, v, w, num_vertices=400)
+    sub = np.arange(400)
+    moved = {}
+    for sz in (1, 2):
+        s = pl.singleton_state(g)
+        os_ = orc.singleton_state(og)
+        s.sizes[:] = sz
+        os_.sizes[:] = sz
+        s, mv = pl.run_iteration(g, s, sub)
+        omv = orc.run_iteration(og, os_, sub)
+        assert mv == omv
+        assert np.array_equal(s.assignment, os_.assignment)
+        assert np.array_equal(s.sizes, os_.sizes)
+        assert np.array_equal(s.a_tot, os_.a_tot)
+        moved[sz] = mv
+    assert moved[1] != moved[2]  # the guard did decide moves in the consistent state
