@@ -155,6 +155,46 @@ __device__ __forceinline__ void clear_rec(AheadRec *p) {
     *reinterpret_cast<int4 *>(p) = make_int4(-1, 0, 0, 0);
 }
 
+// Warp argmax under (gain desc, label asc) with three warp reductions instead
+// of five rounds of whole-record shuffles: the lane holding the best (any of
+// them when equal records tie).  The gain's bits are mapped to an unsigned
+// key of the same order (-0.0 first folded into +0.0, which compares equal);
+// labels are int32 values.
+__device__ __forceinline__ int ah_warp_argmax(const Best &b) {
+    const long long bits = __double_as_longlong(b.g + 0.0);
+    const unsigned long long key =
+        (unsigned long long)bits ^ (bits < 0 ? ~0ull : 0x8000000000000000ull);
+    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+    const unsigned mh = __reduce_max_sync(FULL, hi);
+    bool c = hi == mh;
+    const unsigned ml = __reduce_max_sync(FULL, c ? lo : 0u);
+    c = c && lo == ml;
+    const unsigned lb = (unsigned)(int32_t)b.l ^ 0x80000000u;
+    const unsigned mb = __reduce_min_sync(FULL, c ? lb : 0xffffffffu);
+    c = c && lb == mb;
+    return __ffs(__ballot_sync(FULL, c)) - 1;
+}
+
+__device__ __forceinline__ Best ah_shfl_best(const Best &b, int src) {
+    Best r;
+    r.g = __shfl_sync(FULL, b.g, src);
+    r.l = __shfl_sync(FULL, b.l, src);
+    r.c = __shfl_sync(FULL, b.c, src);
+    r.e = __shfl_sync(FULL, b.e, src);
+    r.n = __shfl_sync(FULL, b.n, src);
+    return r;
+}
+
+// Block argmax; the result is valid in warp 0 (one block barrier).
+__device__ __forceinline__ Best ah_block_best(BestSmem<AH_NT> &S, const Best &b) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == ah_warp_argmax(b)) S.w[wid] = b;
+    __syncthreads();
+    if (wid != 0) return b;
+    const Best c = lane < AH_NT / 32 ? S.w[lane] : Best{-INFINITY, INT32_MAX, -1, 0.0, 0};
+    return ah_shfl_best(c, ah_warp_argmax(c));
+}
+
 // Pass block (ahead vertex g, table slice y): the gains of the slice's
 // communities on the exact sums, the slice's best; the block that completes
 // the vertex's last slice decides it (PL/_kernels.pyx:92-98), records its move
@@ -217,7 +257,7 @@ __global__ void __launch_bounds__(AH_NT, AH_MINB) k_ah_pass(DecideArgs A, AheadD
     }
     if (tr_on && b.g != -1.0) tr.mark();  // (the gains are computed)
     if (nsl > 1) {
-        b = block_best<AH_NT>(S, b);
+        b = ah_block_best(S, b);
         TR_MARK
         if (tid == 0) {
             D.part[D.poff[g] + y] = b;
@@ -237,10 +277,9 @@ __global__ void __launch_bounds__(AH_NT, AH_MINB) k_ah_pass(DecideArgs A, AheadD
             const Best o = ldcg_best(D.part + t);
             consider(bw, o.g, o.l, o.c, o.e, o.n);
         }
-        warp_best(bw);
-        b = bw;
+        b = ah_shfl_best(bw, ah_warp_argmax(bw));
     } else {
-        b = block_best<AH_NT>(S, b);
+        b = ah_block_best(S, b);
     }
     if (tid == 0) {
         const int64_t x = g - g_first;
