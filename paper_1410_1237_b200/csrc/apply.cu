@@ -19,6 +19,7 @@
 #include "csr.cuh"
 #include "pairwise.cuh"
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #ifndef AH_TRIGGER
 #define AH_TRIGGER 0
@@ -369,6 +370,161 @@ __global__ void __launch_bounds__(256) k_stage_fold_long(StageArgs A, const uint
     }
 }
 
+// A stage of a small graph (at most MID_N communities): the events' stable
+// sort by community as a counting sort over the communities -- histogram,
+// one-block scan, scatter of the event ids (any order), then each community's
+// segment put in ascending event id (the stable order of
+// PL/_kernels.pyx:116-144) and folded with the operations of k_stage_fold --
+// four short launches instead of the device radix sort's four plus the two
+// fold launches.  The capped 10,000-iteration phases of small coarse graphs
+// pay these per iteration.  ccnt[] is zero between stages (the fold clears it).
+constexpr int64_t MID_N = 32768;
+#ifndef MID_LOCAL_N
+#define MID_LOCAL_N 16
+#endif
+constexpr int MID_LOCAL = MID_LOCAL_N;  // longer segments are ranked by the whole block
+
+__global__ void k_mid_hist(StageArgs A, int32_t *ccnt) {
+    pdl_wait();  // the events (k_stage_prep) and the live folds
+    const int64_t ne = 2 * A.ns;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ne;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = A.ekey[p];
+        if (c != SENTINEL) atomicAdd(ccnt + c, 1);
+    }
+}
+
+// One block; the counts staged through shared memory so every global access
+// is coalesced (dynamic smem: n ints).
+__global__ void __launch_bounds__(1024) k_mid_scan(const int32_t *ccnt, int32_t *cur, int64_t n) {
+    pdl_wait();
+    typedef cub::BlockScan<int, 1024> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    extern __shared__ int32_t sc[];
+    for (int64_t c = threadIdx.x; c < n; c += 1024) sc[c] = ccnt[c];
+    __syncthreads();
+    const int64_t per = (n + 1023) / 1024;
+    const int64_t c0 = threadIdx.x * per, c1 = c0 + per < n ? c0 + per : n;
+    int sum = 0;
+    for (int64_t c = c0; c < c1; c++) sum += sc[c];
+    int base;
+    Scan(tmp).ExclusiveSum(sum, base);
+    for (int64_t c = c0; c < c1; c++) {
+        const int v = sc[c];
+        sc[c] = base;
+        base += v;
+    }
+    __syncthreads();
+    for (int64_t c = threadIdx.x; c < n; c += 1024) cur[c] = sc[c];
+}
+
+__global__ void k_mid_scatter(StageArgs A, int32_t *cur, int32_t *ids) {
+    pdl_wait();
+    const int64_t ne = 2 * A.ns;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ne;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = A.ekey[p];
+        if (c != SENTINEL) ids[atomicAdd(cur + c, 1)] = (int32_t)p;  // (eval[p] == p)
+    }
+}
+
+// Thread c: community c's segment [cur[c] - ccnt[c], cur[c]).
+__global__ void __launch_bounds__(256) k_mid_fold(StageArgs A, int32_t *ccnt, const int32_t *cur,
+                                                  const int32_t *ids, int32_t *tmp, int64_t n) {
+    pdl_wait();
+    __shared__ int s_nlong;
+    __shared__ int32_t s_long[256];
+    const int tid = threadIdx.x;
+    if (tid == 0) s_nlong = 0;
+    __syncthreads();
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + tid;
+    const int L = c < n ? ccnt[c] : 0;
+    const int s0 = c < n ? cur[c] - L : 0;
+    if (L > MID_LOCAL) {
+        s_long[atomicAdd(&s_nlong, 1)] = (int32_t)c;
+    } else if (L > 0) {
+        int32_t e[MID_LOCAL];
+#pragma unroll
+        for (int t = 0; t < MID_LOCAL; t++) e[t] = t < L ? ids[s0 + t] : INT32_MAX;
+        // insertion sort (ascending event id); most segments hold 1-4 events
+        if (L > 1 && L <= 4) {
+#pragma unroll
+            for (int t = 1; t < 4; t++) {
+#pragma unroll
+                for (int u = 3; u > 0; u--)
+                    if (u <= t && e[u] < e[u - 1]) {
+                        const int32_t x = e[u];
+                        e[u] = e[u - 1];
+                        e[u - 1] = x;
+                    }
+            }
+        } else if (L > 4) {
+#pragma unroll
+            for (int t = 1; t < MID_LOCAL; t++) {
+#pragma unroll
+                for (int u = MID_LOCAL - 1; u > 0; u--)
+                    if (u <= t && e[u] < e[u - 1]) {
+                        const int32_t x = e[u];
+                        e[u] = e[u - 1];
+                        e[u - 1] = x;
+                    }
+            }
+        }
+        // the deltas' loads first, the ordered additions after
+        double dw[MID_LOCAL], da[MID_LOCAL];
+#pragma unroll
+        for (int t = 0; t < MID_LOCAL; t++) {
+            dw[t] = 0.0;
+            da[t] = 0.0;
+            if (t < L) event_delta(A, e[t], dw[t], da[t]);
+        }
+        double W = A.w_int[c], At = A.a_tot[c];
+#pragma unroll
+        for (int t = 0; t < MID_LOCAL; t++) {
+            if (t >= L) break;
+            W = dadd(W, dw[t]);
+            At = dadd(At, da[t]);
+        }
+        A.w_int[c] = W;
+        A.a_tot[c] = At;
+    }
+    if (c < n && L) ccnt[c] = 0;  // back to idle
+    __syncthreads();
+    // long segments of this block's communities: every event's rank by
+    // counting (the whole block), then one thread folds the ranked ids
+    const int nlong = s_nlong;
+    for (int w = 0; w < nlong; w++) {
+        const int64_t cl = s_long[w];
+        const int Ll = cur[cl] - (cl ? cur[cl - 1] : 0);  // (cur[] holds the segment ends)
+        const int sl = cur[cl] - Ll;
+        for (int t = tid; t < Ll; t += blockDim.x) {
+            const int32_t v = ids[sl + t];
+            int r = 0;
+            for (int u = 0; u < Ll; u++) r += ids[sl + u] < v;
+            tmp[sl + r] = v;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double W = A.w_int[cl], At = A.a_tot[cl];
+            for (int t = 0; t < Ll; t++) {
+                double dw, da;
+                event_delta(A, tmp[sl + t], dw, da);
+                W = dadd(W, dw);
+                At = dadd(At, da);
+            }
+            A.w_int[cl] = W;
+            A.a_tot[cl] = At;
+        }
+        __syncthreads();
+    }
+    // every live fold has read the assignment by now: scatter the moves
+    if (!(A.flags & PLV_F_INDEPENDENT))
+        for (int64_t x = blockIdx.x * (int64_t)blockDim.x + tid; x < A.ns;
+             x += (int64_t)gridDim.x * blockDim.x)
+            if (A.moved[x]) A.assign[A.subset[x]] = A.target[x];
+    if (blockIdx.x == 0 && tid == 0 && A.nbig) A.nbig[0] = A.nbig[1] = 0ull;  // next stage
+}
+
 __global__ void k_stage_scatter(StageArgs A) {
     pdl_wait();  // launched programmatically after its predecessor
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < A.ns;
@@ -536,12 +692,20 @@ void ApplyBuffers::alloc(int64_t ta_len, int64_t max_ns, int64_t n, cudaStream_t
     lcnt = dalloc<unsigned long long>(1);
     PLV_CUDA(cudaMemsetAsync(lcnt, 0, sizeof(unsigned long long), s));
     nb = bits_for(n + 1);  // SENTINEL's low nb bits exceed every community id
+    this->n = n;
+    if (n > 0 && n <= MID_N) {  // the counting sort of a small graph's stages
+        ccnt = dalloc<int32_t>(n);
+        ccur = dalloc<int32_t>(n);
+        PLV_CUDA(cudaMemsetAsync(ccnt, 0, sizeof(int32_t) * n, s));
+    }
     PLV_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, ekey, ekey2, eval, eval2, ne, 0, nb, s));
     tmp = pool_alloc(bytes);
     static int dev_done = -1;
     int dev;
     PLV_CUDA(cudaGetDevice(&dev));
     if (dev_done != dev) {
+        PLV_CUDA(cudaFuncSetAttribute(k_mid_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(int32_t) * MID_N)));
         PLV_CUDA(cudaFuncSetAttribute(k_stage_apply_small<SA_ITEMS>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(2 * SA_THREADS * SA_ITEMS * sizeof(double))));
@@ -551,7 +715,8 @@ void ApplyBuffers::alloc(int64_t ta_len, int64_t max_ns, int64_t n, cudaStream_t
 
 void ApplyBuffers::release() {
     cudaDeviceSynchronize();  // buffers go back to the pool idle
-    void *ps[] = {ta, tb, ekey, ekey2, eval, eval2, tmp, dW, dA, lrun, lcnt, big, nbig};
+    void *ps[] = {ta, tb, ekey, ekey2, eval, eval2, tmp, dW, dA, lrun, lcnt, big, nbig, ccnt, ccur};
+    ccnt = ccur = nullptr;
     for (void *p : ps)
         pool_free(p);
     big = nullptr;
@@ -563,6 +728,11 @@ void ApplyBuffers::release() {
     eval = eval2 = nullptr;
     dW = dA = nullptr;
     tmp = nullptr;
+}
+
+static bool mid_off() {  // PLV_APPLY_MID=0: the device radix sort for every stage
+    const char *e = getenv("PLV_APPLY_MID");
+    return e && e[0] == '0';
 }
 
 void launch_live(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {
@@ -618,7 +788,15 @@ void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {
     if (!indep) {
         launch_pdl(k_stage_live, APPLY_HB + APPLY_BB, 256, 0, st, S);
     }
-    if (!integral) {
+    if (!integral && B.n <= MID_N && B.ccnt && !mid_off()) {
+        const int64_t ne = 2 * S.ns;
+        launch_pdl(k_mid_hist, grid_for(ne, 256), 256, 0, st, S, B.ccnt);
+        launch_pdl(k_mid_scan, 1, 1024, sizeof(int32_t) * (size_t)B.n, st, (const int32_t *)B.ccnt,
+                   B.ccur, B.n);
+        launch_pdl(k_mid_scatter, grid_for(ne, 256), 256, 0, st, S, B.ccur, B.eval2);
+        launch_pdl(k_mid_fold, grid_for(B.n > S.ns ? B.n : S.ns, 256), 256, 0, st, S, B.ccnt,
+                   (const int32_t *)B.ccur, (const int32_t *)B.eval2, (int32_t *)B.ekey2, B.n);
+    } else if (!integral) {
         int64_t ne = 2 * S.ns;
         size_t bytes = B.bytes;
         PLV_CUDA(cub::DeviceRadixSort::SortPairs(B.tmp, bytes, B.ekey, B.ekey2, B.eval, B.eval2, ne,

@@ -222,6 +222,8 @@ struct ApplyBuffers {
     unsigned long long *nbig = nullptr;   // [0] big, [1] huge
     int64_t big_cap = 0;
     int nb = 1;
+    int64_t n = 0;  // communities (= vertices of the phase's graph)
+    int32_t *ccnt = nullptr, *ccur = nullptr;  // counting sort of a small graph's events (n each)
     void alloc(int64_t ta_len, int64_t max_ns, int64_t n, cudaStream_t s);
     void release();
 };
