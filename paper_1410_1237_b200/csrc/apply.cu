@@ -206,6 +206,10 @@ __global__ void __launch_bounds__(256) k_stage_prep(StageArgs A) {
                 A.ekey[2 * x + 1] = mover ? (uint32_t)b : SENTINEL;
                 A.eval[2 * x] = (int32_t)(2 * x);
                 A.eval[2 * x + 1] = (int32_t)(2 * x + 1);
+                if (mover && A.ccnt) {  // the counting sort's histogram (k_mid_*)
+                    atomicAdd(A.ccnt + a, 1);
+                    atomicAdd(A.ccnt + b, 1);
+                }
             }
         }
         double e_a = 0.0, e_b = 0.0;
@@ -371,28 +375,18 @@ __global__ void __launch_bounds__(256) k_stage_fold_long(StageArgs A, const uint
 }
 
 // A stage of a small graph (at most MID_N communities): the events' stable
-// sort by community as a counting sort over the communities -- histogram,
-// one-block scan, scatter of the event ids (any order), then each community's
-// segment put in ascending event id (the stable order of
-// PL/_kernels.pyx:116-144) and folded with the operations of k_stage_fold --
-// four short launches instead of the device radix sort's four plus the two
-// fold launches.  The capped 10,000-iteration phases of small coarse graphs
+// sort by community as a counting sort over the communities -- histogram
+// (k_stage_prep counts its movers' events), one-block scan, scatter of the
+// event ids (any order), then each community's segment put in ascending event
+// id (the stable order of PL/_kernels.pyx:116-144) and folded with the
+// operations of k_stage_fold -- three short launches instead of the device
+// radix sort's four plus the two fold launches.  The capped 10,000-iteration phases of small coarse graphs
 // pay these per iteration.  ccnt[] is zero between stages (the fold clears it).
 constexpr int64_t MID_N = 32768;
 #ifndef MID_LOCAL_N
 #define MID_LOCAL_N 16
 #endif
 constexpr int MID_LOCAL = MID_LOCAL_N;  // longer segments are ranked by the whole block
-
-__global__ void k_mid_hist(StageArgs A, int32_t *ccnt) {
-    pdl_wait();  // the events (k_stage_prep) and the live folds
-    const int64_t ne = 2 * A.ns;
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ne;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t c = A.ekey[p];
-        if (c != SENTINEL) atomicAdd(ccnt + c, 1);
-    }
-}
 
 // One block; the counts staged through shared memory so every global access
 // is coalesced (dynamic smem: n ints).
@@ -779,6 +773,8 @@ void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {
     S.lcnt = B.lcnt;
     // worklist counters are zero on entry: allocation clears them, and the
     // apply that used them last cleared them after its last reader
+    const bool mid = !integral && B.n <= MID_N && B.ccnt && !mid_off();
+    if (mid) S.ccnt = B.ccnt;
     unsigned nbp = grid_for((S.ns + 31) / 32 * 32, 256, 148 * 16);
     if (S.fx.n) {  // + one thread per fix entry of an ahead stage
         S.fx.pb = nbp;
@@ -788,9 +784,8 @@ void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {
     if (!indep) {
         launch_pdl(k_stage_live, APPLY_HB + APPLY_BB, 256, 0, st, S);
     }
-    if (!integral && B.n <= MID_N && B.ccnt && !mid_off()) {
+    if (mid) {
         const int64_t ne = 2 * S.ns;
-        launch_pdl(k_mid_hist, grid_for(ne, 256), 256, 0, st, S, B.ccnt);
         launch_pdl(k_mid_scan, 1, 1024, sizeof(int32_t) * (size_t)B.n, st, (const int32_t *)B.ccnt,
                    B.ccur, B.n);
         launch_pdl(k_mid_scatter, grid_for(ne, 256), 256, 0, st, S, B.ccur, B.eval2);

@@ -189,6 +189,7 @@ struct StageArgs {
     uint32_t *ekey;
     int32_t *eval;
     unsigned long long *moves;
+    int32_t *ccnt = nullptr;  // small graphs: events per community (counting sort, apply.cu)
     int32_t *big = nullptr;  // high-degree movers (live folds by whole warps)
     unsigned long long *nbig = nullptr;
     int32_t *huge = nullptr;  // huge movers (live folds by whole blocks)
