@@ -423,8 +423,12 @@ __global__ void k_mid_scatter(StageArgs A, int32_t *cur, int32_t *ids) {
 }
 
 // Thread c: community c's segment [cur[c] - ccnt[c], cur[c]).
+constexpr int MID_RANK2 = 128;                    // segments ranked by counting
+constexpr int MID_WORDS = (int)(2 * MID_N / 32);  // bitmap words of the event ids
+constexpr size_t MID_FOLD_SMEM = sizeof(double) * 4 * FOLD_CH + 2 * sizeof(uint32_t) * MID_WORDS;
 __global__ void __launch_bounds__(256) k_mid_fold(StageArgs A, int32_t *ccnt, const int32_t *cur,
-                                                  const int32_t *ids, int32_t *tmp, int64_t n) {
+                                                  const int32_t *ids, int32_t *tmp, int64_t n,
+                                                  double *dW, double *dA) {
     pdl_wait();
     __shared__ int s_nlong;
     __shared__ int32_t s_long[256];
@@ -484,28 +488,66 @@ __global__ void __launch_bounds__(256) k_mid_fold(StageArgs A, int32_t *ccnt, co
     }
     if (c < n && L) ccnt[c] = 0;  // back to idle
     __syncthreads();
-    // long segments of this block's communities: every event's rank by
-    // counting (the whole block), then one thread folds the ranked ids
+    // long segments of this block's communities, one at a time by the whole
+    // block: every event's rank among the segment's ids -- by counting up to
+    // MID_RANK2 events, beyond that from a bitmap of the ids and the prefix
+    // popcounts of its words (ids are unique and below 2 ns <= 65536) -- then
+    // the deltas in ranked order in parallel and the ordered fold staged
+    // through shared memory (block_fold2), as k_stage_fold_long does
+    extern __shared__ double dyn[];
+    double *sb = dyn;                                  // 4 * FOLD_CH doubles
+    uint32_t *bm = (uint32_t *)(dyn + 4 * FOLD_CH);    // MID_WORDS words
+    int *pre = (int *)(bm + MID_WORDS);                // MID_WORDS prefix popcounts
+    typedef cub::BlockScan<int, 256> Scan;
+    __shared__ typename Scan::TempStorage scan_tmp;
     const int nlong = s_nlong;
+    const int nwords = (int)((2 * A.ns + 31) >> 5);
     for (int w = 0; w < nlong; w++) {
         const int64_t cl = s_long[w];
         const int Ll = cur[cl] - (cl ? cur[cl - 1] : 0);  // (cur[] holds the segment ends)
         const int sl = cur[cl] - Ll;
-        for (int t = tid; t < Ll; t += blockDim.x) {
-            const int32_t v = ids[sl + t];
-            int r = 0;
-            for (int u = 0; u < Ll; u++) r += ids[sl + u] < v;
-            tmp[sl + r] = v;
+        if (Ll <= MID_RANK2) {
+            for (int t = tid; t < Ll; t += blockDim.x) {
+                const int32_t v = ids[sl + t];
+                int r = 0;
+                for (int u = 0; u < Ll; u++) r += ids[sl + u] < v;
+                tmp[sl + r] = v;
+            }
+        } else {
+            for (int q = tid; q < nwords; q += blockDim.x) bm[q] = 0u;
+            __syncthreads();
+            for (int t = tid; t < Ll; t += blockDim.x) {
+                const int32_t v = ids[sl + t];
+                atomicOr(&bm[v >> 5], 1u << (v & 31));
+            }
+            __syncthreads();
+            const int per = (nwords + 255) / 256;
+            const int q0 = tid * per, q1 = q0 + per < nwords ? q0 + per : nwords;
+            int sum = 0;
+            for (int q = q0; q < q1; q++) sum += __popc(bm[q]);
+            int base;
+            Scan(scan_tmp).ExclusiveSum(sum, base);
+            for (int q = q0; q < q1; q++) {
+                pre[q] = base;
+                base += __popc(bm[q]);
+            }
+            __syncthreads();
+            for (int t = tid; t < Ll; t += blockDim.x) {
+                const int32_t v = ids[sl + t];
+                tmp[sl + pre[v >> 5] + __popc(bm[v >> 5] & ((1u << (v & 31)) - 1u))] = v;
+            }
         }
         __syncthreads();
+        for (int t = tid; t < Ll; t += blockDim.x) event_delta(A, tmp[sl + t], dW[sl + t], dA[sl + t]);
+        __syncthreads();
+        double W = A.w_int[cl], At = A.a_tot[cl];
+        block_fold2(
+            [=] __device__(int64_t t, double &x, double &y) {
+                x = dW[sl + t];
+                y = dA[sl + t];
+            },
+            Ll, W, At, sb);
         if (tid == 0) {
-            double W = A.w_int[cl], At = A.a_tot[cl];
-            for (int t = 0; t < Ll; t++) {
-                double dw, da;
-                event_delta(A, tmp[sl + t], dw, da);
-                W = dadd(W, dw);
-                At = dadd(At, da);
-            }
             A.w_int[cl] = W;
             A.a_tot[cl] = At;
         }
@@ -700,6 +742,8 @@ void ApplyBuffers::alloc(int64_t ta_len, int64_t max_ns, int64_t n, cudaStream_t
     if (dev_done != dev) {
         PLV_CUDA(cudaFuncSetAttribute(k_mid_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(sizeof(int32_t) * MID_N)));
+        PLV_CUDA(cudaFuncSetAttribute(k_mid_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)MID_FOLD_SMEM));
         PLV_CUDA(cudaFuncSetAttribute(k_stage_apply_small<SA_ITEMS>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(2 * SA_THREADS * SA_ITEMS * sizeof(double))));
@@ -789,8 +833,9 @@ void launch_apply(StageArgs S, const ApplyBuffers &B, cudaStream_t st) {
         launch_pdl(k_mid_scan, 1, 1024, sizeof(int32_t) * (size_t)B.n, st, (const int32_t *)B.ccnt,
                    B.ccur, B.n);
         launch_pdl(k_mid_scatter, grid_for(ne, 256), 256, 0, st, S, B.ccur, B.eval2);
-        launch_pdl(k_mid_fold, grid_for(B.n > S.ns ? B.n : S.ns, 256), 256, 0, st, S, B.ccnt,
-                   (const int32_t *)B.ccur, (const int32_t *)B.eval2, (int32_t *)B.ekey2, B.n);
+        launch_pdl(k_mid_fold, grid_for(B.n > S.ns ? B.n : S.ns, 256), 256, MID_FOLD_SMEM, st, S,
+                   B.ccnt, (const int32_t *)B.ccur, (const int32_t *)B.eval2, (int32_t *)B.ekey2,
+                   B.n, B.dW, B.dA);
     } else if (!integral) {
         int64_t ne = 2 * S.ns;
         size_t bytes = B.bytes;
