@@ -17,6 +17,7 @@ cp $G/ktrace_c4_ah.txt $P/r02_ktrace_c4_ahead_pass.txt; cp $G/ahead_stats_c4.txt
 [ -f $G/l2_gather.txt ] && cp $G/l2_gather.txt $P/r02_l2_gather.txt
 for c in c2_rmat20 c3_grid c4_chung_lu; do cp $G/rp_$c.txt $P/r02_run_profile_$c.txt; done
 cp $G/rk_c4.txt $P/r02_run_kernels_c4.txt
+[ -f $G/capped_c3_p4.txt ] && cp $G/capped_c3_p4.txt $P/r02_capped_c3_phase4.txt
 python tools/ncu_full_summary.py $G/c4_ah_pass_full.ncu-rep "C4 coloured, ahead pass of a tail stage (k_ah_pass, launch 250 of the iteration), ncu --set full" > $P/r02_c4_ah_pass_full.txt
 python tools/ncu_full_summary.py $G/c4_ah_accum_full.ncu-rep "C4 coloured, ahead accumulation of the window (k_ah_accum), ncu --set full" > $P/r02_c4_ah_accum_full.txt
 python tools/ncu_full_summary.py $G/c4_t0_stage1_full.ncu-rep "C4 coloured, tier-0 decide of stage 1 (k_decide_t0, general path), ncu --set full" > $P/r02_c4_t0_stage1_full.txt

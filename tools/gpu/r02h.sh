@@ -40,3 +40,4 @@ for c in c2_rmat20 c3_grid c4_chung_lu; do timeout 300 python tools/run_profile.
 timeout 300 python tools/run_kernels.py c4_chung_lu 30 > gpurun_out/rk_c4.txt 2>&1
 timeout 300 python tools/ahead_stats.py c4_chung_lu > gpurun_out/ahead_stats_c4.txt 2>&1
 [ -x tools/l2_gather ] && tools/l2_gather > gpurun_out/l2_gather.txt 2>&1
+timeout 300 python tools/capped_timeline.py c3_grid --phase 4 > gpurun_out/capped_c3_p4.txt 2>&1
